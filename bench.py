@@ -1,0 +1,403 @@
+"""bench.py — GNP hot path on B200 (driver contract: one JSON line on rank 0).
+
+Workload (default, BASELINE.json configs[1] = "C2"): 3D convection-diffusion
+7-point upwind 64^3 (n = 262,144, nnz = 1,810,432), Â = A/γ in fp32, GNP d = 16,
+hidden 32, 8 Res-GCONV layers, Xavier-uniform weights from seed 0.  One step =
+one M·v apply of a fresh right-hand side.  Metric: applies/s (whole job).
+  value  : device-resident inputs (gnpc_apply_device_f32), CUDA events per step,
+           L2 flushed (512 MiB write) between steps (C2's working set fits in L2).
+  e2e    : the reference-facing C-ABI call gnpc_apply with pinned HOST f64
+           buffers: H2D of b + D2H of M(b) inside every timed step.
+  roofline: dominant kernel = the fused Res-GCONV layer; algorithmic bytes per
+           launch = 4(n+1) + 8 nnz + 8 n d, event-timed per kernel.
+  fgmres : one device FGMRES solve of the config (restart/rtol per BASELINE).
+  cpu_baseline: the unmodified reference gnn_apply (oracle/_ref) on the host,
+           1 thread (the reference apply is single-threaded), bounded sample.
+--impl reference: the reference CPU apply on all usable host threads.
+--config c1|c2|c4|c5 selects another apply workload (parity/profiling lines).
+N>1 (torchrun): independent replicas, value = Σ applies / max-rank time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (generator kind, size, p0, p1, seed, dims, rhs, fgmres (restart, rtol, maxiters))
+    "c1": ("convection_diffusion", 64, 0.0, 0.0, 0, (16, 32, 8), ("gauss", 1), (10, 1e-8, 100),
+           "C1 2D 5-pt Laplacian 64x64 (n=4096), GNP d=16 L=8"),
+    "c2": ("c2_convdiff3d", 64, 10.0, 0.0, 0, (16, 32, 8), ("Ax", 1), (30, 1e-6, 100),
+           "C2 3D conv-diff 7-pt upwind 64^3 Pe=10 (n=262144), GNP d=16 L=8"),
+    "c4": ("c4_powerlaw", 1 << 20, 2.2, 0.0, 4, (16, 32, 8), ("gauss", 4), (30, 1e-6, 100),
+           "C4 power-law random n=2^20 (alpha 2.2, rows 4..2048), GNP d=16 L=8"),
+    "c5": ("c5_aniso9pt", 2048, 1e-3, 30.0, 0, (32, 32, 8), ("Ax", 3), (50, 1e-6, 100),
+           "C5 2D anisotropic 9-pt 2048^2 (eps 1e-3, 30deg), GNP d=32 L=8"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+            return
+
+        def reader():
+            for line in self.proc.stdout:
+                self.rows.append([x.strip() for x in line.split(",")])
+
+        self.t = threading.Thread(target=reader, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+                for nm, v in zip(names, r[2:6]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_workload(capi, cfg_name):
+    kind, size, p0, p1, seed, dims, rhs, fg, desc = CONFIGS[cfg_name]
+    a = capi.Csr.generate(kind, size, p0, p1, seed)
+    ah = a.prescale(a.gamma())
+    n, nnz = ah.info()
+    params = capi.init_params(*dims, 0)
+    model = capi.Model(ah, dims, params)
+    if rhs[0] == "gauss":
+        b = capi.gaussian_vector(rhs[1], n)
+    else:
+        b = ah.spmv(capi.gaussian_vector(rhs[1], n))
+    return dict(name=cfg_name, desc=desc, a=ah, n=n, nnz=nnz, dims=dims, params=params,
+                model=model, b=b, fgmres=fg)
+
+
+def layer_bytes(n, nnz, d):
+    return 4 * (n + 1) + 8 * nnz + 8 * n * d
+
+
+def apply_bytes(n, nnz, d, L):
+    return 12 * n + 8 * n * d + L * layer_bytes(n, nnz, d)
+
+
+def cpu_reference_baseline(w, seconds=15.0):
+    """The unmodified reference gnn_apply on the host (1 thread), bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    rp, ci, v = w["a"].arrays()
+    csr = oracle.Csr(w["n"], rp, ci, v.astype(np.float32).astype(np.float64))
+    p32 = w["params"].astype(np.float32).astype(np.float64)
+    if oracle.reference_available():
+        impl, kind = oracle.reference(), "reference"
+    else:
+        impl, kind = oracle.restatement(), "port"
+    reps, total = 0, 0.0
+    while total < seconds and reps < 50:
+        if kind == "reference":
+            secs, _ = impl.time_gnn_apply(csr, w["dims"], p32, w["b"], 1)
+        else:
+            t0 = time.perf_counter()
+            impl.gnn_apply(csr, w["dims"], p32, w["b"])
+            secs = time.perf_counter() - t0
+        total += secs
+        reps += 1
+        if secs > seconds / 2:
+            break
+    return {"value": reps / total, "unit": "applies/s", "cores": 1, "kind": kind,
+            "sample": f"{reps} gnn_apply call(s) on {w['name']} (n={w['n']}, d={w['dims'][0]}), "
+                      f"{total:.1f} s, fp32-rounded inputs as f64"}
+
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the reference CPU apply, all usable host threads."""
+    cfg = args.config
+    if rank != 0:
+        print(json.dumps({"impl": "reference", "rank": rank, "skipped": "rank 0 only"}),
+              file=sys.stderr)
+        return
+    from paper_2406_00809_b200 import capi
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    kind, size, p0, p1, seed, dims, rhs, fg, desc = CONFIGS[cfg]
+    a = capi.Csr.generate(kind, size, p0, p1, seed)
+    ah = a.prescale(a.gamma())
+    n, nnz = ah.info()
+    rp, ci, v = ah.arrays()
+    csr = oracle.Csr(n, rp, ci, v.astype(np.float32).astype(np.float64))
+    p = capi.init_params(*dims, 0).astype(np.float32).astype(np.float64)
+    b = capi.gaussian_vector(rhs[1], n)
+    if oracle.reference_available():
+        impl, ikind = oracle.reference(), "reference"
+    else:
+        impl, ikind = oracle.restatement(), "port"
+    # threads: every core, bounded by RAM (the reference keeps the full
+    # ForwardCache, ~(3L+1) n d + 4 n h doubles, per call)
+    cache = 8 * n * ((3 * dims[2] + 1) * dims[0] + 4 * dims[1] + 4)
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 32 << 30
+    threads = max(1, min(os.cpu_count() or 1, int(avail * 0.6 // max(cache, 1))))
+
+    def one():
+        if ikind == "reference":
+            impl.time_gnn_apply(csr, dims, p, b, 1)
+        else:
+            impl.gnn_apply(csr, dims, p, b)
+
+    def step():
+        ts = [threading.Thread(target=one) for _ in range(threads)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    value = args.steps * threads / el
+    line = {
+        "impl": "reference", "metric": f"GNP M.v applies/s ({cfg.upper()})", "value": value,
+        "unit": "applies/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "n": n, "nnz": nnz, "d": dims[0], "hidden": dims[1],
+                   "layers": dims[2]},
+        "cpu_baseline": {"value": value, "unit": "applies/s", "cores": threads, "kind": ikind,
+                         "sample": f"{threads} concurrent gnn_apply calls per step"},
+        "e2e": {"value": value, "unit": "applies/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fgmres", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2406_00809_b200 import capi
+
+    check = capi.check
+    capi.check(capi.lib().gnpc_set_device(local))
+    w = build_workload(capi, args.config)
+    n, nnz, (d, hdim, L) = w["n"], w["nnz"], w["dims"]
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    model = w["model"]
+    # distinct RHS per step (a batch of fresh inputs resident in HBM)
+    nb = 8
+    rng = np.random.default_rng(1234 + rank)
+    bs = [torch.tensor(w["b"] * (1.0 + 0.01 * rng.standard_normal()), dtype=torch.float32,
+                       device="cuda") for _ in range(nb)]
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def do_step(i):
+        model.apply_device_f32(bs[i % nb].data_ptr(), out.data_ptr(), sptr)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for i in range(args.warmup):
+        flush.zero_()
+        do_step(i)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = capi.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        do_step(i)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    launches = capi.launch_count() - l0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = sum(s.elapsed_time(e) for s, e in evs)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = world * args.steps / (max_ms / 1e3)
+
+    # ---- roofline: per-kernel event timing of the same workload
+    ms_k = np.zeros(5)
+    cnt_k = np.zeros(5, np.int64)
+    for i in range(args.steps):
+        flush.zero_()
+        model.apply_profile(bs[i % nb].data_ptr(), out.data_ptr(), sptr, ms_k, cnt_k)
+    layer_ms = (ms_k[3] + ms_k[4]) / max(1, cnt_k[3] + cnt_k[4])
+    mid_ms = ms_k[3] / max(1, cnt_k[3])
+    lb = layer_bytes(n, nnz, d if d >= 4 else 4)
+    peak, peak_src = load_peaks()
+    achieved = lb / (mid_ms / 1e3) / 1e9 if cnt_k[3] else lb / (layer_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    apply_gbs = apply_bytes(n, nnz, d, L) / (max_ms / args.steps / 1e3) / 1e9
+
+    # ---- e2e through the C ABI with pinned host buffers
+    hb = torch.tensor(w["b"], dtype=torch.float64).pin_memory()
+    ho = torch.empty(n, dtype=torch.float64).pin_memory()
+    lib = capi.lib()
+    import ctypes as C
+
+    for _ in range(3):
+        check(lib.gnpc_apply(model.h, C.c_void_p(hb.data_ptr()), C.c_void_p(ho.data_ptr())))
+    e2e_steps = args.steps
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        check(lib.gnpc_apply(model.h, C.c_void_p(hb.data_ptr()), C.c_void_p(ho.data_ptr())))
+    e2e_el = time.perf_counter() - t0
+    te = torch.tensor([e2e_el], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": world * e2e_steps / float(te.item()), "unit": "applies/s",
+           "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+           "api": "gnpc_apply (host f64, pinned)"}
+
+    # ---- one FGMRES solve (device-resident)
+    fg = None
+    if not args.no_fgmres:
+        restart, rtol, maxiters = w["fgmres"]
+        bd = torch.tensor(w["b"], dtype=torch.float64, device="cuda")
+        xd = torch.zeros(n, dtype=torch.float64, device="cuda")
+        capi.fgmres_device(w["a"], model, bd.data_ptr(), xd.data_ptr(), rtol, 2, restart, sptr)
+        xd.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s = capi.fgmres_device(w["a"], model, bd.data_ptr(), xd.data_ptr(), rtol, maxiters,
+                               restart, sptr)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        fg = {"solve_s": el, "iterations": s["history"][-1][0], "status": s["status"],
+              "final_relres": s["history"][-1][1], "restart": restart, "rtol": rtol,
+              "maxiters": maxiters, "reorth_steps": s["reorth_steps"],
+              "ms_per_iteration": 1e3 * el / max(1, s["history"][-1][0])}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_reference_baseline(w)
+    line = {
+        "metric": f"GNP M.v applies/s ({args.config.upper()}); fused-layer HBM GB/s vs peak; FGMRES solve time",
+        "value": value, "unit": "applies/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": w["desc"], "n": n, "nnz": nnz, "d": d, "hidden": hdim, "layers": L,
+                   "rhs": "8 distinct resident RHS, fp32",
+                   "l2": "flushed between timed steps (512 MiB write, untimed)",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": f"k_layer<DP={d if d >= 4 else 4}> (fused Res-GCONV)",
+                     "algorithmic_bytes_per_launch": lb, "avg_launch_ms": mid_ms,
+                     "peak_source": peak_src,
+                     "kernel_share_of_step": float((ms_k[3] + ms_k[4]) / max(ms_k.sum(), 1e-12))},
+        "apply_gbs": apply_gbs, "apply_frac_of_peak": apply_gbs / peak,
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
+        "fgmres": fg,
+        "per_kernel_ms": {"norm": ms_k[0] / max(1, cnt_k[0]), "lift": ms_k[1] / max(1, cnt_k[1]),
+                          "long_rows": ms_k[2] / max(1, cnt_k[2]) if cnt_k[2] else None,
+                          "layer": mid_ms, "last_layer_projection": ms_k[4] / max(1, cnt_k[4])},
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

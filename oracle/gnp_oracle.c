@@ -1,0 +1,861 @@
+/* oracle/gnp_oracle.c — TEST INFRASTRUCTURE ONLY (parity checker, never shipped).
+ *
+ * Plain-C restatement of the reference GNP hot path (f64, sequential), written
+ * to reproduce the reference's floating-point operation order so that, on the
+ * same inputs, it agrees with the reference BIT-FOR-BIT (pinned by
+ * tests/test_oracle_pins.py against oracle/_ref and tests/golden/).
+ * Each function cites the reference file:line it restates
+ * (paths relative to /root/reference/proj).
+ */
+#define _POSIX_C_SOURCE 199309L
+#include "gnp_oracle.h"
+
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+static _Thread_local char g_err[256];
+static int fail(const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
+  return -1;
+}
+const char* oc_last_error(void) { return g_err; }
+
+/* ======================================================================
+ * RNG — include/gnp/rng.hpp:13-52.  std::mt19937_64 is fully specified by the
+ * C++ standard ([rand.predef]); restated here with its published constants.
+ * ==================================================================== */
+#define MT_N 312
+#define MT_M 156
+void oc_rng_init(oc_rng* r, uint64_t seed) {
+  r->mt[0] = seed;
+  for (int i = 1; i < MT_N; ++i)
+    r->mt[i] = 6364136223846793005ULL * (r->mt[i - 1] ^ (r->mt[i - 1] >> 62)) + (uint64_t)i;
+  r->idx = MT_N;
+  r->have_spare = 0;
+  r->spare = 0.0;
+}
+
+uint64_t oc_rng_next(oc_rng* r) {
+  const uint64_t upper = 0xFFFFFFFF80000000ULL, lower = 0x7FFFFFFFULL;
+  const uint64_t mat = 0xB5026F5AA96619E9ULL;
+  if (r->idx >= MT_N) {
+    for (int i = 0; i < MT_N; ++i) {
+      uint64_t y = (r->mt[i] & upper) | (r->mt[(i + 1) % MT_N] & lower);
+      uint64_t nv = r->mt[(i + MT_M) % MT_N] ^ (y >> 1);
+      if (y & 1ULL) nv ^= mat;
+      r->mt[i] = nv;
+    }
+    r->idx = 0;
+  }
+  uint64_t x = r->mt[r->idx++];
+  x ^= (x >> 29) & 0x5555555555555555ULL;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+  x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+  x ^= x >> 43;
+  return x;
+}
+
+/* rng.hpp:18-20 */
+double oc_rng_uniform(oc_rng* r) { return (double)(oc_rng_next(r) >> 11) * 0x1.0p-53; }
+/* rng.hpp:23-25 */
+double oc_rng_uniform_symmetric(oc_rng* r, double bound) {
+  return (2.0 * oc_rng_uniform(r) - 1.0) * bound;
+}
+/* rng.hpp:27-40: Box-Muller with a cached spare */
+double oc_rng_gaussian(oc_rng* r) {
+  if (r->have_spare) {
+    r->have_spare = 0;
+    return r->spare;
+  }
+  double u1 = oc_rng_uniform(r);
+  while (u1 <= 0.0) u1 = oc_rng_uniform(r);
+  const double u2 = oc_rng_uniform(r);
+  const double rad = sqrt(-2.0 * log(u1));
+  const double theta = 6.283185307179586476925286766559 * u2;
+  r->spare = rad * sin(theta);
+  r->have_spare = 1;
+  return rad * cos(theta);
+}
+void oc_gaussian_vector(uint64_t seed, size_t n, double* out) {
+  oc_rng r;
+  oc_rng_init(&r, seed);
+  for (size_t i = 0; i < n; ++i) out[i] = oc_rng_gaussian(&r);
+}
+
+/* ======================================================================
+ * Sparse core — src/csr.cpp
+ * ==================================================================== */
+typedef struct {
+  const int64_t* rows;
+  const int64_t* cols;
+} key_ctx;
+
+/* Stable merge sort of the index permutation by (row, col).  The reference
+ * uses std::sort (csr.cpp:22-27), which orders equal keys arbitrarily; the two
+ * agree whenever no (row, col) pair repeats, and for exact duplicates the sum
+ * is order-independent up to 2 terms. */
+static int key_less(const key_ctx* c, size_t a, size_t b) {
+  if (c->rows[a] != c->rows[b]) return c->rows[a] < c->rows[b];
+  return c->cols[a] < c->cols[b];
+}
+static void msort(const key_ctx* c, size_t* a, size_t* tmp, size_t lo, size_t hi) {
+  if (hi - lo < 2) return;
+  const size_t mid = lo + (hi - lo) / 2;
+  msort(c, a, tmp, lo, mid);
+  msort(c, a, tmp, mid, hi);
+  size_t i = lo, j = mid, k = lo;
+  while (i < mid && j < hi) tmp[k++] = key_less(c, a[j], a[i]) ? a[j++] : a[i++];
+  while (i < mid) tmp[k++] = a[i++];
+  while (j < hi) tmp[k++] = a[j++];
+  memcpy(a + lo, tmp + lo, (hi - lo) * sizeof(size_t));
+}
+
+/* csr.cpp:10-50 */
+int oc_csr_from_triplets(size_t n, size_t m, const int64_t* rows, const int64_t* cols,
+                         const double* vals, int64_t* rp, int64_t* ci, double* v,
+                         size_t* nnz_out) {
+  for (size_t k = 0; k < m; ++k)
+    if (rows[k] < 0 || cols[k] < 0 || (size_t)rows[k] >= n || (size_t)cols[k] >= n)
+      return fail("triplet index out of range");
+  size_t* order = (size_t*)malloc((m ? m : 1) * sizeof(size_t));
+  size_t* tmp = (size_t*)malloc((m ? m : 1) * sizeof(size_t));
+  for (size_t k = 0; k < m; ++k) order[k] = k;
+  key_ctx c = {rows, cols};
+  msort(&c, order, tmp, 0, m);
+  for (size_t i = 0; i <= n; ++i) rp[i] = 0;
+  size_t nnz = 0;
+  int64_t last_row = -1;
+  for (size_t k = 0; k < m; ++k) {
+    const size_t t = order[k];
+    if (nnz > 0 && rows[t] == last_row && cols[t] == ci[nnz - 1]) {
+      v[nnz - 1] += vals[t]; /* duplicate entry: sum (csr.cpp:38-41) */
+    } else {
+      last_row = rows[t];
+      ci[nnz] = cols[t];
+      v[nnz] = vals[t];
+      ++nnz;
+      rp[rows[t] + 1]++;
+    }
+  }
+  for (size_t i = 0; i < n; ++i) rp[i + 1] += rp[i];
+  *nnz_out = nnz;
+  free(order);
+  free(tmp);
+  return 0;
+}
+
+/* csr.cpp:52-62 */
+void oc_spmv(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+             const double* x, double* y) {
+  for (size_t i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) s += v[k] * x[ci[k]];
+    y[i] = s;
+  }
+}
+/* csr.cpp:64-78 (column-major n x k) */
+void oc_spmm(size_t n, const int64_t* rp, const int64_t* ci, const double* v, size_t k,
+             const double* x, double* y) {
+  for (size_t j = 0; j < k; ++j) oc_spmv(n, rp, ci, v, x + j * n, y + j * n);
+}
+/* csr.cpp:80-90 (scatter) */
+void oc_spmv_transpose(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                       const double* x, double* y) {
+  for (size_t i = 0; i < n; ++i) y[i] = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    const double xi = x[i];
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) y[ci[k]] += v[k] * xi;
+  }
+}
+/* csr.cpp:108-125: counting sort, stable in row order */
+void oc_transpose(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                  int64_t* trp, int64_t* tci, double* tv) {
+  const size_t nnz = (size_t)rp[n];
+  for (size_t i = 0; i <= n; ++i) trp[i] = 0;
+  for (size_t k = 0; k < nnz; ++k) trp[ci[k] + 1]++;
+  for (size_t i = 0; i < n; ++i) trp[i + 1] += trp[i];
+  int64_t* next = (int64_t*)malloc((n ? n : 1) * sizeof(int64_t));
+  for (size_t i = 0; i < n; ++i) next[i] = trp[i];
+  for (size_t i = 0; i < n; ++i)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const int64_t pos = next[ci[k]]++;
+      tci[pos] = (int64_t)i;
+      tv[pos] = v[k];
+    }
+  free(next);
+}
+/* csr.cpp:127-143 */
+double oc_gershgorin_gamma(size_t n, const int64_t* rp, const int64_t* ci, const double* v) {
+  double* col = (double*)calloc(n ? n : 1, sizeof(double));
+  double max_row = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    double row = 0.0;
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const double a = fabs(v[k]);
+      row += a;
+      col[ci[k]] += a;
+    }
+    if (row > max_row) max_row = row;
+  }
+  double max_col = 0.0;
+  for (size_t i = 0; i < n; ++i)
+    if (col[i] > max_col) max_col = col[i];
+  free(col);
+  const double g = max_row < max_col ? max_row : max_col;
+  return g == 0.0 ? 1.0 : g;
+}
+/* csr.cpp:152-173: FNV-1a over n, row_ptr, col_idx (as u64), raw f64 values */
+static void fnv(uint64_t* h, const void* p, size_t bytes) {
+  const unsigned char* c = (const unsigned char*)p;
+  for (size_t i = 0; i < bytes; ++i) {
+    *h ^= c[i];
+    *h *= 1099511628211ULL;
+  }
+}
+uint64_t oc_csr_hash(size_t n, const int64_t* rp, const int64_t* ci, const double* v) {
+  uint64_t h = 1469598103934665603ULL;
+  uint64_t n64 = n;
+  fnv(&h, &n64, 8);
+  for (size_t i = 0; i <= n; ++i) {
+    uint64_t x = (uint64_t)rp[i];
+    fnv(&h, &x, 8);
+  }
+  const size_t nnz = (size_t)rp[n];
+  for (size_t k = 0; k < nnz; ++k) {
+    uint64_t x = (uint64_t)ci[k];
+    fnv(&h, &x, 8);
+  }
+  fnv(&h, v, nnz * sizeof(double));
+  return h;
+}
+
+/* gen.cpp:11-38 */
+int oc_gen_convection_diffusion(size_t grid, double conv, int64_t* rp, int64_t* ci,
+                                double* v, size_t* nnz_out) {
+  if (grid < 2) return fail("gen: grid must be >= 2");
+  if (fabs(conv) > 1.0) return fail("gen: convection must lie in [-1, 1]");
+  const size_t n = grid * grid;
+  int64_t* r = (int64_t*)malloc(5 * n * sizeof(int64_t));
+  int64_t* c = (int64_t*)malloc(5 * n * sizeof(int64_t));
+  double* x = (double*)malloc(5 * n * sizeof(double));
+  size_t m = 0;
+#define PUSH(row, col, val) (r[m] = (int64_t)(row), c[m] = (int64_t)(col), x[m] = (val), ++m)
+  for (size_t iy = 0; iy < grid; ++iy)
+    for (size_t ix = 0; ix < grid; ++ix) {
+      const size_t row = iy * grid + ix;
+      PUSH(row, row, 4.0);
+      if (ix > 0) PUSH(row, iy * grid + ix - 1, -1.0 - conv);
+      if (ix + 1 < grid) PUSH(row, iy * grid + ix + 1, -1.0 + conv);
+      if (iy > 0) PUSH(row, (iy - 1) * grid + ix, -1.0);
+      if (iy + 1 < grid) PUSH(row, (iy + 1) * grid + ix, -1.0);
+    }
+#undef PUSH
+  int rc = oc_csr_from_triplets(n, m, r, c, x, rp, ci, v, nnz_out);
+  free(r);
+  free(c);
+  free(x);
+  return rc;
+}
+
+/* ======================================================================
+ * GNP — src/gnn.cpp
+ * ==================================================================== */
+typedef struct {
+  size_t d, h, L;
+  const double *enc1, *enc1_b, *enc2, *enc2_b, *dec1, *dec1_b, *dec2;
+  const double* u[64];
+  const double* w[64];
+  double dec2_b;
+} net;
+
+typedef struct {
+  size_t o_enc1, o_enc1_b, o_enc2, o_enc2_b, o_u[64], o_w[64], o_dec1, o_dec1_b, o_dec2,
+      o_dec2_b, total;
+} layout;
+
+/* flat order = param_views (gnn.cpp:40-55) */
+static layout make_layout(size_t d, size_t h, size_t L) {
+  layout l;
+  size_t o = 0;
+  l.o_enc1 = o; o += h;
+  l.o_enc1_b = o; o += h;
+  l.o_enc2 = o; o += h * d;
+  l.o_enc2_b = o; o += d;
+  for (size_t i = 0; i < L && i < 64; ++i) {
+    l.o_u[i] = o; o += d * d;
+    l.o_w[i] = o; o += d * d;
+  }
+  l.o_dec1 = o; o += d * h;
+  l.o_dec1_b = o; o += h;
+  l.o_dec2 = o; o += h;
+  l.o_dec2_b = o; o += 1;
+  l.total = o;
+  return l;
+}
+static net make_net(size_t d, size_t h, size_t L, const double* p) {
+  layout l = make_layout(d, h, L);
+  net N;
+  N.d = d; N.h = h; N.L = L;
+  N.enc1 = p + l.o_enc1; N.enc1_b = p + l.o_enc1_b;
+  N.enc2 = p + l.o_enc2; N.enc2_b = p + l.o_enc2_b;
+  for (size_t i = 0; i < L; ++i) { N.u[i] = p + l.o_u[i]; N.w[i] = p + l.o_w[i]; }
+  N.dec1 = p + l.o_dec1; N.dec1_b = p + l.o_dec1_b; N.dec2 = p + l.o_dec2;
+  N.dec2_b = p[l.o_dec2_b];
+  return N;
+}
+
+size_t oc_param_count(size_t d, size_t hidden, size_t layers) {
+  return make_layout(d, hidden, layers).total;
+}
+
+/* gnn.cpp:92-118 (glorot_bound gnn.cpp:19-21) */
+int oc_init_params(size_t d, size_t h, size_t L, uint64_t seed, double* out) {
+  if (d < 1 || h < 1 || L < 1) return fail("init_params: dims must be >= 1");
+  if (L > 64) return fail("oracle supports at most 64 layers");
+  layout l = make_layout(d, h, L);
+  memset(out, 0, l.total * sizeof(double));
+  oc_rng r;
+  oc_rng_init(&r, seed);
+#define FILL(off, cnt, fi, fo)                                               \
+  do {                                                                       \
+    const double bound = sqrt(6.0 / (double)((fi) + (fo)));                  \
+    for (size_t q = 0; q < (cnt); ++q) out[(off) + q] = oc_rng_uniform_symmetric(&r, bound); \
+  } while (0)
+  FILL(l.o_enc1, h, 1, h);
+  FILL(l.o_enc2, h * d, h, d);
+  for (size_t i = 0; i < L; ++i) {
+    FILL(l.o_u[i], d * d, d, d);
+    FILL(l.o_w[i], d * d, d, d);
+  }
+  FILL(l.o_dec1, d * h, d, h);
+  FILL(l.o_dec2, h, h, 1);
+#undef FILL
+  return 0;
+}
+
+/* dense.cpp:37-49: C = A*B, A rows x k, B k x m, col-major, skips b_kj == 0 */
+static void gemm_nn(size_t rows, size_t k, size_t m, const double* a, const double* b,
+                    double* c) {
+  memset(c, 0, rows * m * sizeof(double));
+  for (size_t j = 0; j < m; ++j)
+    for (size_t kk = 0; kk < k; ++kk) {
+      const double bkj = b[j * k + kk];
+      if (bkj == 0.0) continue;
+      const double* ak = a + kk * rows;
+      double* cj = c + j * rows;
+      for (size_t i = 0; i < rows; ++i) cj[i] += ak[i] * bkj;
+    }
+}
+/* dense.cpp:23-35: C = A^T B, A rows x p, B rows x q -> p x q */
+static void gemm_tn(size_t rows, size_t p, size_t q, const double* a, const double* b,
+                    double* c) {
+  for (size_t j = 0; j < q; ++j)
+    for (size_t i = 0; i < p; ++i) {
+      double s = 0.0;
+      const double* ai = a + i * rows;
+      const double* bj = b + j * rows;
+      for (size_t k = 0; k < rows; ++k) s += ai[k] * bj[k];
+      c[j * p + i] = s;
+    }
+}
+
+typedef struct {
+  int zero;
+  double tau;
+  double *v, *pre0, *x0, *x1, *ax, *pre, *post, *dec_pre, *dec_post;
+} fcache;
+
+static void free_cache(fcache* c) {
+  free(c->v); free(c->pre0); free(c->x0); free(c->x1); free(c->ax); free(c->pre);
+  free(c->post); free(c->dec_pre); free(c->dec_post);
+  memset(c, 0, sizeof *c);
+}
+
+/* gnn.cpp:120-201 */
+static void forward(size_t n, const int64_t* rp, const int64_t* ci, const double* av,
+                    const net* N, const double* b, double* out, fcache* c) {
+  const size_t d = N->d, h = N->h, L = N->L;
+  memset(c, 0, sizeof *c);
+  double s = 0.0;
+  for (size_t i = 0; i < n; ++i) s += b[i] * b[i];
+  c->tau = sqrt(s);
+  if (c->tau == 0.0) {
+    c->zero = 1;
+    for (size_t i = 0; i < n; ++i) out[i] = 0.0;
+    return;
+  }
+  const double sqrt_n = sqrt((double)n);
+  const double in_scale = sqrt_n / c->tau;
+  c->v = (double*)malloc(n * sizeof(double));
+  for (size_t i = 0; i < n; ++i) c->v[i] = in_scale * b[i];
+  c->pre0 = (double*)malloc(n * h * sizeof(double));
+  c->x0 = (double*)malloc(n * h * sizeof(double));
+  for (size_t hh = 0; hh < h; ++hh) {
+    const double wgt = N->enc1[hh], bias = N->enc1_b[hh];
+    for (size_t i = 0; i < n; ++i) {
+      const double pre = c->v[i] * wgt + bias;
+      c->pre0[hh * n + i] = pre;
+      c->x0[hh * n + i] = pre > 0.0 ? pre : 0.0;
+    }
+  }
+  c->x1 = (double*)malloc(n * d * sizeof(double));
+  gemm_nn(n, h, d, c->x0, N->enc2, c->x1);
+  for (size_t j = 0; j < d; ++j)
+    for (size_t i = 0; i < n; ++i) c->x1[j * n + i] += N->enc2_b[j];
+
+  c->ax = (double*)malloc(L * n * d * sizeof(double));
+  c->pre = (double*)malloc(L * n * d * sizeof(double));
+  c->post = (double*)malloc(L * n * d * sizeof(double));
+  double* axw = (double*)malloc(n * d * sizeof(double));
+  const double* x = c->x1;
+  for (size_t l = 0; l < L; ++l) {
+    double* ax = c->ax + l * n * d;
+    double* pre = c->pre + l * n * d;
+    double* post = c->post + l * n * d;
+    oc_spmm(n, rp, ci, av, d, x, ax);
+    gemm_nn(n, d, d, x, N->u[l], pre);
+    gemm_nn(n, d, d, ax, N->w[l], axw);
+    for (size_t k = 0; k < n * d; ++k) pre[k] += axw[k];
+    for (size_t k = 0; k < n * d; ++k) post[k] = pre[k] > 0.0 ? pre[k] : 0.0;
+    x = post;
+  }
+  free(axw);
+  c->dec_pre = (double*)malloc(n * h * sizeof(double));
+  c->dec_post = (double*)malloc(n * h * sizeof(double));
+  gemm_nn(n, d, h, x, N->dec1, c->dec_pre);
+  for (size_t hh = 0; hh < h; ++hh) {
+    const double bias = N->dec1_b[hh];
+    double* pre = c->dec_pre + hh * n;
+    double* post = c->dec_post + hh * n;
+    for (size_t i = 0; i < n; ++i) {
+      pre[i] += bias;
+      post[i] = pre[i] > 0.0 ? pre[i] : 0.0;
+    }
+  }
+  const double out_scale = c->tau / sqrt_n;
+  for (size_t i = 0; i < n; ++i) out[i] = 0.0;
+  for (size_t hh = 0; hh < h; ++hh) {
+    const double wgt = N->dec2[hh];
+    const double* post = c->dec_post + hh * n;
+    for (size_t i = 0; i < n; ++i) out[i] += post[i] * wgt;
+  }
+  for (size_t i = 0; i < n; ++i) out[i] = (out[i] + N->dec2_b) * out_scale;
+}
+
+/* gnn.cpp:208-307; grads written in flat param order */
+static void backward(size_t n, const int64_t* rp, const int64_t* ci, const double* av,
+                     const net* N, const fcache* c, const double* gout, double* grads) {
+  const size_t d = N->d, h = N->h, L = N->L;
+  const layout lo = make_layout(d, h, L);
+  memset(grads, 0, lo.total * sizeof(double));
+  if (c->zero) return;
+  const double out_scale = c->tau / sqrt((double)n);
+  double* gy = (double*)malloc(n * sizeof(double));
+  for (size_t i = 0; i < n; ++i) gy[i] = gout[i] * out_scale;
+  double db = 0.0;
+  for (size_t i = 0; i < n; ++i) db += gy[i];
+  grads[lo.o_dec2_b] = db;
+  double* gdp = (double*)malloc(n * h * sizeof(double));
+  for (size_t hh = 0; hh < h; ++hh) {
+    const double wgt = N->dec2[hh];
+    const double* post = c->dec_post + hh * n;
+    const double* pre = c->dec_pre + hh * n;
+    double* gp = gdp + hh * n;
+    double acc = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      acc += post[i] * gy[i];
+      gp[i] = pre[i] > 0.0 ? gy[i] * wgt : 0.0;
+    }
+    grads[lo.o_dec2 + hh] = acc;
+  }
+  const double* x_last = L == 0 ? c->x1 : c->post + (L - 1) * n * d;
+  gemm_tn(n, d, h, x_last, gdp, grads + lo.o_dec1);
+  for (size_t hh = 0; hh < h; ++hh) {
+    double acc = 0.0;
+    for (size_t i = 0; i < n; ++i) acc += gdp[hh * n + i];
+    grads[lo.o_dec1_b + hh] = acc;
+  }
+  double* gx = (double*)calloc(n * d, sizeof(double));
+  for (size_t j = 0; j < d; ++j)
+    for (size_t hh = 0; hh < h; ++hh) {
+      const double wgt = N->dec1[hh * d + j];
+      const double* gp = gdp + hh * n;
+      for (size_t i = 0; i < n; ++i) gx[j * n + i] += gp[i] * wgt;
+    }
+  double* gpre = (double*)malloc(n * d * sizeof(double));
+  double* at = (double*)malloc(n * d * sizeof(double));
+  double* gin = (double*)malloc(n * d * sizeof(double));
+  for (size_t l = L; l-- > 0;) {
+    const double* x_in = l == 0 ? c->x1 : c->post + (l - 1) * n * d;
+    const double* pre = c->pre + l * n * d;
+    for (size_t k = 0; k < n * d; ++k) gpre[k] = pre[k] > 0.0 ? gx[k] : 0.0;
+    gemm_tn(n, d, d, x_in, gpre, grads + lo.o_u[l]);
+    gemm_tn(n, d, d, c->ax + l * n * d, gpre, grads + lo.o_w[l]);
+    for (size_t j = 0; j < d; ++j) oc_spmv_transpose(n, rp, ci, av, gpre + j * n, at + j * n);
+    memset(gin, 0, n * d * sizeof(double));
+    for (size_t j = 0; j < d; ++j) {
+      double* o = gin + j * n;
+      for (size_t k = 0; k < d; ++k) {
+        const double uw = N->u[l][k * d + j];
+        const double ww = N->w[l][k * d + j];
+        const double* gp = gpre + k * n;
+        const double* ag = at + k * n;
+        for (size_t i = 0; i < n; ++i) o[i] += gp[i] * uw + ag[i] * ww;
+      }
+    }
+    double* t = gx; gx = gin; gin = t;
+  }
+  gemm_tn(n, h, d, c->x0, gx, grads + lo.o_enc2);
+  for (size_t j = 0; j < d; ++j) {
+    double acc = 0.0;
+    for (size_t i = 0; i < n; ++i) acc += gx[j * n + i];
+    grads[lo.o_enc2_b + j] = acc;
+  }
+  for (size_t hh = 0; hh < h; ++hh) {
+    const double* pre0 = c->pre0 + hh * n;
+    double gw = 0.0, gb = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      double gx0 = 0.0;
+      for (size_t j = 0; j < d; ++j) gx0 += gx[j * n + i] * N->enc2[j * h + hh];
+      if (pre0[i] > 0.0) {
+        gw += c->v[i] * gx0;
+        gb += gx0;
+      }
+    }
+    grads[lo.o_enc1 + hh] = gw;
+    grads[lo.o_enc1_b + hh] = gb;
+  }
+  free(gy); free(gdp); free(gx); free(gpre); free(at); free(gin);
+}
+
+int oc_gnn_apply(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                 size_t d, size_t hidden, size_t layers, const double* params,
+                 const double* b, double* out) {
+  if (layers > 64) return fail("oracle supports at most 64 layers");
+  net N = make_net(d, hidden, layers, params);
+  fcache c;
+  forward(n, rp, ci, v, &N, b, out, &c);
+  free_cache(&c);
+  return 0;
+}
+
+int oc_gnn_forward_backward(size_t n, const int64_t* rp, const int64_t* ci,
+                            const double* v, size_t d, size_t hidden, size_t layers,
+                            const double* params, const double* b, const double* gout,
+                            double* out, double* grads) {
+  if (layers > 64) return fail("oracle supports at most 64 layers");
+  net N = make_net(d, hidden, layers, params);
+  fcache c;
+  forward(n, rp, ci, v, &N, b, out, &c);
+  backward(n, rp, ci, v, &N, &c, gout, grads);
+  free_cache(&c);
+  return 0;
+}
+
+/* gnn.cpp:309-335 */
+int oc_l1_residual_loss(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                        size_t batch, const double* out, const double* x, double* loss,
+                        double* grad) {
+  if (batch == 0) return fail("l1_residual_loss: empty batch");
+  const double inv = 1.0 / (double)batch;
+  double* diff = (double*)malloc(n * sizeof(double));
+  double* r = (double*)malloc(n * sizeof(double));
+  double* sg = (double*)malloc(n * sizeof(double));
+  double* at = (double*)malloc(n * sizeof(double));
+  double acc = 0.0;
+  for (size_t k = 0; k < batch; ++k) {
+    for (size_t i = 0; i < n; ++i) diff[i] = out[k * n + i] - x[k * n + i];
+    oc_spmv(n, rp, ci, v, diff, r);
+    for (size_t i = 0; i < n; ++i) {
+      acc += fabs(r[i]);
+      sg[i] = r[i] > 0.0 ? 1.0 : (r[i] < 0.0 ? -1.0 : 0.0);
+    }
+    oc_spmv_transpose(n, rp, ci, v, sg, at);
+    for (size_t i = 0; i < n; ++i) grad[k * n + i] = inv * at[i];
+  }
+  *loss = acc * inv;
+  free(diff); free(r); free(sg); free(at);
+  return 0;
+}
+
+/* gnn.cpp:345-363 */
+void oc_adam_step(size_t count, double* p, const double* g, double* m1, double* m2,
+                  size_t* t, double lr) {
+  const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+  *t += 1;
+  const double bc1 = 1.0 - pow(beta1, (double)*t);
+  const double bc2 = 1.0 - pow(beta2, (double)*t);
+  for (size_t k = 0; k < count; ++k) {
+    m1[k] = beta1 * m1[k] + (1.0 - beta1) * g[k];
+    m2[k] = beta2 * m2[k] + (1.0 - beta2) * g[k] * g[k];
+    const double mhat = m1[k] / bc1;
+    const double vhat = m2[k] / bc2;
+    p[k] -= lr * mhat / (sqrt(vhat) + eps);
+  }
+}
+
+/* gnn.cpp:426-440 composition: forward per column, loss, backward per column,
+ * accumulate in column order. */
+int oc_batch_loss_grads(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                        size_t d, size_t hidden, size_t layers, const double* params,
+                        size_t batch, const double* x, const double* b, double* loss,
+                        double* grads, double* out_batch) {
+  if (layers > 64) return fail("oracle supports at most 64 layers");
+  net N = make_net(d, hidden, layers, params);
+  const size_t total = oc_param_count(d, hidden, layers);
+  double* out = (double*)malloc(n * batch * sizeof(double));
+  double* g = (double*)malloc(n * batch * sizeof(double));
+  double* gk = (double*)malloc(total * sizeof(double));
+  fcache* caches = (fcache*)calloc(batch, sizeof(fcache));
+  for (size_t k = 0; k < batch; ++k)
+    forward(n, rp, ci, v, &N, b + k * n, out + k * n, &caches[k]);
+  oc_l1_residual_loss(n, rp, ci, v, batch, out, x, loss, g);
+  for (size_t t = 0; t < total; ++t) grads[t] = 0.0;
+  for (size_t k = 0; k < batch; ++k) {
+    backward(n, rp, ci, v, &N, &caches[k], g + k * n, gk);
+    for (size_t t = 0; t < total; ++t) grads[t] += gk[t];
+    free_cache(&caches[k]);
+  }
+  if (out_batch) memcpy(out_batch, out, n * batch * sizeof(double));
+  free(out); free(g); free(gk); free(caches);
+  return 0;
+}
+
+/* sampler.cpp:61-83 with spectral_count = 0: column k draws x_k then b_k = A x_k */
+int oc_gaussian_batch(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                      uint64_t seed, size_t skip_batches, size_t batch, double* x,
+                      double* b) {
+  if (batch == 0) return fail("assemble_batch: empty batch");
+  oc_rng r;
+  oc_rng_init(&r, seed);
+  for (size_t s = 0; s < skip_batches * batch * n; ++s) (void)oc_rng_gaussian(&r);
+  for (size_t k = 0; k < batch; ++k) {
+    for (size_t i = 0; i < n; ++i) x[k * n + i] = oc_rng_gaussian(&r);
+    oc_spmv(n, rp, ci, v, x + k * n, b + k * n);
+  }
+  return 0;
+}
+
+/* ======================================================================
+ * Krylov — src/krylov.cpp
+ * ==================================================================== */
+/* krylov.cpp:136-173 (hbar (k+1) x k col-major) */
+int oc_hessenberg_lstsq(size_t k, const double* hbar, double beta, double* y,
+                        double* tracked, int* singular) {
+  if (k < 1) return fail("hessenberg_lstsq: expected (k+1) x k");
+  const size_t ld = k + 1;
+  double* r = (double*)malloc(ld * k * sizeof(double));
+  double* g = (double*)calloc(ld, sizeof(double));
+  memcpy(r, hbar, ld * k * sizeof(double));
+  g[0] = beta;
+  for (size_t j = 0; j < k; ++j) {
+    const double a = r[j * ld + j], bb = r[j * ld + j + 1];
+    const double den = hypot(a, bb);
+    const double cc = den == 0.0 ? 1.0 : a / den;
+    const double ss = den == 0.0 ? 0.0 : bb / den;
+    for (size_t col = j; col < k; ++col) {
+      const double t1 = r[col * ld + j], t2 = r[col * ld + j + 1];
+      r[col * ld + j] = cc * t1 + ss * t2;
+      r[col * ld + j + 1] = -ss * t1 + cc * t2;
+    }
+    const double t1 = g[j], t2 = g[j + 1];
+    g[j] = cc * t1 + ss * t2;
+    g[j + 1] = -ss * t1 + cc * t2;
+  }
+  for (size_t i = 0; i < k; ++i) y[i] = 0.0;
+  *tracked = fabs(g[k]);
+  *singular = 0;
+  for (size_t jj = k; jj-- > 0;) {
+    if (r[jj * ld + jj] == 0.0) {
+      *singular = 1;
+      break;
+    }
+    double s = g[jj];
+    for (size_t col = jj + 1; col < k; ++col) s -= r[col * ld + jj] * y[col];
+    y[jj] = s / r[jj * ld + jj];
+  }
+  free(r);
+  free(g);
+  return 0;
+}
+
+typedef struct {
+  size_t n;
+  const int64_t *rp, *ci;
+  const double* av;
+  int kind;
+  net N;
+  const double* dense;
+} opctx;
+
+static void op_apply(const opctx* o, const double* in, double* out) {
+  const size_t n = o->n;
+  if (o->kind == 0 || o->kind == 3) {
+    memcpy(out, in, n * sizeof(double));
+  } else if (o->kind == 1) {
+    fcache c;
+    forward(n, o->rp, o->ci, o->av, &o->N, in, out, &c);
+    free_cache(&c);
+  } else {
+    for (size_t i = 0; i < n; ++i) out[i] = 0.0;
+    for (size_t j = 0; j < n; ++j)
+      for (size_t i = 0; i < n; ++i) out[i] += o->dense[j * n + i] * in[j];
+  }
+}
+
+static double dotv(size_t n, const double* a, const double* b) {
+  double s = 0.0;
+  for (size_t i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+/* krylov.cpp:175-277 with ArnoldiProcess (krylov.cpp:17-111) inlined */
+int oc_fgmres(size_t n, const int64_t* rp, const int64_t* ci, const double* av,
+              const double* b, int kind, size_t d, size_t hidden, size_t layers,
+              const double* params, const double* x0, double rtol, size_t maxiters,
+              size_t restart, double timeout_secs, double* x, size_t* hist_iter,
+              double* hist_rel, double* hist_t, size_t hist_cap, size_t* hist_len) {
+  const double bnorm = sqrt(dotv(n, b, b));
+  if (bnorm == 0.0) return fail("fgmres: zero right-hand side");
+  if (restart < 1) return fail("fgmres: restart must be >= 1");
+  if (kind == 1 && layers > 64) return fail("oracle supports at most 64 layers");
+  opctx op = {n, rp, ci, av, kind, {0}, params};
+  if (kind == 1) op.N = make_net(d, hidden, layers, params);
+  const double t0 = now_s();
+  size_t hl = 0;
+#define HPUSH(it, rel, tt) \
+  do { if (hl < hist_cap) { hist_iter[hl] = (it); hist_rel[hl] = (rel); hist_t[hl] = (tt); } ++hl; } while (0)
+#define HSET_LAST(it, rel, tt) \
+  do { if (hl - 1 < hist_cap) { hist_iter[hl - 1] = (it); hist_rel[hl - 1] = (rel); hist_t[hl - 1] = (tt); } } while (0)
+
+  memcpy(x, x0, n * sizeof(double));
+  double* r = (double*)malloc(n * sizeof(double));
+  double* ax = (double*)malloc(n * sizeof(double));
+  const size_t m = restart;
+  double* V = (double*)malloc(n * (m + 1) * sizeof(double));
+  double* Z = (double*)malloc(n * m * sizeof(double));
+  double* Hb = (double*)malloc((m + 1) * m * sizeof(double));
+  double* w = (double*)malloc(n * sizeof(double));
+  double* y = (double*)malloc(m * sizeof(double));
+  int status = 1;
+
+  oc_spmv(n, rp, ci, av, x, ax);
+  for (size_t i = 0; i < n; ++i) r[i] = b[i] + -1.0 * ax[i];
+  double current = sqrt(dotv(n, r, r)) / bnorm;
+  HPUSH(0, current, 0.0);
+  if (current <= rtol) {
+    status = 0;
+    goto done;
+  }
+  size_t iter = 0;
+  while (iter < maxiters) {
+    oc_spmv(n, rp, ci, av, x, ax);
+    for (size_t i = 0; i < n; ++i) r[i] = b[i] + -1.0 * ax[i];
+    const double beta = sqrt(dotv(n, r, r));
+    const size_t cycle = restart < maxiters - iter ? restart : maxiters - iter;
+    if (beta == 0.0) { fail("arnoldi: zero start vector"); status = -1; goto done; }
+    for (size_t i = 0; i < n; ++i) V[i] = r[i] / beta;
+    memset(Hb, 0, (m + 1) * m * sizeof(double));
+    size_t steps = 0;
+    int breakdown = 0, budget_hit = 0, budget_status = 1;
+    double tracked_rel = beta / bnorm, tracked = 0.0;
+    int sing = 0;
+    const size_t ld = m + 1;
+    for (size_t j = 0; j < cycle; ++j) {
+      /* ArnoldiProcess::step (krylov.cpp:30-65) */
+      const double* vj = V + j * n;
+      double* zj = Z + j * n;
+      op_apply(&op, vj, zj);
+      oc_spmv(n, rp, ci, av, zj, w);
+      const double wnorm0 = sqrt(dotv(n, w, w));
+      for (size_t i = 0; i <= j; ++i) {
+        const double* vi = V + i * n;
+        const double hh = dotv(n, w, vi);
+        Hb[j * ld + i] = hh;
+        for (size_t q = 0; q < n; ++q) w[q] -= hh * vi[q];
+      }
+      double wnorm = sqrt(dotv(n, w, w));
+      if (wnorm < 0.70710678118654752440 * wnorm0) {
+        for (size_t i = 0; i <= j; ++i) {
+          const double* vi = V + i * n;
+          const double cc = dotv(n, w, vi);
+          Hb[j * ld + i] += cc;
+          for (size_t q = 0; q < n; ++q) w[q] -= cc * vi[q];
+        }
+        wnorm = sqrt(dotv(n, w, w));
+      }
+      Hb[j * ld + j + 1] = wnorm;
+      ++steps;
+      int ok = 1;
+      if (wnorm <= 1e-14 * wnorm0) {
+        breakdown = 1;
+        ok = 0;
+      } else {
+        double* vn = V + (j + 1) * n;
+        for (size_t q = 0; q < n; ++q) vn[q] = w[q] / wnorm;
+      }
+      ++iter;
+      /* hessenberg_lstsq on the leading (k+1) x k block */
+      {
+        double* hk = (double*)malloc((steps + 1) * steps * sizeof(double));
+        for (size_t cc = 0; cc < steps; ++cc)
+          for (size_t i = 0; i <= steps; ++i) hk[cc * (steps + 1) + i] = Hb[cc * ld + i];
+        oc_hessenberg_lstsq(steps, hk, beta, y, &tracked, &sing);
+        free(hk);
+      }
+      tracked_rel = tracked / bnorm;
+      HPUSH(iter, tracked_rel, now_s() - t0);
+      if (!ok || tracked_rel <= rtol) break;
+      if (timeout_secs >= 0.0 && now_s() - t0 >= timeout_secs) {
+        budget_hit = 1;
+        budget_status = 2;
+        break;
+      }
+      if (iter >= maxiters) {
+        budget_hit = 1;
+        budget_status = 1;
+        break;
+      }
+    }
+    {
+      double* hk = (double*)malloc((steps + 1) * steps * sizeof(double));
+      for (size_t cc = 0; cc < steps; ++cc)
+        for (size_t i = 0; i <= steps; ++i) hk[cc * (steps + 1) + i] = Hb[cc * ld + i];
+      oc_hessenberg_lstsq(steps, hk, beta, y, &tracked, &sing);
+      free(hk);
+    }
+    if (sing) {
+      status = 3;
+      goto done;
+    }
+    for (size_t jj = 0; jj < steps; ++jj) {
+      const double yj = y[jj];
+      for (size_t i = 0; i < n; ++i) x[i] += Z[jj * n + i] * yj;
+    }
+    tracked_rel = tracked / bnorm;
+    oc_spmv(n, rp, ci, av, x, ax);
+    for (size_t i = 0; i < n; ++i) r[i] = b[i] + -1.0 * ax[i];
+    current = sqrt(dotv(n, r, r)) / bnorm;
+    HSET_LAST(iter, current, now_s() - t0);
+    if (current > 10.0 * tracked_rel && current - tracked_rel > 1e-10) { status = 3; goto done; }
+    if (current <= rtol) { status = 0; goto done; }
+    if (breakdown) { status = 4; goto done; }
+    if (budget_hit) { status = budget_status; goto done; }
+    if (timeout_secs >= 0.0 && now_s() - t0 >= timeout_secs) { status = 2; goto done; }
+  }
+  status = 1;
+done:
+  *hist_len = hl;
+  free(r); free(ax); free(V); free(Z); free(Hb); free(w); free(y);
+#undef HPUSH
+#undef HSET_LAST
+  return status;
+}

@@ -1,0 +1,919 @@
+// C ABI (include/gnpc.h) implementation: CSR handles, GNP model upload and the
+// apply pipeline launcher, device FGMRES driver, checkpoints.  Training lives
+// in train.cu.  No exception crosses the boundary; no CPU fallback exists for
+// any device entry point (no device => GNPC_ENODEV).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <new>
+#include <sstream>
+#include <vector>
+
+#include "capi_common.hpp"
+#include "kernels/apply.cuh"
+#include "kernels/krylov.cuh"
+#include "model.hpp"
+
+using namespace gnpc_impl;
+using gnp_b200::CsrHost;
+
+namespace gnpc_impl {
+
+thread_local std::string g_error;
+std::atomic<std::int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_error = msg; }
+
+void require_device() {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    throw NoDevice("no CUDA device available (the GNP device path has no CPU fallback)");
+  }
+}
+
+int num_sms() {
+  int dev = 0, sms = 0;
+  GNPC_CUDA(cudaGetDevice(&dev));
+  GNPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  return sms;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return GNPC_OK;
+  } catch (const NoDevice& e) {
+    set_error(e.what());
+    return GNPC_ENODEV;
+  } catch (const Unsupported& e) {
+    set_error(e.what());
+    return GNPC_EUNSUPPORTED;
+  } catch (const CudaError& e) {
+    set_error(e.what());
+    return GNPC_ECUDA;
+  } catch (const std::bad_alloc&) {
+    set_error("device or host allocation failed");
+    return GNPC_ENOMEM;
+  } catch (const std::out_of_range& e) {
+    set_error(e.what());
+    return GNPC_ERANGE;
+  } catch (const std::invalid_argument& e) {
+    set_error(e.what());
+    return GNPC_EINVAL;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return GNPC_ERUNTIME;
+  } catch (...) {
+    set_error("unknown error");
+    return GNPC_ERUNTIME;
+  }
+}
+
+void need(bool cond, const char* msg) {
+  if (!cond) throw std::invalid_argument(msg);
+}
+
+// ------------------------------------------------------------------ apply launcher
+template <int DP>
+struct ApplyLaunch {
+  template <typename InT, typename OutT>
+  static void run(gnpc_model_s& m, const InT* in, OutT* out, cudaStream_t s, const int* skip,
+                  ApplyProf* prof) {
+    using namespace gnpk;
+    gnpc_csr_s& A = *m.a;
+    DevCsr a = A.dev();
+    const int n = a.n;
+    const NetView& net = m.view;
+    const int sms = m.sms;
+    auto mark = [&](int k) {
+      if (prof) prof->mark(k, s);
+    };
+    // τ
+    mark(0);
+    k_apply_norm<InT><<<m.norm_grid, kThreads, 0, s>>>(in, n, m.partials.p, m.ticket.p, m.sc.p, skip);
+    GNPC_LAUNCHED();
+    // lift
+    {
+      const size_t smem = (size_t)net.hidden * DP * 4 + 2 * (size_t)net.hidden * 4;
+      auto kern = k_lift<DP, InT>;
+      static std::once_flag f;
+      std::call_once(f, [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      });
+      mark(1);
+      const int ng = kThreads / (DP / 4);
+      int grid = std::min((n + ng - 1) / ng, sms * 8);
+      grid = std::max(grid, 1);
+      kern<<<grid, kThreads, smem, s>>>(in, n, net, m.sc.p, m.X[0].p, skip);
+      GNPC_LAUNCHED();
+    }
+    using Cfg = LayerCfg<DP>;
+    const int tiles = (n + Cfg::TM - 1) / Cfg::TM;
+    int cur = 0;
+    for (int l = 0; l < net.layers; ++l) {
+      const float* X = m.X[cur].p;
+      const float* uw = net.uw + (size_t)l * 2 * DP * DP;
+      const float* axl = nullptr;
+      if (A.n_long > 0) {
+        mark(2);
+        k_long_ax<DP><<<A.n_long, kThreads, 0, s>>>(a, X, m.AXL.p, m.sc.p, skip);
+        GNPC_LAUNCHED();
+        axl = m.AXL.p;
+      }
+      const bool last = l + 1 == net.layers;
+      mark(last ? 4 : 3);
+      if (!last) {
+        auto kern = k_layer<DP, false, OutT>;
+        const size_t smem = Cfg::smem_bytes(false, net.hidden);
+        static std::once_flag f;
+        std::call_once(f, [&] {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        });
+        kern<<<tiles, kThreads, smem, s>>>(a, X, m.X[1 - cur].p, uw, axl, net, m.sc.p, out, skip);
+        GNPC_LAUNCHED();
+        cur = 1 - cur;
+      } else {
+        auto kern = k_layer<DP, true, OutT>;
+        const size_t smem = Cfg::smem_bytes(true, net.hidden);
+        static std::once_flag f;
+        std::call_once(f, [&] {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        });
+        kern<<<tiles, kThreads, smem, s>>>(a, X, nullptr, uw, axl, net, m.sc.p, out, skip);
+        GNPC_LAUNCHED();
+      }
+    }
+    mark(-1);
+  }
+};
+
+}  // namespace gnpc_impl
+
+// ====================================================================== CSR
+void gnpc_csr_s::upload() {
+  if (dev_ready) return;
+  require_device();
+  if (h.nnz() >= (std::int64_t(1) << 31) || h.n >= (std::int64_t(1) << 31) - 1)
+    throw Unsupported("device CSR uses int32 indices: n and nnz must be < 2^31");
+  std::vector<int> hrp(h.n + 1), hci(h.nnz());
+  std::vector<float> hv(h.nnz());
+  std::vector<int> longs;
+  max_row = 0;
+  for (std::int64_t i = 0; i <= h.n; ++i) hrp[i] = static_cast<int>(h.row_ptr[i]);
+  for (std::int64_t k = 0; k < h.nnz(); ++k) {
+    hci[k] = static_cast<int>(h.col_idx[k]);
+    hv[k] = static_cast<float>(h.values[k]);
+  }
+  for (std::int64_t i = 0; i < h.n; ++i) {
+    const int len = hrp[i + 1] - hrp[i];
+    max_row = std::max(max_row, len);
+    if (len > gnpk::kLongRow) longs.push_back(static_cast<int>(i));
+  }
+  rp.upload(hrp.data(), hrp.size());
+  ci.upload(hci.data(), hci.size());
+  v.upload(hv.data(), hv.size());
+  n_long = static_cast<int>(longs.size());
+  if (n_long) long_rows.upload(longs.data(), longs.size());
+  GNPC_CUDA(cudaDeviceSynchronize());
+  dev_ready = true;
+}
+
+gnpk::DevCsr gnpc_csr_s::dev() {
+  upload();
+  gnpk::DevCsr d;
+  d.n = static_cast<int>(h.n);
+  d.nnz = static_cast<int>(h.nnz());
+  d.rp = rp.p;
+  d.ci = ci.p;
+  d.v = v.p;
+  d.long_rows = n_long ? long_rows.p : nullptr;
+  d.n_long = n_long;
+  return d;
+}
+
+// ====================================================================== model
+void gnpc_model_s::build_view() {
+  const std::int64_t d = dims.d, H = dims.hidden, L = dims.layers;
+  const gnp_b200::ParamLayout lay = gnp_b200::param_layout(dims);
+  const std::size_t o_enc1 = 0, o_enc1b = H, o_enc2 = 2 * H, o_enc2b = o_enc2 + H * dp;
+  const std::size_t o_uw = o_enc2b + dp, o_dec1 = o_uw + (std::size_t)L * 2 * dp * dp;
+  const std::size_t o_dec1b = o_dec1 + (std::size_t)dp * H, o_dec2 = o_dec1b + H;
+  const std::size_t total = o_dec2 + H;
+  std::vector<float> f(total, 0.0f);
+  const double* p = params.data();
+  for (std::int64_t h = 0; h < H; ++h) {
+    f[o_enc1 + h] = (float)p[lay.enc1 + h];
+    f[o_enc1b + h] = (float)p[lay.enc1_b + h];
+    f[o_dec1b + h] = (float)p[lay.dec1_b + h];
+    f[o_dec2 + h] = (float)p[lay.dec2 + h];
+    for (std::int64_t j = 0; j < d; ++j) {
+      f[o_enc2 + h * dp + j] = (float)p[lay.enc2 + j * H + h];  // enc2 (h, j) col-major H x d
+      f[o_dec1 + j * H + h] = (float)p[lay.dec1 + h * d + j];   // dec1 (j, h) col-major d x H
+    }
+  }
+  for (std::int64_t j = 0; j < d; ++j) f[o_enc2b + j] = (float)p[lay.enc2_b + j];
+  for (std::int64_t l = 0; l < L; ++l) {
+    float* uw = f.data() + o_uw + (std::size_t)l * 2 * dp * dp;
+    for (std::int64_t k = 0; k < d; ++k)
+      for (std::int64_t j = 0; j < d; ++j) {
+        uw[k * dp + j] = (float)p[lay.u[l] + j * d + k];           // U(k, j)
+        uw[(dp + k) * dp + j] = (float)p[lay.w[l] + j * d + k];    // W(k, j)
+      }
+  }
+  P.upload(f.data(), f.size());
+  GNPC_CUDA(cudaDeviceSynchronize());
+  view.enc1 = P.p + o_enc1;
+  view.enc1_b = P.p + o_enc1b;
+  view.enc2 = P.p + o_enc2;
+  view.enc2_b = P.p + o_enc2b;
+  view.uw = P.p + o_uw;
+  view.dec1 = P.p + o_dec1;
+  view.dec1_b = P.p + o_dec1b;
+  view.dec2 = P.p + o_dec2;
+  view.dec2_b = (float)p[lay.dec2_b];
+  view.hidden = (int)H;
+  view.layers = (int)L;
+}
+
+void gnpc_model_s::ensure_workspace() {
+  const std::size_t n = (std::size_t)a->h.n;
+  X[0].ensure(n * dp);
+  X[1].ensure(n * dp);
+  if (a->n_long) AXL.ensure(n * dp);
+  sms = num_sms();
+  norm_grid = 2 * sms;
+  partials.ensure(norm_grid);
+  if (!ticket.p) {
+    ticket.alloc(1);
+    GNPC_CUDA(cudaMemset(ticket.p, 0, sizeof(unsigned)));
+  }
+  sc.ensure(1);
+}
+
+template <typename InT, typename OutT>
+void gnpc_model_s::launch_apply(const InT* in, OutT* out, cudaStream_t s, const int* skip,
+                                ApplyProf* prof) {
+  a->upload();
+  ensure_workspace();
+  switch (dp) {
+    case 4: ApplyLaunch<4>::run(*this, in, out, s, skip, prof); break;
+    case 8: ApplyLaunch<8>::run(*this, in, out, s, skip, prof); break;
+    case 16: ApplyLaunch<16>::run(*this, in, out, s, skip, prof); break;
+    case 32: ApplyLaunch<32>::run(*this, in, out, s, skip, prof); break;
+    case 64: ApplyLaunch<64>::run(*this, in, out, s, skip, prof); break;
+    default: throw Unsupported("unsupported padded width");
+  }
+}
+template void gnpc_model_s::launch_apply<float, float>(const float*, float*, cudaStream_t,
+                                                      const int*, ApplyProf*);
+template void gnpc_model_s::launch_apply<double, double>(const double*, double*, cudaStream_t,
+                                                        const int*, ApplyProf*);
+
+// ====================================================================== FGMRES driver
+namespace {
+
+using gnpk::KrylovDev;
+using gnpk::KState;
+
+struct HostOp {
+  gnpc_host_operator fn;
+  void* ctx;
+};
+
+void* ortho_kernel_for(int ept) {
+  switch (ept) {
+    case 0: return (void*)gnpk::k_krylov_ortho<0>;
+    case 1: return (void*)gnpk::k_krylov_ortho<1>;
+    case 2: return (void*)gnpk::k_krylov_ortho<2>;
+    case 4: return (void*)gnpk::k_krylov_ortho<4>;
+    case 8: return (void*)gnpk::k_krylov_ortho<8>;
+    case 16: return (void*)gnpk::k_krylov_ortho<16>;
+  }
+  return nullptr;
+}
+
+struct OrthoPlan {
+  void* kern;
+  int grid;
+};
+
+OrthoPlan plan_ortho(int n) {
+  const int sms = num_sms();
+  for (int ept : {1, 2, 4, 8, 16}) {
+    int per_sm = 0;
+    GNPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ortho_kernel_for(ept),
+                                                            gnpk::kThreads, 0));
+    const long long cap = (long long)per_sm * sms * gnpk::kThreads * ept;
+    if (per_sm > 0 && n <= cap) return {ortho_kernel_for(ept), per_sm * sms};
+  }
+  int per_sm = 0;
+  GNPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ortho_kernel_for(0),
+                                                          gnpk::kThreads, 0));
+  return {ortho_kernel_for(0), std::max(1, per_sm) * sms};
+}
+
+__global__ void k_init_state(const double* __restrict__ b, int n, double* partials,
+                             unsigned* ticket, KState* st, double rtol, int maxiters,
+                             double timeout_secs) {
+  __shared__ double scratch[32];
+  __shared__ bool last;
+  double p = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p = fma(b[i], b[i], p);
+  p = gnpk::block_sum(p, scratch);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = p;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int z = threadIdx.x; z < (int)gridDim.x; z += blockDim.x)
+    t += reinterpret_cast<volatile double*>(partials)[z];
+  t = gnpk::block_sum(t, scratch);
+  if (threadIdx.x == 0) {
+    const long long now = (long long)gnpk::globaltimer_ns();
+    st->bnorm = sqrt(t);
+    st->rtol = rtol;
+    st->maxiters = maxiters;
+    st->iter = 0;
+    st->reorth = 0;
+    st->t0 = now;
+    st->deadline = timeout_secs < 0.0 ? -1 : now + (long long)(timeout_secs * 1e9);
+    st->stop = 0;
+    *ticket = 0u;
+  }
+}
+
+struct HistSink {
+  gnpc_history* h;
+  std::int64_t len = 0;
+  void push(std::int64_t it, double rel, double t) {
+    if (h && len < h->capacity) {
+      h->iteration[len] = it;
+      h->relres[len] = rel;
+      h->elapsed[len] = t;
+    }
+    ++len;
+  }
+  void set_last(std::int64_t it, double rel, double t) {
+    if (h && len - 1 < h->capacity && len > 0) {
+      h->iteration[len - 1] = it;
+      h->relres[len - 1] = rel;
+      h->elapsed[len - 1] = t;
+    }
+  }
+};
+
+// Core of fgmres_solve (src/krylov.cpp:175-277) on device-resident b/x.
+int fgmres_core(gnpc_csr_s& A, gnpc_model_s* M, const HostOp* hop, const double* b_dev,
+                double* x_dev, const gnpc_solve_config& cfg, gnpc_history* hist,
+                cudaStream_t s) {
+  need(cfg.restart >= 1, "fgmres: restart must be >= 1");
+  need(cfg.maxiters >= 0, "fgmres: maxiters must be >= 0");
+  gnpk::DevCsr a = A.dev();
+  const int n = a.n;
+  const int m = (int)cfg.restart;
+  if (!A.kws || A.kws->n != n || A.kws->m != m) {
+    auto w = std::make_unique<KrylovWs>();
+    w->n = n;
+    w->m = m;
+    w->V.alloc((size_t)n * (m + 1));
+    if (M || hop) w->Z.alloc((size_t)n * m);
+    w->w.alloc(n);
+    w->vin.alloc(n);
+    w->zout.alloc(n);
+    w->r.alloc(n);
+    w->H.alloc((size_t)(m + 1) * m);
+    w->R.alloc((size_t)(m + 1) * m);
+    w->cs.alloc(m);
+    w->sn.alloc(m);
+    w->g.alloc(m + 1);
+    w->y.alloc(m);
+    w->partials.alloc(2 * 2048);
+    w->hist_rel.alloc(m);
+    w->hist_t.alloc(m);
+    w->ticket.alloc(1);
+    GNPC_CUDA(cudaMemset(w->ticket.p, 0, sizeof(unsigned)));
+    w->st.alloc(1);
+    A.kws = std::move(w);
+  }
+  KrylovWs& W = *A.kws;
+  if ((M || hop) && !W.Z.p) W.Z.alloc((size_t)n * m);
+  KrylovDev k{};
+  k.n = n;
+  k.m = m;
+  k.V = W.V.p;
+  k.Z = (M || hop) ? W.Z.p : nullptr;
+  k.w = W.w.p;
+  k.vin = W.vin.p;
+  k.zout = W.zout.p;
+  k.x = x_dev;
+  k.b = b_dev;
+  k.r = W.r.p;
+  k.H = W.H.p;
+  k.R = W.R.p;
+  k.cs = W.cs.p;
+  k.sn = W.sn.p;
+  k.g = W.g.p;
+  k.y = W.y.p;
+  k.partials = W.partials.p;
+  k.ticket = W.ticket.p;
+  k.hist_rel = W.hist_rel.p;
+  k.hist_t = W.hist_t.p;
+  k.st = W.st.p;
+  const int sms = num_sms();
+  const int vgrid = std::max(1, std::min((n + 255) / 256, sms * 8));
+  const int rgrid = std::max(1, std::min((n + 63) / 64, sms * 8));  // 8 rows per warp
+
+  gnpk::KState hs{};
+  auto pull_state = [&] {
+    GNPC_CUDA(cudaMemcpyAsync(&hs, W.st.p, sizeof(KState), cudaMemcpyDeviceToHost, s));
+    GNPC_CUDA(cudaStreamSynchronize(s));
+  };
+
+  k_init_state<<<std::min(rgrid, 2048), gnpk::kThreads, 0, s>>>(
+      b_dev, n, W.partials.p, W.ticket.p, W.st.p, cfg.rtol, (int)cfg.maxiters,
+      cfg.timeout_secs);
+  GNPC_LAUNCHED();
+  pull_state();
+  if (hs.bnorm == 0.0) throw std::invalid_argument("fgmres: zero right-hand side");
+
+  HistSink H{hist};
+  gnpk::k_residual<<<std::min(rgrid, 2048), gnpk::kThreads, 0, s>>>(a, k);
+  GNPC_LAUNCHED();
+  pull_state();
+  H.push(0, hs.current, 0.0);
+  int status = GNPC_MAXITERS;
+  if (hs.current <= cfg.rtol) {
+    status = GNPC_CONVERGED;
+  } else {
+    const OrthoPlan op = plan_ortho(n);
+    std::vector<double> hrel(m);
+    std::vector<long long> ht(m);
+    std::int64_t iter = 0;
+    bool done = false;
+    std::vector<double> hv_in, hv_out;
+    if (hop) {
+      hv_in.resize(n);
+      hv_out.resize(n);
+    }
+    while (iter < cfg.maxiters && !done) {
+      if (hs.beta == 0.0) throw std::invalid_argument("arnoldi: zero start vector");
+      const int cycle = (int)std::min<std::int64_t>(cfg.restart, cfg.maxiters - iter);
+      gnpk::k_cycle_begin<<<vgrid, gnpk::kThreads, 0, s>>>(k, cycle);
+      GNPC_LAUNCHED();
+      for (int j = 0; j < cycle; ++j) {
+        if (hop) {
+          // host FlexibleOperator: z_j = M(v_j) on host vectors
+          pull_state();
+          if (hs.stop) break;
+          GNPC_CUDA(cudaMemcpyAsync(hv_in.data(), W.vin.p, n * sizeof(double),
+                                    cudaMemcpyDeviceToHost, s));
+          GNPC_CUDA(cudaStreamSynchronize(s));
+          if (hop->fn(hop->ctx, hv_in.data(), hv_out.data(), n) != 0)
+            throw std::runtime_error("host preconditioner failed");
+          GNPC_CUDA(cudaMemcpyAsync(W.zout.p, hv_out.data(), n * sizeof(double),
+                                    cudaMemcpyHostToDevice, s));
+        } else if (M) {
+          M->launch_apply<double, double>(W.vin.p, W.zout.p, s, &W.st.p->stop);
+        }
+        gnpk::k_krylov_spmv<<<rgrid, gnpk::kThreads, 0, s>>>(a, k);
+        GNPC_LAUNCHED();
+        void* args[] = {&k};
+        GNPC_CUDA(cudaLaunchCooperativeKernel(op.kern, op.grid, gnpk::kThreads, args, 0, s));
+        GNPC_LAUNCHED();
+      }
+      gnpk::k_cycle_solve<<<1, 32, 0, s>>>(k);
+      GNPC_LAUNCHED();
+      gnpk::k_update_x<<<vgrid, gnpk::kThreads, 0, s>>>(k);
+      GNPC_LAUNCHED();
+      gnpk::k_residual<<<std::min(rgrid, 2048), gnpk::kThreads, 0, s>>>(a, k);
+      GNPC_LAUNCHED();
+      pull_state();
+      GNPC_CUDA(cudaMemcpyAsync(hrel.data(), W.hist_rel.p, m * sizeof(double),
+                                cudaMemcpyDeviceToHost, s));
+      GNPC_CUDA(cudaMemcpyAsync(ht.data(), W.hist_t.p, m * sizeof(long long),
+                                cudaMemcpyDeviceToHost, s));
+      GNPC_CUDA(cudaStreamSynchronize(s));
+      for (int q = 0; q < hs.steps; ++q) H.push(iter + q + 1, hrel[q], 1e-9 * (double)ht[q]);
+      iter += hs.steps;
+      if (hs.singular) {
+        status = GNPC_SOLUTION_FAILURE;
+        break;
+      }
+      const double tracked_rel = hs.tracked_rel;
+      const double current = hs.current;
+      H.set_last(iter, current, 1e-9 * (double)hs.t_end);
+      if (current > 10.0 * tracked_rel && current - tracked_rel > 1e-10) {
+        status = GNPC_SOLUTION_FAILURE;
+        done = true;
+      } else if (current <= cfg.rtol) {
+        status = GNPC_CONVERGED;
+        done = true;
+      } else if (hs.breakdown) {
+        status = GNPC_BREAKDOWN_EXACT;
+        done = true;
+      } else if (hs.budget_hit) {
+        status = hs.budget_status;
+        done = true;
+      } else if (hs.deadline >= 0 && hs.t_end + hs.t0 >= hs.deadline) {
+        status = GNPC_TIMEOUT;
+        done = true;
+      }
+      if (!done && hs.steps == 0) throw std::runtime_error("fgmres: cycle made no progress");
+    }
+    if (!done && status != GNPC_SOLUTION_FAILURE) status = GNPC_MAXITERS;
+  }
+  if (hist) {
+    hist->length = H.len;
+    hist->reorth = hs.reorth;
+  }
+  return status;
+}
+
+int fgmres_host(gnpc_csr a, gnpc_model m, const HostOp* hop, const double* b, const double* x0,
+                const gnpc_solve_config* cfg, double* x, gnpc_history* hist, int* status) {
+  return guarded([&] {
+    need(a && b && x && cfg && status, "fgmres: null argument");
+    require_device();
+    if (m) need(m->a->h.n == a->h.n, "fgmres: preconditioner dimension mismatch");
+    const std::size_t n = (std::size_t)a->h.n;
+    DevBuf<double> db(n), dx(n);
+    cudaStream_t s = m ? m->stream : nullptr;
+    GNPC_CUDA(cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, s));
+    if (x0) {
+      GNPC_CUDA(cudaMemcpyAsync(dx.p, x0, n * 8, cudaMemcpyHostToDevice, s));
+    } else {
+      GNPC_CUDA(cudaMemsetAsync(dx.p, 0, n * 8, s));
+    }
+    *status = fgmres_core(*a, m, hop, db.p, dx.p, *cfg, hist, s);
+    GNPC_CUDA(cudaMemcpyAsync(x, dx.p, n * 8, cudaMemcpyDeviceToHost, s));
+    GNPC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int gnpc_abi_version(void) { return GNPC_ABI_VERSION; }
+const char* gnpc_last_error(void) { return g_error.c_str(); }
+
+int gnpc_device_count(int* count) {
+  return guarded([&] {
+    need(count, "null count");
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *count = c;
+  });
+}
+int gnpc_set_device(int device) {
+  return guarded([&] {
+    require_device();
+    GNPC_CUDA(cudaSetDevice(device));
+  });
+}
+int gnpc_synchronize(void) {
+  return guarded([&] {
+    require_device();
+    GNPC_CUDA(cudaDeviceSynchronize());
+  });
+}
+int gnpc_launch_count(int64_t* count) {
+  return guarded([&] {
+    need(count, "null count");
+    *count = g_launches.load();
+  });
+}
+
+// ---------------------------------------------------------------- CSR
+int gnpc_csr_from_triplets(int64_t n, int64_t m, const int64_t* rows, const int64_t* cols,
+                           const double* vals, gnpc_csr* out) {
+  return guarded([&] {
+    need(out && m >= 0 && (m == 0 || (rows && cols && vals)), "csr_from_triplets: bad arguments");
+    std::vector<std::int64_t> r(rows, rows + m), c(cols, cols + m);
+    std::vector<double> v(vals, vals + m);
+    auto h = std::make_unique<gnpc_csr_s>();
+    h->h = gnp_b200::csr_from_triplets(n, r, c, v);
+    *out = h.release();
+  });
+}
+
+int gnpc_csr_create(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                    const double* values, gnpc_csr* out) {
+  return guarded([&] {
+    need(out && n >= 0 && row_ptr, "csr_create: bad arguments");
+    auto h = std::make_unique<gnpc_csr_s>();
+    h->h.n = n;
+    h->h.row_ptr.assign(row_ptr, row_ptr + n + 1);
+    const std::int64_t nnz = row_ptr[n];
+    need(nnz >= 0 && (nnz == 0 || (col_idx && values)), "csr_create: bad arrays");
+    h->h.col_idx.assign(col_idx, col_idx + nnz);
+    h->h.values.assign(values, values + nnz);
+    gnp_b200::csr_validate(h->h);
+    *out = h.release();
+  });
+}
+
+int gnpc_csr_generate(const char* kind, int64_t size, double p0, double p1, uint64_t seed,
+                      gnpc_csr* out) {
+  return guarded([&] {
+    need(kind && out, "csr_generate: bad arguments");
+    const std::string k(kind);
+    auto h = std::make_unique<gnpc_csr_s>();
+    if (k == "convection_diffusion") h->h = gnp_b200::gen_convection_diffusion(size, p0);
+    else if (k == "random_nonsymmetric")
+      h->h = gnp_b200::gen_random_nonsymmetric(size, (std::int64_t)p0, p1, seed);
+    else if (k == "c2_convdiff3d") h->h = gnp_b200::gen_convection_diffusion_3d(size, p0);
+    else if (k == "c3_varcoeff2d") h->h = gnp_b200::gen_varcoeff_diffusion_2d(size, p0, seed);
+    else if (k == "c4_powerlaw") h->h = gnp_b200::gen_powerlaw_random(size, p0, 4, 2048, seed);
+    else if (k == "c5_aniso9pt") h->h = gnp_b200::gen_anisotropic_9pt(size, p0, p1);
+    else throw std::invalid_argument("csr_generate: unknown kind " + k);
+    *out = h.release();
+  });
+}
+
+int gnpc_csr_read_matrix_market(const char* path, gnpc_csr* out) {
+  return guarded([&] {
+    need(path && out, "read_matrix_market: bad arguments");
+    auto h = std::make_unique<gnpc_csr_s>();
+    h->h = gnp_b200::read_matrix_market_file(path);
+    *out = h.release();
+  });
+}
+
+int gnpc_csr_info(gnpc_csr a, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    need(a, "null csr");
+    if (n) *n = a->h.n;
+    if (nnz) *nnz = a->h.nnz();
+  });
+}
+
+int gnpc_csr_export(gnpc_csr a, int64_t* row_ptr, int64_t* col_idx, double* values) {
+  return guarded([&] {
+    need(a, "null csr");
+    if (row_ptr) std::copy(a->h.row_ptr.begin(), a->h.row_ptr.end(), row_ptr);
+    if (col_idx) std::copy(a->h.col_idx.begin(), a->h.col_idx.end(), col_idx);
+    if (values) std::copy(a->h.values.begin(), a->h.values.end(), values);
+  });
+}
+
+int gnpc_csr_gershgorin_gamma(gnpc_csr a, double* gamma) {
+  return guarded([&] {
+    need(a && gamma, "null argument");
+    *gamma = gnp_b200::gershgorin_gamma(a->h);
+  });
+}
+
+int gnpc_csr_prescale(gnpc_csr a, double gamma, gnpc_csr* out) {
+  return guarded([&] {
+    need(a && out, "null argument");
+    auto h = std::make_unique<gnpc_csr_s>();
+    h->h = gnp_b200::prescale(a->h, gamma);
+    *out = h.release();
+  });
+}
+
+int gnpc_csr_transpose(gnpc_csr a, gnpc_csr* out) {
+  return guarded([&] {
+    need(a && out, "null argument");
+    auto h = std::make_unique<gnpc_csr_s>();
+    h->h = gnp_b200::transpose(a->h);
+    *out = h.release();
+  });
+}
+
+int gnpc_csr_hash(gnpc_csr a, uint64_t* hash) {
+  return guarded([&] {
+    need(a && hash, "null argument");
+    *hash = gnp_b200::csr_content_hash(a->h);
+  });
+}
+
+int gnpc_csr_destroy(gnpc_csr a) {
+  return guarded([&] { delete a; });
+}
+
+int gnpc_spmv(gnpc_csr a, const double* x, double* y) {
+  return guarded([&] {
+    need(a && x && y, "spmv: null argument");
+    gnpk::DevCsr d = a->dev();
+    const std::size_t n = (std::size_t)a->h.n;
+    DevBuf<double> dx(n), dy(n);
+    GNPC_CUDA(cudaMemcpy(dx.p, x, n * 8, cudaMemcpyHostToDevice));
+    const int grid = std::max(1, std::min((int)((n + 63) / 64), num_sms() * 8));
+    gnpk::k_spmv_f64<<<grid, gnpk::kThreads>>>(d, dx.p, dy.p);
+    GNPC_LAUNCHED();
+    GNPC_CUDA(cudaMemcpy(y, dy.p, n * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+int gnpc_gaussian_vector(uint64_t seed, int64_t n, double* out) {
+  return guarded([&] {
+    need(out && n >= 0, "gaussian_vector: bad arguments");
+    gnp_b200::Rng rng(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = rng.gaussian();
+  });
+}
+
+// ---------------------------------------------------------------- model
+int gnpc_param_count(int64_t d, int64_t hidden, int64_t layers, int64_t* count) {
+  return guarded([&] {
+    need(count, "null count");
+    need(d >= 1 && hidden >= 1 && layers >= 1, "init_params: dims must be >= 1");
+    *count = gnp_b200::param_layout({d, hidden, layers}).total;
+  });
+}
+
+int gnpc_init_params(int64_t d, int64_t hidden, int64_t layers, uint64_t seed, double* params) {
+  return guarded([&] {
+    need(params, "null params");
+    const auto p = gnp_b200::init_params({d, hidden, layers}, seed);
+    std::copy(p.begin(), p.end(), params);
+  });
+}
+
+int gnpc_model_create(gnpc_csr ahat, int64_t d, int64_t hidden, int64_t layers,
+                      const double* params, gnpc_model* out) {
+  return guarded([&] {
+    need(ahat && params && out, "model_create: null argument");
+    need(d >= 1 && hidden >= 1 && layers >= 1, "model_create: dims must be >= 1");
+    if (d > 64) throw Unsupported("model_create: d > 64 is not supported by the device kernels");
+    if (hidden > 256) throw Unsupported("model_create: hidden > 256 is not supported");
+    require_device();
+    auto m = std::make_unique<gnpc_model_s>();
+    m->a = ahat;
+    m->dims = {d, hidden, layers};
+    m->dp = 4;
+    while (m->dp < d) m->dp *= 2;
+    m->params.assign(params, params + gnp_b200::param_layout(m->dims).total);
+    GNPC_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+    m->build_view();
+    *out = m.release();
+  });
+}
+
+int gnpc_model_set_params(gnpc_model m, const double* params) {
+  return guarded([&] {
+    need(m && params, "null argument");
+    m->params.assign(params, params + m->params.size());
+    GNPC_CUDA(cudaStreamSynchronize(m->stream));
+    m->build_view();
+  });
+}
+
+int gnpc_model_get_params(gnpc_model m, double* params) {
+  return guarded([&] {
+    need(m && params, "null argument");
+    std::copy(m->params.begin(), m->params.end(), params);
+  });
+}
+
+int gnpc_model_dims(gnpc_model m, int64_t* d, int64_t* hidden, int64_t* layers) {
+  return guarded([&] {
+    need(m, "null model");
+    if (d) *d = m->dims.d;
+    if (hidden) *hidden = m->dims.hidden;
+    if (layers) *layers = m->dims.layers;
+  });
+}
+
+int gnpc_model_destroy(gnpc_model m) {
+  return guarded([&] {
+    if (!m) return;
+    if (m->stream) cudaStreamSynchronize(m->stream);
+    cudaStream_t s = m->stream;
+    delete m;
+    if (s) cudaStreamDestroy(s);
+  });
+}
+
+int gnpc_apply(gnpc_model m, const double* b, double* out) {
+  return guarded([&] {
+    need(m && b && out, "apply: null argument");
+    const std::size_t n = (std::size_t)m->a->h.n;
+    m->io_in.ensure(n);
+    m->io_out.ensure(n);
+    GNPC_CUDA(cudaMemcpyAsync(m->io_in.p, b, n * 8, cudaMemcpyHostToDevice, m->stream));
+    m->launch_apply<double, double>(m->io_in.p, m->io_out.p, m->stream, nullptr);
+    GNPC_CUDA(cudaMemcpyAsync(out, m->io_out.p, n * 8, cudaMemcpyDeviceToHost, m->stream));
+    GNPC_CUDA(cudaStreamSynchronize(m->stream));
+  });
+}
+
+int gnpc_apply_device_f32(gnpc_model m, const float* b, float* out, void* stream) {
+  return guarded([&] {
+    need(m && b && out, "apply: null argument");
+    m->launch_apply<float, float>(b, out, (cudaStream_t)stream, nullptr);
+  });
+}
+
+int gnpc_apply_device_f64(gnpc_model m, const double* b, double* out, void* stream) {
+  return guarded([&] {
+    need(m && b && out, "apply: null argument");
+    m->launch_apply<double, double>(b, out, (cudaStream_t)stream, nullptr);
+  });
+}
+
+int gnpc_apply_profile(gnpc_model m, const float* b, float* out, void* stream, double* ms_by_kind,
+                       int64_t* count_by_kind) {
+  return guarded([&] {
+    need(m && b && out && ms_by_kind && count_by_kind, "apply_profile: null argument");
+    ApplyProf prof;
+    cudaStream_t s = (cudaStream_t)stream;
+    m->launch_apply<float, float>(b, out, s, nullptr, &prof);
+    GNPC_CUDA(cudaStreamSynchronize(s));
+    for (std::size_t i = 0; i + 1 < prof.ev.size(); ++i) {
+      float ms = 0.f;
+      GNPC_CUDA(cudaEventElapsedTime(&ms, prof.ev[i], prof.ev[i + 1]));
+      ms_by_kind[prof.kind[i]] += ms;
+      count_by_kind[prof.kind[i]] += 1;
+    }
+    for (cudaEvent_t e : prof.ev) cudaEventDestroy(e);
+  });
+}
+
+// ---------------------------------------------------------------- checkpoints
+int gnpc_checkpoint_save(const char* path, int64_t d, int64_t hidden, int64_t layers,
+                         const double* params, gnpc_csr a) {
+  return guarded([&] {
+    need(path && params && a, "checkpoint_save: null argument");
+    const gnp_b200::Dims dm{d, hidden, layers};
+    std::vector<double> p(params, params + gnp_b200::param_layout(dm).total);
+    gnp_b200::MatrixMeta meta{a->h.n, a->h.nnz(), gnp_b200::csr_content_hash(a->h)};
+    const std::string bytes = gnp_b200::checkpoint_bytes(dm, p, meta);
+    std::ofstream f(path, std::ios::binary);
+    if (!f) throw std::runtime_error(std::string("cannot open ") + path + " for writing");
+    f.write(bytes.data(), (std::streamsize)bytes.size());
+  });
+}
+
+int gnpc_checkpoint_load(const char* path, int64_t* dims3, uint64_t* meta3, double* params) {
+  return guarded([&] {
+    need(path, "checkpoint_load: null path");
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw std::runtime_error(std::string("cannot open ") + path);
+    std::stringstream ss;
+    ss << f.rdbuf();
+    gnp_b200::Dims dm;
+    std::vector<double> p;
+    gnp_b200::MatrixMeta meta;
+    gnp_b200::checkpoint_parse(ss.str(), &dm, &p, &meta);
+    if (dims3) {
+      dims3[0] = dm.d;
+      dims3[1] = dm.hidden;
+      dims3[2] = dm.layers;
+    }
+    if (meta3) {
+      meta3[0] = (uint64_t)meta.n;
+      meta3[1] = (uint64_t)meta.nnz;
+      meta3[2] = meta.hash;
+    }
+    if (params) std::copy(p.begin(), p.end(), params);
+  });
+}
+
+// ---------------------------------------------------------------- FGMRES
+int gnpc_fgmres(gnpc_csr a, gnpc_model m, const double* b, const double* x0,
+                const gnpc_solve_config* cfg, double* x, gnpc_history* hist, int* status) {
+  return fgmres_host(a, m, nullptr, b, x0, cfg, x, hist, status);
+}
+
+int gnpc_fgmres_host_operator(gnpc_csr a, gnpc_host_operator op, void* ctx, const double* b,
+                              const double* x0, const gnpc_solve_config* cfg, double* x,
+                              gnpc_history* hist, int* status) {
+  if (!op) {
+    set_error("fgmres_host_operator: null operator");
+    return GNPC_EINVAL;
+  }
+  HostOp h{op, ctx};
+  return fgmres_host(a, nullptr, &h, b, x0, cfg, x, hist, status);
+}
+
+int gnpc_fgmres_device(gnpc_csr a, gnpc_model m, const double* b_dev, double* x_dev,
+                       const gnpc_solve_config* cfg, gnpc_history* hist, int* status,
+                       void* stream) {
+  return guarded([&] {
+    need(a && b_dev && x_dev && cfg && status, "fgmres_device: null argument");
+    require_device();
+    if (m) need(m->a->h.n == a->h.n, "fgmres: preconditioner dimension mismatch");
+    *status = fgmres_core(*a, m, nullptr, b_dev, x_dev, *cfg, hist, (cudaStream_t)stream);
+  });
+}
+
+}  // extern "C"

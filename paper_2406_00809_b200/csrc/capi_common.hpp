@@ -1,0 +1,115 @@
+// Internal C++ side of the C ABI: error plumbing, device buffers, handle
+// structs.  Not part of the public boundary (include/gnpc.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gnpc.h"
+#include "host/gnp_host.hpp"
+#include "kernels/common.cuh"
+
+namespace gnpc_impl {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Unsupported : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NoDevice : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void set_error(const std::string& msg);
+extern std::atomic<std::int64_t> g_launches;
+
+#define GNPC_CUDA(expr)                                                                  \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      throw ::gnpc_impl::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e));  \
+  } while (0)
+
+#define GNPC_LAUNCHED()                                           \
+  do {                                                            \
+    ::gnpc_impl::g_launches.fetch_add(1, std::memory_order_relaxed); \
+    GNPC_CUDA(cudaGetLastError());                                \
+  } while (0)
+
+void require_device();
+int num_sms();
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  std::size_t count = 0;
+  DevBuf() = default;
+  explicit DevBuf(std::size_t n) { alloc(n); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), count(o.count) { o.p = nullptr; o.count = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; count = o.count;
+      o.p = nullptr; o.count = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(std::size_t n) {
+    release();
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      throw std::bad_alloc();
+    }
+    count = n;
+  }
+  void ensure(std::size_t n) {
+    if (count < n || p == nullptr) alloc(n);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    count = 0;
+  }
+  void upload(const T* h, std::size_t n, cudaStream_t s = nullptr) {
+    ensure(n);
+    GNPC_CUDA(cudaMemcpyAsync(p, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+// Krylov workspace, cached per (n, restart) on the matrix handle.
+struct KrylovWs {
+  int n = 0, m = 0;
+  DevBuf<double> V, Z, w, vin, zout, x, b, r, H, R, cs, sn, g, y, partials, hist_rel;
+  DevBuf<long long> hist_t;
+  DevBuf<unsigned> ticket;
+  DevBuf<gnpk::KState> st;
+};
+
+}  // namespace gnpc_impl
+
+struct gnpc_csr_s {
+  gnp_b200::CsrHost h;
+  // device copy (lazy): int32 row_ptr / col_idx, fp32 values, long-row list
+  bool dev_ready = false;
+  gnpc_impl::DevBuf<int> rp, ci, long_rows;
+  gnpc_impl::DevBuf<float> v;
+  int n_long = 0;
+  int max_row = 0;
+  std::unique_ptr<gnpc_csr_s> tr;  // Âᵀ (lazy, for training backward)
+  std::unique_ptr<gnpc_impl::KrylovWs> kws;
+  void upload();
+  gnpk::DevCsr dev();
+};

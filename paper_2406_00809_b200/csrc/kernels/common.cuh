@@ -1,0 +1,126 @@
+// Shared device helpers for the sm_100a GNP kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace gnpk {
+
+constexpr int kThreads = 256;     // CTA size used by the streaming kernels
+constexpr int kLongRow = 32;      // rows with more nonzeros take the long-row path
+
+// Device view of Â (or Âᵀ): int32 indices (nnz < 2^31 enforced on upload),
+// fp32 values.  long_rows lists the rows with > kLongRow nonzeros.
+struct DevCsr {
+  int n;
+  int nnz;
+  const int* __restrict__ rp;
+  const int* __restrict__ ci;
+  const float* __restrict__ v;
+  const int* __restrict__ long_rows;
+  int n_long;
+};
+
+// Per-apply scalars produced by the norm kernel (scale sandwich,
+// src/gnn.cpp:128-139,191-199).
+struct ApplyScalars {
+  double tau;        // ||b||_2
+  double in_scale;   // sqrt(n)/tau
+  double out_scale;  // tau/sqrt(n)
+  int zero;          // tau == 0 → M(b) = 0
+  int pad;
+};
+
+// ---- device FGMRES state (kernels in krylov.cuh)
+struct KState {
+  int j;             // next step within the cycle
+  int steps;         // completed steps in the cycle
+  int stop;          // cycle finished (all later step kernels are no-ops)
+  int cycle;         // steps planned for this cycle
+  int breakdown;
+  int budget_hit;
+  int budget_status; // 1 maxiters, 2 timeout
+  int iter;          // outer iterations so far (all cycles)
+  int maxiters;
+  int singular;
+  int reorth;        // steps that took the re-orthogonalisation pass
+  int pad;
+  double rtol, bnorm, beta;
+  double tracked_rel;  // after the last step
+  double current;      // true relres after the cycle
+  long long t0;        // globaltimer at solve start (ns)
+  long long deadline;  // < 0: no timeout
+  long long t_end;     // globaltimer when the cycle's true residual was formed
+};
+
+struct KrylovDev {
+  int n, m;                 // restart length m
+  double* V;                // n x (m+1)
+  double* Z;                // n x m, or nullptr (unpreconditioned: Z = V)
+  double* w;                // n
+  double* vin;              // n: next preconditioner input (= v_j)
+  const double* zout;       // n: preconditioner output z_j
+  double* x;                // n
+  const double* b;          // n
+  double* r;                // n
+  double* H;                // (m+1) x m raw Hessenberg, col-major
+  double* R;                // (m+1) x m rotated
+  double* cs;               // m
+  double* sn;               // m
+  double* g;                // m+1
+  double* y;                // m
+  double* partials;         // 2 x grid
+  unsigned* ticket;
+  double* hist_rel;         // m per cycle
+  long long* hist_t;        // m per cycle
+  KState* st;
+};
+
+__device__ __forceinline__ float4 ldg4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void fma4(float4& acc, float s, float4 x) {
+  acc.x = fmaf(s, x.x, acc.x);
+  acc.y = fmaf(s, x.y, acc.y);
+  acc.z = fmaf(s, x.z, acc.z);
+  acc.w = fmaf(s, x.w, acc.w);
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float relu(float x) { return x > 0.f ? x : 0.f; }
+__device__ __forceinline__ float4 relu4(float4 a) {
+  return make_float4(relu(a.x), relu(a.y), relu(a.z), relu(a.w));
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum (fixed shuffle tree + fixed smem order).  All
+// threads receive the total.  `scratch` >= 32 entries.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  T t = lane < nw ? scratch[lane] : T(0);
+  t = warp_sum(t);
+  return t;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace gnpk

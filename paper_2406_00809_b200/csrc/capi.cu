@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <mutex>
@@ -16,6 +17,7 @@
 #include "capi_common.hpp"
 #include "kernels/apply.cuh"
 #include "kernels/krylov.cuh"
+#include "kernels/layer_tc.cuh"
 #include "model.hpp"
 
 using namespace gnpc_impl;
@@ -57,6 +59,7 @@ int guarded(F&& f) {
     return GNPC_EUNSUPPORTED;
   } catch (const CudaError& e) {
     set_error(e.what());
+    cudaGetLastError();  // do not leave a stale error for the next launch check
     return GNPC_ECUDA;
   } catch (const std::bad_alloc&) {
     set_error("device or host allocation failed");
@@ -129,6 +132,46 @@ struct ApplyLaunch {
       }
       const bool last = l + 1 == net.layers;
       mark(last ? 4 : 3);
+      if constexpr (DP == 16 || DP == 32) {
+        if (m.use_tc) {
+          using T = TcCfg<DP>;
+          const float* uwtc = m.UWTC.p + (size_t)l * 2 * T::B_FLOATS;
+          auto kern = last ? k_layer_tc<DP, true, OutT> : k_layer_tc<DP, false, OutT>;
+          const size_t smem = T::smem_bytes(last, net.hidden);
+          // launch geometry is computed once per model (host queries would
+          // otherwise starve the GPU between the 8 layer launches)
+          int& per_sm = m.tc_per_sm[(last ? 2 : 0) + (sizeof(OutT) == 8 ? 1 : 0)];
+          if (per_sm == 0) {
+            GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            // The occupancy API reports 1 CTA/SM for kernels that allocate
+            // TMEM; each CTA here holds only TCOLS of the 512 TMEM columns, so
+            // residency is bounded by registers / smem / warps / TMEM instead.
+            cudaFuncAttributes fa{};
+            GNPC_CUDA(cudaFuncGetAttributes(&fa, kern));
+            int dev = 0, smem_sm = 0, regs_sm = 0;
+            GNPC_CUDA(cudaGetDevice(&dev));
+            GNPC_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+            GNPC_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+            const int regs_cta = ((fa.numRegs + 7) / 8) * 8 * kThreads;
+            const int by_regs = regs_sm / std::max(regs_cta, 1);
+            const int by_smem = smem_sm / (int)(smem + fa.sharedSizeBytes + 1024);
+            const int by_warps = 64 / (kThreads / 32);
+            const int by_tmem = 512 / T::TCOLS;
+            per_sm = std::min(std::min(by_regs, by_smem), std::min(by_warps, by_tmem));
+            if (const char* dbg = std::getenv("GNPC_DEBUG"); dbg && dbg[0] == '1')
+              fprintf(stderr, "[gnpc] k_layer_tc<%d,%d> smem=%zu per_sm=%d sms=%d\n", DP, (int)last,
+                      smem, per_sm, sms);
+            per_sm = std::max(per_sm, 1);
+          }
+          const int tiles_tc = (n + T::TM - 1) / T::TM;
+          const int grid = std::max(1, std::min(tiles_tc, per_sm * sms));
+          kern<<<grid, kThreads, smem, s>>>(a, X, last ? nullptr : m.X[1 - cur].p, uwtc, axl, net,
+                                            m.sc.p, out, skip);
+          GNPC_LAUNCHED();
+          cur = 1 - cur;
+          continue;
+        }
+      }
       if (!last) {
         auto kern = k_layer<DP, false, OutT>;
         const size_t smem = Cfg::smem_bytes(false, net.hidden);
@@ -202,10 +245,13 @@ gnpk::DevCsr gnpc_csr_s::dev() {
 void gnpc_model_s::build_view() {
   const std::int64_t d = dims.d, H = dims.hidden, L = dims.layers;
   const gnp_b200::ParamLayout lay = gnp_b200::param_layout(dims);
-  const std::size_t o_enc1 = 0, o_enc1b = H, o_enc2 = 2 * H, o_enc2b = o_enc2 + H * dp;
+  // every section starts on a 16-byte boundary (float4 loads)
+  auto al = [](std::size_t x) { return (x + 3) & ~std::size_t(3); };
+  const std::size_t Ha = al(H);
+  const std::size_t o_enc1 = 0, o_enc1b = Ha, o_enc2 = 2 * Ha, o_enc2b = o_enc2 + Ha * dp;
   const std::size_t o_uw = o_enc2b + dp, o_dec1 = o_uw + (std::size_t)L * 2 * dp * dp;
-  const std::size_t o_dec1b = o_dec1 + (std::size_t)dp * H, o_dec2 = o_dec1b + H;
-  const std::size_t total = o_dec2 + H;
+  const std::size_t o_dec1b = o_dec1 + al((std::size_t)dp * H), o_dec2 = o_dec1b + Ha;
+  const std::size_t total = o_dec2 + Ha;
   std::vector<float> f(total, 0.0f);
   const double* p = params.data();
   for (std::int64_t h = 0; h < H; ++h) {
@@ -240,6 +286,36 @@ void gnpc_model_s::build_view() {
   view.dec2_b = (float)p[lay.dec2_b];
   view.hidden = (int)H;
   view.layers = (int)L;
+  // tcgen05 B operand per layer: B[j][k] = [U; W](k, j), split into tf32 hi
+  // (round-to-nearest) and lo = v - hi, in the K-major core-matrix layout.
+  if (dp >= 16) {
+    const int K = 2 * dp, KC = K / 4;
+    const std::size_t bf = (std::size_t)dp * K;
+    std::vector<float> t((std::size_t)L * 2 * bf, 0.0f);
+    auto tf32 = [](float x) {
+      std::uint32_t u;
+      std::memcpy(&u, &x, 4);
+      u = (u + 0x1000u) & ~0x1FFFu;  // round half away from zero on the magnitude (cvt.rna)
+      float r;
+      std::memcpy(&r, &u, 4);
+      return r;
+    };
+    for (std::int64_t l = 0; l < L; ++l) {
+      const float* uwl = f.data() + o_uw + (std::size_t)l * 2 * dp * dp;
+      float* hi = t.data() + (std::size_t)l * 2 * bf;
+      float* lo = hi + bf;
+      for (int j = 0; j < dp; ++j)
+        for (int k = 0; k < K; ++k) {
+          const float v = uwl[(std::size_t)k * dp + j];
+          const float h = tf32(v);
+          const std::uint32_t off = gnpk::tc::sw128_off(j, k, dp) / 4;
+          hi[off] = h;
+          lo[off] = v - h;
+        }
+    }
+    UWTC.upload(t.data(), t.size());
+    GNPC_CUDA(cudaDeviceSynchronize());
+  }
 }
 
 void gnpc_model_s::ensure_workspace() {
@@ -247,7 +323,7 @@ void gnpc_model_s::ensure_workspace() {
   X[0].ensure(n * dp);
   X[1].ensure(n * dp);
   if (a->n_long) AXL.ensure(n * dp);
-  sms = num_sms();
+  if (sms == 0) sms = num_sms();
   norm_grid = 2 * sms;
   partials.ensure(norm_grid);
   if (!ticket.p) {
@@ -761,6 +837,8 @@ int gnpc_model_create(gnpc_csr ahat, int64_t d, int64_t hidden, int64_t layers,
     m->dims = {d, hidden, layers};
     m->dp = 4;
     while (m->dp < d) m->dp *= 2;
+    const char* no_tc = std::getenv("GNPC_NO_TC");
+    m->use_tc = (m->dp == 16 || m->dp == 32) && !(no_tc && no_tc[0] == '1');
     m->params.assign(params, params + gnp_b200::param_layout(m->dims).total);
     GNPC_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
     m->build_view();

@@ -1,0 +1,374 @@
+// Fused Res-GCONV layer with the dense transform on the 5th-gen tensor cores.
+//
+//   Y = relu([X | ÂX] · [U; W])          (src/gnn.cpp:164-176)
+//
+// Persistent CTAs walk 128-row tiles in a software pipeline:
+//   stage   : the NEXT tile's row_ptr slice and (col, val) range are loaded
+//             into registers while the current tile gathers, then parked in
+//             a double-buffered smem slot (coalesced, off the critical path);
+//   gather  : G = DP/4 lanes per row; each group streams all of its R rows at
+//             once, U nonzeros per row per round (R*U independent 128-bit
+//             X-row loads in flight per lane), fp32 sums in stored order;
+//   epilogue: of the PREVIOUS tile, overlapping its MMA with this gather:
+//             tcgen05.ld of the TMEM accumulator (warp w owns lanes
+//             32(w%4)..+31; warps w, w+4 split the columns), relu, store Y;
+//             LAST: the projection MLP (src/gnn.cpp:178-199) per row;
+//   MMA     : [x | ÂX] split into tf32 hi + lo, written in the K-major
+//             core-matrix layout; one thread issues 3 x (2DP/8)
+//             tcgen05.mma.kind::tf32 (M=128, N=DP, K=8):
+//             A_lo·B_hi + A_hi·B_lo + A_hi·B_hi ("3xTF32", ~2^-21 relative per
+//             product) into TMEM, committed to an mbarrier.
+// [U; W] arrives pre-split (hi/lo) and pre-laid-out by the host (capi.cu).
+#pragma once
+
+#include "apply.cuh"
+#include "tc.cuh"
+
+namespace gnpk {
+
+template <int DP>
+struct TcCfg {
+  static constexpr int TM = 128;
+  static constexpr int K = 2 * DP;
+  static constexpr int KC = K / 4;  // 16-byte chunks per operand row
+  static constexpr int KS = K / 8;  // MMA K-steps (8 tf32 per instruction)
+  static constexpr int G = DP / 4;
+  static constexpr int NG = kThreads / G;
+  static constexpr int R = TM / NG;                // rows per gather group
+  static constexpr int U = 4;                      // nonzeros per row per gather round
+  static constexpr int CAP = 1536;                 // staged (col, val) entries per tile
+  static constexpr int CPT = CAP / kThreads;       // staged entries per thread
+  static constexpr int TCOLS = DP < 32 ? 32 : DP;  // TMEM columns (power of two >= 32)
+  static constexpr int SST = DP + 4;               // LAST staging row stride (floats)
+  static constexpr int RPS = TM + 4;               // staged row_ptr slot
+  static constexpr size_t A_FLOATS = (size_t)TM * K;
+  static constexpr size_t B_FLOATS = (size_t)DP * K;
+  static size_t smem_bytes(bool last, int hidden) {
+    size_t f = 2 * A_FLOATS + 2 * B_FLOATS + 2 * (size_t)RPS + 4 * (size_t)CAP;
+    if (last) f += (size_t)TM * SST + (size_t)DP * hidden + 2 * (size_t)hidden;
+    return f * 4 + 64 + 1024;  // + mbarrier / tmem slot + 1024-B atom alignment
+  }
+};
+
+// One group's R rows, U nonzeros per row per round: (col, val) for all R*U
+// slots first, then all R*U 128-bit X-row loads, then the FMAs in stored
+// column order — so every round keeps R*U independent loads in flight.
+template <int DP, int R, int U, typename LD>
+__device__ __forceinline__ void gather_rounds(const float* __restrict__ X, LD load,
+                                              int (&pos)[R], const int (&end)[R],
+                                              float4 (&acc)[R], int gl) {
+  while (true) {
+    bool more = false;
+#pragma unroll
+    for (int j = 0; j < R; ++j) more |= pos[j] < end[j];
+    if (!more) break;
+    int c[R][U];
+    float w[R][U];
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = pos[j] + u;
+        if (k < end[j]) {
+          load(k, c[j][u], w[j][u]);
+        } else {
+          c[j][u] = -1;
+          w[j][u] = 0.f;
+        }
+      }
+    float4 x[R][U];
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        x[j][u] = c[j][u] >= 0 ? ldg4(X + static_cast<size_t>(c[j][u]) * DP + 4 * gl) : f4zero();
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) fma4(acc[j], w[j][u], x[j][u]);
+      pos[j] += U;
+    }
+  }
+}
+
+template <int DP, bool LAST, typename OutT>
+__global__ void __launch_bounds__(kThreads)
+k_layer_tc(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
+           const float* __restrict__ uwtc, const float* __restrict__ axlong, NetView net,
+           const ApplyScalars* __restrict__ sc, OutT* __restrict__ out,
+           const int* __restrict__ skip) {
+  using C = TcCfg<DP>;
+  constexpr int TM = C::TM, KC = C::KC, KS = C::KS, G = C::G, NG = C::NG, R = C::R;
+  constexpr int U = C::U, CAP = C::CAP, CPT = C::CPT, RPS = C::RPS;
+  if (skip && *skip) return;
+  const int ntiles = (a.n + TM - 1) / TM;
+  if (sc->zero) {
+    if constexpr (LAST) {
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x)
+        out[i] = OutT(0);
+    }
+    return;
+  }
+  // Swizzle atoms need 1024-B alignment in the shared window; pointers are
+  // derived from the __shared__ array so they stay in the shared state space.
+  extern __shared__ float4 smem_raw[];
+  const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+  float* Ahi = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(smem_raw) + pad);
+  float* Alo = Ahi + C::A_FLOATS;
+  float* Bhi = Alo + C::A_FLOATS;
+  float* Blo = Bhi + C::B_FLOATS;
+  int* s_rp = reinterpret_cast<int*>(Blo + C::B_FLOATS);  // [2][RPS]
+  int2* s_cv = reinterpret_cast<int2*>(s_rp + 2 * RPS);    // [2][CAP] (col, val bits)
+  float* Stg = reinterpret_cast<float*>(s_cv + 2 * CAP);   // LAST: [TM][SST]
+  float* D1 = Stg + (LAST ? TM * C::SST : 0);              // LAST: [DP][H]
+  float* B1 = D1 + (LAST ? DP * net.hidden : 0);
+  float* D2 = B1 + (LAST ? net.hidden : 0);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(D2 + (LAST ? net.hidden : 0) + 4);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int t = tid; t < int(2 * C::B_FLOATS / 4); t += kThreads)
+    reinterpret_cast<float4*>(Bhi)[t] = reinterpret_cast<const float4*>(uwtc)[t];
+  if constexpr (LAST) {
+    const int H = net.hidden;
+    for (int t = tid; t < DP * H; t += kThreads) D1[t] = net.dec1[t];
+    for (int t = tid; t < H; t += kThreads) {
+      B1[t] = net.dec1_b[t];
+      D2[t] = net.dec2[t];
+    }
+  }
+  if (tid == 0) tc::mbar_init(bar, 1);
+  if (warp == 0) tc::tmem_alloc(tslot, C::TCOLS);
+
+  // ---- staging of a tile's row_ptr slice + (col, val) range (two halves so
+  //      the loads can be issued early and the smem stores done late)
+  struct Stage {
+    int rp;            // row_ptr[row0 + tid] (tid <= TM)
+    int kb, ke;        // the tile's nonzero range
+    int c[CPT];
+    float v[CPT];
+  };
+  auto stage_rp = [&](int tile, Stage& s) {
+    if (tile >= ntiles) return;
+    const int row0 = tile * TM;
+    if (tid <= TM) s.rp = __ldg(a.rp + min(row0 + tid, a.n));
+    s.kb = __ldg(a.rp + row0);
+    s.ke = __ldg(a.rp + min(row0 + TM, a.n));
+  };
+  auto stage_cv = [&](int tile, Stage& s) {
+    if (tile >= ntiles || s.ke - s.kb > CAP) return;
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const int k = s.kb + tid + q * kThreads;
+      if (k < s.ke) {
+        s.c[q] = __ldg(a.ci + k);
+        s.v[q] = __ldg(a.v + k);
+      }
+    }
+  };
+  auto stage_store = [&](int tile, const Stage& s, int slot) {
+    if (tile >= ntiles) return;
+    if (tid <= TM) s_rp[slot * RPS + tid] = s.rp;
+    if (s.ke - s.kb > CAP) return;
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const int k = tid + q * kThreads;
+      if (s.kb + k < s.ke) s_cv[slot * CAP + k] = make_int2(s.c[q], __float_as_int(s.v[q]));
+    }
+  };
+
+  int tile = blockIdx.x;
+  {
+    Stage s0;
+    stage_rp(tile, s0);
+    stage_cv(tile, s0);
+    stage_store(tile, s0, 0);
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  constexpr uint32_t idesc = tc::idesc_tf32(128, DP);
+  const uint32_t sAhi = tc::smem_u32(Ahi), sAlo = tc::smem_u32(Alo);
+  const uint32_t sBhi = tc::smem_u32(Bhi), sBlo = tc::smem_u32(Blo);
+  const int gl = tid % G, gid = tid / G;
+  uint32_t phase = 0;
+  int slot = 0;
+  int prev_row0 = -1;  // tile whose MMA is in flight
+
+  // ---- epilogue of the tile whose accumulator sits in TMEM
+  auto epilogue = [&](int row0) {
+    tc::mbar_wait(bar, phase);
+    phase ^= 1;
+    tc::fence_after();
+    constexpr int HC = DP / 2;  // columns per warp half
+    const int q = warp & 3, half = warp >> 2;
+    const int m = 32 * q + lane;
+    const int i = row0 + m;
+    float v[HC];
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * q) << 16) + half * HC;
+    if constexpr (HC == 8) {
+      tc::tmem_ld8(taddr, v);
+    } else {
+      tc::tmem_ld16(taddr, v);
+    }
+    if constexpr (!LAST) {
+      if (i < a.n) {
+        float* yrow = Y + static_cast<size_t>(i) * DP + half * HC;
+#pragma unroll
+        for (int c = 0; c < HC; c += 4)
+          st4(yrow + c, make_float4(relu(v[c]), relu(v[c + 1]), relu(v[c + 2]), relu(v[c + 3])));
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < HC; c += 4)
+        st4(Stg + m * C::SST + half * HC + c,
+            make_float4(relu(v[c]), relu(v[c + 1]), relu(v[c + 2]), relu(v[c + 3])));
+    }
+    tc::fence_before();
+  };
+  // LAST: projection MLP of the staged tile (after a barrier)
+  auto project = [&](int row0) {
+    if constexpr (LAST) {
+      const int H = net.hidden;
+      const double out_scale = sc->out_scale;
+      if (tid < TM) {
+        const int i = row0 + tid;
+        if (i < a.n) {
+          float y[DP];
+#pragma unroll
+          for (int j = 0; j < DP; j += 4) {
+            const float4 t = *reinterpret_cast<const float4*>(Stg + tid * C::SST + j);
+            y[j] = t.x; y[j + 1] = t.y; y[j + 2] = t.z; y[j + 3] = t.w;
+          }
+          float o = 0.f;
+          for (int h = 0; h < H; ++h) {
+            float t = 0.f;
+#pragma unroll
+            for (int j = 0; j < DP; ++j) t = fmaf(y[j], D1[j * H + h], t);
+            o = fmaf(relu(t + B1[h]), D2[h], o);
+          }
+          out[i] = static_cast<OutT>(static_cast<double>(o + net.dec2_b) * out_scale);
+        }
+      }
+    }
+  };
+
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int row0 = tile * TM;
+    const int next = tile + gridDim.x;
+    Stage sn;
+    stage_rp(next, sn);  // loads only; consumed at the end of the iteration
+
+    // ---------------------------------------------------------------- gather
+    const int* rp = s_rp + slot * RPS;
+    const int kb = rp[0], ke = rp[TM];
+    const bool staged = ke - kb <= CAP;
+    float4 acc[R], xs[R];
+    {
+      int pos[R], end[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int r = gid + j * NG;
+        const int i = row0 + r;
+        const int s = rp[r], e = rp[r + 1];
+        const bool valid = i < a.n;
+        const bool longrow = axlong != nullptr && e - s > kLongRow;
+        pos[j] = s;
+        end[j] = (valid && !longrow) ? e : s;
+        acc[j] = (valid && longrow) ? ldg4(axlong + static_cast<size_t>(i) * DP + 4 * gl) : f4zero();
+        xs[j] = valid ? ldg4(X + static_cast<size_t>(i) * DP + 4 * gl) : f4zero();
+      }
+      if (staged) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          pos[j] -= kb;
+          end[j] -= kb;
+        }
+        const int2* cv = s_cv + slot * CAP;
+        gather_rounds<DP, R, U>(
+            X,
+            [cv](int k, int& c, float& w) {
+              const int2 e = cv[k];
+              c = e.x;
+              w = __int_as_float(e.y);
+            },
+            pos, end, acc, gl);
+      } else {
+        gather_rounds<DP, R, U>(
+            X,
+            [&a](int k, int& c, float& w) {
+              c = __ldg(a.ci + k);
+              w = __ldg(a.v + k);
+            },
+            pos, end, acc, gl);
+      }
+    }
+    stage_cv(next, sn);
+
+    // ------------------------------------------------ previous tile: epilogue
+    if (prev_row0 >= 0) epilogue(prev_row0);
+
+    // ------------------------------------------------ A tile, staging, barrier
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int r = gid + j * NG;
+      const float4 xi = xs[j], ax = acc[j];
+      const float4 xh = make_float4(tc::to_tf32(xi.x), tc::to_tf32(xi.y), tc::to_tf32(xi.z), tc::to_tf32(xi.w));
+      const float4 ah = make_float4(tc::to_tf32(ax.x), tc::to_tf32(ax.y), tc::to_tf32(ax.z), tc::to_tf32(ax.w));
+      const float4 xl = make_float4(xi.x - xh.x, xi.y - xh.y, xi.z - xh.z, xi.w - xh.w);
+      const float4 al = make_float4(ax.x - ah.x, ax.y - ah.y, ax.z - ah.z, ax.w - ah.w);
+      const uint32_t ox = tc::sw128_off(r, 4 * gl, TM), oa = tc::sw128_off(r, DP + 4 * gl, TM);
+      *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Ahi) + ox) = xh;
+      *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Alo) + ox) = xl;
+      *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Ahi) + oa) = ah;
+      *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Alo) + oa) = al;
+    }
+    stage_store(next, sn, slot ^ 1);
+    tc::fence_proxy_async();
+    __syncthreads();
+
+    if constexpr (LAST) {
+      if (prev_row0 >= 0) {
+        project(prev_row0);
+        __syncthreads();  // Stg is rewritten by the next epilogue
+      }
+    }
+
+    // ---------------------------------------------------------------- MMA
+    if (tid == 0) {
+      tc::fence_after();
+      uint32_t accf = 0;
+#pragma unroll
+      for (int pass = 0; pass < 3; ++pass) {
+        const uint32_t sa = pass == 0 ? sAlo : sAhi;
+        const uint32_t sb = pass == 1 ? sBlo : sBhi;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          // K-step s: atom s/4 (atom-major along K), +32 B per step inside it
+          const uint64_t ad = tc::make_desc_sw128(sa + (s >> 2) * TM * 128 + (s & 3) * 32, 1024);
+          const uint64_t bd = tc::make_desc_sw128(sb + (s >> 2) * DP * 128 + (s & 3) * 32, 1024);
+          tc::mma_tf32(tmem, ad, bd, idesc, accf);
+          accf = 1;
+        }
+      }
+      tc::mma_commit(bar);
+    }
+    prev_row0 = row0;
+    slot ^= 1;
+  }
+  if (prev_row0 >= 0) {
+    epilogue(prev_row0);
+    if constexpr (LAST) {
+      __syncthreads();
+      project(prev_row0);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0) tc::tmem_dealloc(tmem, C::TCOLS);
+}
+
+}  // namespace gnpk

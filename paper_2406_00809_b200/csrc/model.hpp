@@ -25,6 +25,9 @@ struct gnpc_model_s {
   int dp = 16;                 // d padded to a power of two >= 4 (zero weights)
   std::vector<double> params;  // reference layout, f64
   gnpc_impl::DevBuf<float> P;  // device fp32 params (NetView points into it)
+  gnpc_impl::DevBuf<float> UWTC;  // per layer [U;W]^T split tf32 hi/lo, tcgen05 layout
+  bool use_tc = true;             // DP 16/32: tcgen05 transform (GNPC_NO_TC=1: CUDA cores)
+  int tc_per_sm[4] = {0, 0, 0, 0};  // cached occupancy per (last, OutT) tcgen05 kernel
   gnpk::NetView view{};
   // apply workspace
   gnpc_impl::DevBuf<float> X[2], AXL;

@@ -177,12 +177,17 @@ int gnpc_train_step_synthetic(gnpc_trainer t, uint64_t seed, double* loss);
 /* Loss of the current params on a batch (monitoring_loss, src/gnn.cpp:390-397). */
 int gnpc_monitor_loss(gnpc_trainer t, const double* x, const double* b, int64_t batch,
                       double* loss);
-/* Data-parallel split of a step: the flat fp32 device gradient buffer a
- * collective (NCCL all-reduce) may sum in place between the two calls. */
-int gnpc_trainer_grad_buffer(gnpc_trainer t, float** dev_ptr, int64_t* count);
+/* Data-parallel split of a step: the flat f64 device gradient buffer (batch
+ * sum, reference flat order) that a collective (NCCL all-reduce) sums in
+ * place between gnpc_train_backward_only and gnpc_train_apply_grads. */
+int gnpc_trainer_grad_buffer(gnpc_trainer t, double** dev_ptr, int64_t* count);
 int gnpc_train_backward_only(gnpc_trainer t, const double* x, const double* b, double* loss);
 int gnpc_train_apply_grads(gnpc_trainer t);
 int gnpc_trainer_adam_state(gnpc_trainer t, double* m1, double* m2, int64_t* step);
+/* Current f64 master parameters (flat reference order). */
+int gnpc_trainer_params(gnpc_trainer t, double* params);
+/* Copy the trainer's parameters into its model (inference view rebuilt). */
+int gnpc_trainer_sync_model(gnpc_trainer t);
 
 /* train_preconditioner (src/gnn.cpp:401-451) with Gaussian pairs only
  * (spectral_count must be 0 in this build).  losses: steps+1 entries. */

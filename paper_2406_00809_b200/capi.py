@@ -273,6 +273,103 @@ def fgmres(csr: Csr, b, model: Model | None = None, x0=None, rtol=1e-8, maxiters
             "reorth_steps": int(h.reorth)}
 
 
+class Trainer:
+    """gnpc_trainer handle: batched forward/backward/Adam on the device.
+    Batches cross the ABI as n x B column-major f64 (the reference
+    TrainingBatch layout, src/sampler.cpp:68-83)."""
+
+    def __init__(self, model: Model, batch: int, lr: float = 1e-3):
+        self.model = model
+        self.batch = batch
+        h = vp()
+        check(lib().gnpc_trainer_create(model.h, C.c_int64(batch), C.c_double(lr), C.byref(h)))
+        self.h = h
+        self.count = param_count(*model.dims)
+
+    def __del__(self):
+        try:
+            if self.h and _lib is not None:
+                _lib.gnpc_trainer_destroy(self.h)
+        except Exception:
+            pass
+
+    @staticmethod
+    def _cm(a):
+        return np.ascontiguousarray(a, np.float64)
+
+    def forward_backward(self, x, b):
+        x, b = self._cm(x), self._cm(b)
+        loss = C.c_double()
+        grads = np.empty(self.count)
+        out = np.empty_like(x)
+        check(lib().gnpc_forward_backward(self.h, x.ctypes.data_as(vp), b.ctypes.data_as(vp),
+                                          C.byref(loss), grads.ctypes.data_as(vp),
+                                          out.ctypes.data_as(vp)))
+        return loss.value, grads, out
+
+    def step(self, x, b):
+        x, b = self._cm(x), self._cm(b)
+        loss = C.c_double()
+        check(lib().gnpc_train_step(self.h, x.ctypes.data_as(vp), b.ctypes.data_as(vp),
+                                    C.byref(loss)))
+        return loss.value
+
+    def step_synthetic(self, seed: int):
+        loss = C.c_double()
+        check(lib().gnpc_train_step_synthetic(self.h, C.c_uint64(seed), C.byref(loss)))
+        return loss.value
+
+    def monitor_loss(self, x, b):
+        x, b = self._cm(x), self._cm(b)
+        loss = C.c_double()
+        check(lib().gnpc_monitor_loss(self.h, x.ctypes.data_as(vp), b.ctypes.data_as(vp),
+                                      C.c_int64(self.batch), C.byref(loss)))
+        return loss.value
+
+    def backward_only(self, x, b):
+        x, b = self._cm(x), self._cm(b)
+        loss = C.c_double()
+        check(lib().gnpc_train_backward_only(self.h, x.ctypes.data_as(vp), b.ctypes.data_as(vp),
+                                             C.byref(loss)))
+        return loss.value
+
+    def apply_grads(self):
+        check(lib().gnpc_train_apply_grads(self.h))
+
+    def grad_buffer(self):
+        p = C.c_void_p()
+        cnt = C.c_int64()
+        check(lib().gnpc_trainer_grad_buffer(self.h, C.byref(p), C.byref(cnt)))
+        return p.value, cnt.value
+
+    def params(self):
+        out = np.empty(self.count)
+        check(lib().gnpc_trainer_params(self.h, out.ctypes.data_as(vp)))
+        return out
+
+    def adam_state(self):
+        m1 = np.empty(self.count)
+        m2 = np.empty(self.count)
+        t = C.c_int64()
+        check(lib().gnpc_trainer_adam_state(self.h, m1.ctypes.data_as(vp), m2.ctypes.data_as(vp),
+                                            C.byref(t)))
+        return m1, m2, t.value
+
+    def sync_model(self):
+        check(lib().gnpc_trainer_sync_model(self.h))
+
+
+def train_preconditioner(csr: Csr, dims=(16, 32, 8), lr=1e-3, steps=2000, batch=16, spectral=0,
+                         arnoldi_m=40, seed=0, monitor_batch=16):
+    cfg = TrainConfig(lr, steps, batch, spectral, arnoldi_m, seed, monitor_batch, *dims)
+    best = np.empty(param_count(*dims))
+    losses = np.empty(steps + 1)
+    bl = C.c_double()
+    check(lib().gnpc_train_preconditioner(csr.h, C.byref(cfg), best.ctypes.data_as(vp),
+                                          losses.ctypes.data_as(vp), C.byref(bl)))
+    return best, losses, bl.value
+
+
 def fgmres_device(csr: Csr, model: Model | None, b_ptr: int, x_ptr: int, rtol, maxiters, restart,
                   stream: int = 0):
     cfg = SolveConfig(rtol, maxiters, restart, -1.0)

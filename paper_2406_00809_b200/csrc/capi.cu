@@ -46,41 +46,31 @@ int num_sms() {
   return sms;
 }
 
-template <class F>
-int guarded(F&& f) {
-  try {
-    f();
-    return GNPC_OK;
-  } catch (const NoDevice& e) {
-    set_error(e.what());
-    return GNPC_ENODEV;
-  } catch (const Unsupported& e) {
-    set_error(e.what());
-    return GNPC_EUNSUPPORTED;
-  } catch (const CudaError& e) {
-    set_error(e.what());
-    cudaGetLastError();  // do not leave a stale error for the next launch check
-    return GNPC_ECUDA;
-  } catch (const std::bad_alloc&) {
-    set_error("device or host allocation failed");
-    return GNPC_ENOMEM;
-  } catch (const std::out_of_range& e) {
-    set_error(e.what());
-    return GNPC_ERANGE;
-  } catch (const std::invalid_argument& e) {
-    set_error(e.what());
-    return GNPC_EINVAL;
-  } catch (const std::exception& e) {
-    set_error(e.what());
-    return GNPC_ERUNTIME;
-  } catch (...) {
-    set_error("unknown error");
-    return GNPC_ERUNTIME;
-  }
-}
-
 void need(bool cond, const char* msg) {
   if (!cond) throw std::invalid_argument(msg);
+}
+
+// CTAs per SM for a tcgen05 kernel.  The occupancy API reports 1 CTA/SM for
+// kernels that allocate TMEM; each CTA here holds only `tcols` of the 512 TMEM
+// columns, so residency is bounded by registers / smem / warps / TMEM instead.
+// Also raises the kernel's dynamic-smem limit to `smem`.
+int tc_ctas_per_sm(const void* kern, size_t smem, int tcols) {
+  GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaFuncAttributes fa{};
+  GNPC_CUDA(cudaFuncGetAttributes(&fa, kern));
+  int dev = 0, smem_sm = 0, regs_sm = 0;
+  GNPC_CUDA(cudaGetDevice(&dev));
+  GNPC_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  GNPC_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+  const int regs_cta = ((fa.numRegs + 7) / 8) * 8 * gnpk::kThreads;
+  const int by_regs = regs_sm / std::max(regs_cta, 1);
+  const int by_smem = smem_sm / (int)(smem + fa.sharedSizeBytes + 1024);
+  const int by_warps = 64 / (gnpk::kThreads / 32);
+  const int by_tmem = 512 / tcols;
+  const int per_sm = std::min(std::min(by_regs, by_smem), std::min(by_warps, by_tmem));
+  if (const char* dbg = std::getenv("GNPC_DEBUG"); dbg && dbg[0] == '1')
+    fprintf(stderr, "[gnpc] tcgen05 kernel smem=%zu regs=%d ctas/SM=%d\n", smem, fa.numRegs, per_sm);
+  return std::max(per_sm, 1);
 }
 
 // ------------------------------------------------------------------ apply launcher
@@ -104,11 +94,11 @@ struct ApplyLaunch {
     GNPC_LAUNCHED();
     // lift
     {
-      const size_t smem = (size_t)net.hidden * DP * 4 + 2 * (size_t)net.hidden * 4;
-      auto kern = k_lift<DP, InT>;
+      const size_t smem = (size_t)(net.nbreak + 1) * DP * 8 + (size_t)net.nbreak * 4 + 16;
+      auto kern = k_lift_pw<DP, InT>;
       static std::once_flag f;
       std::call_once(f, [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
       });
       mark(1);
       const int ng = kThreads / (DP / 4);
@@ -126,7 +116,14 @@ struct ApplyLaunch {
       const float* axl = nullptr;
       if (A.n_long > 0) {
         mark(2);
-        k_long_ax<DP><<<A.n_long, kThreads, 0, s>>>(a, X, m.AXL.p, m.sc.p, skip);
+        LongPlan lp{A.n_chunks, A.ch_row.p, A.ch_k0.p, A.ch_k1.p, A.n_long,
+                    A.long_rows.p, A.long_c0.p, m.LPART.p};
+        const int wpb = kThreads / 32;
+        k_long_chunks<DP><<<(A.n_chunks + wpb - 1) / wpb, kThreads, 0, s>>>(a, lp, X, m.sc.p, skip);
+        GNPC_LAUNCHED();
+        const int thr = A.n_long * (DP / 4);
+        k_long_combine<DP><<<(thr + kThreads - 1) / kThreads, kThreads, 0, s>>>(lp, m.AXL.p, m.sc.p,
+                                                                              skip);
         GNPC_LAUNCHED();
         axl = m.AXL.p;
       }
@@ -136,37 +133,16 @@ struct ApplyLaunch {
         if (m.use_tc) {
           using T = TcCfg<DP>;
           const float* uwtc = m.UWTC.p + (size_t)l * 2 * T::B_FLOATS;
-          auto kern = last ? k_layer_tc<DP, true, OutT> : k_layer_tc<DP, false, OutT>;
+          auto kern = last ? k_layer_tc<DP, kEpiLast, OutT> : k_layer_tc<DP, kEpiRelu, OutT>;
           const size_t smem = T::smem_bytes(last, net.hidden);
           // launch geometry is computed once per model (host queries would
           // otherwise starve the GPU between the 8 layer launches)
           int& per_sm = m.tc_per_sm[(last ? 2 : 0) + (sizeof(OutT) == 8 ? 1 : 0)];
-          if (per_sm == 0) {
-            GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            // The occupancy API reports 1 CTA/SM for kernels that allocate
-            // TMEM; each CTA here holds only TCOLS of the 512 TMEM columns, so
-            // residency is bounded by registers / smem / warps / TMEM instead.
-            cudaFuncAttributes fa{};
-            GNPC_CUDA(cudaFuncGetAttributes(&fa, kern));
-            int dev = 0, smem_sm = 0, regs_sm = 0;
-            GNPC_CUDA(cudaGetDevice(&dev));
-            GNPC_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-            GNPC_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
-            const int regs_cta = ((fa.numRegs + 7) / 8) * 8 * kThreads;
-            const int by_regs = regs_sm / std::max(regs_cta, 1);
-            const int by_smem = smem_sm / (int)(smem + fa.sharedSizeBytes + 1024);
-            const int by_warps = 64 / (kThreads / 32);
-            const int by_tmem = 512 / T::TCOLS;
-            per_sm = std::min(std::min(by_regs, by_smem), std::min(by_warps, by_tmem));
-            if (const char* dbg = std::getenv("GNPC_DEBUG"); dbg && dbg[0] == '1')
-              fprintf(stderr, "[gnpc] k_layer_tc<%d,%d> smem=%zu per_sm=%d sms=%d\n", DP, (int)last,
-                      smem, per_sm, sms);
-            per_sm = std::max(per_sm, 1);
-          }
+          if (per_sm == 0) per_sm = tc_ctas_per_sm((const void*)kern, smem, T::TCOLS);
           const int tiles_tc = (n + T::TM - 1) / T::TM;
           const int grid = std::max(1, std::min(tiles_tc, per_sm * sms));
-          kern<<<grid, kThreads, smem, s>>>(a, X, last ? nullptr : m.X[1 - cur].p, uwtc, axl, net,
-                                            m.sc.p, out, skip);
+          LayerIO io{X, last ? nullptr : m.X[1 - cur].p, uwtc, axl, nullptr, nullptr, 1};
+          kern<<<grid, kThreads, smem, s>>>(a, io, net, m.sc.p, out, skip);
           GNPC_LAUNCHED();
           cur = 1 - cur;
           continue;
@@ -223,7 +199,23 @@ void gnpc_csr_s::upload() {
   ci.upload(hci.data(), hci.size());
   v.upload(hv.data(), hv.size());
   n_long = static_cast<int>(longs.size());
-  if (n_long) long_rows.upload(longs.data(), longs.size());
+  if (n_long) {
+    long_rows.upload(longs.data(), longs.size());
+    std::vector<int> crow, ck0, ck1, c0(1, 0);
+    for (int i : longs) {
+      for (int k = hrp[i]; k < hrp[i + 1]; k += gnpk::kChunk) {
+        crow.push_back(i);
+        ck0.push_back(k);
+        ck1.push_back(std::min(k + gnpk::kChunk, hrp[i + 1]));
+      }
+      c0.push_back(static_cast<int>(crow.size()));
+    }
+    n_chunks = static_cast<int>(crow.size());
+    ch_row.upload(crow.data(), crow.size());
+    ch_k0.upload(ck0.data(), ck0.size());
+    ch_k1.upload(ck1.data(), ck1.size());
+    long_c0.upload(c0.data(), c0.size());
+  }
   GNPC_CUDA(cudaDeviceSynchronize());
   dev_ready = true;
 }
@@ -242,37 +234,102 @@ gnpk::DevCsr gnpc_csr_s::dev() {
 }
 
 // ====================================================================== model
-void gnpc_model_s::build_view() {
+// Index maps from the flat f64 parameter vector (reference order,
+// src/gnn.cpp:40-55) into the device fp32 layout and the per-layer operands.
+// The host uses them here; the trainer uploads them and regenerates the device
+// copies on the GPU after every Adam step (k_gather_params / k_gather_split).
+void gnpc_model_s::build_maps() {
+  if (!map_view.empty()) return;
   const std::int64_t d = dims.d, H = dims.hidden, L = dims.layers;
   const gnp_b200::ParamLayout lay = gnp_b200::param_layout(dims);
   // every section starts on a 16-byte boundary (float4 loads)
   auto al = [](std::size_t x) { return (x + 3) & ~std::size_t(3); };
   const std::size_t Ha = al(H);
-  const std::size_t o_enc1 = 0, o_enc1b = Ha, o_enc2 = 2 * Ha, o_enc2b = o_enc2 + Ha * dp;
-  const std::size_t o_uw = o_enc2b + dp, o_dec1 = o_uw + (std::size_t)L * 2 * dp * dp;
-  const std::size_t o_dec1b = o_dec1 + al((std::size_t)dp * H), o_dec2 = o_dec1b + Ha;
-  const std::size_t total = o_dec2 + Ha;
-  std::vector<float> f(total, 0.0f);
-  const double* p = params.data();
+  o_enc1 = 0;
+  o_enc1b = Ha;
+  o_enc2 = 2 * Ha;
+  o_enc2b = o_enc2 + Ha * dp;
+  o_uw = o_enc2b + dp;
+  o_dec1 = o_uw + (std::size_t)L * 2 * dp * dp;
+  o_dec1b = o_dec1 + al((std::size_t)dp * H);
+  o_dec2 = o_dec1b + Ha;
+  o_dec2b = o_dec2 + Ha;
+  const std::size_t total = o_dec2b + 4;
+  map_view.assign(total, -1);
   for (std::int64_t h = 0; h < H; ++h) {
-    f[o_enc1 + h] = (float)p[lay.enc1 + h];
-    f[o_enc1b + h] = (float)p[lay.enc1_b + h];
-    f[o_dec1b + h] = (float)p[lay.dec1_b + h];
-    f[o_dec2 + h] = (float)p[lay.dec2 + h];
+    map_view[o_enc1 + h] = (int)(lay.enc1 + h);
+    map_view[o_enc1b + h] = (int)(lay.enc1_b + h);
+    map_view[o_dec1b + h] = (int)(lay.dec1_b + h);
+    map_view[o_dec2 + h] = (int)(lay.dec2 + h);
     for (std::int64_t j = 0; j < d; ++j) {
-      f[o_enc2 + h * dp + j] = (float)p[lay.enc2 + j * H + h];  // enc2 (h, j) col-major H x d
-      f[o_dec1 + j * H + h] = (float)p[lay.dec1 + h * d + j];   // dec1 (j, h) col-major d x H
+      map_view[o_enc2 + h * dp + j] = (int)(lay.enc2 + j * H + h);  // enc2 (h, j), col-major H x d
+      map_view[o_dec1 + j * H + h] = (int)(lay.dec1 + h * d + j);   // dec1 (j, h), col-major d x H
     }
   }
-  for (std::int64_t j = 0; j < d; ++j) f[o_enc2b + j] = (float)p[lay.enc2_b + j];
-  for (std::int64_t l = 0; l < L; ++l) {
-    float* uw = f.data() + o_uw + (std::size_t)l * 2 * dp * dp;
-    for (std::int64_t k = 0; k < d; ++k)
-      for (std::int64_t j = 0; j < d; ++j) {
-        uw[k * dp + j] = (float)p[lay.u[l] + j * d + k];           // U(k, j)
-        uw[(dp + k) * dp + j] = (float)p[lay.w[l] + j * d + k];    // W(k, j)
+  for (std::int64_t j = 0; j < d; ++j) map_view[o_enc2b + j] = (int)(lay.enc2_b + j);
+  map_view[o_dec2b] = (int)lay.dec2_b;
+  // per-layer B operands, element (output j, input k), k < DP: x part, DP.. : ÂX part
+  //   forward  : [U; W](k, j)   = U(k, j), W(k - DP, j)
+  //   backward : [Uᵀ; Wᵀ](k, j) = U(j, k), W(j, k - DP)   (gX = gpre Uᵀ + Âᵀgpre Wᵀ)
+  auto fwd_src = [&](std::int64_t l, int j, int k) -> int {
+    if (j >= d) return -1;
+    if (k < d) return (int)(lay.u[l] + j * d + k);
+    if (k >= dp && k - dp < d) return (int)(lay.w[l] + j * d + (k - dp));
+    return -1;
+  };
+  auto bwd_src = [&](std::int64_t l, int j, int k) -> int {
+    if (j >= d) return -1;
+    if (k < d) return (int)(lay.u[l] + k * d + j);
+    if (k >= dp && k - dp < d) return (int)(lay.w[l] + (k - dp) * d + j);
+    return -1;
+  };
+  const int K = 2 * dp;
+  const std::size_t bf = (std::size_t)dp * K;
+  for (std::int64_t l = 0; l < L; ++l)
+    for (int k = 0; k < K; ++k)
+      for (int j = 0; j < dp; ++j) map_view[o_uw + (std::size_t)l * 2 * dp * dp + (std::size_t)k * dp + j] =
+          fwd_src(l, j, k);
+  map_bt_fwd.assign((std::size_t)L * bf, -1);
+  map_bt_bwd.assign((std::size_t)L * bf, -1);
+  for (std::int64_t l = 0; l < L; ++l)
+    for (int j = 0; j < dp; ++j)
+      for (int k = 0; k < K; ++k) {
+        map_bt_fwd[(std::size_t)l * bf + (std::size_t)j * K + k] = fwd_src(l, j, k);
+        map_bt_bwd[(std::size_t)l * bf + (std::size_t)j * K + k] = bwd_src(l, j, k);
       }
+  if (dp == 16 || dp == 32) {
+    map_tc_fwd.assign((std::size_t)L * 2 * bf, -1);
+    map_tc_bwd.assign((std::size_t)L * 2 * bf, -1);
+    part_tc.assign((std::size_t)L * 2 * bf, 0);
+    for (std::int64_t l = 0; l < L; ++l)
+      for (int j = 0; j < dp; ++j)
+        for (int k = 0; k < K; ++k) {
+          const std::size_t off = gnpk::tc::sw128_off(j, k, dp) / 4;
+          const std::size_t hi = (std::size_t)l * 2 * bf + off, lo = hi + bf;
+          map_tc_fwd[hi] = map_tc_fwd[lo] = fwd_src(l, j, k);
+          map_tc_bwd[hi] = map_tc_bwd[lo] = bwd_src(l, j, k);
+          part_tc[lo] = 1;
+        }
   }
+}
+
+static float tf32_rna(float x) {
+  std::uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u = (u + 0x1000u) & ~0x1FFFu;  // cvt.rna: round half away from zero on the magnitude
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+void gnpc_model_s::build_view() {
+  build_maps();
+  const std::int64_t d = dims.d, H = dims.hidden, L = dims.layers;
+  const gnp_b200::ParamLayout lay = gnp_b200::param_layout(dims);
+  auto al = [](std::size_t x) { return (x + 3) & ~std::size_t(3); };
+  const double* p = params.data();
+  std::vector<float> f(map_view.size());
+  for (std::size_t i = 0; i < f.size(); ++i) f[i] = map_view[i] >= 0 ? (float)p[map_view[i]] : 0.f;
   P.upload(f.data(), f.size());
   GNPC_CUDA(cudaDeviceSynchronize());
   view.enc1 = P.p + o_enc1;
@@ -283,46 +340,82 @@ void gnpc_model_s::build_view() {
   view.dec1 = P.p + o_dec1;
   view.dec1_b = P.p + o_dec1b;
   view.dec2 = P.p + o_dec2;
+  view.dec2_bp = P.p + o_dec2b;
   view.dec2_b = (float)p[lay.dec2_b];
   view.hidden = (int)H;
   view.layers = (int)L;
-  // tcgen05 B operand per layer: B[j][k] = [U; W](k, j), split into tf32 hi
-  // (round-to-nearest) and lo = v - hi, in the K-major core-matrix layout.
-  if (dp >= 16) {
-    const int K = 2 * dp, KC = K / 4;
-    const std::size_t bf = (std::size_t)dp * K;
-    std::vector<float> t((std::size_t)L * 2 * bf, 0.0f);
-    auto tf32 = [](float x) {
-      std::uint32_t u;
-      std::memcpy(&u, &x, 4);
-      u = (u + 0x1000u) & ~0x1FFFu;  // round half away from zero on the magnitude (cvt.rna)
-      float r;
-      std::memcpy(&r, &u, 4);
-      return r;
-    };
-    for (std::int64_t l = 0; l < L; ++l) {
-      const float* uwl = f.data() + o_uw + (std::size_t)l * 2 * dp * dp;
-      float* hi = t.data() + (std::size_t)l * 2 * bf;
-      float* lo = hi + bf;
-      for (int j = 0; j < dp; ++j)
-        for (int k = 0; k < K; ++k) {
-          const float v = uwl[(std::size_t)k * dp + j];
-          const float h = tf32(v);
-          const std::uint32_t off = gnpk::tc::sw128_off(j, k, dp) / 4;
-          hi[off] = h;
-          lo[off] = v - h;
+  // Lift as an exact piecewise-linear function of the scalar v (f64 tables):
+  // kinks t_h = -b1_h/enc1_h; on each interval the active hidden set is fixed,
+  // so x1 = (Σ_active enc1_h enc2_h) v + (Σ_active b1_h enc2_h + enc2_b).
+  {
+    std::vector<double> kinks;
+    for (std::int64_t h = 0; h < H; ++h)
+      if (p[lay.enc1 + h] != 0.0) kinks.push_back(-p[lay.enc1_b + h] / p[lay.enc1 + h]);
+    std::sort(kinks.begin(), kinks.end());
+    kinks.erase(std::unique(kinks.begin(), kinks.end()), kinks.end());
+    const int nb = (int)kinks.size();
+    std::vector<float> lt(std::max(nb, 1)), la((std::size_t)(nb + 1) * dp, 0.f),
+        lb((std::size_t)(nb + 1) * dp, 0.f);
+    for (int k = 0; k < nb; ++k) lt[k] = (float)kinks[k];
+    for (int k = 0; k <= nb; ++k) {
+      // representative point strictly inside interval k
+      double vr;
+      if (nb == 0) vr = 0.0;
+      else if (k == 0) vr = kinks[0] - 1.0 - std::abs(kinks[0]);
+      else if (k == nb) vr = kinks[nb - 1] + 1.0 + std::abs(kinks[nb - 1]);
+      else vr = 0.5 * (kinks[k - 1] + kinks[k]);
+      for (std::int64_t j = 0; j < d; ++j) {
+        double a_ = 0.0, b_ = p[lay.enc2_b + j];
+        for (std::int64_t h = 0; h < H; ++h) {
+          const double w = p[lay.enc1 + h], bb = p[lay.enc1_b + h];
+          if (w * vr + bb > 0.0) {
+            const double e = p[lay.enc2 + j * H + h];
+            a_ += w * e;
+            b_ += bb * e;
+          }
         }
+        la[(std::size_t)k * dp + j] = (float)a_;
+        lb[(std::size_t)k * dp + j] = (float)b_;
+      }
+    }
+    std::vector<float> lift;
+    lift.insert(lift.end(), lt.begin(), lt.end());
+    const std::size_t oa = al(lift.size());
+    lift.resize(oa, 0.f);
+    lift.insert(lift.end(), la.begin(), la.end());
+    const std::size_t ob = al(lift.size());
+    lift.resize(ob, 0.f);
+    lift.insert(lift.end(), lb.begin(), lb.end());
+    LIFT.upload(lift.data(), lift.size());
+    GNPC_CUDA(cudaDeviceSynchronize());
+    view.lift_t = LIFT.p;
+    view.lift_a = LIFT.p + oa;
+    view.lift_b = LIFT.p + ob;
+    view.nbreak = nb;
+  }
+  // tcgen05 B operands (forward): [U; W]ᵀ split into tf32 hi (round-to-nearest)
+  // and lo = v - hi, 128-byte-swizzled K-major.
+  if (!map_tc_fwd.empty()) {
+    std::vector<float> t(map_tc_fwd.size());
+    for (std::size_t i = 0; i < t.size(); ++i) {
+      const float v = map_tc_fwd[i] >= 0 ? (float)p[map_tc_fwd[i]] : 0.f;
+      const float h = tf32_rna(v);
+      t[i] = part_tc[i] ? v - h : h;
     }
     UWTC.upload(t.data(), t.size());
     GNPC_CUDA(cudaDeviceSynchronize());
   }
+  (void)L;
 }
 
 void gnpc_model_s::ensure_workspace() {
   const std::size_t n = (std::size_t)a->h.n;
   X[0].ensure(n * dp);
   X[1].ensure(n * dp);
-  if (a->n_long) AXL.ensure(n * dp);
+  if (a->n_long) {
+    AXL.ensure(n * dp);
+    LPART.ensure((std::size_t)a->n_chunks * dp);
+  }
   if (sms == 0) sms = num_sms();
   norm_grid = 2 * sms;
   partials.ensure(norm_grid);

@@ -43,8 +43,43 @@ extern std::atomic<std::int64_t> g_launches;
     GNPC_CUDA(cudaGetLastError());                                \
   } while (0)
 
+// Runs f and maps any exception onto a gnpc_status (nothing escapes the ABI).
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return GNPC_OK;
+  } catch (const NoDevice& e) {
+    set_error(e.what());
+    return GNPC_ENODEV;
+  } catch (const Unsupported& e) {
+    set_error(e.what());
+    return GNPC_EUNSUPPORTED;
+  } catch (const CudaError& e) {
+    set_error(e.what());
+    cudaGetLastError();  // do not leave a stale error for the next launch check
+    return GNPC_ECUDA;
+  } catch (const std::bad_alloc&) {
+    set_error("device or host allocation failed");
+    return GNPC_ENOMEM;
+  } catch (const std::out_of_range& e) {
+    set_error(e.what());
+    return GNPC_ERANGE;
+  } catch (const std::invalid_argument& e) {
+    set_error(e.what());
+    return GNPC_EINVAL;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return GNPC_ERUNTIME;
+  } catch (...) {
+    set_error("unknown error");
+    return GNPC_ERUNTIME;
+  }
+}
+
 void require_device();
 int num_sms();
+int tc_ctas_per_sm(const void* kern, size_t smem, int tcols);
 
 template <typename T>
 struct DevBuf {
@@ -108,6 +143,9 @@ struct gnpc_csr_s {
   gnpc_impl::DevBuf<float> v;
   int n_long = 0;
   int max_row = 0;
+  // long-row chunk plan (kChunk nonzeros per warp)
+  gnpc_impl::DevBuf<int> ch_row, ch_k0, ch_k1, long_c0;
+  int n_chunks = 0;
   std::unique_ptr<gnpc_csr_s> tr;  // Âᵀ (lazy, for training backward)
   std::unique_ptr<gnpc_impl::KrylovWs> kws;
   void upload();

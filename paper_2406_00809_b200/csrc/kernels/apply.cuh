@@ -20,9 +20,55 @@ struct NetView {
   const float* dec1_b;  // [hidden]
   const float* dec2;    // [hidden]
   float dec2_b;
+  const float* dec2_bp;  // the same value in device memory (training reads it)
   int hidden;
   int layers;
+  // Exact piecewise-linear form of the lift v -> enc2ᵀ relu(v enc1 + b1) + b2:
+  // nbreak sorted kinks t_k = -b1_h/enc1_h; on interval k (#kinks <= v),
+  // x1 = lift_a[k] * v + lift_b[k]   ([nbreak+1][DP] each, built in f64).
+  const float* lift_t;
+  const float* lift_a;
+  const float* lift_b;
+  int nbreak;
 };
+
+// ------------------------------------------------------------------ lift (piecewise)
+// Same map as k_lift: per row one binary search over <= hidden kinks, then
+// DP FMAs (the H x DP MLP collapses because its input is a scalar).
+template <int DP, typename T>
+__global__ void __launch_bounds__(kThreads)
+k_lift_pw(const T* __restrict__ in, int n, NetView net, const ApplyScalars* __restrict__ sc,
+          float* __restrict__ X, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  if (sc->zero) return;
+  constexpr int G = DP / 4, NG = kThreads / G;
+  extern __shared__ float4 sm4[];
+  const int nb = net.nbreak;
+  float* s_a = reinterpret_cast<float*>(sm4);  // [nb+1][DP]
+  float* s_b = s_a + (nb + 1) * DP;            // [nb+1][DP]
+  float* s_t = s_b + (nb + 1) * DP;            // [nb]
+  for (int t = threadIdx.x; t < (nb + 1) * DP; t += kThreads) {
+    s_a[t] = net.lift_a[t];
+    s_b[t] = net.lift_b[t];
+  }
+  for (int t = threadIdx.x; t < nb; t += kThreads) s_t[t] = net.lift_t[t];
+  __syncthreads();
+  const int gl = threadIdx.x % G;
+  const double in_scale = sc->in_scale;
+  for (int row = blockIdx.x * NG + threadIdx.x / G; row < n; row += gridDim.x * NG) {
+    const float v = static_cast<float>(in_scale * static_cast<double>(in[row]));
+    int lo = 0, hi = nb;  // interval = #kinks <= v
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s_t[mid] <= v) lo = mid + 1;
+      else hi = mid;
+    }
+    const float4 al = *reinterpret_cast<const float4*>(s_a + lo * DP + 4 * gl);
+    const float4 be = *reinterpret_cast<const float4*>(s_b + lo * DP + 4 * gl);
+    st4(X + static_cast<size_t>(row) * DP + 4 * gl,
+        make_float4(fmaf(al.x, v, be.x), fmaf(al.y, v, be.y), fmaf(al.z, v, be.z), fmaf(al.w, v, be.w)));
+  }
+}
 
 // ------------------------------------------------------------------ τ = ||b||
 // Block partials in f64 + last-block finalisation in a fixed order, so the
@@ -124,6 +170,78 @@ k_long_ax(DevCsr a, const float* __restrict__ X, float* __restrict__ AXL,
     __syncthreads();
   }
   if (gid == 0) st4(AXL + static_cast<size_t>(i) * DP + 4 * gl, red[threadIdx.x]);
+}
+
+// Long rows, load-balanced: every long row is cut into chunks of <= kChunk
+// nonzeros; one warp per chunk (32/G groups striding the chunk, shuffle tree
+// across groups) writes a partial (ÂX) row, then k_long_combine sums each
+// row's partials in chunk order (deterministic) into AXL.
+constexpr int kChunk = 128;
+
+struct LongPlan {
+  int nchunks;
+  const int* chunk_row;   // [nchunks]
+  const int* chunk_k0;    // [nchunks]
+  const int* chunk_k1;    // [nchunks]
+  int nrows;
+  const int* rows;        // [nrows] long rows
+  const int* row_c0;      // [nrows + 1] chunk range of each long row
+  float* partial;         // [nchunks][DP]
+};
+
+template <int DP>
+__global__ void __launch_bounds__(kThreads)
+k_long_chunks(DevCsr a, LongPlan lp, const float* __restrict__ X,
+              const ApplyScalars* __restrict__ sc, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  if (sc && sc->zero) return;
+  constexpr int G = DP / 4, NGW = 32 / G;  // groups per warp
+  const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= lp.nchunks) return;
+  const int k0 = lp.chunk_k0[c], k1 = lp.chunk_k1[c];
+  float4 acc = f4zero();
+  int k = k0 + grp;
+  for (; k + 3 * NGW < k1; k += 4 * NGW) {
+    const int c0 = __ldg(a.ci + k), c1 = __ldg(a.ci + k + NGW);
+    const int c2 = __ldg(a.ci + k + 2 * NGW), c3 = __ldg(a.ci + k + 3 * NGW);
+    const float v0 = __ldg(a.v + k), v1 = __ldg(a.v + k + NGW);
+    const float v2 = __ldg(a.v + k + 2 * NGW), v3 = __ldg(a.v + k + 3 * NGW);
+    const float4 x0 = ldg4(X + static_cast<size_t>(c0) * DP + 4 * gl);
+    const float4 x1 = ldg4(X + static_cast<size_t>(c1) * DP + 4 * gl);
+    const float4 x2 = ldg4(X + static_cast<size_t>(c2) * DP + 4 * gl);
+    const float4 x3 = ldg4(X + static_cast<size_t>(c3) * DP + 4 * gl);
+    fma4(acc, v0, x0);
+    fma4(acc, v1, x1);
+    fma4(acc, v2, x2);
+    fma4(acc, v3, x3);
+  }
+  for (; k < k1; k += NGW)
+    fma4(acc, __ldg(a.v + k), ldg4(X + static_cast<size_t>(__ldg(a.ci + k)) * DP + 4 * gl));
+#pragma unroll
+  for (int o = G; o < 32; o <<= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+    acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+  }
+  if (grp == 0) st4(lp.partial + static_cast<size_t>(c) * DP + 4 * gl, acc);
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kThreads)
+k_long_combine(LongPlan lp, float* __restrict__ AXL, const ApplyScalars* __restrict__ sc,
+               const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  if (sc && sc->zero) return;
+  constexpr int G = DP / 4;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lr = t / G, gl = t % G;
+  if (lr >= lp.nrows) return;
+  float4 s = f4zero();
+  for (int c = lp.row_c0[lr]; c < lp.row_c0[lr + 1]; ++c)
+    s = add4(s, ldg4(lp.partial + static_cast<size_t>(c) * DP + 4 * gl));
+  st4(AXL + static_cast<size_t>(lp.rows[lr]) * DP + 4 * gl, s);
 }
 
 // ------------------------------------------------------------------ fused layer

@@ -45,7 +45,7 @@ struct TcCfg {
   static constexpr size_t B_FLOATS = (size_t)DP * K;
   static size_t smem_bytes(bool last, int hidden) {
     size_t f = 2 * A_FLOATS + 2 * B_FLOATS + 2 * (size_t)RPS + 4 * (size_t)CAP;
-    if (last) f += (size_t)TM * SST + (size_t)DP * hidden + 2 * (size_t)hidden;
+    if (last) f += (size_t)TM * SST + (size_t)DP * hidden + 2 * (size_t)hidden + 2 * TM;
     return f * 4 + 64 + 1024;  // + mbarrier / tmem slot + 1024-B atom alignment
   }
 };
@@ -56,6 +56,7 @@ struct TcCfg {
 template <int DP, int R, int U, typename LD>
 __device__ __forceinline__ void gather_rounds(const float* __restrict__ X, LD load,
                                               int (&pos)[R], const int (&end)[R],
+                                              const int (&kk)[R], int bs,
                                               float4 (&acc)[R], int gl) {
   while (true) {
     bool more = false;
@@ -81,7 +82,9 @@ __device__ __forceinline__ void gather_rounds(const float* __restrict__ X, LD lo
     for (int j = 0; j < R; ++j)
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        x[j][u] = c[j][u] >= 0 ? ldg4(X + static_cast<size_t>(c[j][u]) * DP + 4 * gl) : f4zero();
+        x[j][u] = c[j][u] >= 0
+                      ? ldg4(X + (static_cast<size_t>(c[j][u]) * bs + kk[j]) * DP + 4 * gl)
+                      : f4zero();
 #pragma unroll
     for (int j = 0; j < R; ++j) {
 #pragma unroll
@@ -91,24 +94,46 @@ __device__ __forceinline__ void gather_rounds(const float* __restrict__ X, LD lo
   }
 }
 
-template <int DP, bool LAST, typename OutT>
-__global__ void __launch_bounds__(kThreads)
-k_layer_tc(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
-           const float* __restrict__ uwtc, const float* __restrict__ axlong, NetView net,
-           const ApplyScalars* __restrict__ sc, OutT* __restrict__ out,
-           const int* __restrict__ skip) {
+// Epilogue modes: relu (forward layer), LAST (forward layer + projection MLP),
+// MASK (backward: D ⊙ [mask > 0], identity when mask == nullptr).
+enum { kEpiRelu = 0, kEpiLast = 1, kEpiMask = 2 };
+
+// Virtual rows: the GEMM row v = node * bs + k (bs = batch samples resident
+// per node, 1 for an apply); a row gathers X rows (col * bs + k) of the
+// neighbours of `node`, so one Â row serves all bs samples of the batch.
+struct LayerIO {
+  const float* X;      // [nodes * bs][DP]
+  float* Y;            // [nodes * bs][DP]
+  const float* uwtc;   // this layer's pre-split swizzled B operand
+  const float* axlong; // bs == 1 only: (ÂX) of long rows
+  float* axout;        // optional: (ÂX) rows written out (training forward)
+  const float* mask;   // kEpiMask: multiply by [mask > 0]
+  int bs;
+};
+
+template <int DP, int MODE, typename OutT>
+__global__ void __launch_bounds__(kThreads, 2)
+k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ sc,
+           OutT* __restrict__ out, const int* __restrict__ skip) {
   using C = TcCfg<DP>;
+  constexpr bool LAST = MODE == kEpiLast;
   constexpr int TM = C::TM, KC = C::KC, KS = C::KS, G = C::G, NG = C::NG, R = C::R;
   constexpr int U = C::U, CAP = C::CAP, CPT = C::CPT, RPS = C::RPS;
   if (skip && *skip) return;
-  const int ntiles = (a.n + TM - 1) / TM;
-  if (sc->zero) {
+  const float* __restrict__ X = io.X;
+  float* __restrict__ Y = io.Y;
+  const float* __restrict__ axlong = io.axlong;
+  const int bs = io.bs;
+  const int nv = a.n * bs;  // virtual rows
+  const int ntiles = (nv + TM - 1) / TM;
+  if (sc && sc->zero) {
     if constexpr (LAST) {
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x)
         out[i] = OutT(0);
     }
     return;
   }
+  (void)KC;
   // Swizzle atoms need 1024-B alignment in the shared window; pointers are
   // derived from the __shared__ array so they stay in the shared state space.
   extern __shared__ float4 smem_raw[];
@@ -123,12 +148,13 @@ k_layer_tc(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
   float* D1 = Stg + (LAST ? TM * C::SST : 0);              // LAST: [DP][H]
   float* B1 = D1 + (LAST ? DP * net.hidden : 0);
   float* D2 = B1 + (LAST ? net.hidden : 0);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(D2 + (LAST ? net.hidden : 0) + 4);
+  float* Part = D2 + (LAST ? net.hidden : 0);              // LAST: [2][TM]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Part + (LAST ? 2 * TM : 0) + 4);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int t = tid; t < int(2 * C::B_FLOATS / 4); t += kThreads)
-    reinterpret_cast<float4*>(Bhi)[t] = reinterpret_cast<const float4*>(uwtc)[t];
+    reinterpret_cast<float4*>(Bhi)[t] = reinterpret_cast<const float4*>(io.uwtc)[t];
   if constexpr (LAST) {
     const int H = net.hidden;
     for (int t = tid; t < DP * H; t += kThreads) D1[t] = net.dec1[t];
@@ -143,7 +169,7 @@ k_layer_tc(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
   // ---- staging of a tile's row_ptr slice + (col, val) range (two halves so
   //      the loads can be issued early and the smem stores done late)
   struct Stage {
-    int rp;            // row_ptr[row0 + tid] (tid <= TM)
+    int rp;            // row_ptr[n0 + tid] for the tile's nodes n0..n1
     int kb, ke;        // the tile's nonzero range
     int c[CPT];
     float v[CPT];
@@ -151,9 +177,10 @@ k_layer_tc(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
   auto stage_rp = [&](int tile, Stage& s) {
     if (tile >= ntiles) return;
     const int row0 = tile * TM;
-    if (tid <= TM) s.rp = __ldg(a.rp + min(row0 + tid, a.n));
-    s.kb = __ldg(a.rp + row0);
-    s.ke = __ldg(a.rp + min(row0 + TM, a.n));
+    const int n0 = row0 / bs, n1 = min((row0 + TM - 1) / bs + 1, a.n);
+    if (tid <= TM) s.rp = __ldg(a.rp + min(n0 + tid, n1));
+    s.kb = __ldg(a.rp + n0);
+    s.ke = __ldg(a.rp + n1);
   };
   auto stage_cv = [&](int tile, Stage& s) {
     if (tile >= ntiles || s.ke - s.kb > CAP) return;
@@ -169,6 +196,10 @@ k_layer_tc(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
   auto stage_store = [&](int tile, const Stage& s, int slot) {
     if (tile >= ntiles) return;
     if (tid <= TM) s_rp[slot * RPS + tid] = s.rp;
+    if (tid == 0) {
+      s_rp[slot * RPS + TM + 2] = s.kb;
+      s_rp[slot * RPS + TM + 3] = s.ke;
+    }
     if (s.ke - s.kb > CAP) return;
 #pragma unroll
     for (int q = 0; q < CPT; ++q) {
@@ -213,12 +244,29 @@ k_layer_tc(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
     } else {
       tc::tmem_ld16(taddr, v);
     }
-    if constexpr (!LAST) {
-      if (i < a.n) {
+    if constexpr (MODE == kEpiRelu) {
+      if (i < nv) {
         float* yrow = Y + static_cast<size_t>(i) * DP + half * HC;
 #pragma unroll
         for (int c = 0; c < HC; c += 4)
           st4(yrow + c, make_float4(relu(v[c]), relu(v[c + 1]), relu(v[c + 2]), relu(v[c + 3])));
+      }
+    } else if constexpr (MODE == kEpiMask) {
+      if (i < nv) {
+        float* yrow = Y + static_cast<size_t>(i) * DP + half * HC;
+        const float* mrow = io.mask ? io.mask + static_cast<size_t>(i) * DP + half * HC : nullptr;
+#pragma unroll
+        for (int c = 0; c < HC; c += 4) {
+          float4 o = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+          if (mrow) {
+            const float4 mk = ldg4(mrow + c);
+            o.x = mk.x > 0.f ? o.x : 0.f;
+            o.y = mk.y > 0.f ? o.y : 0.f;
+            o.z = mk.z > 0.f ? o.z : 0.f;
+            o.w = mk.w > 0.f ? o.w : 0.f;
+          }
+          st4(yrow + c, o);
+        }
       }
     } else {
 #pragma unroll
@@ -229,28 +277,43 @@ k_layer_tc(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
     tc::fence_before();
   };
   // LAST: projection MLP of the staged tile (after a barrier)
+  // two threads per row, each owning half of the hidden units; dec1 read as
+  // warp-uniform float4 broadcasts (4 hidden units per smem wavefront)
   auto project = [&](int row0) {
     if constexpr (LAST) {
       const int H = net.hidden;
-      const double out_scale = sc->out_scale;
+      const int r = tid % TM, part = tid / TM;
+      const int h0 = part * (H / 2), h1 = part ? H : H / 2;
+      float y[DP];
+#pragma unroll
+      for (int j = 0; j < DP; j += 4) {
+        const float4 t = *reinterpret_cast<const float4*>(Stg + r * C::SST + j);
+        y[j] = t.x; y[j + 1] = t.y; y[j + 2] = t.z; y[j + 3] = t.w;
+      }
+      float o = 0.f;
+      int h = h0;
+      for (; (H & 7) == 0 && h + 4 <= h1; h += 4) {  // float4-aligned dec1 columns
+        float4 t = f4zero();
+#pragma unroll
+        for (int j = 0; j < DP; ++j) fma4(t, y[j], *reinterpret_cast<const float4*>(D1 + j * H + h));
+        o = fmaf(relu(t.x + B1[h]), D2[h], o);
+        o = fmaf(relu(t.y + B1[h + 1]), D2[h + 1], o);
+        o = fmaf(relu(t.z + B1[h + 2]), D2[h + 2], o);
+        o = fmaf(relu(t.w + B1[h + 3]), D2[h + 3], o);
+      }
+      for (; h < h1; ++h) {
+        float t = 0.f;
+#pragma unroll
+        for (int j = 0; j < DP; ++j) t = fmaf(y[j], D1[j * H + h], t);
+        o = fmaf(relu(t + B1[h]), D2[h], o);
+      }
+      Part[part * TM + r] = o;
+      __syncthreads();
       if (tid < TM) {
         const int i = row0 + tid;
-        if (i < a.n) {
-          float y[DP];
-#pragma unroll
-          for (int j = 0; j < DP; j += 4) {
-            const float4 t = *reinterpret_cast<const float4*>(Stg + tid * C::SST + j);
-            y[j] = t.x; y[j + 1] = t.y; y[j + 2] = t.z; y[j + 3] = t.w;
-          }
-          float o = 0.f;
-          for (int h = 0; h < H; ++h) {
-            float t = 0.f;
-#pragma unroll
-            for (int j = 0; j < DP; ++j) t = fmaf(y[j], D1[j * H + h], t);
-            o = fmaf(relu(t + B1[h]), D2[h], o);
-          }
-          out[i] = static_cast<OutT>(static_cast<double>(o + net.dec2_b) * out_scale);
-        }
+        if (i < a.n)
+          out[i] = static_cast<OutT>(static_cast<double>(Part[tid] + Part[TM + tid] + net.dec2_b) *
+                                     sc->out_scale);
       }
     }
   };
@@ -263,17 +326,20 @@ k_layer_tc(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
 
     // ---------------------------------------------------------------- gather
     const int* rp = s_rp + slot * RPS;
-    const int kb = rp[0], ke = rp[TM];
+    const int kb = rp[TM + 2], ke = rp[TM + 3];
     const bool staged = ke - kb <= CAP;
+    const int n0 = row0 / bs;
     float4 acc[R], xs[R];
     {
-      int pos[R], end[R];
+      int pos[R], end[R], kk[R];
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         const int r = gid + j * NG;
-        const int i = row0 + r;
-        const int s = rp[r], e = rp[r + 1];
-        const bool valid = i < a.n;
+        const int i = row0 + r;  // virtual row
+        const bool valid = i < nv;
+        const int node = valid ? i / bs : n0;
+        kk[j] = i - node * bs;
+        const int s = rp[node - n0], e = rp[node - n0 + 1];
         const bool longrow = axlong != nullptr && e - s > kLongRow;
         pos[j] = s;
         end[j] = (valid && !longrow) ? e : s;
@@ -294,7 +360,7 @@ k_layer_tc(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
               c = e.x;
               w = __int_as_float(e.y);
             },
-            pos, end, acc, gl);
+            pos, end, kk, bs, acc, gl);
       } else {
         gather_rounds<DP, R, U>(
             X,
@@ -302,7 +368,14 @@ k_layer_tc(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
               c = __ldg(a.ci + k);
               w = __ldg(a.v + k);
             },
-            pos, end, acc, gl);
+            pos, end, kk, bs, acc, gl);
+      }
+      if (io.axout != nullptr) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const int i = row0 + gid + j * NG;
+          if (i < nv) st4(io.axout + static_cast<size_t>(i) * DP + 4 * gl, acc[j]);
+        }
       }
     }
     stage_cv(next, sn);

@@ -1,0 +1,495 @@
+// Batched GNP training on sm_100a (src/gnn.cpp:208-451).
+//
+// A batch of B (b, x) pairs is resident as [n][B][·]: virtual row v = i*B + k
+// is sample k at node i, so every Â / Âᵀ row gather serves all B samples
+// (one 4 KiB contiguous block per neighbour at B = d = 32).  Forward layers
+// and the backward data-gradient layers run on k_layer_tc (tcgen05) for
+// d in {16, 32}, else on k_layer_batched below.  Weight gradients are
+// deterministic two-stage outer-product reductions over the n*B rows.
+#pragma once
+
+#include "apply.cuh"
+
+namespace gnpk {
+
+struct SampleScales {
+  double in_scale;   // sqrt(n)/tau_k
+  double out_scale;  // tau_k/sqrt(n)
+  int zero;          // tau_k == 0: sample contributes M(b)=0 and no gradient
+  int pad;
+};
+
+// ------------------------------------------------------------------ tau_k
+// [n][B] f64 column norms: block partials [grid][B] then one block finishes
+// in fixed order (deterministic).  blockDim = 256, B <= 1024.
+__global__ void __launch_bounds__(kThreads)
+k_col_norm_partials(const double* __restrict__ b, int n, int B, double* __restrict__ partials) {
+  extern __shared__ double red[];  // [256]
+  for (int k0 = 0; k0 < B; k0 += 32) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int k = k0 + lane;
+    double s = 0.0;
+    if (k < B)
+      for (int i = blockIdx.x * 8 + w; i < n; i += gridDim.x * 8) {
+        const double x = b[static_cast<size_t>(i) * B + k];
+        s = fma(x, x, s);
+      }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (w == 0 && k < B) {
+      double t = 0.0;
+      for (int q = 0; q < 8; ++q) t += red[q * 32 + lane];
+      partials[static_cast<size_t>(blockIdx.x) * B + k] = t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_col_norm_finish(const double* __restrict__ partials, int nblk, int n, int B,
+                                  SampleScales* __restrict__ sc) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= B) return;
+  double t = 0.0;
+  for (int q = 0; q < nblk; ++q) t += partials[static_cast<size_t>(q) * B + k];
+  const double tau = sqrt(t), sn = sqrt(static_cast<double>(n));
+  sc[k].zero = tau == 0.0;
+  sc[k].in_scale = tau == 0.0 ? 0.0 : sn / tau;
+  sc[k].out_scale = tau / sn;
+}
+
+// ------------------------------------------------------------------ lift (batched)
+// X0[v] = enc2ᵀ relu(vv enc1 + enc1_b) + enc2_b, vv = (float)(in_scale_k b[v])
+// (src/gnn.cpp:138-157); also writes vv (needed by the encoder backward).
+template <int DP>
+__global__ void __launch_bounds__(kThreads)
+k_lift_batched(const double* __restrict__ b, int nv, int B, NetView net,
+               const SampleScales* __restrict__ sc, float* __restrict__ X0,
+               float* __restrict__ vv_out) {
+  constexpr int G = DP / 4, NG = kThreads / G;
+  extern __shared__ float4 sm4[];
+  const int H = net.hidden;
+  float* s_enc2 = reinterpret_cast<float*>(sm4);  // [H][DP]
+  float* s_enc1 = s_enc2 + H * DP;
+  float* s_b1 = s_enc1 + H;
+  for (int t = threadIdx.x; t < H * DP; t += kThreads) s_enc2[t] = net.enc2[t];
+  for (int t = threadIdx.x; t < H; t += kThreads) {
+    s_enc1[t] = net.enc1[t];
+    s_b1[t] = net.enc1_b[t];
+  }
+  __syncthreads();
+  const int gl = threadIdx.x % G;
+  const float4 b2 = ldg4(net.enc2_b + 4 * gl);
+  for (int v = blockIdx.x * NG + threadIdx.x / G; v < nv; v += gridDim.x * NG) {
+    const int k = v % B;
+    const float x = static_cast<float>(sc[k].in_scale * b[v]);
+    if (gl == 0) vv_out[v] = x;
+    float4 acc = f4zero();
+    for (int h = 0; h < H; ++h) {
+      const float t = relu(fmaf(x, s_enc1[h], s_b1[h]));
+      fma4(acc, t, *reinterpret_cast<const float4*>(s_enc2 + h * DP + 4 * gl));
+    }
+    st4(X0 + static_cast<size_t>(v) * DP + 4 * gl, add4(acc, b2));
+  }
+}
+
+// ------------------------------------------------------------------ generic batched layer
+// CUDA-core layer for widths without a tcgen05 path (small test dims):
+// Y = epi([X | ÂX] · Bt) with Bt[j][k] (k < 2DP) in smem; one thread per
+// output element, the row's [x | ax] staged in smem.  MODE as k_layer_tc.
+template <int DP, int MODE>
+__global__ void __launch_bounds__(kThreads)
+k_layer_batched(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
+                const float* __restrict__ bt /*[DP][2DP] = B operand, row j*/,
+                float* __restrict__ axout, const float* __restrict__ mask, int bs) {
+  constexpr int RPB = kThreads / DP;  // virtual rows per block iteration
+  __shared__ float s_bt[DP * 2 * DP];
+  __shared__ float s_row[RPB][2 * DP];
+  for (int t = threadIdx.x; t < DP * 2 * DP; t += kThreads) s_bt[t] = bt[t];
+  __syncthreads();
+  const int nv = a.n * bs;
+  const int rl = threadIdx.x / DP, j = threadIdx.x % DP;
+  for (int v0 = blockIdx.x * RPB; v0 < nv; v0 += gridDim.x * RPB) {
+    const int v = v0 + rl;
+    if (v < nv) {
+      const int node = v / bs, kk = v - node * bs;
+      float ax = 0.f;
+      for (int q = a.rp[node]; q < a.rp[node + 1]; ++q)
+        ax = fmaf(a.v[q], X[(static_cast<size_t>(a.ci[q]) * bs + kk) * DP + j], ax);
+      s_row[rl][j] = X[static_cast<size_t>(v) * DP + j];
+      s_row[rl][DP + j] = ax;
+      if (axout) axout[static_cast<size_t>(v) * DP + j] = ax;
+    }
+    __syncthreads();
+    if (v < nv) {
+      float y = 0.f;
+      for (int k = 0; k < 2 * DP; ++k) y = fmaf(s_row[rl][k], s_bt[j * 2 * DP + k], y);
+      if (MODE == 0) y = relu(y);
+      else if (mask && !(mask[static_cast<size_t>(v) * DP + j] > 0.f)) y = 0.f;
+      Y[static_cast<size_t>(v) * DP + j] = y;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ decoder
+// out[v] = (dec2 · relu(dec1ᵀ x_L + dec1_b) + dec2_b) * out_scale_k (f64 store)
+// (src/gnn.cpp:178-199).  One thread per virtual row, dec1 in smem.
+template <int DP>
+__global__ void __launch_bounds__(kThreads)
+k_decoder_fwd(const float* __restrict__ XL, int nv, int B, NetView net,
+              const SampleScales* __restrict__ sc, double* __restrict__ out) {
+  extern __shared__ float4 sm4[];
+  const int H = net.hidden;
+  float* D1 = reinterpret_cast<float*>(sm4);  // [DP][H]
+  float* B1 = D1 + DP * H;
+  float* D2 = B1 + H;
+  for (int t = threadIdx.x; t < DP * H; t += kThreads) D1[t] = net.dec1[t];
+  for (int t = threadIdx.x; t < H; t += kThreads) {
+    B1[t] = net.dec1_b[t];
+    D2[t] = net.dec2[t];
+  }
+  __syncthreads();
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    const int k = v % B;
+    if (sc[k].zero) {
+      out[v] = 0.0;
+      continue;
+    }
+    float y[DP];
+#pragma unroll
+    for (int j = 0; j < DP; j += 4) {
+      const float4 t = ldg4(XL + static_cast<size_t>(v) * DP + j);
+      y[j] = t.x; y[j + 1] = t.y; y[j + 2] = t.z; y[j + 3] = t.w;
+    }
+    float o = 0.f;
+    for (int h = 0; h < H; ++h) {
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < DP; ++j) t = fmaf(y[j], D1[j * H + h], t);
+      o = fmaf(relu(t + B1[h]), D2[h], o);
+    }
+    out[v] = static_cast<double>(o + *net.dec2_bp) * sc[k].out_scale;
+  }
+}
+
+// Decoder backward (src/gnn.cpp:219-256) for one virtual row:
+//   gy = gout[v] * out_scale_k (0 for a zero sample)
+//   stage 0: post[v][h] = relu(dec_pre_h), gy[v]      (for dec2 / dec2_b grads)
+//   stage 1: gdp[v][h] = [dec_pre_h > 0] gy dec2_h      (for dec1 / dec1_b grads)
+//            gpre[v][j] = [x_L > 0] Σ_h gdp_h dec1(j,h)  (mask of the last layer)
+template <int DP>
+__global__ void __launch_bounds__(kThreads)
+k_decoder_bwd(const float* __restrict__ XL, int nv, int B, NetView net,
+              const SampleScales* __restrict__ sc, const double* __restrict__ gout,
+              float* __restrict__ post, float* __restrict__ gyv, float* __restrict__ gdp,
+              float* __restrict__ gpre) {
+  extern __shared__ float4 sm4[];
+  const int H = net.hidden;
+  float* D1 = reinterpret_cast<float*>(sm4);  // [DP][H]
+  float* B1 = D1 + DP * H;
+  float* D2 = B1 + H;
+  for (int t = threadIdx.x; t < DP * H; t += kThreads) D1[t] = net.dec1[t];
+  for (int t = threadIdx.x; t < H; t += kThreads) {
+    B1[t] = net.dec1_b[t];
+    D2[t] = net.dec2[t];
+  }
+  __syncthreads();
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    const int k = v % B;
+    const float gy = sc[k].zero ? 0.f : static_cast<float>(gout[v] * sc[k].out_scale);
+    gyv[v] = gy;
+    float y[DP], gx[DP];
+#pragma unroll
+    for (int j = 0; j < DP; j += 4) {
+      const float4 t = ldg4(XL + static_cast<size_t>(v) * DP + j);
+      y[j] = t.x; y[j + 1] = t.y; y[j + 2] = t.z; y[j + 3] = t.w;
+    }
+#pragma unroll
+    for (int j = 0; j < DP; ++j) gx[j] = 0.f;
+    for (int h = 0; h < H; ++h) {
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < DP; ++j) t = fmaf(y[j], D1[j * H + h], t);
+      const float pre = t + B1[h];
+      post[static_cast<size_t>(v) * H + h] = relu(pre);
+      const float g = pre > 0.f ? gy * D2[h] : 0.f;
+      gdp[static_cast<size_t>(v) * H + h] = g;
+#pragma unroll
+      for (int j = 0; j < DP; ++j) gx[j] = fmaf(g, D1[j * H + h], gx[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < DP; ++j) gpre[static_cast<size_t>(v) * DP + j] = y[j] > 0.f ? gx[j] : 0.f;
+  }
+}
+
+// Encoder backward (src/gnn.cpp:283-305) for one virtual row: recompute
+// x0 = relu(vv enc1 + b1), g_x0 = enc2 gX0, gp0 = [pre0 > 0] g_x0.
+template <int DP>
+__global__ void __launch_bounds__(kThreads)
+k_encoder_bwd(const float* __restrict__ vv, const float* __restrict__ gx0, int nv, NetView net,
+              float* __restrict__ x0, float* __restrict__ gp0) {
+  extern __shared__ float4 sm4[];
+  const int H = net.hidden;
+  float* s_enc2 = reinterpret_cast<float*>(sm4);  // [H][DP]
+  float* s_enc1 = s_enc2 + H * DP;
+  float* s_b1 = s_enc1 + H;
+  for (int t = threadIdx.x; t < H * DP; t += kThreads) s_enc2[t] = net.enc2[t];
+  for (int t = threadIdx.x; t < H; t += kThreads) {
+    s_enc1[t] = net.enc1[t];
+    s_b1[t] = net.enc1_b[t];
+  }
+  __syncthreads();
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    float g[DP];
+#pragma unroll
+    for (int j = 0; j < DP; j += 4) {
+      const float4 t = ldg4(gx0 + static_cast<size_t>(v) * DP + j);
+      g[j] = t.x; g[j + 1] = t.y; g[j + 2] = t.z; g[j + 3] = t.w;
+    }
+    const float x = vv[v];
+    for (int h = 0; h < H; ++h) {
+      const float pre = fmaf(x, s_enc1[h], s_b1[h]);
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < DP; ++j) t = fmaf(g[j], s_enc2[h * DP + j], t);
+      x0[static_cast<size_t>(v) * H + h] = relu(pre);
+      gp0[static_cast<size_t>(v) * H + h] = pre > 0.f ? t : 0.f;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ L1 loss
+// r = A (out - x) per sample (src/gnn.cpp:319-328), f64; loss partials per
+// block; sgn = sign(r).  One warp per node row, lanes over samples.
+__global__ void __launch_bounds__(kThreads)
+k_loss_residual(DevCsr a, int B, const double* __restrict__ out, const double* __restrict__ x,
+                double* __restrict__ sgn, double* __restrict__ partials) {
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  double acc = 0.0;
+  for (int i = wg; i < a.n; i += nw) {
+    for (int k = lane; k < B; k += 32) {
+      double r = 0.0;
+      for (int q = a.rp[i]; q < a.rp[i + 1]; ++q) {
+        const size_t j = static_cast<size_t>(a.ci[q]) * B + k;
+        r = fma(static_cast<double>(a.v[q]), out[j] - x[j], r);
+      }
+      acc += fabs(r);
+      sgn[static_cast<size_t>(i) * B + k] = r > 0.0 ? 1.0 : (r < 0.0 ? -1.0 : 0.0);
+    }
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
+// gout = (1/B) Âᵀ sgn (src/gnn.cpp:329-331) with the explicit transpose CSR.
+__global__ void __launch_bounds__(kThreads)
+k_loss_grad(DevCsr at, int B, const double* __restrict__ sgn, double* __restrict__ gout) {
+  const int lane = threadIdx.x & 31;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const double inv = 1.0 / static_cast<double>(B);
+  for (int i = wg; i < at.n; i += nw)
+    for (int k = lane; k < B; k += 32) {
+      double g = 0.0;
+      for (int q = at.rp[i]; q < at.rp[i + 1]; ++q)
+        g = fma(static_cast<double>(at.v[q]), sgn[static_cast<size_t>(at.ci[q]) * B + k], g);
+      gout[static_cast<size_t>(i) * B + k] = inv * g;
+    }
+}
+
+// ------------------------------------------------------------------ outer-product sums
+// S[p][q] = Σ_v A[v][p] B[v][q] (weight / bias gradients, src/gnn.cpp:240,265-266,
+// 284 gemm_tn and the bias column sums): A = [A1 | A2 | ones?] (P cols, padded
+// to P4 = P rounded up to 4), B (Q cols, padded to Q2).  Rows are split into
+// contiguous per-block ranges; each thread owns a 4 x 2 register block of S,
+// fp32 sums over 32-row smem tiles folded into f64 — per-block partials
+// [grid.x][P4*Q2] are then summed in block order (deterministic).
+struct OuterArgs {
+  const float* A1;
+  int P1, s1;
+  const float* A2;
+  int P2, s2;
+  int ones;  // append a column of ones to A (bias gradients)
+  const float* Bm;
+  int Q, sq;
+  int nv;
+  double* partials;
+};
+
+__host__ __device__ inline int outer_P4(const OuterArgs& o) { return (o.P1 + o.P2 + o.ones + 3) & ~3; }
+__host__ __device__ inline int outer_Q2(const OuterArgs& o) { return (o.Q + 1) & ~1; }
+
+__global__ void __launch_bounds__(kThreads) k_outer_sum(OuterArgs o) {
+  const int P = o.P1 + o.P2 + o.ones, P4 = outer_P4(o), Q2 = outer_Q2(o);
+  constexpr int RT = 32;  // rows per smem tile
+  extern __shared__ float4 sm4[];
+  float* sA = reinterpret_cast<float*>(sm4);  // [RT][P4]
+  float* sB = sA + RT * P4;                   // [RT][Q2]
+  const int nbq = Q2 / 2, nblocks = (P4 / 4) * nbq;
+  const int e = blockIdx.y * kThreads + threadIdx.x;
+  const bool active = e < nblocks;
+  const int p0 = active ? (e / nbq) * 4 : 0, q0 = active ? (e % nbq) * 2 : 0;
+  double acc[4][2] = {};
+  const int rows_per_blk = (o.nv + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * rows_per_blk, r1 = min(o.nv, r0 + rows_per_blk);
+  for (int t0 = r0; t0 < r1; t0 += RT) {
+    const int nr = min(RT, r1 - t0);
+    for (int t = threadIdx.x; t < RT * P4; t += kThreads) {
+      const int r = t / P4, p = t % P4;
+      float val = 0.f;
+      if (r < nr) {
+        if (p < o.P1) val = o.A1[static_cast<size_t>(t0 + r) * o.s1 + p];
+        else if (p < o.P1 + o.P2) val = o.A2[static_cast<size_t>(t0 + r) * o.s2 + (p - o.P1)];
+        else if (p < P) val = 1.f;
+      }
+      sA[t] = val;
+    }
+    for (int t = threadIdx.x; t < RT * Q2; t += kThreads) {
+      const int r = t / Q2, q = t % Q2;
+      sB[t] = (r < nr && q < o.Q) ? o.Bm[static_cast<size_t>(t0 + r) * o.sq + q] : 0.f;
+    }
+    __syncthreads();
+    if (active) {
+      float s[4][2] = {};
+      for (int r = 0; r < nr; ++r) {
+        const float4 av = *reinterpret_cast<const float4*>(sA + r * P4 + p0);
+        const float2 bv = *reinterpret_cast<const float2*>(sB + r * Q2 + q0);
+        s[0][0] = fmaf(av.x, bv.x, s[0][0]); s[0][1] = fmaf(av.x, bv.y, s[0][1]);
+        s[1][0] = fmaf(av.y, bv.x, s[1][0]); s[1][1] = fmaf(av.y, bv.y, s[1][1]);
+        s[2][0] = fmaf(av.z, bv.x, s[2][0]); s[2][1] = fmaf(av.z, bv.y, s[2][1]);
+        s[3][0] = fmaf(av.w, bv.x, s[3][0]); s[3][1] = fmaf(av.w, bv.y, s[3][1]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j] += static_cast<double>(s[i][j]);
+    }
+    __syncthreads();
+  }
+  if (active) {
+    double* dst = o.partials + static_cast<size_t>(blockIdx.x) * P4 * Q2;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) dst[(p0 + i) * Q2 + q0 + j] = acc[i][j];
+  }
+}
+
+// Sum the block partials in block order and scatter into the flat f64
+// gradient: grad[dst[p*Q2+q]] = Σ_blk partial (dst < 0: padding, dropped).
+__global__ void k_outer_finish(const double* __restrict__ partials, int nblk, int PQ,
+                               const int* __restrict__ dst, double* __restrict__ grad) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= PQ) return;
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += partials[static_cast<size_t>(b) * PQ + idx];
+  const int d = dst[idx];
+  if (d >= 0) grad[d] = s;
+}
+
+// ------------------------------------------------------------------ Adam
+// src/gnn.cpp:345-363 in f64 on the flat parameter vector.
+__global__ void k_adam(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m1,
+                       double* __restrict__ m2, int count, double lr, double bc1, double bc2) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+  const double gk = g[k];
+  m1[k] = beta1 * m1[k] + (1.0 - beta1) * gk;
+  m2[k] = beta2 * m2[k] + (1.0 - beta2) * gk * gk;
+  const double mhat = m1[k] / bc1;
+  const double vhat = m2[k] / bc2;
+  p[k] -= lr * mhat / (sqrt(vhat) + eps);
+}
+
+// ------------------------------------------------------------------ device param rebuild
+// From the flat f64 parameters (reference order) to the fp32 device layout
+// and the per-layer B operands: gather map src[dst] (index into flat, -1 = 0).
+__global__ void k_gather_params(const double* __restrict__ flat, const int* __restrict__ src,
+                                int count, float* __restrict__ dst) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const int s = src[k];
+  dst[k] = s >= 0 ? static_cast<float>(flat[s]) : 0.f;
+}
+
+// tcgen05 B operands (hi/lo, swizzled): dst[k] = split(flat[src[k]]),
+// part[k] = 0 (hi) or 1 (lo).
+__global__ void k_gather_split(const double* __restrict__ flat, const int* __restrict__ src,
+                               const unsigned char* __restrict__ part, int count,
+                               float* __restrict__ dst) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const int s = src[k];
+  const float v = s >= 0 ? static_cast<float>(flat[s]) : 0.f;
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  const float hi = __uint_as_float(r);
+  dst[k] = part[k] ? v - hi : hi;
+}
+
+// ------------------------------------------------------------------ data movement
+// n x B column-major (host TrainingBatch layout) -> [n][B] (device layout).
+__global__ void k_colmajor_to_nb(const double* __restrict__ src, int n, int B,
+                                 double* __restrict__ dst) {
+  const size_t t = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<size_t>(n) * B) return;
+  const int i = static_cast<int>(t / B), k = static_cast<int>(t % B);
+  dst[t] = src[static_cast<size_t>(k) * n + i];
+}
+__global__ void k_nb_to_colmajor(const double* __restrict__ src, int n, int B,
+                                 double* __restrict__ dst) {
+  const size_t t = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<size_t>(n) * B) return;
+  const int i = static_cast<int>(t / B), k = static_cast<int>(t % B);
+  dst[static_cast<size_t>(k) * n + i] = src[t];
+}
+
+// Throughput-mode pairs: x ~ N(0,1) from Philox4x32-10 keyed by (seed, step),
+// Box-Muller in fp32, stored f64 in [n][B]; b = A x follows via k_spmm_nb.
+__device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+__global__ void k_philox_normal(unsigned long long seed, unsigned long long step, size_t count,
+                                double* __restrict__ x) {
+  const size_t t = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (4 * t >= count) return;
+  const uint4 r = philox(make_uint4(static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32),
+                                    static_cast<uint32_t>(step), static_cast<uint32_t>(step >> 32)),
+                         make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)));
+  const float u[4] = {(r.x + 1.0f) * 2.3283064e-10f, r.y * 2.3283064e-10f,
+                      (r.z + 1.0f) * 2.3283064e-10f, r.w * 2.3283064e-10f};
+  const float rad0 = sqrtf(-2.f * logf(u[0])), rad1 = sqrtf(-2.f * logf(u[2]));
+  float s0, c0, s1, c1;
+  sincospif(2.f * u[1], &s0, &c0);
+  sincospif(2.f * u[3], &s1, &c1);
+  const float z[4] = {rad0 * c0, rad0 * s0, rad1 * c1, rad1 * s1};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (4 * t + q < count) x[4 * t + q] = z[q];
+}
+
+// y[i][k] = Σ_j a_ij x[j][k] for all B samples ([n][B] f64).
+__global__ void __launch_bounds__(kThreads)
+k_spmm_nb(DevCsr a, int B, const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = wg; i < a.n; i += nw)
+    for (int k = lane; k < B; k += 32) {
+      double s = 0.0;
+      for (int q = a.rp[i]; q < a.rp[i + 1]; ++q)
+        s = fma(static_cast<double>(a.v[q]), x[static_cast<size_t>(a.ci[q]) * B + k], s);
+      y[static_cast<size_t>(i) * B + k] = s;
+    }
+}
+
+}  // namespace gnpk

@@ -25,18 +25,25 @@ struct gnpc_model_s {
   int dp = 16;                 // d padded to a power of two >= 4 (zero weights)
   std::vector<double> params;  // reference layout, f64
   gnpc_impl::DevBuf<float> P;  // device fp32 params (NetView points into it)
+  gnpc_impl::DevBuf<float> LIFT;  // piecewise-linear lift tables (kinks, alpha, beta)
   gnpc_impl::DevBuf<float> UWTC;  // per layer [U;W]^T split tf32 hi/lo, tcgen05 layout
   bool use_tc = true;             // DP 16/32: tcgen05 transform (GNPC_NO_TC=1: CUDA cores)
   int tc_per_sm[4] = {0, 0, 0, 0};  // cached occupancy per (last, OutT) tcgen05 kernel
   gnpk::NetView view{};
   // apply workspace
-  gnpc_impl::DevBuf<float> X[2], AXL;
+  gnpc_impl::DevBuf<float> X[2], AXL, LPART;  // LPART: long-row chunk partials
   gnpc_impl::DevBuf<double> partials, io_in, io_out;
   gnpc_impl::DevBuf<unsigned> ticket;
   gnpc_impl::DevBuf<gnpk::ApplyScalars> sc;
   int sms = 0, norm_grid = 0;
   cudaStream_t stream = nullptr;
 
+  // flat-parameter index maps (see capi.cu build_maps)
+  std::vector<int> map_view, map_bt_fwd, map_bt_bwd, map_tc_fwd, map_tc_bwd;
+  std::vector<unsigned char> part_tc;
+  std::size_t o_enc1 = 0, o_enc1b = 0, o_enc2 = 0, o_enc2b = 0, o_uw = 0, o_dec1 = 0,
+              o_dec1b = 0, o_dec2 = 0, o_dec2b = 0;
+  void build_maps();
   void build_view();
   void ensure_workspace();
   template <typename InT, typename OutT>

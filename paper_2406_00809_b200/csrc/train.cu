@@ -1,21 +1,607 @@
-// Batched GNP training (placeholder until the training kernels land).
+// Batched GNP training: C ABI entry points (include/gnpc.h, "training").
+//
+// One step = forward over the B resident samples ([n][B][d] activations),
+// L1 residual loss and its Âᵀ gradient, backward through decoder / layers /
+// encoder, deterministic weight-gradient reductions, f64 Adam on the flat
+// parameter vector, then the fp32 device parameters and tcgen05 operands are
+// regenerated on the GPU from the f64 master copy.  Restates
+// src/gnn.cpp:208-451 (train_preconditioner's step body) with τ treated as a
+// constant of b (SPEC) exactly like the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
 #include "capi_common.hpp"
+#include "kernels/layer_tc.cuh"
+#include "kernels/train.cuh"
+#include "model.hpp"
+
+using namespace gnpc_impl;
+
+struct gnpc_trainer_s {
+  gnpc_model_s* m = nullptr;
+  std::unique_ptr<gnpc_csr_s> At;  // Âᵀ (explicit transpose, src/csr.cpp:108-125)
+  int B = 0, n = 0, nv = 0, dp = 0, d = 0, H = 0, L = 0;
+  double lr = 1e-3;
+  std::int64_t t = 0;
+  std::int64_t P = 0;
+  bool tc = false;
+  int sms = 0;
+  cudaStream_t s = nullptr;
+  // flat f64 master parameters, gradient, Adam moments
+  DevBuf<double> p64, g64, m1, m2;
+  // regeneration maps (see gnpc_model_s::build_maps)
+  DevBuf<int> map_view, map_bt_fwd, map_bt_bwd, map_tc_fwd, map_tc_bwd;
+  DevBuf<unsigned char> part_tc;
+  DevBuf<float> BT_fwd, BT_bwd, UWTC_bwd;
+  // batch
+  DevBuf<double> xb, bb, out, sgn, gout, colpart, losspart, tmp;
+  DevBuf<gnpk::SampleScales> scl;
+  // activations
+  DevBuf<float> Xs, AXs, G[2], vv, hb1, hb2, gyv;
+  // reductions
+  struct Red {
+    gnpk::OuterArgs o;
+    DevBuf<int> dst;
+    int P4 = 0, Q2 = 0;
+  };
+  Red red_layer[64], red_dec1, red_dec2, red_enc2, red_enc1;
+  DevBuf<double> opart;
+  int rowblk = 0;
+  int tc_per_sm_fwd = 0, tc_per_sm_bwd = 0;
+  int loss_grid = 0;
+  std::int64_t nbytes_act = 0;
+};
+
+namespace {
+
+constexpr int kTh = gnpk::kThreads;
+
+int grid_for(std::int64_t work, int per_block, int cap) {
+  return (int)std::max<std::int64_t>(1, std::min<std::int64_t>((work + per_block - 1) / per_block, cap));
+}
+
+void upload_i(DevBuf<int>& b, const std::vector<int>& v) {
+  if (!v.empty()) b.upload(v.data(), v.size());
+}
+
+// Build one reduction: A = [A1 | A2 | ones], B = Bm, dst map from (p, q).
+template <class F>
+void make_red(gnpc_trainer_s::Red& r, const float* A1, int P1, int s1, const float* A2, int P2,
+              int s2, int ones, const float* Bm, int Q, int sq, int nv, F dstfn) {
+  r.o = gnpk::OuterArgs{A1, P1, s1, A2, P2, s2, ones, Bm, Q, sq, nv, nullptr};
+  r.P4 = gnpk::outer_P4(r.o);
+  r.Q2 = gnpk::outer_Q2(r.o);
+  std::vector<int> dst((std::size_t)r.P4 * r.Q2, -1);
+  for (int p = 0; p < r.P4; ++p)
+    for (int q = 0; q < r.Q2; ++q) dst[(std::size_t)p * r.Q2 + q] = dstfn(p, q);
+  upload_i(r.dst, dst);
+}
+
+void run_red(gnpc_trainer_s& T, gnpc_trainer_s::Red& r) {
+  r.o.partials = T.opart.p;
+  const int nblocks = (r.P4 / 4) * (r.Q2 / 2);
+  dim3 grid(T.rowblk, (nblocks + kTh - 1) / kTh);
+  const size_t smem = (size_t)(32 * r.P4 + 32 * r.Q2) * 4;
+  gnpk::k_outer_sum<<<grid, kTh, smem, T.s>>>(r.o);
+  GNPC_LAUNCHED();
+  const int PQ = r.P4 * r.Q2;
+  gnpk::k_outer_finish<<<(PQ + kTh - 1) / kTh, kTh, 0, T.s>>>(T.opart.p, T.rowblk, PQ, r.dst.p,
+                                                              T.g64.p);
+  GNPC_LAUNCHED();
+}
+
+// fp32 device params + layer operands from the f64 master copy
+void regenerate(gnpc_trainer_s& T) {
+  gnpc_model_s& m = *T.m;
+  const int nview = (int)m.map_view.size();
+  gnpk::k_gather_params<<<(nview + kTh - 1) / kTh, kTh, 0, T.s>>>(T.p64.p, T.map_view.p, nview, m.P.p);
+  GNPC_LAUNCHED();
+  if (T.tc) {
+    const int c = (int)m.map_tc_fwd.size();
+    gnpk::k_gather_split<<<(c + kTh - 1) / kTh, kTh, 0, T.s>>>(T.p64.p, T.map_tc_fwd.p, T.part_tc.p, c,
+                                                               m.UWTC.p);
+    GNPC_LAUNCHED();
+    gnpk::k_gather_split<<<(c + kTh - 1) / kTh, kTh, 0, T.s>>>(T.p64.p, T.map_tc_bwd.p, T.part_tc.p, c,
+                                                               T.UWTC_bwd.p);
+    GNPC_LAUNCHED();
+  } else {
+    const int c = (int)m.map_bt_fwd.size();
+    gnpk::k_gather_params<<<(c + kTh - 1) / kTh, kTh, 0, T.s>>>(T.p64.p, T.map_bt_fwd.p, c, T.BT_fwd.p);
+    GNPC_LAUNCHED();
+    gnpk::k_gather_params<<<(c + kTh - 1) / kTh, kTh, 0, T.s>>>(T.p64.p, T.map_bt_bwd.p, c, T.BT_bwd.p);
+    GNPC_LAUNCHED();
+  }
+}
+
+template <int DP>
+struct TrainLaunch {
+  // one Res-GCONV layer over the B-sample batch: forward (relu, ÂX out) or
+  // backward data gradient (over Âᵀ, [Uᵀ; Wᵀ], mask by the layer input)
+  static void layer(gnpc_trainer_s& T, bool fwd, int l, const float* X, float* Y, float* axout,
+                    const float* mask) {
+    gnpc_csr_s& A = fwd ? *T.m->a : *T.At;
+    gnpk::DevCsr a = A.dev();
+    if constexpr (DP == 16 || DP == 32) {
+      if (T.tc) {
+        using C = gnpk::TcCfg<DP>;
+        const float* uw = (fwd ? T.m->UWTC.p : T.UWTC_bwd.p) + (size_t)l * 2 * C::B_FLOATS;
+        auto kern = fwd ? gnpk::k_layer_tc<DP, gnpk::kEpiRelu, float>
+                        : gnpk::k_layer_tc<DP, gnpk::kEpiMask, float>;
+        const size_t smem = C::smem_bytes(false, T.H);
+        int& per_sm = fwd ? T.tc_per_sm_fwd : T.tc_per_sm_bwd;
+        if (per_sm == 0) per_sm = tc_ctas_per_sm((const void*)kern, smem, C::TCOLS);
+        const int tiles = (T.nv + C::TM - 1) / C::TM;
+        const int grid = std::max(1, std::min(tiles, per_sm * T.sms));
+        gnpk::LayerIO io{X, Y, uw, nullptr, axout, mask, T.B};
+        kern<<<grid, kTh, smem, T.s>>>(a, io, T.m->view, nullptr, (float*)nullptr, nullptr);
+        GNPC_LAUNCHED();
+        return;
+      }
+    }
+    const float* bt = (fwd ? T.BT_fwd.p : T.BT_bwd.p) + (size_t)l * DP * 2 * DP;
+    const int grid = grid_for((std::int64_t)T.nv, kTh / DP, T.sms * 8);
+    if (fwd)
+      gnpk::k_layer_batched<DP, 0><<<grid, kTh, 0, T.s>>>(a, X, Y, bt, axout, mask, T.B);
+    else
+      gnpk::k_layer_batched<DP, 2><<<grid, kTh, 0, T.s>>>(a, X, Y, bt, axout, mask, T.B);
+    GNPC_LAUNCHED();
+  }
+
+  // forward: norms, lift, L layers, decoder -> out (f64 [n][B])
+  static void forward(gnpc_trainer_s& T) {
+    const gnpk::NetView& net = T.m->view;
+    const std::size_t act = (std::size_t)T.nv * DP;
+    const int cg = grid_for(T.n, 8, 1024);
+    gnpk::k_col_norm_partials<<<cg, kTh, kTh * sizeof(double), T.s>>>(T.bb.p, T.n, T.B, T.colpart.p);
+    GNPC_LAUNCHED();
+    gnpk::k_col_norm_finish<<<(T.B + 63) / 64, 64, 0, T.s>>>(T.colpart.p, cg, T.n, T.B, T.scl.p);
+    GNPC_LAUNCHED();
+    {
+      const size_t smem = (size_t)T.H * DP * 4 + 2 * (size_t)T.H * 4;
+      const int g = grid_for(T.nv, kTh / (DP / 4), T.sms * 8);
+      gnpk::k_lift_batched<DP><<<g, kTh, smem, T.s>>>(T.bb.p, T.nv, T.B, net, T.scl.p, T.Xs.p, T.vv.p);
+      GNPC_LAUNCHED();
+    }
+    for (int l = 0; l < T.L; ++l)
+      layer(T, true, l, T.Xs.p + l * act, T.Xs.p + (l + 1) * act, T.AXs.p + l * act, nullptr);
+    const size_t smem = ((size_t)DP * T.H + 2 * (size_t)T.H) * 4;
+    const int g = grid_for(T.nv, kTh, T.sms * 8);
+    gnpk::k_decoder_fwd<DP><<<g, kTh, smem, T.s>>>(T.Xs.p + T.L * act, T.nv, T.B, net, T.scl.p,
+                                                   T.out.p);
+    GNPC_LAUNCHED();
+  }
+
+  static void backward(gnpc_trainer_s& T) {
+    const gnpk::NetView& net = T.m->view;
+    const std::size_t act = (std::size_t)T.nv * DP;
+    GNPC_CUDA(cudaMemsetAsync(T.g64.p, 0, T.P * sizeof(double), T.s));
+    {
+      const size_t smem = ((size_t)DP * T.H + 2 * (size_t)T.H) * 4;
+      const int g = grid_for(T.nv, kTh, T.sms * 8);
+      gnpk::k_decoder_bwd<DP><<<g, kTh, smem, T.s>>>(T.Xs.p + T.L * act, T.nv, T.B, net, T.scl.p,
+                                                     T.gout.p, T.hb1.p, T.gyv.p, T.hb2.p, T.G[0].p);
+      GNPC_LAUNCHED();
+    }
+    run_red(T, T.red_dec2);
+    run_red(T, T.red_dec1);
+    int cur = 0;
+    for (int l = T.L - 1; l >= 0; --l) {
+      T.red_layer[l].o.Bm = T.G[cur].p;
+      run_red(T, T.red_layer[l]);
+      layer(T, false, l, T.G[cur].p, T.G[1 - cur].p, nullptr, l >= 1 ? T.Xs.p + l * act : nullptr);
+      cur = 1 - cur;
+    }
+    {
+      const size_t smem = (size_t)T.H * DP * 4 + 2 * (size_t)T.H * 4;
+      const int g = grid_for(T.nv, kTh, T.sms * 8);
+      gnpk::k_encoder_bwd<DP><<<g, kTh, smem, T.s>>>(T.vv.p, T.G[cur].p, T.nv, net, T.hb1.p, T.hb2.p);
+      GNPC_LAUNCHED();
+    }
+    T.red_enc2.o.Bm = T.G[cur].p;
+    run_red(T, T.red_enc2);
+    run_red(T, T.red_enc1);
+  }
+};
+
+template <class F>
+void dispatch(int dp, F&& f) {
+  switch (dp) {
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 8: f(std::integral_constant<int, 8>{}); break;
+    case 16: f(std::integral_constant<int, 16>{}); break;
+    case 32: f(std::integral_constant<int, 32>{}); break;
+    case 64: f(std::integral_constant<int, 64>{}); break;
+    default: throw Unsupported("unsupported width");
+  }
+}
+
+void forward(gnpc_trainer_s& T) {
+  dispatch(T.dp, [&](auto c) { TrainLaunch<decltype(c)::value>::forward(T); });
+}
+void backward(gnpc_trainer_s& T) {
+  dispatch(T.dp, [&](auto c) { TrainLaunch<decltype(c)::value>::backward(T); });
+}
+
+// loss over the batch (f64, src/gnn.cpp:309-335); also produces gout
+double loss_and_grad(gnpc_trainer_s& T, bool want_grad) {
+  gnpk::DevCsr a = T.m->a->dev();
+  gnpk::k_loss_residual<<<T.loss_grid, kTh, 0, T.s>>>(a, T.B, T.out.p, T.xb.p, T.sgn.p, T.losspart.p);
+  GNPC_LAUNCHED();
+  if (want_grad) {
+    gnpk::DevCsr at = T.At->dev();
+    gnpk::k_loss_grad<<<T.loss_grid, kTh, 0, T.s>>>(at, T.B, T.sgn.p, T.gout.p);
+    GNPC_LAUNCHED();
+  }
+  std::vector<double> part(T.loss_grid);
+  GNPC_CUDA(cudaMemcpyAsync(part.data(), T.losspart.p, part.size() * 8, cudaMemcpyDeviceToHost, T.s));
+  GNPC_CUDA(cudaStreamSynchronize(T.s));
+  double acc = 0.0;
+  for (double v : part) acc += v;
+  return acc / (double)T.B;
+}
+
+void adam(gnpc_trainer_s& T) {
+  T.t += 1;
+  const double bc1 = 1.0 - std::pow(0.9, (double)T.t);
+  const double bc2 = 1.0 - std::pow(0.999, (double)T.t);
+  gnpk::k_adam<<<(int)((T.P + kTh - 1) / kTh), kTh, 0, T.s>>>(T.p64.p, T.g64.p, T.m1.p, T.m2.p, (int)T.P,
+                                                              T.lr, bc1, bc2);
+  GNPC_LAUNCHED();
+  regenerate(T);
+}
+
+// host n x B column-major f64 -> device [n][B]
+void upload_batch(gnpc_trainer_s& T, const double* host, DevBuf<double>& dst) {
+  const std::size_t cnt = (std::size_t)T.n * T.B;
+  GNPC_CUDA(cudaMemcpyAsync(T.tmp.p, host, cnt * 8, cudaMemcpyHostToDevice, T.s));
+  gnpk::k_colmajor_to_nb<<<(int)((cnt + kTh - 1) / kTh), kTh, 0, T.s>>>(T.tmp.p, T.n, T.B, dst.p);
+  GNPC_LAUNCHED();
+}
+
+void sync_model_params(gnpc_trainer_s& T) {
+  GNPC_CUDA(cudaMemcpyAsync(T.m->params.data(), T.p64.p, T.P * 8, cudaMemcpyDeviceToHost, T.s));
+  GNPC_CUDA(cudaStreamSynchronize(T.s));
+  T.m->build_view();
+}
+
+void need(bool c, const char* msg) {
+  if (!c) throw std::invalid_argument(msg);
+}
+
+gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
+  need(m && batch >= 1, "trainer_create: bad arguments");
+  require_device();
+  auto T = std::make_unique<gnpc_trainer_s>();
+  T->m = m;
+  T->B = (int)batch;
+  T->lr = lr;
+  T->n = (int)m->a->h.n;
+  need(T->n >= 1, "trainer_create: empty matrix");
+  if ((std::int64_t)T->n * batch >= (std::int64_t(1) << 31))
+    throw Unsupported("trainer: n * batch must be < 2^31");
+  T->nv = T->n * T->B;
+  T->dp = m->dp;
+  T->d = (int)m->dims.d;
+  T->H = (int)m->dims.hidden;
+  T->L = (int)m->dims.layers;
+  if (T->L > 64) throw Unsupported("trainer: at most 64 layers");
+  T->P = (std::int64_t)m->params.size();
+  T->tc = m->use_tc;
+  T->sms = num_sms();
+  T->s = m->stream;
+  m->a->upload();
+  T->At = std::make_unique<gnpc_csr_s>();
+  T->At->h = gnp_b200::transpose(m->a->h);
+  T->At->upload();
+  // master params / Adam
+  T->p64.upload(m->params.data(), T->P, T->s);
+  T->g64.alloc(T->P);
+  T->m1.alloc(T->P);
+  T->m2.alloc(T->P);
+  GNPC_CUDA(cudaMemsetAsync(T->m1.p, 0, T->P * 8, T->s));
+  GNPC_CUDA(cudaMemsetAsync(T->m2.p, 0, T->P * 8, T->s));
+  m->build_maps();
+  upload_i(T->map_view, m->map_view);
+  if (T->tc) {
+    upload_i(T->map_tc_fwd, m->map_tc_fwd);
+    upload_i(T->map_tc_bwd, m->map_tc_bwd);
+    T->part_tc.upload(m->part_tc.data(), m->part_tc.size());
+    T->UWTC_bwd.alloc(m->map_tc_bwd.size());
+  } else {
+    upload_i(T->map_bt_fwd, m->map_bt_fwd);
+    upload_i(T->map_bt_bwd, m->map_bt_bwd);
+    T->BT_fwd.alloc(m->map_bt_fwd.size());
+    T->BT_bwd.alloc(m->map_bt_bwd.size());
+  }
+  // batch + activations
+  const std::size_t nvs = (std::size_t)T->nv, act = nvs * T->dp;
+  T->xb.alloc(nvs);
+  T->bb.alloc(nvs);
+  T->out.alloc(nvs);
+  T->sgn.alloc(nvs);
+  T->gout.alloc(nvs);
+  T->tmp.alloc(nvs);
+  T->colpart.alloc((std::size_t)1024 * T->B);
+  T->scl.alloc(T->B);
+  T->loss_grid = grid_for((std::int64_t)T->n * 32, kTh, T->sms * 8);
+  T->losspart.alloc(T->loss_grid);
+  T->Xs.alloc(act * (T->L + 1));
+  T->AXs.alloc(act * T->L);
+  T->G[0].alloc(act);
+  T->G[1].alloc(act);
+  T->vv.alloc(nvs);
+  T->hb1.alloc(nvs * T->H);
+  T->hb2.alloc(nvs * T->H);
+  T->gyv.alloc(nvs);
+  T->nbytes_act = (std::int64_t)(act * (2 * T->L + 3) + nvs * (2 * T->H + 2)) * 4;
+  // reductions (destinations in the flat reference layout)
+  const gnp_b200::ParamLayout lay = gnp_b200::param_layout(m->dims);
+  const int d = T->d, H = T->H, dp = T->dp;
+  T->rowblk = std::max(1, std::min(2 * T->sms, (T->nv + 255) / 256));
+  int maxpq = 0;
+  for (int l = 0; l < T->L; ++l) {
+    make_red(T->red_layer[l], T->Xs.p + l * act, dp, dp, T->AXs.p + l * act, dp, dp, 0, nullptr, dp, dp,
+             T->nv, [&](int p, int q) -> int {
+               if (q >= d) return -1;
+               if (p < d) return (int)(lay.u[l] + (std::int64_t)q * d + p);           // U(k=p, j=q)
+               if (p >= dp && p - dp < d) return (int)(lay.w[l] + (std::int64_t)q * d + (p - dp));
+               return -1;
+             });
+    maxpq = std::max(maxpq, T->red_layer[l].P4 * T->red_layer[l].Q2);
+  }
+  make_red(T->red_dec1, T->Xs.p + T->L * act, dp, dp, nullptr, 0, 0, 1, T->hb2.p, H, H, T->nv,
+           [&](int p, int q) -> int {
+             if (q >= H) return -1;
+             if (p < d) return (int)(lay.dec1 + (std::int64_t)q * d + p);  // dec1(j=p, h=q)
+             if (p == dp) return (int)(lay.dec1_b + q);
+             return -1;
+           });
+  make_red(T->red_dec2, T->hb1.p, H, H, nullptr, 0, 0, 1, T->gyv.p, 1, 1, T->nv,
+           [&](int p, int q) -> int {
+             if (q != 0) return -1;
+             if (p < H) return (int)(lay.dec2 + p);
+             if (p == H) return (int)lay.dec2_b;
+             return -1;
+           });
+  make_red(T->red_enc2, T->hb1.p, H, H, nullptr, 0, 0, 1, nullptr, dp, dp, T->nv,
+           [&](int p, int q) -> int {
+             if (q >= d) return -1;
+             if (p < H) return (int)(lay.enc2 + (std::int64_t)q * H + p);  // enc2(h=p, j=q)
+             if (p == H) return (int)(lay.enc2_b + q);
+             return -1;
+           });
+  make_red(T->red_enc1, T->vv.p, 1, 1, nullptr, 0, 0, 1, T->hb2.p, H, H, T->nv,
+           [&](int p, int q) -> int {
+             if (q >= H) return -1;
+             if (p == 0) return (int)(lay.enc1 + q);
+             if (p == 1) return (int)(lay.enc1_b + q);
+             return -1;
+           });
+  for (auto* r : {&T->red_dec1, &T->red_dec2, &T->red_enc2, &T->red_enc1})
+    maxpq = std::max(maxpq, r->P4 * r->Q2);
+  T->opart.alloc((std::size_t)T->rowblk * maxpq);
+  for (auto* r : {&T->red_dec1, &T->red_dec2, &T->red_enc2, &T->red_enc1}) {
+    const size_t smem = (size_t)(32 * r->P4 + 32 * r->Q2) * 4;
+    if (smem > 48 * 1024)
+      GNPC_CUDA(cudaFuncSetAttribute(gnpk::k_outer_sum, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  }
+  if ((std::size_t)(32 * T->red_layer[0].P4 + 32 * T->red_layer[0].Q2) * 4 > 48 * 1024)
+    GNPC_CUDA(cudaFuncSetAttribute(gnpk::k_outer_sum, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   96 * 1024));
+  regenerate(*T);
+  GNPC_CUDA(cudaStreamSynchronize(T->s));
+  return T.release();
+}
+
+// x, b host n x B column-major: forward + loss (+ grad + backward)
+double step_fb(gnpc_trainer_s& T, const double* x, const double* b, bool bwd) {
+  upload_batch(T, x, T.xb);
+  upload_batch(T, b, T.bb);
+  forward(T);
+  const double loss = loss_and_grad(T, bwd);
+  if (bwd) backward(T);
+  return loss;
+}
+
+}  // namespace
 
 extern "C" {
-#define GNPC_TRAIN_STUB(sig)                                        \
-  int sig {                                                         \
-    gnpc_impl::set_error("training path not built in this revision"); \
-    return GNPC_EUNSUPPORTED;                                       \
-  }
-GNPC_TRAIN_STUB(gnpc_trainer_create(gnpc_model, int64_t, double, gnpc_trainer*))
-GNPC_TRAIN_STUB(gnpc_trainer_destroy(gnpc_trainer))
-GNPC_TRAIN_STUB(gnpc_forward_backward(gnpc_trainer, const double*, const double*, double*, double*, double*))
-GNPC_TRAIN_STUB(gnpc_train_step(gnpc_trainer, const double*, const double*, double*))
-GNPC_TRAIN_STUB(gnpc_train_step_synthetic(gnpc_trainer, uint64_t, double*))
-GNPC_TRAIN_STUB(gnpc_monitor_loss(gnpc_trainer, const double*, const double*, int64_t, double*))
-GNPC_TRAIN_STUB(gnpc_trainer_grad_buffer(gnpc_trainer, float**, int64_t*))
-GNPC_TRAIN_STUB(gnpc_train_backward_only(gnpc_trainer, const double*, const double*, double*))
-GNPC_TRAIN_STUB(gnpc_train_apply_grads(gnpc_trainer))
-GNPC_TRAIN_STUB(gnpc_trainer_adam_state(gnpc_trainer, double*, double*, int64_t*))
-GNPC_TRAIN_STUB(gnpc_train_preconditioner(gnpc_csr, const gnpc_train_config*, double*, double*, double*))
+
+int gnpc_trainer_create(gnpc_model m, int64_t batch, double lr, gnpc_trainer* out) {
+  return guarded([&] {
+    need(out != nullptr, "trainer_create: null out");
+    *out = create(m, batch, lr);
+  });
 }
+
+int gnpc_trainer_destroy(gnpc_trainer t) {
+  return guarded([&] {
+    if (!t) return;
+    cudaStreamSynchronize(t->s);
+    delete t;
+  });
+}
+
+int gnpc_forward_backward(gnpc_trainer t, const double* x, const double* b, double* loss,
+                          double* grads, double* out) {
+  return guarded([&] {
+    need(t && x && b, "forward_backward: null argument");
+    const double l = step_fb(*t, x, b, true);
+    if (loss) *loss = l;
+    if (grads) {
+      GNPC_CUDA(cudaMemcpyAsync(grads, t->g64.p, t->P * 8, cudaMemcpyDeviceToHost, t->s));
+    }
+    if (out) {
+      const std::size_t cnt = (std::size_t)t->n * t->B;
+      gnpk::k_nb_to_colmajor<<<(int)((cnt + kTh - 1) / kTh), kTh, 0, t->s>>>(t->out.p, t->n, t->B,
+                                                                            t->tmp.p);
+      GNPC_LAUNCHED();
+      GNPC_CUDA(cudaMemcpyAsync(out, t->tmp.p, cnt * 8, cudaMemcpyDeviceToHost, t->s));
+    }
+    GNPC_CUDA(cudaStreamSynchronize(t->s));
+  });
+}
+
+int gnpc_train_step(gnpc_trainer t, const double* x, const double* b, double* loss) {
+  return guarded([&] {
+    need(t && x && b, "train_step: null argument");
+    const double l = step_fb(*t, x, b, true);
+    adam(*t);
+    GNPC_CUDA(cudaStreamSynchronize(t->s));
+    if (loss) *loss = l;
+  });
+}
+
+int gnpc_train_step_synthetic(gnpc_trainer t, uint64_t seed, double* loss) {
+  return guarded([&] {
+    need(t != nullptr, "train_step_synthetic: null trainer");
+    const std::size_t cnt = (std::size_t)t->n * t->B;
+    gnpk::k_philox_normal<<<(int)((cnt / 4 + kTh) / kTh), kTh, 0, t->s>>>(seed, (unsigned long long)t->t,
+                                                                          cnt, t->xb.p);
+    GNPC_LAUNCHED();
+    gnpk::DevCsr a = t->m->a->dev();
+    gnpk::k_spmm_nb<<<t->loss_grid, kTh, 0, t->s>>>(a, t->B, t->xb.p, t->bb.p);
+    GNPC_LAUNCHED();
+    forward(*t);
+    const double l = loss_and_grad(*t, true);
+    backward(*t);
+    adam(*t);
+    if (loss) *loss = l;
+  });
+}
+
+int gnpc_monitor_loss(gnpc_trainer t, const double* x, const double* b, int64_t batch, double* loss) {
+  return guarded([&] {
+    need(t && x && b && loss, "monitor_loss: null argument");
+    if (batch != t->B)
+      throw std::invalid_argument("monitor_loss: batch must equal the trainer batch");
+    *loss = step_fb(*t, x, b, false);
+  });
+}
+
+int gnpc_trainer_grad_buffer(gnpc_trainer t, double** dev_ptr, int64_t* count) {
+  return guarded([&] {
+    need(t && dev_ptr && count, "null argument");
+    *dev_ptr = t->g64.p;
+    *count = t->P;
+  });
+}
+
+int gnpc_train_backward_only(gnpc_trainer t, const double* x, const double* b, double* loss) {
+  return guarded([&] {
+    need(t && x && b, "train_backward_only: null argument");
+    const double l = step_fb(*t, x, b, true);
+    GNPC_CUDA(cudaStreamSynchronize(t->s));
+    if (loss) *loss = l;
+  });
+}
+
+int gnpc_train_apply_grads(gnpc_trainer t) {
+  return guarded([&] {
+    need(t != nullptr, "null trainer");
+    adam(*t);
+    GNPC_CUDA(cudaStreamSynchronize(t->s));
+  });
+}
+
+int gnpc_trainer_adam_state(gnpc_trainer t, double* m1, double* m2, int64_t* step) {
+  return guarded([&] {
+    need(t != nullptr, "null trainer");
+    if (m1) GNPC_CUDA(cudaMemcpyAsync(m1, t->m1.p, t->P * 8, cudaMemcpyDeviceToHost, t->s));
+    if (m2) GNPC_CUDA(cudaMemcpyAsync(m2, t->m2.p, t->P * 8, cudaMemcpyDeviceToHost, t->s));
+    GNPC_CUDA(cudaStreamSynchronize(t->s));
+    if (step) *step = t->t;
+  });
+}
+
+int gnpc_trainer_params(gnpc_trainer t, double* params) {
+  return guarded([&] {
+    need(t && params, "null argument");
+    GNPC_CUDA(cudaMemcpyAsync(params, t->p64.p, t->P * 8, cudaMemcpyDeviceToHost, t->s));
+    GNPC_CUDA(cudaStreamSynchronize(t->s));
+  });
+}
+
+int gnpc_trainer_sync_model(gnpc_trainer t) {
+  return guarded([&] {
+    need(t != nullptr, "null trainer");
+    sync_model_params(*t);
+  });
+}
+
+// train_preconditioner (src/gnn.cpp:401-451), Gaussian pairs drawn with the
+// reference Rng streams (seed+2 monitor, seed+3 training) on the host and
+// b = A x formed with the reference's f64 spmv, so the sampled data are
+// bit-identical to the reference's.
+int gnpc_train_preconditioner(gnpc_csr a, const gnpc_train_config* cfg, double* best,
+                              double* losses, double* best_loss) {
+  return guarded([&] {
+    need(a && cfg && best && losses && best_loss, "train_preconditioner: null argument");
+    if (cfg->batch < cfg->spectral_count)
+      throw std::invalid_argument("train: batch must be >= spectral_count");
+    if (cfg->spectral_count != 0)
+      throw Unsupported("train_preconditioner: spectral training pairs are not in this build "
+                        "(spectral_count must be 0)");
+    if (cfg->arnoldi_m < 1) throw std::invalid_argument("spectral sampler: m must be >= 1");
+    if (a->h.n < 2) throw std::invalid_argument("spectral sampler: n must be >= 2");
+    const gnp_b200::Dims dims{cfg->d, cfg->hidden, cfg->layers};
+    std::vector<double> p0 = gnp_b200::init_params(dims, cfg->seed);
+    gnpc_model mm = nullptr;
+    if (int rc = gnpc_model_create(a, dims.d, dims.hidden, dims.layers, p0.data(), &mm))
+      throw std::runtime_error(gnpc_last_error());
+    std::unique_ptr<gnpc_model_s, void (*)(gnpc_model_s*)> model(mm, [](gnpc_model_s* q) {
+      gnpc_model_destroy(q);
+    });
+    const std::int64_t n = a->h.n, B = cfg->batch, MB = cfg->monitor_batch;
+    auto batch_from = [&](gnp_b200::Rng& rng, std::int64_t cols, std::vector<double>& x,
+                          std::vector<double>& b) {
+      x.resize(n * cols);
+      b.resize(n * cols);
+      for (std::int64_t k = 0; k < cols; ++k) {
+        std::vector<double> xk = rng.gaussian_vector(n);
+        std::vector<double> bk = gnp_b200::spmv(a->h, xk);
+        std::copy(xk.begin(), xk.end(), x.begin() + k * n);
+        std::copy(bk.begin(), bk.end(), b.begin() + k * n);
+      }
+    };
+    std::vector<double> mx, mb, x, b;
+    gnp_b200::Rng monitor_rng(cfg->seed + 2);
+    batch_from(monitor_rng, MB, mx, mb);
+    gnp_b200::Rng train_rng(cfg->seed + 3);
+    std::unique_ptr<gnpc_trainer_s> tr(create(model.get(), B, cfg->lr));
+    std::unique_ptr<gnpc_trainer_s> mon(MB == B ? nullptr : create(model.get(), MB, cfg->lr));
+    gnpc_trainer_s& M = mon ? *mon : *tr;
+    auto monitoring = [&]() {
+      if (mon) {  // the monitor trainer reads the current params
+        GNPC_CUDA(cudaMemcpyAsync(M.p64.p, tr->p64.p, tr->P * 8, cudaMemcpyDeviceToDevice, tr->s));
+        regenerate(M);
+      }
+      return step_fb(M, mx.data(), mb.data(), false);
+    };
+    std::vector<double> bestp = p0;
+    double bl = monitoring();
+    losses[0] = bl;
+    for (std::int64_t step = 0; step < cfg->steps; ++step) {
+      batch_from(train_rng, B, x, b);
+      step_fb(*tr, x.data(), b.data(), true);
+      adam(*tr);
+      const double ml = monitoring();
+      losses[step + 1] = ml;
+      if (ml < bl) {
+        bl = ml;
+        GNPC_CUDA(cudaMemcpyAsync(bestp.data(), tr->p64.p, tr->P * 8, cudaMemcpyDeviceToHost, tr->s));
+        GNPC_CUDA(cudaStreamSynchronize(tr->s));
+      }
+    }
+    std::copy(bestp.begin(), bestp.end(), best);
+    *best_loss = bl;
+  });
+}
+
+}  // extern "C"

@@ -112,6 +112,26 @@ def main():
     s8 = R.fgmres(c8h32, b8, kind=1, dims=(8, 16, 4), params=f32(best8), maxiters=100, restart=20)
     np.savez_compressed(os.path.join(HERE, "trained_conv8.npz"), params=best8, losses=losses8,
                         status=s8["status"], hist=np.array([h[:2] for h in s8["history"]]))
+    # 6. a short reference training run with Gaussian pairs only (spectral = 0)
+    c6 = R.gen_convection_diffusion(6, 0.5)
+    c6h = R.prescale(c6, R.gershgorin_gamma(c6))
+    best6, losses6, bl6 = R.train(c6h, (4, 8, 2), steps=20, batch=8, spectral=0, arnoldi_m=10,
+                                  seed=41, monitor_batch=8)
+    np.savez_compressed(os.path.join(HERE, "train_run.npz"), best=best6, losses=losses6, best_loss=bl6)
+    # 7. one batch at d=32 (tcgen05 width) on a variable-coefficient 2D problem
+    import ctypes  # noqa: F401
+    sys.path.insert(0, ROOT)
+    from paper_2406_00809_b200 import capi
+
+    cv = capi.Csr.generate("c3_varcoeff2d", 24, 2.0, 0.0, 2)
+    rp, ci, v = cv.arrays()
+    c3 = O.Csr(cv.n, rp, ci, v)
+    c3h = R.prescale(c3, R.gershgorin_gamma(c3)).rounded_f32()
+    p3 = f32(R.init_params(32, 32, 8, 0))
+    x3, b3 = R.gaussian_batch(c3h, 3, 0, 8)
+    l3, g3 = R.batch_loss_grads(c3h, (32, 32, 8), p3, x3, b3, 8)
+    np.savez_compressed(os.path.join(HERE, "c3_small_train_step.npz"), **csr_dict("a", c3h), params=p3,
+                        x=x3, b=b3, loss=l3, grads=g3)
     print("golden fixtures written to", HERE)
 
 

@@ -1,0 +1,137 @@
+"""GPU parity of batched training (forward, L1 loss, backward, Adam) against
+the oracle.  The device computes in fp32 (tf32x3 on the tensor cores for
+d = 16/32) with f64 reductions; tolerance per parameter tensor, norm-wise:
+1e-4 for gradients (north_star's GNP bar), tighter for the loss."""
+import numpy as np
+import pytest
+from conftest import csr_of, f32, golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def slices(d, h, L):
+    names, o = [], 0
+    for nm, sz in [("enc1", h), ("enc1_b", h), ("enc2", h * d), ("enc2_b", d)]:
+        names.append((nm, o, o + sz))
+        o += sz
+    for l in range(L):
+        names.append((f"u{l}", o, o + d * d))
+        o += d * d
+        names.append((f"w{l}", o, o + d * d))
+        o += d * d
+    for nm, sz in [("dec1", d * h), ("dec1_b", h), ("dec2", h), ("dec2_b", 1)]:
+        names.append((nm, o, o + sz))
+        o += sz
+    return names
+
+
+def check_grads(got, want, dims, tol=1e-4):
+    worst = 0.0
+    for nm, a, b in slices(*dims):
+        den = np.linalg.norm(want[a:b])
+        if den == 0.0:
+            assert np.linalg.norm(got[a:b]) <= 1e-12, nm
+            continue
+        e = np.linalg.norm(got[a:b] - want[a:b]) / den
+        worst = max(worst, e)
+        assert e <= tol, (nm, e)
+    return worst
+
+
+def dev_csr(capi, a):
+    return capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
+
+
+def test_small_batch_loss_and_grads(capi, cuda):
+    g = golden("train_step.npz")  # dims (4, 8, 2): CUDA-core batched path
+    a = csr_of("a", g)
+    A = dev_csr(capi, a)
+    m = capi.Model(A, (4, 8, 2), g["params"])
+    t = capi.Trainer(m, 4)
+    loss, grads, out = t.forward_backward(g["x"], g["b"])
+    assert abs(loss - float(g["loss"])) <= 1e-5 * float(g["loss"])
+    assert rel_l2(out, g["out"]) <= 1e-5
+    check_grads(grads, g["grads"], (4, 8, 2))
+
+
+def test_c1_batch_grads_tensor_cores(capi, oc, cuda):
+    # d = 16: tcgen05 forward + backward layers, B = 4 on the C1 matrix
+    g = golden("c1.npz")
+    gs = golden("c1_train_step.npz")
+    ah = oc.prescale(oc.gen_convection_diffusion(64, 0.0), 8.0)
+    x, b = oc.gaussian_batch(ah, 3, 0, 4)
+    A = dev_csr(capi, ah)
+    m = capi.Model(A, (16, 32, 8), g["params"])
+    t = capi.Trainer(m, 4)
+    loss, grads, _ = t.forward_backward(x, b)
+    assert abs(loss - float(gs["loss"])) <= 1e-5 * float(gs["loss"])
+    check_grads(grads, gs["grads"], (16, 32, 8))
+
+
+def test_d32_batch_grads_tensor_cores(capi, cuda):
+    g = golden("c3_small_train_step.npz")  # d = 32, B = 8, var-coeff 24x24
+    a = csr_of("a", g)
+    m = capi.Model(dev_csr(capi, a), (32, 32, 8), g["params"])
+    t = capi.Trainer(m, 8)
+    loss, grads, _ = t.forward_backward(g["x"], g["b"])
+    assert abs(loss - float(g["loss"])) <= 1e-5 * float(g["loss"])
+    check_grads(grads, g["grads"], (32, 32, 8))
+
+
+def test_adam_step_matches_oracle(capi, oc, cuda):
+    g = golden("train_step.npz")
+    a = csr_of("a", g)
+    m = capi.Model(dev_csr(capi, a), (4, 8, 2), g["params"])
+    t = capi.Trainer(m, 4, lr=1e-3)
+    _, grads, _ = t.forward_backward(g["x"], g["b"])
+    t.apply_grads()
+    z = np.zeros_like(grads)
+    want, m1w, m2w, _ = oc.adam_step((4, 8, 2), g["params"], grads, z, z, 0, 1e-3)
+    assert np.allclose(t.params(), want, rtol=0, atol=1e-15 + 1e-13 * np.abs(want).max())
+    m1, m2, step = t.adam_state()
+    assert step == 1 and np.allclose(m1, m1w, atol=1e-18) and np.allclose(m2, m2w, rtol=1e-12)
+
+
+def test_training_is_deterministic(capi, cuda):
+    g = golden("train_step.npz")
+    a = csr_of("a", g)
+    runs = []
+    for _ in range(2):
+        m = capi.Model(dev_csr(capi, a), (4, 8, 2), g["params"])
+        t = capi.Trainer(m, 4)
+        runs.append([t.step(g["x"], g["b"]) for _ in range(5)] + list(t.params()))
+    assert runs[0] == runs[1]
+
+
+def test_train_preconditioner_tracks_reference(capi, oc, cuda):
+    # reference train_preconditioner, Gaussian pairs only (spectral = 0), 20 steps
+    g = golden("train_run.npz")
+    a = oc.gen_convection_diffusion(6, 0.5)
+    ah = oc.prescale(a, oc.gershgorin_gamma(a))
+    best, losses, bl = capi.train_preconditioner(dev_csr(capi, ah), dims=(4, 8, 2), steps=20, batch=8,
+                                                 spectral=0, arnoldi_m=10, seed=41, monitor_batch=8)
+    want = g["losses"]
+    assert abs(losses[0] - want[0]) <= 1e-5 * want[0]
+    assert np.max(np.abs(losses - want) / want) <= 1e-3
+    assert bl == min(losses) and bl < losses[0]
+    assert rel_l2(best, g["best"]) <= 1e-3
+
+
+def test_synthetic_steps_reduce_loss(capi, gnp, cuda):
+    a = capi.Csr.generate("c3_varcoeff2d", 64, 2.0, 0.0, 2)
+    ah = a.prescale(a.gamma())
+    m = capi.Model(ah, (32, 32, 8), capi.init_params(32, 32, 8, 0))
+    t = capi.Trainer(m, 8, lr=1e-3)
+    losses = [t.step_synthetic(7) for _ in range(30)]
+    assert all(np.isfinite(losses))
+    assert np.mean(losses[-5:]) < np.mean(losses[:5])
+
+
+def test_python_train_drop_in(gnp, cuda):
+    a = gnp.prescale(gnp.gen_convection_diffusion(6, 0.5), 8.0)
+    params, losses = gnp.train(a, steps=10, batch=8, spectral=0, arnoldi_m=10, seed=1, d=4, hidden=8,
+                               layers=2)
+    assert len(losses) == 11 and min(losses) <= losses[0]
+    b = gnp.spmv(a, [1.0] * a.n)
+    out = gnp.solve(a, b, precond="gnp", params=params, maxiters=200)
+    assert out["status"] in ("converged", "maxiters")

@@ -82,11 +82,42 @@ __device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr, uint32_t sbo
   return d;
 }
 
+// MN-major, 128-byte swizzle: the contiguous 128 B rows run along M/N (32
+// tf32 per atom row), 8 K-rows per 1024 B group.  LBO = stride between
+// 32-element M/N atoms, SBO = stride between 8-row K groups.
+__device__ __forceinline__ uint64_t make_desc_sw128_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
 // Byte offset of fp32/tf32 element (row, k) in a swizzled K-major operand of
 // `rows` rows: K is split into 32-element (128 B) atoms stored atom-major.
 __host__ __device__ constexpr uint32_t sw128_off(int row, int k, int rows) {
   return static_cast<uint32_t>((k >> 5) * rows * 128 + (row >> 3) * 1024 + (row & 7) * 128 +
                                ((((k & 31) >> 2) ^ (row & 7)) << 4) + (k & 3) * 4);
+}
+
+// ---- TMA (cp.async.bulk.tensor) ----------------------------------------
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// 2-D tile load (inner coordinate x, row coordinate y) completing on `bar`.
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
 // Instruction descriptor: kind::tf32, D fp32, A/B tf32, both K-major, M x N.
@@ -96,6 +127,11 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
          | (2u << 10)                                // b_format TF32
          | (static_cast<uint32_t>(N >> 3) << 17)     // n_dim
          | (static_cast<uint32_t>(M >> 4) << 24);    // m_dim
+}
+
+// Same with both operands MN-major (A: M x K stored K-rows of M elements).
+__host__ __device__ constexpr uint32_t idesc_tf32_mn(int M, int N) {
+  return idesc_tf32(M, N) | (1u << 15) | (1u << 16);
 }
 
 // D[tmem] (+)= A[smem] · B[smem]^T, issued by ONE thread.

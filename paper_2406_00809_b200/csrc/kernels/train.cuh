@@ -388,6 +388,54 @@ __global__ void k_outer_finish(const double* __restrict__ partials, int nblk, in
   if (d >= 0) grad[d] = s;
 }
 
+// ------------------------------------------------------------------ weighted column sums
+// For the one-column reductions (src/gnn.cpp:222-235 dec2 / dec2_bias and
+// :292-305 enc1 / enc1_bias): per block, out1[h] = Σ A[v][h] w[v],
+// out2[h] = Σ A[v][h], out3 = Σ w[v] over the block's contiguous rows; lanes
+// own the (<= 32) columns, warps stride rows; partials [grid][3][32] (f64).
+__global__ void __launch_bounds__(kThreads)
+k_weighted_colsum(const float* __restrict__ A, int W, const float* __restrict__ w, int nv,
+                  double* __restrict__ partials) {
+  __shared__ double red[8][3][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per = (nv + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * per, r1 = min(nv, r0 + per);
+  double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (int v0 = r0 + warp * 4; v0 < r1; v0 += 32) {  // 4 rows per warp per step
+    float s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int v = v0 + u;
+      if (v < r1) {
+        const float x = lane < W ? __ldg(A + static_cast<size_t>(v) * W + lane) : 0.f;
+        const float wv = __ldg(w + v);
+        s1 = fmaf(x, wv, s1);
+        s2 += x;
+        s3 += wv;
+      }
+    }
+    a1 += s1;
+    a2 += s2;
+    a3 += s3;
+  }
+  red[warp][0][lane] = a1;
+  red[warp][1][lane] = a2;
+  red[warp][2][lane] = a3;
+  __syncthreads();
+  if (warp == 0) {
+    double t1 = 0.0, t2 = 0.0, t3 = 0.0;
+    for (int q = 0; q < 8; ++q) {
+      t1 += red[q][0][lane];
+      t2 += red[q][1][lane];
+      t3 += red[q][2][lane];
+    }
+    double* dst = partials + static_cast<size_t>(blockIdx.x) * 96;
+    dst[lane] = t1;
+    dst[32 + lane] = t2;
+    dst[64 + lane] = t3;  // every lane holds Σ w; entry 64 is used
+  }
+}
+
 // ------------------------------------------------------------------ Adam
 // src/gnn.cpp:345-363 in f64 on the flat parameter vector.
 __global__ void k_adam(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m1,

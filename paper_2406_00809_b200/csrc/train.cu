@@ -7,6 +7,8 @@
 // regenerated on the GPU from the f64 master copy.  Restates
 // src/gnn.cpp:208-451 (train_preconditioner's step body) with τ treated as a
 // constant of b (SPEC) exactly like the reference.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -18,6 +20,7 @@
 #include "capi_common.hpp"
 #include "kernels/layer_tc.cuh"
 #include "kernels/train.cuh"
+#include "kernels/wgrad_tc.cuh"
 #include "model.hpp"
 
 using namespace gnpc_impl;
@@ -48,7 +51,18 @@ struct gnpc_trainer_s {
     gnpk::OuterArgs o;
     DevBuf<int> dst;
     int P4 = 0, Q2 = 0;
+    bool tc = false;       // tcgen05 path (k_wgrad_tc): partial layout [64][32]
+    gnpk::WgradArgs w{};
+    bool tma = false;      // TMA-fed variant (k_wgrad_tma) with its tensor maps
+    const float* tma_b = nullptr;
+    gnpk::WgradTmaArgs ta{};
+    bool colsum = false;   // one-column reduction (k_weighted_colsum)
+    const float* cs_A = nullptr;
+    const float* cs_w = nullptr;
+    int cs_W = 0, cs_nv = 0;
   };
+  int colsum_grid = 0;
+  int wgrad_grid = 0, wgrad_grid_tma = 0;
   Red red_layer[64], red_dec1, red_dec2, red_enc2, red_enc1;
   DevBuf<double> opart;
   int rowblk = 0;
@@ -82,7 +96,101 @@ void make_red(gnpc_trainer_s::Red& r, const float* A1, int P1, int s1, const flo
   upload_i(r.dst, dst);
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q{};
+    void* p = nullptr;
+    GNPC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// [nv][32] fp32 rows viewed as a 2-D tensor, box {32 features, 128 rows}, 128B swizzle.
+CUtensorMap rows32_map(const float* base, int nv) {
+  CUtensorMap m{};
+  const cuuint64_t dims[2] = {32, (cuuint64_t)nv};
+  const cuuint64_t strides[1] = {32 * sizeof(float)};
+  const cuuint32_t box[2] = {32, 128};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(
+      &m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed");
+  return m;
+}
+
+// tcgen05 reduction: A = [A1 | A2 or ones] (<= 32 features each), B (<= 32),
+// dst map over the [64][32] partial (m < 32: A1 feature, m >= 32: A2 / bias).
+template <class F>
+void make_red_tc(gnpc_trainer_s::Red& r, const float* A1, int wa1, int sa1, const float* A2, int wa2,
+                 int sa2, int ones, const float* Bm, int wb, int sb, int nv, F dstfn) {
+  r.tc = true;
+  r.w = gnpk::WgradArgs{A1, wa1, sa1, A2, wa2, sa2, ones, Bm, wb, sb, nv, nullptr};
+  r.P4 = 64;
+  r.Q2 = 32;
+  std::vector<int> dst(64 * 32, -1);
+  for (int m = 0; m < 64; ++m)
+    for (int q = 0; q < 32; ++q) dst[m * 32 + q] = dstfn(m, q);
+  upload_i(r.dst, dst);
+}
+
+// one-column reduction (k_weighted_colsum): dst over [out1(32) | out2(32) | out3]
+template <class F>
+void make_red_colsum(gnpc_trainer_s::Red& r, const float* A, int W, const float* w, int nv, F dstfn) {
+  r.colsum = true;
+  r.cs_A = A;
+  r.cs_W = W;
+  r.cs_w = w;
+  r.cs_nv = nv;
+  std::vector<int> dst(96, -1);
+  for (int i = 0; i < 96; ++i) dst[i] = dstfn(i);
+  upload_i(r.dst, dst);
+}
+
 void run_red(gnpc_trainer_s& T, gnpc_trainer_s::Red& r) {
+  if (r.colsum) {
+    gnpk::k_weighted_colsum<<<T.colsum_grid, kTh, 0, T.s>>>(r.cs_A, r.cs_W, r.cs_w, r.cs_nv, T.opart.p);
+    GNPC_LAUNCHED();
+    gnpk::k_outer_finish<<<1, 96, 0, T.s>>>(T.opart.p, T.colsum_grid, 96, r.dst.p, T.g64.p);
+    GNPC_LAUNCHED();
+    return;
+  }
+  if (r.tc && r.w.wa1 == 32 && r.w.sa1 == 32 && r.w.wb == 32 && r.w.sb == 32 &&
+      (r.w.ones || !r.w.A2 || (r.w.wa2 == 32 && r.w.sa2 == 32))) {
+    // TMA-fed variant (32-float rows); tensor maps re-encoded when Bm moves
+    const float* Bm = r.o.Bm ? r.o.Bm : r.w.Bm;
+    if (!r.tma || r.tma_b != Bm) {
+      r.ta.a1 = rows32_map(r.w.A1, r.w.nv);
+      r.ta.a2 = r.w.A2 ? rows32_map(r.w.A2, r.w.nv) : r.ta.a1;
+      r.ta.a2_mode = r.w.ones ? 2 : (r.w.A2 ? 1 : 0);
+      r.ta.b = rows32_map(Bm, r.w.nv);
+      r.ta.nv = r.w.nv;
+      r.tma = true;
+      r.tma_b = Bm;
+    }
+    r.ta.partials = T.opart.p;
+    gnpk::k_wgrad_tma<<<T.wgrad_grid_tma, gnpk::wgt::TH, gnpk::wgt::smem_bytes(), T.s>>>(r.ta);
+    GNPC_LAUNCHED();
+    gnpk::k_outer_finish<<<(64 * 32 + kTh - 1) / kTh, kTh, 0, T.s>>>(T.opart.p, T.wgrad_grid_tma,
+                                                                   64 * 32, r.dst.p, T.g64.p);
+    GNPC_LAUNCHED();
+    return;
+  }
+  if (r.tc) {
+    r.w.partials = T.opart.p;
+    r.w.Bm = r.o.Bm ? r.o.Bm : r.w.Bm;
+    gnpk::k_wgrad_tc<<<T.wgrad_grid, kTh, gnpk::wg::smem_bytes(), T.s>>>(r.w);
+    GNPC_LAUNCHED();
+    gnpk::k_outer_finish<<<(64 * 32 + kTh - 1) / kTh, kTh, 0, T.s>>>(T.opart.p, T.wgrad_grid, 64 * 32,
+                                                                   r.dst.p, T.g64.p);
+    GNPC_LAUNCHED();
+    return;
+  }
   r.o.partials = T.opart.p;
   const int nblocks = (r.P4 / 4) * (r.Q2 / 2);
   dim3 grid(T.rowblk, (nblocks + kTh - 1) / kTh);
@@ -384,7 +492,71 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
            });
   for (auto* r : {&T->red_dec1, &T->red_dec2, &T->red_enc2, &T->red_enc1})
     maxpq = std::max(maxpq, r->P4 * r->Q2);
-  T->opart.alloc((std::size_t)T->rowblk * maxpq);
+  // tcgen05 reductions whenever every operand fits one 32-feature atom
+  const char* no_tc = std::getenv("GNPC_NO_TC");
+  if (dp <= 32 && H <= 32 && !(no_tc && no_tc[0] == '1')) {
+    for (int l = 0; l < T->L; ++l)
+      make_red_tc(T->red_layer[l], T->Xs.p + l * act, dp, dp, T->AXs.p + l * act, dp, dp, 0, nullptr, dp,
+                  dp, T->nv, [&](int m_, int q) -> int {
+                    if (q >= d) return -1;
+                    if (m_ < d) return (int)(lay.u[l] + (std::int64_t)q * d + m_);
+                    if (m_ >= 32 && m_ - 32 < d) return (int)(lay.w[l] + (std::int64_t)q * d + (m_ - 32));
+                    return -1;
+                  });
+    make_red_tc(T->red_dec1, T->Xs.p + T->L * act, dp, dp, nullptr, 0, 0, 1, T->hb2.p, H, H, T->nv,
+                [&](int m_, int q) -> int {
+                  if (q >= H) return -1;
+                  if (m_ < d) return (int)(lay.dec1 + (std::int64_t)q * d + m_);
+                  if (m_ == 32) return (int)(lay.dec1_b + q);
+                  return -1;
+                });
+    make_red_tc(T->red_dec2, T->hb1.p, H, H, nullptr, 0, 0, 1, T->gyv.p, 1, 1, T->nv,
+                [&](int m_, int q) -> int {
+                  if (q != 0) return -1;
+                  if (m_ < H) return (int)(lay.dec2 + m_);
+                  if (m_ == 32) return (int)lay.dec2_b;
+                  return -1;
+                });
+    make_red_tc(T->red_enc2, T->hb1.p, H, H, nullptr, 0, 0, 1, nullptr, dp, dp, T->nv,
+                [&](int m_, int q) -> int {
+                  if (q >= d) return -1;
+                  if (m_ < H) return (int)(lay.enc2 + (std::int64_t)q * H + m_);
+                  if (m_ == 32) return (int)(lay.enc2_b + q);
+                  return -1;
+                });
+    make_red_tc(T->red_enc1, T->vv.p, 1, 1, nullptr, 0, 0, 1, T->hb2.p, H, H, T->nv,
+                [&](int m_, int q) -> int {
+                  if (q >= H) return -1;
+                  if (m_ == 0) return (int)(lay.enc1 + q);
+                  if (m_ == 32) return (int)(lay.enc1_b + q);
+                  return -1;
+                });
+    GNPC_CUDA(cudaFuncSetAttribute(gnpk::k_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)gnpk::wg::smem_bytes()));
+    const int per_sm = tc_ctas_per_sm((const void*)gnpk::k_wgrad_tc, gnpk::wg::smem_bytes(), 32);
+    T->wgrad_grid = std::max(1, std::min(per_sm * T->sms, (T->nv + 127) / 128));
+    GNPC_CUDA(cudaFuncSetAttribute(gnpk::k_wgrad_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)gnpk::wgt::smem_bytes()));
+    T->wgrad_grid_tma = std::max(1, std::min(T->sms, (T->nv + 127) / 128));
+    T->wgrad_grid = std::max(T->wgrad_grid, T->wgrad_grid_tma);
+    maxpq = std::max(maxpq, 64 * 32 * T->wgrad_grid / std::max(T->rowblk, 1) + 64 * 32);
+  }
+  // the two one-column reductions as weighted column sums
+  if (H <= 32) {
+    make_red_colsum(T->red_dec2, T->hb1.p, H, T->gyv.p, T->nv, [&](int i) -> int {
+      if (i < H) return (int)(lay.dec2 + i);  // Σ post_h gy
+      if (i == 64) return (int)lay.dec2_b;    // Σ gy
+      return -1;
+    });
+    make_red_colsum(T->red_enc1, T->hb2.p, H, T->vv.p, T->nv, [&](int i) -> int {
+      if (i < H) return (int)(lay.enc1 + i);                 // Σ gp0_h vv
+      if (i >= 32 && i < 32 + H) return (int)(lay.enc1_b + i - 32);  // Σ gp0_h
+      return -1;
+    });
+    T->colsum_grid = std::max(1, std::min(4 * T->sms, (T->nv + 1023) / 1024));
+  }
+  T->opart.alloc(std::max({(std::size_t)T->rowblk * maxpq, (std::size_t)T->wgrad_grid * 64 * 32,
+                           (std::size_t)T->colsum_grid * 96}));
   for (auto* r : {&T->red_dec1, &T->red_dec2, &T->red_enc2, &T->red_enc1}) {
     const size_t smem = (size_t)(32 * r->P4 + 32 * r->Q2) * 4;
     if (smem > 48 * 1024)
@@ -423,7 +595,8 @@ int gnpc_trainer_create(gnpc_model m, int64_t batch, double lr, gnpc_trainer* ou
 int gnpc_trainer_destroy(gnpc_trainer t) {
   return guarded([&] {
     if (!t) return;
-    cudaStreamSynchronize(t->s);
+    // the model (and its stream) may already be gone at interpreter teardown
+    cudaDeviceSynchronize();
     delete t;
   });
 }

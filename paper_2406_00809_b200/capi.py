@@ -124,6 +124,12 @@ class Csr:
         check(lib().gnpc_csr_info(self.h, C.byref(n), C.byref(z)))
         return n.value, z.value
 
+    def device_layout(self):
+        """(uploaded, sliced_ell, long_rows) of the device copy."""
+        u, s, l = C.c_int(), C.c_int(), C.c_int()
+        check(lib().gnpc_csr_device_layout(self.h, C.byref(u), C.byref(s), C.byref(l)))
+        return bool(u.value), bool(s.value), l.value
+
     @property
     def n(self):
         return self.info()[0]

@@ -2,6 +2,8 @@
 // apply pipeline launcher, device FGMRES driver, checkpoints.  Training lives
 // in train.cu.  No exception crosses the boundary; no CPU fallback exists for
 // any device entry point (no device => GNPC_ENODEV).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -17,6 +19,7 @@
 #include "capi_common.hpp"
 #include "kernels/apply.cuh"
 #include "kernels/krylov.cuh"
+#include "kernels/layer_sell.cuh"
 #include "kernels/layer_tc.cuh"
 #include "model.hpp"
 
@@ -130,18 +133,47 @@ struct ApplyLaunch {
       const bool last = l + 1 == net.layers;
       mark(last ? 4 : 3);
       if constexpr (DP == 16 || DP == 32) {
+        static const bool sell_off = [] {
+          const char* e = std::getenv("GNPC_NO_SELL_KERNEL");
+          return e && std::string(e) == "1";
+        }();
+        if (m.use_tc && a.sell && !sell_off) {
+          // sliced-ELL TMA pipeline, one 512-thread CTA per SM
+          using S = SellCfg<DP>;
+          const size_t smem = S::smem_bytes(last, net.hidden);
+          auto kern = last ? k_layer_sell<DP, true, OutT> : k_layer_sell<DP, false, OutT>;
+          static std::once_flag f[2];
+          std::call_once(f[last ? 1 : 0], [&] {
+            GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+          });
+          const int tiles_s = (n + S::TM - 1) / S::TM;
+          const int grid = std::max(1, std::min(tiles_s, sms));
+          SellMaps maps{m.tmX[cur], m.tmX[1 - cur]};
+          const float* uwp = m.UWP.p + (size_t)l * 4 * DP * DP;
+          kern<<<grid, S::NT, smem, s>>>(a, maps, X, axl, uwp, net, m.sc.p, out, skip);
+          GNPC_LAUNCHED();
+          cur = 1 - cur;
+          continue;
+        }
         if (m.use_tc) {
           using T = TcCfg<DP>;
           const float* uwtc = m.UWTC.p + (size_t)l * 2 * T::B_FLOATS;
-          auto kern = last ? k_layer_tc<DP, kEpiLast, OutT> : k_layer_tc<DP, kEpiRelu, OutT>;
+          auto kern = a.sell ? (last ? k_layer_tc<DP, kEpiLast, OutT, kPathSell>
+                                     : k_layer_tc<DP, kEpiRelu, OutT, kPathSell>)
+                             : (last ? k_layer_tc<DP, kEpiLast, OutT, kPathCsr1>
+                                     : k_layer_tc<DP, kEpiRelu, OutT, kPathCsr1>);
           const size_t smem = T::smem_bytes(last, net.hidden);
           // launch geometry is computed once per model (host queries would
           // otherwise starve the GPU between the 8 layer launches)
-          int& per_sm = m.tc_per_sm[(last ? 2 : 0) + (sizeof(OutT) == 8 ? 1 : 0)];
+          int& per_sm = m.tc_per_sm[(last ? 2 : 0) + (sizeof(OutT) == 8 ? 1 : 0) + (a.sell ? 4 : 0)];
           if (per_sm == 0) per_sm = tc_ctas_per_sm((const void*)kern, smem, T::TCOLS);
           const int tiles_tc = (n + T::TM - 1) / T::TM;
           const int grid = std::max(1, std::min(tiles_tc, per_sm * sms));
-          LayerIO io{X, last ? nullptr : m.X[1 - cur].p, uwtc, axl, nullptr, nullptr, 1};
+          static const int dbg = [] {
+            const char* e = std::getenv("GNPC_LAYER_DBG");
+            return e ? std::atoi(e) : 0;
+          }();
+          LayerIO io{X, last ? nullptr : m.X[1 - cur].p, uwtc, axl, nullptr, nullptr, 1, dbg};
           kern<<<grid, kThreads, smem, s>>>(a, io, net, m.sc.p, out, skip);
           GNPC_LAUNCHED();
           cur = 1 - cur;
@@ -173,6 +205,36 @@ struct ApplyLaunch {
   }
 };
 
+}  // namespace gnpc_impl
+
+// ====================================================================== TMA maps
+namespace gnpc_impl {
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q{};
+    void* p = nullptr;
+    GNPC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+CUtensorMap make_rows_map(const float* base, std::int64_t rows, int width, int box_rows,
+                          CUtensorMapSwizzle swizzle) {
+  CUtensorMap m{};
+  const cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)width * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)width, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(
+      &m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed");
+  return m;
+}
 }  // namespace gnpc_impl
 
 // ====================================================================== CSR
@@ -216,8 +278,71 @@ void gnpc_csr_s::upload() {
     ch_k1.upload(ck1.data(), ck1.size());
     long_c0.upload(c0.data(), c0.size());
   }
+  build_sell(hrp, hci, hv);
   GNPC_CUDA(cudaDeviceSynchronize());
   dev_ready = true;
+}
+
+// Sliced ELL over 128-row slices (the tensor-core layer's tile): slice t holds
+// K_t = max short-row length entries per row, column-major within the slice so
+// one bulk copy stages a tile and a warp's (col, val) reads are contiguous.
+// Built only when the padding stays small (stencil-like matrices); long rows
+// (> kLongRow) keep their chunked path and get padding entries here.
+void gnpc_csr_s::build_sell(const std::vector<int>& hrp, const std::vector<int>& hci,
+                            const std::vector<float>& hv) {
+  constexpr int TM = 128;
+  const std::int64_t n = h.n;
+  const std::int64_t ntiles = (n + TM - 1) / TM;
+  if (n == 0) return;
+  if (const char* e = std::getenv("GNPC_NO_SELL"); e && std::string(e) == "1") return;
+  std::vector<int> K(ntiles, 0), off(ntiles, 0);
+  std::int64_t total = 0, short_nnz = 0;
+  for (std::int64_t t = 0; t < ntiles; ++t) {
+    int kt = 0;
+    bool haslong = false;
+    for (std::int64_t i = t * TM; i < std::min(n, (t + 1) * TM); ++i) {
+      const int len = hrp[i + 1] - hrp[i];
+      if (len > gnpk::kLongRow) {
+        haslong = true;
+      } else {
+        kt = std::max(kt, len);
+        short_nnz += len;
+      }
+    }
+    if (total + (std::int64_t)kt * TM >= (std::int64_t(1) << 31)) return;
+    off[t] = static_cast<int>(total);
+    total += (std::int64_t)kt * TM;
+    K[t] = kt | (haslong ? 1 << 16 : 0);
+  }
+  if ((double)total > 1.25 * (double)short_nnz + 4.0 * TM) return;  // too ragged
+  std::vector<int2> ent(std::max<std::int64_t>(total, 1));
+  for (std::int64_t t = 0; t < ntiles; ++t) {
+    const int kt = K[t] & 0xffff;
+    for (int r = 0; r < TM; ++r) {
+      const std::int64_t i = t * TM + r;
+      int s = 0, len = 0;
+      if (i < n) {
+        s = hrp[i];
+        len = hrp[i + 1] - s;
+        if (len > gnpk::kLongRow) len = 0;
+      }
+      for (int k = 0; k < kt; ++k) {
+        int2 e;
+        if (k < len) {
+          e.x = hci[s + k];
+          std::memcpy(&e.y, &hv[s + k], 4);
+        } else {
+          e.x = i < n ? static_cast<int>(i) : 0;  // own row, weight 0
+          e.y = 0;
+        }
+        ent[off[t] + (std::size_t)k * TM + r] = e;
+      }
+    }
+  }
+  sell.upload(ent.data(), ent.size());
+  sell_off.upload(off.data(), off.size());
+  sell_k.upload(K.data(), K.size());
+  has_sell = true;
 }
 
 gnpk::DevCsr gnpc_csr_s::dev() {
@@ -230,6 +355,9 @@ gnpk::DevCsr gnpc_csr_s::dev() {
   d.v = v.p;
   d.long_rows = n_long ? long_rows.p : nullptr;
   d.n_long = n_long;
+  d.sell = has_sell ? sell.p : nullptr;
+  d.sell_off = has_sell ? sell_off.p : nullptr;
+  d.sell_k = has_sell ? sell_k.p : nullptr;
   return d;
 }
 
@@ -310,6 +438,21 @@ void gnpc_model_s::build_maps() {
           map_tc_bwd[hi] = map_tc_bwd[lo] = bwd_src(l, j, k);
           part_tc[lo] = 1;
         }
+    // k_layer_sell: per layer four DP x DP operands, block b = 2*part + hi
+    // ([Bu_lo | Bu_hi | Bw_lo | Bw_hi]) in the DP-wide swizzle; element (j, k)
+    // of part p = [U; W](k + p*DP, j)
+    const std::size_t pb = (std::size_t)dp * dp;
+    map_tc_pair.assign((std::size_t)L * 4 * pb, -1);
+    part_pair.assign((std::size_t)L * 4 * pb, 0);
+    for (std::int64_t l = 0; l < L; ++l)
+      for (int b = 0; b < 4; ++b)
+        for (int j = 0; j < dp; ++j)
+          for (int k = 0; k < dp; ++k) {
+            const std::size_t off = (dp == 32 ? gnpk::tc::swz_off<32>(j, k) : gnpk::tc::swz_off<16>(j, k)) / 4;
+            const std::size_t i = (std::size_t)l * 4 * pb + b * pb + off;
+            map_tc_pair[i] = fwd_src(l, j, k + (b >> 1) * dp);
+            part_pair[i] = (b & 1) ? 0 : 1;  // 1 = lo part
+          }
   }
 }
 
@@ -403,6 +546,13 @@ void gnpc_model_s::build_view() {
       t[i] = part_tc[i] ? v - h : h;
     }
     UWTC.upload(t.data(), t.size());
+    std::vector<float> u(map_tc_pair.size());
+    for (std::size_t i = 0; i < u.size(); ++i) {
+      const float v = map_tc_pair[i] >= 0 ? (float)p[map_tc_pair[i]] : 0.f;
+      const float h = tf32_rna(v);
+      u[i] = part_pair[i] ? v - h : h;
+    }
+    UWP.upload(u.data(), u.size());
     GNPC_CUDA(cudaDeviceSynchronize());
   }
   (void)L;
@@ -424,6 +574,14 @@ void gnpc_model_s::ensure_workspace() {
     GNPC_CUDA(cudaMemset(ticket.p, 0, sizeof(unsigned)));
   }
   sc.ensure(1);
+  if ((dp == 16 || dp == 32) && n > 0) {
+    for (int c = 0; c < 2; ++c)
+      if (tm_base[c] != X[c].p) {
+        tmX[c] = make_rows_map(X[c].p, (std::int64_t)n, dp, 128,
+                               dp == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+        tm_base[c] = X[c].p;
+      }
+  }
 }
 
 template <typename InT, typename OutT>
@@ -830,6 +988,15 @@ int gnpc_csr_info(gnpc_csr a, int64_t* n, int64_t* nnz) {
     need(a, "null csr");
     if (n) *n = a->h.n;
     if (nnz) *nnz = a->h.nnz();
+  });
+}
+
+int gnpc_csr_device_layout(gnpc_csr a, int* uploaded, int* sliced_ell, int* long_rows) {
+  return guarded([&] {
+    need(a, "null csr");
+    if (uploaded) *uploaded = a->dev_ready ? 1 : 0;
+    if (sliced_ell) *sliced_ell = a->has_sell ? 1 : 0;
+    if (long_rows) *long_rows = a->n_long;
   });
 }
 

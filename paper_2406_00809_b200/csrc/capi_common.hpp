@@ -2,6 +2,7 @@
 // structs.  Not part of the public boundary (include/gnpc.h is).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -28,6 +29,10 @@ struct NoDevice : std::runtime_error {
 };
 
 void set_error(const std::string& msg);
+
+// [rows][width] fp32 rows as a 2-D TMA tensor, box {width, box_rows}.
+CUtensorMap make_rows_map(const float* base, std::int64_t rows, int width, int box_rows,
+                          CUtensorMapSwizzle swizzle);
 extern std::atomic<std::int64_t> g_launches;
 
 #define GNPC_CUDA(expr)                                                                  \
@@ -146,8 +151,14 @@ struct gnpc_csr_s {
   // long-row chunk plan (kChunk nonzeros per warp)
   gnpc_impl::DevBuf<int> ch_row, ch_k0, ch_k1, long_c0;
   int n_chunks = 0;
+  // sliced-ELL copy for the tensor-core layer (see DevCsr)
+  gnpc_impl::DevBuf<int2> sell;
+  gnpc_impl::DevBuf<int> sell_off, sell_k;
+  bool has_sell = false;
   std::unique_ptr<gnpc_csr_s> tr;  // Âᵀ (lazy, for training backward)
   std::unique_ptr<gnpc_impl::KrylovWs> kws;
   void upload();
+  void build_sell(const std::vector<int>& hrp, const std::vector<int>& hci,
+                  const std::vector<float>& hv);
   gnpk::DevCsr dev();
 };

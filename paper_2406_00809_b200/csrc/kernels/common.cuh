@@ -19,6 +19,12 @@ struct DevCsr {
   const float* __restrict__ v;
   const int* __restrict__ long_rows;
   int n_long;
+  // Sliced-ELL copy (128-row slices, entry (r, k) of slice t at
+  // sell_off[t] + k*128 + r, padding (row, 0.0)); nullptr when the matrix's
+  // row lengths are too ragged for it.  sell_k[t] = K_t | (has long row) << 16.
+  const int2* __restrict__ sell;
+  const int* __restrict__ sell_off;
+  const int* __restrict__ sell_k;
 };
 
 // Per-apply scalars produced by the norm kernel (scale sandwich,

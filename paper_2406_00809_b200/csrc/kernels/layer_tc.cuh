@@ -35,7 +35,8 @@ struct TcCfg {
   static constexpr int G = DP / 4;
   static constexpr int NG = kThreads / G;
   static constexpr int R = TM / NG;                // rows per gather group
-  static constexpr int U = 4;                      // nonzeros per row per gather round
+  static constexpr int U = DP == 16 ? 4 : 2;       // nonzeros per row per gather round
+  static constexpr int US = DP == 16 ? 7 : 3;      // same, sliced-ELL path (no bounds state)
   static constexpr int CAP = 1536;                 // staged (col, val) entries per tile
   static constexpr int CPT = CAP / kThreads;       // staged entries per thread
   static constexpr int TCOLS = DP < 32 ? 32 : DP;  // TMEM columns (power of two >= 32)
@@ -53,11 +54,13 @@ struct TcCfg {
 // One group's R rows, U nonzeros per row per round: (col, val) for all R*U
 // slots first, then all R*U 128-bit X-row loads, then the FMAs in stored
 // column order — so every round keeps R*U independent loads in flight.
+// Slots past a row's end read a clamped in-range entry (a real neighbour of
+// the tile, so the X row is in bounds) with weight 0: acc + 0*x == acc, and
+// no predicated loads or register zeroing sit on the issue path.
 template <int DP, int R, int U, typename LD>
-__device__ __forceinline__ void gather_rounds(const float* __restrict__ X, LD load,
-                                              int (&pos)[R], const int (&end)[R],
-                                              const int (&kk)[R], int bs,
-                                              float4 (&acc)[R], int gl) {
+__device__ __forceinline__ void gather_rounds(const char* const (&xb)[R], long long rowbytes,
+                                              LD load, int last, int (&pos)[R],
+                                              const int (&end)[R], float4 (&acc)[R]) {
   while (true) {
     bool more = false;
 #pragma unroll
@@ -70,21 +73,15 @@ __device__ __forceinline__ void gather_rounds(const float* __restrict__ X, LD lo
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int k = pos[j] + u;
-        if (k < end[j]) {
-          load(k, c[j][u], w[j][u]);
-        } else {
-          c[j][u] = -1;
-          w[j][u] = 0.f;
-        }
+        load(min(k, last), c[j][u], w[j][u]);
+        w[j][u] = k < end[j] ? w[j][u] : 0.f;
       }
     float4 x[R][U];
 #pragma unroll
     for (int j = 0; j < R; ++j)
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        x[j][u] = c[j][u] >= 0
-                      ? ldg4(X + (static_cast<size_t>(c[j][u]) * bs + kk[j]) * DP + 4 * gl)
-                      : f4zero();
+        x[j][u] = ldg4(reinterpret_cast<const float*>(xb[j] + c[j][u] * rowbytes));
 #pragma unroll
     for (int j = 0; j < R; ++j) {
 #pragma unroll
@@ -92,6 +89,53 @@ __device__ __forceinline__ void gather_rounds(const float* __restrict__ X, LD lo
       pos[j] += U;
     }
   }
+}
+
+// Sliced-ELL gather: every row of the tile has K entries (padding carries
+// weight 0 and the row's own column), so the rounds need no bounds checks.
+template <int DP, int R, int U, int TM, int NG>
+__device__ __forceinline__ void gather_sell(const char* const (&xb)[R], const int2* cv, int K,
+                                           int gid, float4 (&acc)[R]) {
+  // rounds of U entries; the last round's missing slots are warp-uniformly
+  // predicated off, so a tile costs ceil(K/U) dependent load latencies
+  for (int k = 0; k < K; k += U) {
+    int c[R][U];
+    float w[R][U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool on = k + u < K;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int2 e = on ? cv[(k + u) * TM + gid + j * NG] : make_int2(0, 0);
+        c[j][u] = e.x;
+        w[j][u] = __int_as_float(e.y);
+      }
+    }
+    float4 x[R][U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool on = k + u < K;
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        x[j][u] = on ? ldg4(reinterpret_cast<const float*>(xb[j] + static_cast<long long>(c[j][u]) * (DP * 4)))
+                     : f4zero();
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < R; ++j) fma4(acc[j], w[j][u], x[j][u]);
+  }
+}
+
+// tf32 hi/lo split by truncation: hi keeps the top 10 mantissa bits, lo = x -
+// hi is exact in fp32; the tensor core reads lo's top 10 bits, so the split
+// loses < 2^-21 |x| (two integer/fp ops instead of cvt.rna's emulation).
+__device__ __forceinline__ void tf32_split(float4 v, float4& hi, float4& lo) {
+  hi = make_float4(__int_as_float(__float_as_int(v.x) & 0xffffe000),
+                   __int_as_float(__float_as_int(v.y) & 0xffffe000),
+                   __int_as_float(__float_as_int(v.z) & 0xffffe000),
+                   __int_as_float(__float_as_int(v.w) & 0xffffe000));
+  lo = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
 }
 
 // Epilogue modes: relu (forward layer), LAST (forward layer + projection MLP),
@@ -109,9 +153,13 @@ struct LayerIO {
   float* axout;        // optional: (ÂX) rows written out (training forward)
   const float* mask;   // kEpiMask: multiply by [mask > 0]
   int bs;
+  int dbg;             // timing experiments only (GNPC_LAYER_DBG): 1 no gather, 2 no MMA, 4 no store
 };
 
-template <int DP, int MODE, typename OutT>
+// PATH: kPathCsr (any bs), kPathCsr1 (bs == 1, the apply path: node ==
+// virtual row), kPathSell (bs == 1, sliced-ELL staging; a.sell required).
+enum { kPathCsr = 0, kPathCsr1 = 1, kPathSell = 2 };
+template <int DP, int MODE, typename OutT, int PATH = kPathCsr>
 __global__ void __launch_bounds__(kThreads, 2)
 k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ sc,
            OutT* __restrict__ out, const int* __restrict__ skip) {
@@ -123,7 +171,8 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
   const float* __restrict__ X = io.X;
   float* __restrict__ Y = io.Y;
   const float* __restrict__ axlong = io.axlong;
-  const int bs = io.bs;
+  constexpr bool BS1 = PATH != kPathCsr;
+  const int bs = BS1 ? 1 : io.bs;
   const int nv = a.n * bs;  // virtual rows
   const int ntiles = (nv + TM - 1) / TM;
   if (sc && sc->zero) {
@@ -150,7 +199,8 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
   float* D2 = B1 + (LAST ? net.hidden : 0);
   float* Part = D2 + (LAST ? net.hidden : 0);              // LAST: [2][TM]
   uint64_t* bar = reinterpret_cast<uint64_t*>(Part + (LAST ? 2 * TM : 0) + 4);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint64_t* fullb = bar + 1;  // SELL staging barriers [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int t = tid; t < int(2 * C::B_FLOATS / 4); t += kThreads)
@@ -163,7 +213,20 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
       D2[t] = net.dec2[t];
     }
   }
-  if (tid == 0) tc::mbar_init(bar, 1);
+  // sliced-ELL staging: one bulk copy per tile (thread 0), completion on fullb
+  constexpr bool sell = PATH == kPathSell;
+  auto sell_issue = [&](int t, int sl) {
+    if (t >= ntiles) return;
+    const int K = __ldg(a.sell_k + t) & 0xffff;
+    if (K == 0 || K * TM > CAP) return;
+    tc::mbar_expect_tx(&fullb[sl], K * TM * 8);
+    tc::bulk_load(s_cv + sl * CAP, a.sell + __ldg(a.sell_off + t), K * TM * 8, &fullb[sl]);
+  };
+  if (tid == 0) {
+    tc::mbar_init(bar, 1);
+    tc::mbar_init(&fullb[0], 1);
+    tc::mbar_init(&fullb[1], 1);
+  }
   if (warp == 0) tc::tmem_alloc(tslot, C::TCOLS);
 
   // ---- staging of a tile's row_ptr slice + (col, val) range (two halves so
@@ -209,7 +272,7 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
   };
 
   int tile = blockIdx.x;
-  {
+  if constexpr (!sell) {
     Stage s0;
     stage_rp(tile, s0);
     stage_cv(tile, s0);
@@ -219,6 +282,8 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+  if (sell && tid == 0) sell_issue(tile, 0);
+  uint32_t fph = 0;  // SELL barrier phases (bit per slot)
   const uint32_t tmem = *tslot;
   constexpr uint32_t idesc = tc::idesc_tf32(128, DP);
   const uint32_t sAhi = tc::smem_u32(Ahi), sAlo = tc::smem_u32(Alo);
@@ -230,6 +295,7 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
 
   // ---- epilogue of the tile whose accumulator sits in TMEM
   auto epilogue = [&](int row0) {
+    if (io.dbg & 2) return;
     tc::mbar_wait(bar, phase);
     phase ^= 1;
     tc::fence_after();
@@ -245,7 +311,7 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
       tc::tmem_ld16(taddr, v);
     }
     if constexpr (MODE == kEpiRelu) {
-      if (i < nv) {
+      if (i < nv && !(io.dbg & 4)) {
         float* yrow = Y + static_cast<size_t>(i) * DP + half * HC;
 #pragma unroll
         for (int c = 0; c < HC; c += 4)
@@ -322,6 +388,37 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
     const int row0 = tile * TM;
     const int next = tile + gridDim.x;
     Stage sn;
+    float4 acc[R], xs[R];
+    if constexpr (sell) {
+      // ------------------------------------------------------ gather (SELL)
+      if (tid == 0) sell_issue(next, slot ^ 1);  // slot^1 was released by the last barrier
+      const int kw = __ldg(a.sell_k + tile);
+      const int K = kw & 0xffff;
+      const bool staged = K > 0 && K * TM <= CAP;
+      const int2* cv = staged ? s_cv + slot * CAP : a.sell + __ldg(a.sell_off + tile);
+      const char* xb[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int i = row0 + gid + j * NG;
+        const bool valid = i < nv;
+        xb[j] = reinterpret_cast<const char*>(X + 4 * gl);
+        acc[j] = f4zero();
+        if ((kw >> 16) && valid && __ldg(a.rp + i + 1) - __ldg(a.rp + i) > kLongRow)
+          acc[j] = ldg4(axlong + static_cast<size_t>(i) * DP + 4 * gl);
+      }
+      if (staged) {
+        tc::mbar_wait(&fullb[slot], (fph >> slot) & 1);
+        fph ^= 1u << slot;
+      }
+      if (!(io.dbg & 1)) gather_sell<DP, R, C::US, TM, NG>(xb, cv, K, gid, acc);
+      // own rows after the gather (registers go to the gather's loads; for
+      // stencil-like rows the own row was just gathered and sits in L1)
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int i = row0 + gid + j * NG;
+        xs[j] = (i < nv && !(io.dbg & 16)) ? ldg4(X + static_cast<size_t>(i) * DP + 4 * gl) : f4zero();
+      }
+    } else {
     stage_rp(next, sn);  // loads only; consumed at the end of the iteration
 
     // ---------------------------------------------------------------- gather
@@ -329,16 +426,17 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
     const int kb = rp[TM + 2], ke = rp[TM + 3];
     const bool staged = ke - kb <= CAP;
     const int n0 = row0 / bs;
-    float4 acc[R], xs[R];
     {
-      int pos[R], end[R], kk[R];
+      int pos[R], end[R];
+      const char* xb[R];
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         const int r = gid + j * NG;
         const int i = row0 + r;  // virtual row
         const bool valid = i < nv;
         const int node = valid ? i / bs : n0;
-        kk[j] = i - node * bs;
+        const int kk = i - node * bs;
+        xb[j] = reinterpret_cast<const char*>(X + static_cast<size_t>(kk) * DP + 4 * gl);
         const int s = rp[node - n0], e = rp[node - n0 + 1];
         const bool longrow = axlong != nullptr && e - s > kLongRow;
         pos[j] = s;
@@ -346,6 +444,7 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
         acc[j] = (valid && longrow) ? ldg4(axlong + static_cast<size_t>(i) * DP + 4 * gl) : f4zero();
         xs[j] = valid ? ldg4(X + static_cast<size_t>(i) * DP + 4 * gl) : f4zero();
       }
+      const long long rowbytes = static_cast<long long>(bs) * DP * 4;
       if (staged) {
 #pragma unroll
         for (int j = 0; j < R; ++j) {
@@ -354,21 +453,21 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
         }
         const int2* cv = s_cv + slot * CAP;
         gather_rounds<DP, R, U>(
-            X,
+            xb, rowbytes,
             [cv](int k, int& c, float& w) {
               const int2 e = cv[k];
               c = e.x;
               w = __int_as_float(e.y);
             },
-            pos, end, kk, bs, acc, gl);
+            ke - kb - 1, pos, end, acc);
       } else {
         gather_rounds<DP, R, U>(
-            X,
+            xb, rowbytes,
             [&a](int k, int& c, float& w) {
               c = __ldg(a.ci + k);
               w = __ldg(a.v + k);
             },
-            pos, end, kk, bs, acc, gl);
+            ke - 1, pos, end, acc);
       }
       if (io.axout != nullptr) {
 #pragma unroll
@@ -379,6 +478,7 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
       }
     }
     stage_cv(next, sn);
+    }
 
     // ------------------------------------------------ previous tile: epilogue
     if (prev_row0 >= 0) epilogue(prev_row0);
@@ -388,17 +488,17 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
     for (int j = 0; j < R; ++j) {
       const int r = gid + j * NG;
       const float4 xi = xs[j], ax = acc[j];
-      const float4 xh = make_float4(tc::to_tf32(xi.x), tc::to_tf32(xi.y), tc::to_tf32(xi.z), tc::to_tf32(xi.w));
-      const float4 ah = make_float4(tc::to_tf32(ax.x), tc::to_tf32(ax.y), tc::to_tf32(ax.z), tc::to_tf32(ax.w));
-      const float4 xl = make_float4(xi.x - xh.x, xi.y - xh.y, xi.z - xh.z, xi.w - xh.w);
-      const float4 al = make_float4(ax.x - ah.x, ax.y - ah.y, ax.z - ah.z, ax.w - ah.w);
+      float4 xh, xl, ah, al;
+      tf32_split(xi, xh, xl);
+      tf32_split(ax, ah, al);
+      if (io.dbg & 8) continue;
       const uint32_t ox = tc::sw128_off(r, 4 * gl, TM), oa = tc::sw128_off(r, DP + 4 * gl, TM);
       *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Ahi) + ox) = xh;
       *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Alo) + ox) = xl;
       *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Ahi) + oa) = ah;
       *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Alo) + oa) = al;
     }
-    stage_store(next, sn, slot ^ 1);
+    if constexpr (!sell) stage_store(next, sn, slot ^ 1);
     tc::fence_proxy_async();
     __syncthreads();
 
@@ -410,7 +510,7 @@ k_layer_tc(DevCsr a, LayerIO io, NetView net, const ApplyScalars* __restrict__ s
     }
 
     // ---------------------------------------------------------------- MMA
-    if (tid == 0) {
+    if (tid == 0 && !(io.dbg & 2)) {
       tc::fence_after();
       uint32_t accf = 0;
 #pragma unroll

@@ -27,8 +27,9 @@ struct gnpc_model_s {
   gnpc_impl::DevBuf<float> P;  // device fp32 params (NetView points into it)
   gnpc_impl::DevBuf<float> LIFT;  // piecewise-linear lift tables (kinks, alpha, beta)
   gnpc_impl::DevBuf<float> UWTC;  // per layer [U;W]^T split tf32 hi/lo, tcgen05 layout
+  gnpc_impl::DevBuf<float> UWP;   // per layer [Bu_hi|Bw_hi|Bu_lo|Bw_lo], k_layer_sell layout
   bool use_tc = true;             // DP 16/32: tcgen05 transform (GNPC_NO_TC=1: CUDA cores)
-  int tc_per_sm[4] = {0, 0, 0, 0};  // cached occupancy per (last, OutT) tcgen05 kernel
+  int tc_per_sm[8] = {};  // cached occupancy per (last, OutT, path) tcgen05 kernel
   gnpk::NetView view{};
   // apply workspace
   gnpc_impl::DevBuf<float> X[2], AXL, LPART;  // LPART: long-row chunk partials
@@ -41,6 +42,11 @@ struct gnpc_model_s {
   // flat-parameter index maps (see capi.cu build_maps)
   std::vector<int> map_view, map_bt_fwd, map_bt_bwd, map_tc_fwd, map_tc_bwd;
   std::vector<unsigned char> part_tc;
+  std::vector<int> map_tc_pair;  // flat param -> UWP (same entries as map_tc_fwd, permuted)
+  std::vector<unsigned char> part_pair;
+  // TMA maps over the two activation buffers (k_layer_sell)
+  CUtensorMap tmX[2]{};
+  const float* tm_base[2] = {nullptr, nullptr};
   std::size_t o_enc1 = 0, o_enc1b = 0, o_enc2 = 0, o_enc2b = 0, o_uw = 0, o_dec1 = 0,
               o_dec1b = 0, o_dec2 = 0, o_dec2b = 0;
   void build_maps();

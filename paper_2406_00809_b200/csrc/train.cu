@@ -39,7 +39,8 @@ struct gnpc_trainer_s {
   DevBuf<double> p64, g64, m1, m2;
   // regeneration maps (see gnpc_model_s::build_maps)
   DevBuf<int> map_view, map_bt_fwd, map_bt_bwd, map_tc_fwd, map_tc_bwd;
-  DevBuf<unsigned char> part_tc;
+  DevBuf<unsigned char> part_tc, part_pair;
+  DevBuf<int> map_tc_pair;
   DevBuf<float> BT_fwd, BT_bwd, UWTC_bwd;
   // batch
   DevBuf<double> xb, bb, out, sgn, gout, colpart, losspart, tmp;
@@ -97,31 +98,9 @@ void make_red(gnpc_trainer_s::Red& r, const float* A1, int P1, int s1, const flo
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q{};
-    void* p = nullptr;
-    GNPC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    if (q != cudaDriverEntryPointSuccess || !p) throw CudaError("cuTensorMapEncodeTiled unavailable");
-    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
 // [nv][32] fp32 rows viewed as a 2-D tensor, box {32 features, 128 rows}, 128B swizzle.
 CUtensorMap rows32_map(const float* base, int nv) {
-  CUtensorMap m{};
-  const cuuint64_t dims[2] = {32, (cuuint64_t)nv};
-  const cuuint64_t strides[1] = {32 * sizeof(float)};
-  const cuuint32_t box[2] = {32, 128};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = tensor_map_encoder()(
-      &m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed");
-  return m;
+  return make_rows_map(base, nv, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 // tcgen05 reduction: A = [A1 | A2 or ones] (<= 32 features each), B (<= 32),
@@ -216,6 +195,9 @@ void regenerate(gnpc_trainer_s& T) {
     GNPC_LAUNCHED();
     gnpk::k_gather_split<<<(c + kTh - 1) / kTh, kTh, 0, T.s>>>(T.p64.p, T.map_tc_bwd.p, T.part_tc.p, c,
                                                                T.UWTC_bwd.p);
+    GNPC_LAUNCHED();
+    gnpk::k_gather_split<<<(c + kTh - 1) / kTh, kTh, 0, T.s>>>(T.p64.p, T.map_tc_pair.p, T.part_pair.p, c,
+                                                               m.UWP.p);
     GNPC_LAUNCHED();
   } else {
     const int c = (int)m.map_bt_fwd.size();
@@ -419,6 +401,8 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
     upload_i(T->map_tc_fwd, m->map_tc_fwd);
     upload_i(T->map_tc_bwd, m->map_tc_bwd);
     T->part_tc.upload(m->part_tc.data(), m->part_tc.size());
+    upload_i(T->map_tc_pair, m->map_tc_pair);
+    T->part_pair.upload(m->part_pair.data(), m->part_pair.size());
     T->UWTC_bwd.alloc(m->map_tc_bwd.size());
   } else {
     upload_i(T->map_bt_fwd, m->map_bt_fwd);

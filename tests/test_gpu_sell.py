@@ -1,0 +1,115 @@
+"""Parity of the sliced-ELL TMA layer pipeline (k_layer_sell) against the
+oracle, and against the CSR tensor-core layer on the same inputs.
+
+The device CSR builds its sliced-ELL copy at upload when row lengths are
+regular enough (GNPC_NO_SELL=1 suppresses it for one upload), so the same
+matrix can be pushed through both kernel paths in one process.  Cases cover
+the shapes the pipeline special-cases: staged slices (K <= 24), slices read
+straight from HBM (24 < K <= 32), tiles holding long rows (> 32 nonzeros,
+chunked path + sliced-ELL padding), a partial last tile, and the projection
+epilogue of both widths."""
+import os
+
+import numpy as np
+import pytest
+from conftest import f32, max_rel, rel_l2
+
+from oracle import Csr
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def apply_path(capi, a: Csr, dims, p, b, sell):
+    # the device copy (and its sliced-ELL slices) is built at the first apply
+    if not sell:
+        os.environ["GNPC_NO_SELL"] = "1"
+    try:
+        c = capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
+        y = capi.Model(c, dims, p).apply(b)
+        uploaded, sell_built, _ = c.device_layout()
+        assert uploaded and sell_built == sell
+        return y
+    finally:
+        os.environ.pop("GNPC_NO_SELL", None)
+
+
+def apply_both(capi, oc, a, dims, seed):
+    p = f32(oc.init_params(*dims, seed))
+    b = oc.gaussian_vector(seed + 1, a.n)
+    want = oc.gnn_apply(a, dims, p, b)
+    y_sell = apply_path(capi, a, dims, p, b, True)
+    y_csr = apply_path(capi, a, dims, p, b, False)
+    return y_sell, y_csr, want
+
+
+def check(y, want, tol=TOL):
+    assert rel_l2(y, want) <= tol, rel_l2(y, want)
+    assert max_rel(y, want) <= tol, max_rel(y, want)
+
+
+def stencil_plus(oc, grid, extra_rows=(), extra_len=0, seed=0):
+    """5-point stencil on grid x grid, optionally with some rows widened to
+    extra_len nonzeros (random columns, small values)."""
+    a = oc.gen_convection_diffusion(grid, 0.3)
+    n = a.n
+    rows, cols, vals = [], [], []
+    rng = np.random.default_rng(seed)
+    for i in range(n):
+        s, e = a.row_ptr[i], a.row_ptr[i + 1]
+        rows += [i] * (e - s)
+        cols += list(a.col_idx[s:e])
+        vals += list(a.values[s:e])
+        if i in extra_rows:
+            have = set(a.col_idx[s:e].tolist())
+            c = [int(x) for x in rng.choice(n, size=extra_len + 8, replace=False) if int(x) not in have]
+            c = c[: extra_len - (e - s)]
+            rows += [i] * len(c)
+            cols += c
+            vals += list(0.01 * rng.standard_normal(len(c)))
+    t = oc.csr_from_triplets(n, rows, cols, vals)
+    return oc.prescale(t, oc.gershgorin_gamma(t)).rounded_f32()
+
+
+@pytest.mark.parametrize("d", [16, 32])
+def test_sell_stencil_partial_tile(capi, oc, cuda, d):
+    a = stencil_plus(oc, 45)  # n = 2025: last tile holds 105 rows
+    y_sell, y_csr, want = apply_both(capi, oc, a, (d, 32, 8), 5)
+    check(y_sell, want)
+    check(y_csr, want)
+    assert rel_l2(y_sell, y_csr) <= 2e-6
+
+
+@pytest.mark.parametrize("d", [16, 32])
+def test_sell_with_long_rows(capi, oc, cuda, d):
+    a = stencil_plus(oc, 40, extra_rows={3, 130, 131, 700, 1599}, extra_len=300)
+    assert np.diff(a.row_ptr).max() >= 300
+    y_sell, y_csr, want = apply_both(capi, oc, a, (d, 32, 4), 7)
+    check(y_sell, want)
+    check(y_csr, want)
+
+
+@pytest.mark.parametrize("d", [16, 32])
+def test_sell_unstaged_wide_slices(capi, oc, cuda, d):
+    # every row of some tiles has 28 entries: K > 24 -> slices read from HBM
+    n = 1000
+    rng = np.random.default_rng(11)
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        k = 28 if (i // 128) % 2 == 0 else 6
+        c = rng.choice(n, size=k, replace=False)
+        rows += [i] * k
+        cols += c.tolist()
+        vals += (rng.standard_normal(k) / k).tolist()
+    t = oc.csr_from_triplets(n, rows, cols, vals)
+    a = oc.prescale(t, oc.gershgorin_gamma(t)).rounded_f32()
+    y_sell, y_csr, want = apply_both(capi, oc, a, (d, 32, 3), 9)
+    check(y_sell, want)
+    check(y_csr, want)
+
+
+def test_sell_odd_hidden_projection(capi, oc, cuda):
+    # hidden not a multiple of 4: scalar projection loop
+    a = stencil_plus(oc, 33)
+    y_sell, _, want = apply_both(capi, oc, a, (32, 13, 2), 3)
+    check(y_sell, want)

@@ -55,58 +55,86 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
-
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: NVML polled every 2 ms from a thread (the timed regions are tens
+    of ms), nvidia-smi -lms 100 as the fallback."""
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.rows = []  # (sm_mhz, sm_max_mhz, set(reasons))
+        self.stop_ev = threading.Event()
         self.t = None
+        self.proc = None
 
     def start(self):
         try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
+                    "hw_power_brake_slowdown": nv.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+
+            def poll():
+                while not self.stop_ev.is_set():
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((float(sm), float(mx), {k for k, v in bits.items() if r & v}))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            pass
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except FileNotFoundError:
-            self.proc = None
             return
 
         def reader():
             for line in self.proc.stdout:
-                self.rows.append([x.strip() for x in line.split(",")])
+                r = [x.strip() for x in line.split(",")]
+                try:
+                    self.rows.append((float(r[0]), float(r[1]),
+                                      {nm for nm, v in zip(names, r[2:6]) if v.lower() == "active"}))
+                except (ValueError, IndexError):
+                    continue
 
         self.t = threading.Thread(target=reader, daemon=True)
         self.t.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        self.t.join(timeout=2)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        self.stop_ev.set()
+        if self.proc is not None:
+            self.proc.terminate()
             try:
-                sm.append(float(r[0]))
-                mx.append(float(r[1]))
-                for nm, v in zip(names, r[2:6]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
-            except (ValueError, IndexError):
-                continue
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.t is not None:
+            self.t.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0}
+        reasons = set()
+        for r in self.rows:
+            reasons |= r[2]
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": max(r[1] for r in self.rows), "reasons": sorted(reasons),
+                "samples": len(self.rows)}
 
 
 def build_workload(capi, cfg_name):
@@ -254,17 +282,26 @@ def run_train_bench(args, capi, torch, rank, world, local, dist):
     dims = (32, 32, 8)
     m = capi.Model(ah, dims, capi.init_params(*dims, 0))
     t = capi.Trainer(m, B, lr=1e-3)
+    if dist:
+        # data-parallel over samples: B per rank, one NCCL all-reduce of the
+        # flat f64 gradient per step (paper_2406_00809_b200.dp)
+        from paper_2406_00809_b200.dp import DataParallelTrainer, TrainerEngine
+
+        dp = DataParallelTrainer(TrainerEngine(t))
+        do = dp.step_synthetic
+    else:
+        do = t.step_synthetic
     clocks = ClockSampler(local)
     clocks.start()
     for i in range(args.warmup):
-        t.step_synthetic(1000 + rank)
+        do(1000)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     l0 = capi.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    losses = [t.step_synthetic(1000 + rank) for _ in range(args.steps)]
+    losses = [do(1000) for _ in range(args.steps)]
     ev1.record()
     torch.cuda.synchronize()
     launches = capi.launch_count() - l0
@@ -285,7 +322,8 @@ def run_train_bench(args, capi, torch, rank, world, local, dist):
         "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32", "data": "synthetic (device Philox x ~ N(0,I), b = A x)",
         "config": {"workload": "C3 2D var-coeff diffusion 512^2 lognormal(0,2^2), d=32 L=8 B=32, Adam 1e-3",
-                   "n": n, "nnz": nnz, "batch": B,
+                   "n": n, "nnz": nnz, "batch": B, "global_batch": B * world,
+                   "parallelism": f"dp{world} (gradient all-reduce, NCCL)" if world > 1 else "dp1",
                    "l2": "activations 18 GiB >> L2 (no flush needed)"},
         "roofline": {"bound": "hbm", "achieved": sb / step_s / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": sb / step_s / 1e9 / peak, "traffic": None,
@@ -380,6 +418,14 @@ def main():
     value = world * args.steps / (max_ms / 1e3)
 
     # ---- roofline: per-kernel event timing of the same workload
+    dp = 4 if d <= 4 else (8 if d <= 8 else (16 if d <= 16 else (32 if d <= 32 else 64)))
+    sell = w["a"].device_layout()[1]
+    if dp in (16, 32) and sell:
+        layer_kernel = f"k_layer_sell<DP={dp}> (fused Res-GCONV, sliced-ELL TMA pipeline, tcgen05 3xTF32)"
+    elif dp in (16, 32):
+        layer_kernel = f"k_layer_tc<DP={dp}> (fused Res-GCONV, CSR gather, tcgen05 3xTF32)"
+    else:
+        layer_kernel = f"k_layer<DP={dp}> (fused Res-GCONV, CUDA cores)"
     ms_k = np.zeros(5)
     cnt_k = np.zeros(5, np.int64)
     for i in range(args.steps):
@@ -387,7 +433,7 @@ def main():
         model.apply_profile(bs[i % nb].data_ptr(), out.data_ptr(), sptr, ms_k, cnt_k)
     layer_ms = (ms_k[3] + ms_k[4]) / max(1, cnt_k[3] + cnt_k[4])
     mid_ms = ms_k[3] / max(1, cnt_k[3])
-    lb = layer_bytes(n, nnz, d if d >= 4 else 4)
+    lb = layer_bytes(n, nnz, dp)
     peak, peak_src = load_peaks()
     achieved = lb / (mid_ms / 1e3) / 1e9 if cnt_k[3] else lb / (layer_ms / 1e3) / 1e9
     traffic = None
@@ -453,7 +499,7 @@ def main():
                    "parallelism": f"replicas x{world}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": f"k_layer<DP={d if d >= 4 else 4}> (fused Res-GCONV)",
+                     "kernel": layer_kernel,
                      "algorithmic_bytes_per_launch": lb, "avg_launch_ms": mid_ms,
                      "peak_source": peak_src,
                      "kernel_share_of_step": float((ms_k[3] + ms_k[4]) / max(ms_k.sum(), 1e-12))},

@@ -182,11 +182,14 @@ int gnpc_train_step_synthetic(gnpc_trainer t, uint64_t seed, double* loss);
 /* Loss of the current params on a batch (monitoring_loss, src/gnn.cpp:390-397). */
 int gnpc_monitor_loss(gnpc_trainer t, const double* x, const double* b, int64_t batch,
                       double* loss);
-/* Data-parallel split of a step: the flat f64 device gradient buffer (batch
- * sum, reference flat order) that a collective (NCCL all-reduce) sums in
- * place between gnpc_train_backward_only and gnpc_train_apply_grads. */
+/* Data-parallel split of a step: the flat f64 device gradient
+ * buffer (gradient of this trainer's batch loss (1/B)Σ_k, reference flat
+ * order) that a collective averages in place over ranks between
+ * gnpc_train_backward_only / gnpc_train_backward_synthetic and
+ * gnpc_train_apply_grads (replaces accumulate, src/gnn.cpp:439-440). */
 int gnpc_trainer_grad_buffer(gnpc_trainer t, double** dev_ptr, int64_t* count);
 int gnpc_train_backward_only(gnpc_trainer t, const double* x, const double* b, double* loss);
+int gnpc_train_backward_synthetic(gnpc_trainer t, uint64_t seed, double* loss);
 int gnpc_train_apply_grads(gnpc_trainer t);
 int gnpc_trainer_adam_state(gnpc_trainer t, double* m1, double* m2, int64_t* step);
 /* Current f64 master parameters (flat reference order). */

@@ -339,6 +339,11 @@ class Trainer:
                                              C.byref(loss)))
         return loss.value
 
+    def backward_synthetic(self, seed: int):
+        loss = C.c_double()
+        check(lib().gnpc_train_backward_synthetic(self.h, C.c_uint64(seed), C.byref(loss)))
+        return loss.value
+
     def apply_grads(self):
         check(lib().gnpc_train_apply_grads(self.h))
 

@@ -615,20 +615,38 @@ int gnpc_train_step(gnpc_trainer t, const double* x, const double* b, double* lo
   });
 }
 
+namespace {
+// device pairs x ~ N(0, I) (Philox keyed by seed and the Adam step), b = A x,
+// then forward + loss + backward into g64
+double synthetic_fb(gnpc_trainer_s& T, uint64_t seed) {
+  const std::size_t cnt = (std::size_t)T.n * T.B;
+  gnpk::k_philox_normal<<<(int)((cnt / 4 + kTh) / kTh), kTh, 0, T.s>>>(seed, (unsigned long long)T.t, cnt,
+                                                                      T.xb.p);
+  GNPC_LAUNCHED();
+  gnpk::DevCsr a = T.m->a->dev();
+  gnpk::k_spmm_nb<<<T.loss_grid, kTh, 0, T.s>>>(a, T.B, T.xb.p, T.bb.p);
+  GNPC_LAUNCHED();
+  forward(T);
+  const double l = loss_and_grad(T, true);
+  backward(T);
+  return l;
+}
+}  // namespace
+
 int gnpc_train_step_synthetic(gnpc_trainer t, uint64_t seed, double* loss) {
   return guarded([&] {
     need(t != nullptr, "train_step_synthetic: null trainer");
-    const std::size_t cnt = (std::size_t)t->n * t->B;
-    gnpk::k_philox_normal<<<(int)((cnt / 4 + kTh) / kTh), kTh, 0, t->s>>>(seed, (unsigned long long)t->t,
-                                                                          cnt, t->xb.p);
-    GNPC_LAUNCHED();
-    gnpk::DevCsr a = t->m->a->dev();
-    gnpk::k_spmm_nb<<<t->loss_grid, kTh, 0, t->s>>>(a, t->B, t->xb.p, t->bb.p);
-    GNPC_LAUNCHED();
-    forward(*t);
-    const double l = loss_and_grad(*t, true);
-    backward(*t);
+    const double l = synthetic_fb(*t, seed);
     adam(*t);
+    if (loss) *loss = l;
+  });
+}
+
+int gnpc_train_backward_synthetic(gnpc_trainer t, uint64_t seed, double* loss) {
+  return guarded([&] {
+    need(t != nullptr, "train_backward_synthetic: null trainer");
+    const double l = synthetic_fb(*t, seed);
+    GNPC_CUDA(cudaStreamSynchronize(t->s));
     if (loss) *loss = l;
   });
 }

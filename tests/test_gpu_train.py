@@ -135,3 +135,26 @@ def test_python_train_drop_in(gnp, cuda):
     b = gnp.spmv(a, [1.0] * a.n)
     out = gnp.solve(a, b, precond="gnp", params=params, maxiters=200)
     assert out["status"] in ("converged", "maxiters")
+
+
+def test_data_parallel_driver_single_rank_equals_step(capi, cuda):
+    # paper_2406_00809_b200.dp on one rank (no process group): local backward,
+    # (no-op) all-reduce, Adam — bit-identical to the fused trainer step
+    import torch  # noqa: F401  (CUDA context for the zero-copy gradient view)
+    from paper_2406_00809_b200.dp import DataParallelTrainer, TrainerEngine
+
+    a = capi.Csr.generate("c3_varcoeff2d", 48, 2.0, 0.0, 2)
+    ah = a.prescale(a.gamma())
+    p0 = capi.init_params(32, 32, 8, 0)
+    t1 = capi.Trainer(capi.Model(ah, (32, 32, 8), p0), 8, lr=1e-3)
+    t2 = capi.Trainer(capi.Model(ah, (32, 32, 8), p0), 8, lr=1e-3)
+    dp = DataParallelTrainer(TrainerEngine(t2))
+    l1 = [t1.step_synthetic(11) for _ in range(4)]
+    l2 = [dp.step_synthetic(11) for _ in range(4)]
+    assert l1 == l2
+    assert np.array_equal(t1.params(), t2.params())
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((ah.n, 8))
+    b = np.stack([ah.spmv(x[:, k]) for k in range(8)], axis=1)
+    assert dp.step(x, b) == t1.step(x.ravel(order="F"), b.ravel(order="F"))
+    assert np.array_equal(t1.params(), t2.params())

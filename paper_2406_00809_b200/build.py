@@ -27,6 +27,8 @@ CXX = "/usr/bin/g++"  # the system g++ links libstdc++.so dynamically (numpy loa
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
                      "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+if os.environ.get("GNPC_DEBUG_HANG") == "1":  # bounded pipeline waits that trap (debug only)
+    NVCC_FLAGS += ["-DGNPC_DEBUG_HANG"]
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-Wall"]
 
 CU_SOURCES = ["capi.cu", "train.cu"]

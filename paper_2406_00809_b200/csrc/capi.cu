@@ -137,17 +137,21 @@ struct ApplyLaunch {
           const char* e = std::getenv("GNPC_NO_SELL_KERNEL");
           return e && std::string(e) == "1";
         }();
-        if (m.use_tc && a.sell && !sell_off) {
-          // sliced-ELL TMA pipeline, one 512-thread CTA per SM
-          using S = SellCfg<DP>;
-          const size_t smem = S::smem_bytes(last, net.hidden);
-          auto kern = last ? k_layer_sell<DP, true, OutT> : k_layer_sell<DP, false, OutT>;
-          static std::once_flag f[2];
-          std::call_once(f[last ? 1 : 0], [&] {
+        if (m.use_tc && !sell_off) {
+          // TMA pipeline, one 544-thread CTA per SM: sliced-ELL slices on
+          // regular matrices, the short-row CSR ranges on ragged ones
+          const bool csr = a.sell == nullptr;
+          using S = SellCfg<DP, false>;
+          using SC = SellCfg<DP, true>;
+          const size_t smem = csr ? SC::smem_bytes(last, net.hidden) : S::smem_bytes(last, net.hidden);
+          auto kern = csr ? (last ? k_layer_sell<DP, true, OutT, true> : k_layer_sell<DP, false, OutT, true>)
+                          : (last ? k_layer_sell<DP, true, OutT> : k_layer_sell<DP, false, OutT>);
+          static std::once_flag f[4];
+          std::call_once(f[(last ? 1 : 0) + (csr ? 2 : 0)], [&] {
             GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
           });
           const int tiles_s = (n + S::TM - 1) / S::TM;
-          const int grid = std::max(1, std::min(tiles_s, sms));
+          const int grid = std::max(1, std::min(tiles_s, S::CPS * sms));
           SellMaps maps{m.tmX[cur], m.tmX[1 - cur]};
           const float* uwp = m.UWP.p + (size_t)l * 4 * DP * DP;
           kern<<<grid, S::NT, smem, s>>>(a, maps, X, axl, uwp, net, m.sc.p, out, skip);
@@ -279,6 +283,34 @@ void gnpc_csr_s::upload() {
     long_c0.upload(c0.data(), c0.size());
   }
   build_sell(hrp, hci, hv);
+  // short-row CSR (long rows emptied), padded for the TMA pipeline's bulk copies
+  {
+    const std::int64_t n = h.n;
+    std::vector<int> srp(n + 1 + 132), sci, tf((n + 127) / 128, 0);
+    std::vector<float> sv;
+    sci.reserve(hci.size() + 4);
+    sv.reserve(hv.size() + 4);
+    srp[0] = 0;
+    for (std::int64_t i = 0; i < n; ++i) {
+      const int s = hrp[i], e = hrp[i + 1];
+      if (e - s > gnpk::kLongRow) {
+        tf[i / 128] = 1;
+      } else {
+        sci.insert(sci.end(), hci.begin() + s, hci.begin() + e);
+        sv.insert(sv.end(), hv.begin() + s, hv.begin() + e);
+      }
+      srp[i + 1] = static_cast<int>(sci.size());
+    }
+    for (std::size_t i = n + 1; i < srp.size(); ++i) srp[i] = srp[n];
+    for (int k = 0; k < 4; ++k) {
+      sci.push_back(0);
+      sv.push_back(0.f);
+    }
+    rps.upload(srp.data(), srp.size());
+    cis.upload(sci.data(), sci.size());
+    vs.upload(sv.data(), sv.size());
+    tflag.upload(tf.data(), tf.size());
+  }
   GNPC_CUDA(cudaDeviceSynchronize());
   dev_ready = true;
 }
@@ -355,6 +387,10 @@ gnpk::DevCsr gnpc_csr_s::dev() {
   d.v = v.p;
   d.long_rows = n_long ? long_rows.p : nullptr;
   d.n_long = n_long;
+  d.rps = rps.p;
+  d.cis = cis.p;
+  d.vs = vs.p;
+  d.tflag = tflag.p;
   d.sell = has_sell ? sell.p : nullptr;
   d.sell_off = has_sell ? sell_off.p : nullptr;
   d.sell_k = has_sell ? sell_k.p : nullptr;

@@ -155,6 +155,9 @@ struct gnpc_csr_s {
   gnpc_impl::DevBuf<int2> sell;
   gnpc_impl::DevBuf<int> sell_off, sell_k;
   bool has_sell = false;
+  // padded short-row CSR + per-tile long flags for the TMA CSR layer (see DevCsr)
+  gnpc_impl::DevBuf<int> rps, cis, tflag;
+  gnpc_impl::DevBuf<float> vs;
   std::unique_ptr<gnpc_csr_s> tr;  // Âᵀ (lazy, for training backward)
   std::unique_ptr<gnpc_impl::KrylovWs> kws;
   void upload();

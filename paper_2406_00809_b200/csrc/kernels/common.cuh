@@ -25,6 +25,14 @@ struct DevCsr {
   const int2* __restrict__ sell;
   const int* __restrict__ sell_off;
   const int* __restrict__ sell_k;
+  // Short-row CSR (rows with > kLongRow nonzeros emptied; they take the
+  // chunked long-row path), padded for 16-byte bulk copies: rps has n+1+132
+  // entries (tail = nnz_short), cis/vs nnz_short+4.  tflag[t] = 1 if the
+  // 128-row tile t holds a long row.  Aliases the full CSR when n_long == 0.
+  const int* __restrict__ rps;
+  const int* __restrict__ cis;
+  const float* __restrict__ vs;
+  const int* __restrict__ tflag;
 };
 
 // Per-apply scalars produced by the norm kernel (scale sandwich,

@@ -33,6 +33,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// Debug builds (-DGNPC_DEBUG_HANG): a bounded wait that reports and traps
+// instead of spinning forever on a pipeline protocol bug.
+__device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t phase, int tag, int it) {
+#ifdef GNPC_DEBUG_HANG
+  long long spins = 0;
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (ok) return;
+    if (++spins == (1ll << (tag == 1 ? 25 : 22))) {
+      printf("HANG block %d warp %d tag %d it %d phase %u\n", blockIdx.x, threadIdx.x >> 5, tag, it, phase);
+      asm volatile("trap;");
+    }
+  }
+#else
+  (void)tag;
+  (void)it;
+  mbar_wait(bar, phase);
+#endif
+}
+
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }

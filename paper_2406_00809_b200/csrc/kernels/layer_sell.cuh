@@ -97,12 +97,15 @@ struct SellCfg {
   static constexpr int R = TM / NG;              // rows per group
   static constexpr int US = DP == 16 ? 8 : 3;    // slice entries per gather round
   static constexpr int USC = DP == 16 ? 8 : 4;   // CSR entries per gather round
-  static constexpr int NS = DP == 16 ? 4 : 3;    // TMA ring depth (tiles)
+  // TMA ring depth (tiles) and epilogue lag (A/TMEM buffer sets), measured
+  // per format: SELL DP16 (C2) best at NS 4 / LAG 1 (LAG 2 + NS 5: 25.7 vs
+  // 24.4 us); CSR DP16 (C4) at NS 5 (166 vs 197 us at NS 4); DP32 fills smem
+  static constexpr int NS = DP == 16 ? (CSR ? 5 : 4) : 3;
   static constexpr int KCAP = 24;                // slices with K <= KCAP are staged (mult. of US)
   static constexpr uint32_t OPB = TM * DP * 4;   // one A-type operand / X tile / Y tile (bytes)
   static constexpr uint32_t BB = DP * DP * 4;    // one B operand (bytes)
   static constexpr int TCOLS = 2 * DP;           // TMEM accumulator columns (two halves)
-  static constexpr int LAG = 1;                  // epilogue lag = A/TMEM buffer sets (2 measured slower)
+  static constexpr int LAG = 1;
   static constexpr int TALLOC = LAG * TCOLS < 32 ? 32 : LAG * TCOLS;  // power of two >= 32
   static constexpr uint32_t CVB = KCAP * TM * 8; // staged slice (bytes)
   // CSR: [X tile | row_ptr slice (TM+4 ints, 1 KiB) | col_idx (CAPC) | values (CAPC)]

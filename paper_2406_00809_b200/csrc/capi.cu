@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -91,6 +92,56 @@ struct ApplyLaunch {
     auto mark = [&](int k) {
       if (prof) prof->mark(k, s);
     };
+    static const bool sell_off = [] {
+      const char* e = std::getenv("GNPC_NO_SELL_KERNEL");
+      return e && std::string(e) == "1";
+    }();
+    static const bool fused_off = [] {
+      const char* e = std::getenv("GNPC_NO_FUSED_APPLY");
+      return e && std::string(e) == "1";
+    }();
+    if constexpr (DP == 16 || DP == 32) {
+      // the whole apply as one persistent cooperative launch (no long rows:
+      // those need their chunk kernels between layers).  The per-kernel
+      // profile keeps the per-layer launches so each phase can be timed.
+      // DP=16 only: at DP=32 the in-kernel layers measured slower than
+      // separate launches (C5: 499 vs 450 us per layer) while DP=16 gains
+      // (C2: 17 vs 24 us per layer: no launch gap or prologue per layer)
+      if (DP == 16 && m.use_tc && !sell_off && !fused_off && A.n_long == 0 && prof == nullptr && n > 0) {
+        const bool csr = a.sell == nullptr;
+        using S = SellCfg<DP, false>;
+        using SC = SellCfg<DP, true>;
+        const size_t smem = csr ? SC::smem_bytes(net.hidden) : S::smem_bytes(net.hidden);
+        auto kern = csr ? k_apply_sell<DP, InT, OutT, true> : k_apply_sell<DP, InT, OutT, false>;
+        static std::once_flag f[2];
+        std::call_once(f[csr ? 1 : 0], [&] {
+          cudaFuncAttributes fa{};
+          GNPC_CUDA(cudaFuncGetAttributes(&fa, (const void*)kern));  // static smem counts against 227 KB
+          GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024 - (int)fa.sharedSizeBytes));
+        });
+        const int tiles = (n + S::TM - 1) / S::TM;
+        const int grid = std::max(1, std::min(tiles, sms));
+        static const bool times = std::getenv("GNPC_FUSED_TIMES") != nullptr;
+        static gnpc_impl::DevBuf<unsigned long long> tbuf;
+        if (times && !tbuf.p) tbuf.alloc(64);
+        ApplyFused fa{m.tmX[0], m.tmX[1], m.X[0].p, m.X[1].p, m.UWP.p, m.partials.p, m.gbar.p,
+                      m.gbar_host, m.sc.p, times ? tbuf.p : nullptr};
+        m.gbar_host += (unsigned long long)grid * (1 + net.layers);
+        void* args[] = {(void*)&a, (void*)&fa, (void*)&in, (void*)&net, (void*)&out, (void*)&skip};
+        GNPC_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(S::NT), args, smem, s));
+        GNPC_LAUNCHED();
+        if (times) {
+          unsigned long long h[64];
+          GNPC_CUDA(cudaMemcpyAsync(h, tbuf.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+          GNPC_CUDA(cudaStreamSynchronize(s));
+          std::fprintf(stderr, "fused phases (us):");
+          for (int k = 1; k < 2 * net.layers + 2; ++k) std::fprintf(stderr, " %.1f", (h[k] - h[k - 1]) * 1e-3);
+          std::fprintf(stderr, "\n");
+        }
+        return;
+      }
+    }
     // τ
     mark(0);
     k_apply_norm<InT><<<m.norm_grid, kThreads, 0, s>>>(in, n, m.partials.p, m.ticket.p, m.sc.p, skip);
@@ -133,17 +184,13 @@ struct ApplyLaunch {
       const bool last = l + 1 == net.layers;
       mark(last ? 4 : 3);
       if constexpr (DP == 16 || DP == 32) {
-        static const bool sell_off = [] {
-          const char* e = std::getenv("GNPC_NO_SELL_KERNEL");
-          return e && std::string(e) == "1";
-        }();
         if (m.use_tc && !sell_off) {
           // TMA pipeline, one 544-thread CTA per SM: sliced-ELL slices on
           // regular matrices, the short-row CSR ranges on ragged ones
           const bool csr = a.sell == nullptr;
           using S = SellCfg<DP, false>;
           using SC = SellCfg<DP, true>;
-          const size_t smem = csr ? SC::smem_bytes(last, net.hidden) : S::smem_bytes(last, net.hidden);
+          const size_t smem = csr ? SC::smem_bytes(net.hidden) : S::smem_bytes(net.hidden);
           auto kern = csr ? (last ? k_layer_sell<DP, true, OutT, true> : k_layer_sell<DP, false, OutT, true>)
                           : (last ? k_layer_sell<DP, true, OutT> : k_layer_sell<DP, false, OutT>);
           static std::once_flag f[4];
@@ -151,7 +198,7 @@ struct ApplyLaunch {
             GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
           });
           const int tiles_s = (n + S::TM - 1) / S::TM;
-          const int grid = std::max(1, std::min(tiles_s, S::CPS * sms));
+          const int grid = std::max(1, std::min(tiles_s, sms));
           SellMaps maps{m.tmX[cur], m.tmX[1 - cur]};
           const float* uwp = m.UWP.p + (size_t)l * 4 * DP * DP;
           kern<<<grid, S::NT, smem, s>>>(a, maps, X, axl, uwp, net, m.sc.p, out, skip);
@@ -604,7 +651,12 @@ void gnpc_model_s::ensure_workspace() {
   }
   if (sms == 0) sms = num_sms();
   norm_grid = 2 * sms;
-  partials.ensure(norm_grid);
+  partials.ensure(std::max(norm_grid, sms));
+  if (!gbar.p) {
+    gbar.alloc(1);
+    GNPC_CUDA(cudaMemset(gbar.p, 0, sizeof(unsigned long long)));
+    gbar_host = 0;
+  }
   if (!ticket.p) {
     ticket.alloc(1);
     GNPC_CUDA(cudaMemset(ticket.p, 0, sizeof(unsigned)));

@@ -97,16 +97,18 @@ struct SellCfg {
   static constexpr int R = TM / NG;              // rows per group
   static constexpr int US = DP == 16 ? 8 : 3;    // slice entries per gather round
   static constexpr int USC = DP == 16 ? 8 : 4;   // CSR entries per gather round
-  // TMA ring depth (tiles) and epilogue lag (A/TMEM buffer sets), measured
-  // per format: SELL DP16 (C2) best at NS 4 / LAG 1 (LAG 2 + NS 5: 25.7 vs
-  // 24.4 us); CSR DP16 (C4) at NS 5 (166 vs 197 us at NS 4); DP32 fills smem
+  // TMA ring depth (tiles), measured per format: SELL DP16 (C2) best at 4
+  // (an epilogue lag of 2 tiles with double-buffered A/TMEM and NS 5 measured
+  // 25.7 vs 24.4 us); CSR DP16 (C4) at 5 (166 vs 197 us at 4); DP32 fills smem
   static constexpr int NS = DP == 16 ? (CSR ? 5 : 4) : 3;
-  static constexpr int KCAP = 24;                // slices with K <= KCAP are staged (mult. of US)
+  // slices with K <= KCAP are staged; a multiple of US (the last round reads
+  // up to round(K, US) words).  Kept small: every KB of shared memory is L1
+  // the X-row gathers hit (C5 fused layer 531 -> 499 us going 24 -> 12)
+  static constexpr int KCAP = DP == 16 ? 16 : 12;
   static constexpr uint32_t OPB = TM * DP * 4;   // one A-type operand / X tile / Y tile (bytes)
   static constexpr uint32_t BB = DP * DP * 4;    // one B operand (bytes)
   static constexpr int TCOLS = 2 * DP;           // TMEM accumulator columns (two halves)
-  static constexpr int LAG = 1;
-  static constexpr int TALLOC = LAG * TCOLS < 32 ? 32 : LAG * TCOLS;  // power of two >= 32
+  static constexpr int TALLOC = TCOLS < 32 ? 32 : TCOLS;  // power of two >= 32
   static constexpr uint32_t CVB = KCAP * TM * 8; // staged slice (bytes)
   // CSR: [X tile | row_ptr slice (TM+4 ints, 1 KiB) | col_idx (CAPC) | values (CAPC)]
   static constexpr int CAPC = 2048;              // staged short-row nonzeros per tile
@@ -117,14 +119,12 @@ struct SellCfg {
   // layout (offsets from the 1024-aligned base)
   static constexpr uint32_t O_RING = 0;
   static constexpr uint32_t O_A = O_RING + NS * SLOT;     // A1_lo, A2_hi, A2_lo
-  static constexpr uint32_t O_B = O_A + LAG * 3 * OPB;    // Bu_lo, Bu_hi, Bw_lo, Bw_hi
+  static constexpr uint32_t O_B = O_A + 3 * OPB;          // Bu_lo, Bu_hi, Bw_lo, Bw_hi
   static constexpr uint32_t O_Y = O_B + 4 * BB;           // Y staging [2]
-  static constexpr int NY = LAG + 1;                      // Y staging buffers
-  static constexpr uint32_t O_P = O_Y + NY * OPB;         // LAST: dec1 [DP][H], b1 [H], dec2 [H]
-  static size_t smem_bytes(bool last, int hidden) {
-    size_t b = O_P + (last ? (size_t)(DP + 2) * hidden * 4 : 0);
-    b = (b + 15) & ~size_t(15);
-    return b + 128 + 1024;  // barriers + TMEM slot, 1024-B alignment slack
+  static constexpr uint32_t O_P = O_Y + 2 * OPB;          // projection: dec1 [DP][H], b1 [H], dec2 [H]
+  static constexpr uint32_t o_bar(int hidden) { return (O_P + (DP + 2) * hidden * 4 + 15) & ~15u; }
+  static size_t smem_bytes(int hidden) {
+    return o_bar(hidden) + 128 + 1024;  // barriers + TMEM slot, 1024-B alignment slack
   }
 };
 
@@ -239,65 +239,100 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
 }
 
-// LAST = true: projection epilogue writing out[i] (no Y).  uwp: this layer's
-// B operands [Bu_lo | Bu_hi | Bw_lo | Bw_hi] in the swz_off<DP> layout.
+// ---------------------------------------------------------------------------
+// The layer pipeline as device functions shared by the per-layer kernel
+// (k_layer_sell) and the whole-apply persistent kernel (k_apply_sell).
 //
-// Synchronisation (no CTA-wide barrier inside the loop).  Local iteration it
-// gathers/splits tile it and runs the epilogue of tile it - LAG (LAG = 2
-// double-buffers the A operands and the TMEM accumulator, so a warp waits for
-// an MMA issued a whole iteration earlier; LAG = 1 where shared memory is
-// short):
-//   full[s]     : ring slot s landed (TMA tx-count), control -> math warps
-//   afull[b]    : tile it's A operands and tile it-LAG's Y staging are
-//                 written (one arrival per math warp; it % LAG == b), math ->
-//                 control warp.  One barrier per lag slot: with a single one
-//                 the math warps could complete two phases before the control
-//                 warp observes the first (parity ABA)
-//   mma_bar[b]  : MMA of a tile with it % LAG == b committed, control -> math
-//                 warps.  Its completion also means the Y staging buffer the
-//                 next epilogue writes is free (the control warp waits for the
-//                 older store's smem reads before committing).
-// afull(it) also tells the control warp that every warp passed its wait for
-// MMA(it-LAG), so that tile's ring slot may be refilled.
-template <int DP, bool LAST, typename OutT, bool CSR = false>
-__global__ void __launch_bounds__(SellCfg<DP>::NT, SellCfg<DP>::CPS)
-k_layer_sell(DevCsr a, const __grid_constant__ SellMaps maps, const float* __restrict__ X,
-             const float* __restrict__ axlong, const float* __restrict__ uwp, NetView net,
-             const ApplyScalars* __restrict__ sc, OutT* __restrict__ out, const int* __restrict__ skip) {
+// Synchronisation inside a layer (no CTA-wide barrier in the tile loop):
+//   full[s]  : ring slot s landed (TMA tx-count), control -> math warps
+//   afull    : a tile's A operands and the previous tile's Y staging are
+//              written (one arrival per math warp), math -> control warp
+//   mma_bar  : MMA committed, control -> math warps.  Its completion also
+//              means the Y staging buffer the next epilogue writes is free
+//              (the control warp waits for older stores' smem reads first).
+// afull(t) tells the control warp every warp passed its wait for MMA(t-1),
+// so tile t-1's ring slot may be refilled.  The phase counters run on across
+// the layers of the persistent kernel.
+template <int DP, bool CSR>
+struct SellPipe {
   using C = SellCfg<DP, CSR>;
-  constexpr int TM = C::TM, G = C::G, R = C::R, NS = C::NS, NW = C::NW, NQ = C::NQ, LAG = C::LAG;
-  if (skip && *skip) return;
-  const int n = a.n;
-  const int ntiles = (n + TM - 1) / TM;
-  if (sc->zero) {
-    if constexpr (LAST) {
-      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        out[i] = OutT(0);
-    }
-    return;
-  }
+  uint8_t* ring;
+  uint8_t* A;  // [A1_lo | A2_hi | A2_lo]
+  uint8_t* Bs;
+  uint8_t* Ystg;
+  float* D1;
+  uint64_t* full;
+  uint64_t* mma_bar;
+  uint64_t* afull;
+  uint32_t tmem;
+  int ring_it = 0, mma_it = 0, af_it = 0;  // phase counters (identical in every thread)
+};
+
+// smem carve-up, barrier init, TMEM allocation (all threads of the CTA)
+template <int DP, bool CSR>
+__device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden) {
+  using C = SellCfg<DP, CSR>;
   extern __shared__ float4 smem_raw[];
   const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* base = reinterpret_cast<uint8_t*>(smem_raw) + pad;
-  uint8_t* ring = base + C::O_RING;
-  uint8_t* Abuf = base + C::O_A;  // [LAG][A1_lo | A2_hi | A2_lo]
-  uint8_t* Bs = base + C::O_B;
-  uint8_t* Ystg = base + C::O_Y;
-  float* D1 = reinterpret_cast<float*>(base + C::O_P);
+  SellPipe<DP, CSR> p;
+  p.ring = base + C::O_RING;
+  p.A = base + C::O_A;
+  p.Bs = base + C::O_B;
+  p.Ystg = base + C::O_Y;
+  p.D1 = reinterpret_cast<float*>(base + C::O_P);
+  p.full = reinterpret_cast<uint64_t*>(base + C::o_bar(hidden));
+  p.mma_bar = p.full + C::NS;
+  p.afull = p.mma_bar + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(p.afull + 1);
+  const int tid = threadIdx.x;
+  for (int t = tid; t < int(C::NS * C::SLOT / 16); t += C::NT)  // stale slice words must be valid columns
+    reinterpret_cast<float4*>(p.ring)[t] = f4zero();
+  if (tid == 0) {
+    for (int s = 0; s < C::NS; ++s) tc::mbar_init(&p.full[s], 1);
+    tc::mbar_init(p.mma_bar, 1);
+    tc::mbar_init(p.afull, C::NW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if ((tid >> 5) == 0) tc::tmem_alloc(tslot, C::TALLOC);
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  p.tmem = *tslot;
+  return p;
+}
+
+template <int DP, bool CSR>
+__device__ __forceinline__ void sell_teardown(const SellPipe<DP, CSR>& p) {
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc(p.tmem, SellCfg<DP, CSR>::TALLOC);
+}
+
+// One fused Res-GCONV layer over this CTA's tiles (all threads call it).
+// LAST: projection epilogue writing out[i] = (dec2ᵀ relu(dec1ᵀ y + b1) + b2)
+// · out_scale (no Y).  uwp: the layer's B operands [Bu_lo | Bu_hi | Bw_lo |
+// Bw_hi] in the swz_off<DP> layout.
+template <int DP, bool LAST, typename OutT, bool CSR>
+__device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a, const CUtensorMap* mapx,
+                                           const CUtensorMap* mapy, const float* __restrict__ X,
+                                           const float* __restrict__ axlong, const float* __restrict__ uwp,
+                                           const NetView& net, double out_scale, OutT* __restrict__ out) {
+  using C = SellCfg<DP, CSR>;
+  constexpr int TM = C::TM, G = C::G, R = C::R, NS = C::NS, NW = C::NW, NQ = C::NQ;
+  const int n = a.n;
+  const int ntiles = (n + TM - 1) / TM;
   const int H = net.hidden;
+  float* D1 = p.D1;
   float* B1 = D1 + DP * H;
   float* D2 = B1 + H;
-  uint64_t* full = reinterpret_cast<uint64_t*>(
-      base + ((C::O_P + (LAST ? (DP + 2) * H * 4 : 0) + 15) & ~15u));
-  uint64_t* mma_bar = full + NS;  // [LAG]
-  uint64_t* afull = mma_bar + LAG;  // [LAG]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(afull + LAG);
-
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // this layer's operands; every MMA of the previous layer has completed
+  // (its epilogues waited for them before the caller's barrier)
   for (int t = tid; t < int(4 * C::BB / 16); t += C::NT)
-    reinterpret_cast<float4*>(Bs)[t] = reinterpret_cast<const float4*>(uwp)[t];
-  for (int t = tid; t < int(NS * C::SLOT / 16); t += C::NT)  // stale slice words must be valid columns
-    reinterpret_cast<float4*>(ring)[t] = f4zero();
+    reinterpret_cast<float4*>(p.Bs)[t] = reinterpret_cast<const float4*>(uwp)[t];
   if constexpr (LAST) {
     for (int t = tid; t < DP * H; t += C::NT) D1[t] = net.dec1[t];
     for (int t = tid; t < H; t += C::NT) {
@@ -305,74 +340,64 @@ k_layer_sell(DevCsr a, const __grid_constant__ SellMaps maps, const float* __res
       D2[t] = net.dec2[t];
     }
   }
-  if (tid == 0) {
-    for (int s = 0; s < NS; ++s) tc::mbar_init(&full[s], 1);
-    for (int b = 0; b < LAG; ++b) {
-      tc::mbar_init(&mma_bar[b], 1);
-      tc::mbar_init(&afull[b], NW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) tc::tmem_alloc(tslot, C::TALLOC);
   tc::fence_proxy_async();
-  tc::fence_before();
   __syncthreads();
-  tc::fence_after();
-  const uint32_t tmem = *tslot;
-  // local iterations: one per tile of this CTA, plus LAG drain iterations
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int iters = my_tiles > 0 ? my_tiles + LAG : 0;
+  const int rb = p.ring_it, mb = p.mma_it, ab = p.af_it;
+  p.ring_it += my_tiles;
+  p.mma_it += my_tiles;
+  p.af_it += my_tiles > 0 ? my_tiles + 1 : 0;
+  if (my_tiles == 0) return;
 
   if (warp == NW) {
     // ============================================================ control warp
     if (lane == 0) {
-      tc::tma_prefetch_desc(&maps.x);
-      if (!LAST) tc::tma_prefetch_desc(&maps.y);
-      auto issue = [&](int it) {
+      tc::tma_prefetch_desc(mapx);
+      if (!LAST) tc::tma_prefetch_desc(mapy);
+      auto issue = [&](int it) {  // tile `it` of this CTA into ring slot (rb + it) % NS
         if (it >= my_tiles) return;
         const int t = blockIdx.x + it * gridDim.x;
-        const int s = it % NS;
-        uint8_t* slot = ring + s * C::SLOT;
+        const int r = rb + it;
+        const int s = r % NS;
+        uint8_t* slot = p.ring + s * C::SLOT;
         if constexpr (CSR) {
           // the tile's short-row CSR range, 16-byte aligned superset [a0, a1)
           const int kb = __ldg(a.rps + t * TM), ke = __ldg(a.rps + min((t + 1) * TM, n));
           const int a0 = kb & ~3, cnt = ((ke + 3) & ~3) - a0;
           const bool staged = cnt <= C::CAPC;
-          tc::mbar_expect_tx(&full[s], C::OPB + C::RPB + (staged ? 8 * cnt : 0));
-          tc::tma_load_2d(slot, &maps.x, 0, t * TM, &full[s]);
-          tc::bulk_load(slot + C::O_RP, a.rps + t * TM, C::RPB, &full[s]);
+          tc::mbar_expect_tx(&p.full[s], C::OPB + C::RPB + (staged ? 8 * cnt : 0));
+          tc::tma_load_2d(slot, mapx, 0, t * TM, &p.full[s]);
+          tc::bulk_load(slot + C::O_RP, a.rps + t * TM, C::RPB, &p.full[s]);
           if (staged && cnt > 0) {
-            tc::bulk_load(slot + C::O_CI, a.cis + a0, 4 * cnt, &full[s]);
-            tc::bulk_load(slot + C::O_V, a.vs + a0, 4 * cnt, &full[s]);
+            tc::bulk_load(slot + C::O_CI, a.cis + a0, 4 * cnt, &p.full[s]);
+            tc::bulk_load(slot + C::O_V, a.vs + a0, 4 * cnt, &p.full[s]);
           }
         } else {
           const int K = __ldg(a.sell_k + t) & 0xffff;
           const bool staged = K > 0 && K <= C::KCAP;
-          tc::mbar_expect_tx(&full[s], C::OPB + (staged ? K * TM * 8 : 0));
-          tc::tma_load_2d(slot, &maps.x, 0, t * TM, &full[s]);
-          if (staged) tc::bulk_load(slot + C::OPB, a.sell + __ldg(a.sell_off + t), K * TM * 8, &full[s]);
+          tc::mbar_expect_tx(&p.full[s], C::OPB + (staged ? K * TM * 8 : 0));
+          tc::tma_load_2d(slot, mapx, 0, t * TM, &p.full[s]);
+          if (staged) tc::bulk_load(slot + C::OPB, a.sell + __ldg(a.sell_off + t), K * TM * 8, &p.full[s]);
         }
       };
-      for (int it = 0; it < NS - LAG; ++it) issue(it);
+      for (int it = 0; it < NS - 1; ++it) issue(it);
       constexpr uint32_t idesc = tc::idesc_tf32(128, DP);
       constexpr uint32_t idesc2 = tc::idesc_tf32(128, 2 * DP);
-      const uint32_t sBstk = tc::smem_u32(Bs);
-      for (int it = 0; it < iters; ++it) {
-        tc::mbar_wait_dbg(&afull[it % LAG], (it / LAG) & 1, 1, it);
+      const uint32_t sBstk = tc::smem_u32(p.Bs);
+      const uint32_t sA1lo = tc::smem_u32(p.A), sA2hi = sA1lo + C::OPB, sA2lo = sA1lo + 2 * C::OPB;
+      for (int it = 0; it <= my_tiles; ++it) {
+        tc::mbar_wait_dbg(p.afull, (ab + it) & 1, 1, it);
         tc::fence_after();
-        // stores issued up to iteration it-1 have left the Y staging: the
-        // buffer the epilogue after this MMA writes ((it) % NY) is free
+        // stores issued up to the previous iteration have left the Y staging:
+        // the buffer the epilogue after this MMA writes is free
         tc::bulk_wait_read0();
         if (it < my_tiles) {
-          const int b = it % LAG;
-          const uint32_t sA = tc::smem_u32(Abuf + b * 3 * C::OPB);
-          const uint32_t sA1lo = sA, sA2hi = sA + C::OPB, sA2lo = sA + 2 * C::OPB;
-          const uint32_t sX = tc::smem_u32(ring + (it % NS) * C::SLOT);
-          const uint32_t acc = tmem + b * C::TCOLS;
+          const uint32_t sX = tc::smem_u32(p.ring + ((rb + it) % NS) * C::SLOT);
           // 3xTF32 with the two A_hi products stacked along N (A_hi is read
           // once for both): D[:, 0:DP] = A_hi·B_lo, D[:, DP:2DP] = A_hi·B_hi +
           // A_lo·B_hi; the epilogue adds the halves.  Each part's B operands
-          // are stored [B_lo | B_hi], i.e. as one 2DP-row operand.
+          // are stored [B_lo | B_hi], i.e. as one 2DP-row operand.  The
+          // landed X tile is A_hi of the X·U part (kind::tf32 truncates).
           uint32_t accf = 0;
 #pragma unroll
           for (int part = 0; part < 2; ++part) {
@@ -381,194 +406,355 @@ k_layer_sell(DevCsr a, const __grid_constant__ SellMaps maps, const float* __res
             const uint32_t sbh = sbs + C::BB;                // B_hi rows alone
 #pragma unroll
             for (int k8 = 0; k8 < DP / 8; ++k8) {
-              tc::mma_tf32(acc, tc::make_desc_swz<DP>(sah + k8 * 32), tc::make_desc_swz<DP>(sbs + k8 * 32),
-                           idesc2, accf);
+              tc::mma_tf32(p.tmem, tc::make_desc_swz<DP>(sah + k8 * 32),
+                           tc::make_desc_swz<DP>(sbs + k8 * 32), idesc2, accf);
               accf = 1;
-              tc::mma_tf32(acc + DP, tc::make_desc_swz<DP>(sal + k8 * 32),
+              tc::mma_tf32(p.tmem + DP, tc::make_desc_swz<DP>(sal + k8 * 32),
                            tc::make_desc_swz<DP>(sbh + k8 * 32), idesc, 1);
             }
           }
-          tc::mma_commit(&mma_bar[b]);
+          tc::mma_commit(p.mma_bar);
         }
-        if (!LAST && it >= LAG) {  // tile it-LAG is fully staged
-          tc::tma_store_2d(&maps.y, Ystg + ((it - LAG) % C::NY) * C::OPB, 0,
-                           (blockIdx.x + (it - LAG) * gridDim.x) * TM);
+        if (!LAST && it >= 1) {  // tile it-1 is fully staged
+          tc::tma_store_2d(mapy, p.Ystg + ((mb + it - 1) & 1) * C::OPB, 0,
+                           (blockIdx.x + (it - 1) * gridDim.x) * TM);
           tc::bulk_commit();
         }
-        // every warp passed its wait for MMA(it-LAG): that slot takes tile it+NS-LAG
-        issue(it + NS - LAG);
+        // every warp passed its wait for MMA(it-1): that slot takes tile it+NS-1
+        issue(it + NS - 1);
       }
+      // the layer's output is in global memory before the caller's barrier
       tc::bulk_wait0();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncwarp();
-  } else {
-    // ============================================================== math warps
-    const int gl = tid % G, gid = tid / G;
-    // epilogue of tile itp (accumulator in TMEM buffer itp % LAG).
-    // Non-last layers: relu'd rows -> Ystg[itp % NY] (warp w: lanes 32(w%4)..,
-    // column group w/4), stored by the control warp's TMA.  Last layer: the
-    // projection group of this tile (warps 4*(itp%NQ)..+3, one per lane
-    // quarter) pulls whole rows into registers `y` and projects them after
-    // arriving — the groups rotate, so no CTA-wide barrier is needed.
-    float y[LAST ? DP : 1];
-    auto epilogue = [&](int itp) -> bool {
-      const int b = itp % LAG;
-      tc::mbar_wait_dbg(&mma_bar[b], (itp / LAG) & 1, 2, itp);
-      tc::fence_after();
-      const int q = warp & 3, cq = warp >> 2;  // lane quarter, column group
-      const uint32_t trow = tmem + b * C::TCOLS + (static_cast<uint32_t>(32 * q) << 16);
-      if constexpr (LAST) {
-        if (cq != itp % NQ) return false;
-#pragma unroll
-        for (int c0 = 0; c0 < DP; c0 += 16) {
-          float v[16], v2[16];
-          tc::tmem_ld16(trow + c0, v);
-          tc::tmem_ld16(trow + DP + c0, v2);
-#pragma unroll
-          for (int c = 0; c < 16; ++c) y[c0 + c] = relu(v[c] + v2[c]);
-        }
-        tc::fence_before();
-        return true;
-      } else {
-        const int m = 32 * q + lane;
-        constexpr int CW = DP / NQ;  // columns per warp: 4, 8 or 16
-        uint8_t* ys = Ystg + (itp % C::NY) * C::OPB;
-        const uint32_t taddr = trow + cq * CW;
-        float v[CW];
-        if constexpr (CW == 4) {
-          float v2[4];
-          tc::tmem_ld4(taddr, v);
-          tc::tmem_ld4(taddr + DP, v2);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) v[c] += v2[c];
-        } else {
-#pragma unroll
-          for (int c0 = 0; c0 < CW; c0 += 8) {
-            float u1[8], u2[8];
-            tc::tmem_ld8(taddr + c0, u1);
-            tc::tmem_ld8(taddr + DP + c0, u2);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) v[c0 + c] = u1[c] + u2[c];
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < CW; c += 4)
-          *reinterpret_cast<float4*>(ys + tc::swz_off<DP>(m, cq * CW + c)) =
-              make_float4(relu(v[c]), relu(v[c + 1]), relu(v[c + 2]), relu(v[c + 3]));
-        tc::fence_before();
-        return false;
-      }
-    };
-    auto arrive = [&](int it) {
-      tc::fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&afull[it % LAG]);
-    };
-    // LAST: projection MLP (src/gnn.cpp:178-199) of the row this lane holds
-    // (row 32*(warp%4) + lane of the tile at row0): dec1 read as warp-uniform
-    // float4 broadcasts.
-    auto project = [&](int row0) {
-      if constexpr (LAST) {
-        float o = 0.f;
-        if ((H & 3) == 0) {
-          for (int h0 = 0; h0 < H; h0 += 4) {
-            float4 t = f4zero();
-#pragma unroll
-            for (int j = 0; j < DP; ++j) fma4(t, y[j], *reinterpret_cast<const float4*>(D1 + j * H + h0));
-            o = fmaf(relu(t.x + B1[h0]), D2[h0], o);
-            o = fmaf(relu(t.y + B1[h0 + 1]), D2[h0 + 1], o);
-            o = fmaf(relu(t.z + B1[h0 + 2]), D2[h0 + 2], o);
-            o = fmaf(relu(t.w + B1[h0 + 3]), D2[h0 + 3], o);
-          }
-        } else {
-          for (int h = 0; h < H; ++h) {
-            float t = 0.f;
-#pragma unroll
-            for (int j = 0; j < DP; ++j) t = fmaf(y[j], D1[j * H + h], t);
-            o = fmaf(relu(t + B1[h]), D2[h], o);
-          }
-        }
-        const int i = row0 + 32 * (warp & 3) + lane;
-        if (i < n) out[i] = static_cast<OutT>(static_cast<double>(o + net.dec2_b) * sc->out_scale);
-      }
-    };
-
-    const int* tinfo = CSR ? a.tflag : a.sell_k;  // per tile: K_t | has-long << 16 (SELL), has-long (CSR)
-    int kw = my_tiles > 0 ? __ldg(tinfo + blockIdx.x) : 0;
-    for (int it = 0; it < iters; ++it) {
-      const bool have = it < my_tiles;
-      const int tile = blockIdx.x + it * gridDim.x;
-      const int row0 = tile * TM;
-      const int s = it % NS;
-      uint8_t* slot = ring + s * C::SLOT;
-      float4 acc[R];
-      if (have) {
-        const int K = CSR ? 0 : (kw & 0xffff);
-        const bool haslong = CSR ? kw != 0 : (kw >> 16) != 0;
-        const bool staged = K > 0 && K <= C::KCAP;
-        kw = it + 1 < my_tiles ? __ldg(tinfo + tile + gridDim.x) : 0;  // prefetch
-
-        // --------------------------------------------------------- gather
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-          const int i = row0 + R * gid + j;
-          acc[j] = f4zero();
-          if (haslong && i < n && __ldg(a.rp + i + 1) - __ldg(a.rp + i) > kLongRow)
-            acc[j] = ldg4(axlong + static_cast<size_t>(i) * DP + 4 * gl);
-        }
-        tc::mbar_wait_dbg(&full[s], (it / NS) & 1, 3, it);
-        if constexpr (CSR) {
-          const int* rpt = reinterpret_cast<const int*>(slot + C::O_RP);
-          const int kb = rpt[0], ke = rpt[min(TM, n - row0)];
-          const int a0 = kb & ~3;
-          const bool st = ((ke + 3) & ~3) - a0 <= C::CAPC;
-          int sj[R], lj[R], self[R];
-#pragma unroll
-          for (int j = 0; j < R; ++j) {
-            const int r = R * gid + j;
-            const int e0 = rpt[r], e1 = rpt[r + 1];
-            sj[j] = st ? e0 - a0 : e0;
-            lj[j] = row0 + r < n ? e1 - e0 : 0;
-            self[j] = min(row0 + r, n - 1);
-          }
-          if (st)
-            gather_csr_rows<DP, R, C::USC>(X, gl, reinterpret_cast<const int*>(slot + C::O_CI),
-                                           reinterpret_cast<const float*>(slot + C::O_V), sj, lj, self, acc);
-          else
-            gather_csr_rows<DP, R, C::USC>(X, gl, a.cis, a.vs, sj, lj, self, acc);
-        } else {
-          if (staged)
-            gather_sell_rows<DP, R, C::US, TM, true>(X, gl, reinterpret_cast<const int2*>(slot + C::OPB), K,
-                                                     gid, acc);
-          else
-            gather_sell_rows<DP, R, C::US, TM, false>(X, gl, a.sell + __ldg(a.sell_off + tile), K, gid, acc);
-        }
-      }
-
-      // ------------------------------------- epilogue of tile it - LAG
-      const bool proj = it >= LAG && epilogue(it - LAG);
-
-      // -------------------------------------------------------------- split
-      if (have) {
-        uint8_t* A = Abuf + (it % LAG) * 3 * C::OPB;
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-          const int r = R * gid + j;
-          const uint32_t o = tc::swz_off<DP>(r, 4 * gl);
-          const float4 xv = *reinterpret_cast<const float4*>(slot + o);
-          *reinterpret_cast<float4*>(A + o) = f4_trunc_lo(xv);
-          *reinterpret_cast<float4*>(A + C::OPB + o) = acc[j];
-          *reinterpret_cast<float4*>(A + 2 * C::OPB + o) = f4_trunc_lo(acc[j]);
-        }
-      }
-      arrive(it);
-      if (proj) project((blockIdx.x + (it - LAG) * gridDim.x) * TM);
-    }
+    return;
   }
-  tc::fence_before();
+
+  // ================================================================ math warps
+  const int gl = tid % G, gid = tid / G;
+  float y[LAST ? DP : 1];
+  // epilogue of local tile itp (accumulator in TMEM).  Non-last layers:
+  // relu'd rows -> Ystg (warp w: lanes 32(w%4).., column group w/4), stored
+  // by the control warp's TMA.  Last layer: the projection group of this tile
+  // (warps 4*(itp%NQ)..+3, one per lane quarter) pulls whole rows into
+  // registers `y` and projects them after arriving — the groups rotate, so
+  // no CTA-wide barrier is needed.
+  auto epilogue = [&](int itp) -> bool {
+    tc::mbar_wait_dbg(p.mma_bar, (mb + itp) & 1, 2, itp);
+    tc::fence_after();
+    const int q = warp & 3, cq = warp >> 2;  // lane quarter, column group
+    const uint32_t trow = p.tmem + (static_cast<uint32_t>(32 * q) << 16);
+    if constexpr (LAST) {
+      if (cq != itp % NQ) return false;
+#pragma unroll
+      for (int c0 = 0; c0 < DP; c0 += 16) {
+        float v[16], v2[16];
+        tc::tmem_ld16(trow + c0, v);
+        tc::tmem_ld16(trow + DP + c0, v2);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) y[c0 + c] = relu(v[c] + v2[c]);
+      }
+      tc::fence_before();
+      return true;
+    } else {
+      const int m = 32 * q + lane;
+      constexpr int CW = DP / NQ;  // columns per warp: 4 or 8
+      uint8_t* ys = p.Ystg + ((mb + itp) & 1) * C::OPB;
+      const uint32_t taddr = trow + cq * CW;
+      float v[CW];
+      if constexpr (CW == 4) {
+        float v2[4];
+        tc::tmem_ld4(taddr, v);
+        tc::tmem_ld4(taddr + DP, v2);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] += v2[c];
+      } else {
+#pragma unroll
+        for (int c0 = 0; c0 < CW; c0 += 8) {
+          float u1[8], u2[8];
+          tc::tmem_ld8(taddr + c0, u1);
+          tc::tmem_ld8(taddr + DP + c0, u2);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c0 + c] = u1[c] + u2[c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CW; c += 4)
+        *reinterpret_cast<float4*>(ys + tc::swz_off<DP>(m, cq * CW + c)) =
+            make_float4(relu(v[c]), relu(v[c + 1]), relu(v[c + 2]), relu(v[c + 3]));
+      tc::fence_before();
+      return false;
+    }
+  };
+  auto arrive = [&]() {
+    tc::fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(p.afull);
+  };
+  // LAST: projection MLP (src/gnn.cpp:178-199) of the row this lane holds
+  // (row 32*(warp%4) + lane of the tile at row0); dec1 read as warp-uniform
+  // float4 broadcasts.
+  auto project = [&](int row0) {
+    if constexpr (LAST) {
+      float o = 0.f;
+      if ((H & 3) == 0) {
+        for (int h0 = 0; h0 < H; h0 += 4) {
+          float4 t = f4zero();
+#pragma unroll
+          for (int j = 0; j < DP; ++j) fma4(t, y[j], *reinterpret_cast<const float4*>(D1 + j * H + h0));
+          o = fmaf(relu(t.x + B1[h0]), D2[h0], o);
+          o = fmaf(relu(t.y + B1[h0 + 1]), D2[h0 + 1], o);
+          o = fmaf(relu(t.z + B1[h0 + 2]), D2[h0 + 2], o);
+          o = fmaf(relu(t.w + B1[h0 + 3]), D2[h0 + 3], o);
+        }
+      } else {
+        for (int h = 0; h < H; ++h) {
+          float t = 0.f;
+#pragma unroll
+          for (int j = 0; j < DP; ++j) t = fmaf(y[j], D1[j * H + h], t);
+          o = fmaf(relu(t + B1[h]), D2[h], o);
+        }
+      }
+      const int i = row0 + 32 * (warp & 3) + lane;
+      if (i < n) out[i] = static_cast<OutT>(static_cast<double>(o + net.dec2_b) * out_scale);
+    }
+  };
+
+  const int* tinfo = CSR ? a.tflag : a.sell_k;  // per tile: K_t | has-long << 16 (SELL), has-long (CSR)
+  int kw = __ldg(tinfo + blockIdx.x);
+  for (int it = 0; it <= my_tiles; ++it) {
+    const bool have = it < my_tiles;
+    const int tile = blockIdx.x + it * gridDim.x;
+    const int row0 = tile * TM;
+    const int r = rb + it;
+    uint8_t* slot = p.ring + (r % NS) * C::SLOT;
+    float4 acc[R];
+    if (have) {
+      const int K = CSR ? 0 : (kw & 0xffff);
+      const bool haslong = CSR ? kw != 0 : (kw >> 16) != 0;
+      const bool staged = K > 0 && K <= C::KCAP;
+      kw = it + 1 < my_tiles ? __ldg(tinfo + tile + gridDim.x) : 0;  // prefetch
+
+      // ----------------------------------------------------------- gather
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int i = row0 + R * gid + j;
+        acc[j] = f4zero();
+        if (haslong && i < n && __ldg(a.rp + i + 1) - __ldg(a.rp + i) > kLongRow)
+          acc[j] = ldg4(axlong + static_cast<size_t>(i) * DP + 4 * gl);
+      }
+      tc::mbar_wait_dbg(&p.full[r % NS], (r / NS) & 1, 3, it);
+      if constexpr (CSR) {
+        const int* rpt = reinterpret_cast<const int*>(slot + C::O_RP);
+        const int kb = rpt[0], ke = rpt[min(TM, n - row0)];
+        const int a0 = kb & ~3;
+        const bool st = ((ke + 3) & ~3) - a0 <= C::CAPC;
+        int sj[R], lj[R], self[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const int rr = R * gid + j;
+          const int e0 = rpt[rr], e1 = rpt[rr + 1];
+          sj[j] = st ? e0 - a0 : e0;
+          lj[j] = row0 + rr < n ? e1 - e0 : 0;
+          self[j] = min(row0 + rr, n - 1);
+        }
+        if (st)
+          gather_csr_rows<DP, R, C::USC>(X, gl, reinterpret_cast<const int*>(slot + C::O_CI),
+                                         reinterpret_cast<const float*>(slot + C::O_V), sj, lj, self, acc);
+        else
+          gather_csr_rows<DP, R, C::USC>(X, gl, a.cis, a.vs, sj, lj, self, acc);
+      } else {
+        if (staged)
+          gather_sell_rows<DP, R, C::US, TM, true>(X, gl, reinterpret_cast<const int2*>(slot + C::OPB), K,
+                                                   gid, acc);
+        else
+          gather_sell_rows<DP, R, C::US, TM, false>(X, gl, a.sell + __ldg(a.sell_off + tile), K, gid, acc);
+      }
+    }
+
+    // ------------------------------------------- epilogue of the previous tile
+    const bool proj = it >= 1 && epilogue(it - 1);
+
+    // ---------------------------------------------------------------- split
+    if (have) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int rr = R * gid + j;
+        const uint32_t o = tc::swz_off<DP>(rr, 4 * gl);
+        const float4 xv = *reinterpret_cast<const float4*>(slot + o);
+        *reinterpret_cast<float4*>(p.A + o) = f4_trunc_lo(xv);
+        *reinterpret_cast<float4*>(p.A + C::OPB + o) = acc[j];
+        *reinterpret_cast<float4*>(p.A + 2 * C::OPB + o) = f4_trunc_lo(acc[j]);
+      }
+    }
+    arrive();
+    if (proj) project((blockIdx.x + (it - 1) * gridDim.x) * TM);
+  }
+}
+
+// One layer as its own launch (norm/lift/layers pipeline of ApplyLaunch).
+template <int DP, bool LAST, typename OutT, bool CSR = false>
+__global__ void __launch_bounds__(SellCfg<DP>::NT, 1)
+k_layer_sell(DevCsr a, const __grid_constant__ SellMaps maps, const float* __restrict__ X,
+             const float* __restrict__ axlong, const float* __restrict__ uwp, NetView net,
+             const ApplyScalars* __restrict__ sc, OutT* __restrict__ out, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  if (sc->zero) {
+    if constexpr (LAST) {
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x)
+        out[i] = OutT(0);
+    }
+    return;
+  }
+  auto p = sell_setup<DP, CSR>(net.hidden);
+  sell_layer<DP, LAST, OutT, CSR>(p, a, &maps.x, &maps.y, X, axlong, uwp, net, sc->out_scale, out);
+  sell_teardown(p);
+}
+
+// ---------------------------------------------------------------------------
+// The whole apply M(b) in one persistent launch (one CTA per SM, cooperative
+// so all CTAs are resident): τ = ‖b‖ (f64 block partials, every CTA sums them
+// in the same order), the piecewise-linear lift into X[0], then the L layers,
+// with a grid barrier after each phase.  Replaces the 2 + L launches of
+// ApplyLaunch for matrices without long rows (src/gnn.cpp:120-201).
+struct ApplyFused {
+  CUtensorMap x0, x1;           // TMA maps over X[0], X[1]
+  float* X0;
+  float* X1;
+  const float* uwp;             // [L][4 DP DP] B operands
+  double* partials;             // [gridDim.x]
+  unsigned long long* gbar;     // grid-barrier counter (monotonic)
+  unsigned long long gbase;     // its value when this launch started
+  ApplyScalars* sc;             // τ and scales (written by block 0 for callers)
+  unsigned long long* times;    // debug (GNPC_FUSED_TIMES): block 0 phase timestamps, or null
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned long long* ctr, unsigned long long target) {
   __syncthreads();
-  tc::fence_after();
-  if (warp == 0) tc::tmem_dealloc(tmem, C::TALLOC);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1ull);
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+      if (v < target) __nanosleep(64);
+    } while (v < target);
+    __threadfence();  // gpu-scope: invalidates this SM's L1 before re-reading X
+  }
+  __syncthreads();
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <int DP, typename InT, typename OutT, bool CSR>
+__global__ void __launch_bounds__(SellCfg<DP>::NT, 1)
+k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restrict__ in, NetView net,
+             OutT* __restrict__ out, const int* __restrict__ skip) {
+  using C = SellCfg<DP, CSR>;
+  if (skip && *skip) return;
+  const int n = a.n;
+  const int tid = threadIdx.x;
+  unsigned long long target = f.gbase;
+  int tk = 0;
+  auto stamp = [&]() {
+    if (f.times && blockIdx.x == 0 && threadIdx.x == 0) f.times[tk] = globaltimer_ns();
+    ++tk;
+  };
+  stamp();
+  // ------------------------------------------------------------ τ = ‖b‖₂
+  __shared__ double red[32];
+  __shared__ double s_scale[2];
+  {
+    double s = 0.0;
+    for (int i = blockIdx.x * C::NT + tid; i < n; i += gridDim.x * C::NT) {
+      const double x = static_cast<double>(in[i]);
+      s = fma(x, x, s);
+    }
+    s = warp_sum(s);
+    if ((tid & 31) == 0) red[tid >> 5] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < C::NT / 32; ++w) t += red[w];
+      f.partials[blockIdx.x] = t;
+    }
+    target += gridDim.x;
+    grid_barrier(f.gbar, target);
+    if (tid == 0) {
+      double t = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) t += reinterpret_cast<volatile double*>(f.partials)[b];
+      const double tau = sqrt(t);
+      const double sn = sqrt(static_cast<double>(n));
+      s_scale[0] = tau == 0.0 ? 0.0 : sn / tau;
+      s_scale[1] = tau / sn;
+      if (blockIdx.x == 0) {
+        f.sc->tau = tau;
+        f.sc->zero = tau == 0.0;
+        f.sc->in_scale = s_scale[0];
+        f.sc->out_scale = s_scale[1];
+      }
+    }
+    __syncthreads();
+  }
+  const double in_scale = s_scale[0], out_scale = s_scale[1];
+  if (in_scale == 0.0) {  // τ = 0: M(0) = 0
+    for (int i = blockIdx.x * C::NT + tid; i < n; i += gridDim.x * C::NT) out[i] = OutT(0);
+    return;
+  }
+  auto p = sell_setup<DP, CSR>(net.hidden);
+  // ------------------------------------------- lift into X[0] (own tiles' rows)
+  {
+    const int nb = net.nbreak;
+    float* s_a = reinterpret_cast<float*>(p.ring);  // ring is idle until the first layer
+    float* s_b = s_a + (nb + 1) * DP;
+    float* s_t = s_b + (nb + 1) * DP;
+    for (int t = tid; t < (nb + 1) * DP; t += C::NT) {
+      s_a[t] = net.lift_a[t];
+      s_b[t] = net.lift_b[t];
+    }
+    for (int t = tid; t < nb; t += C::NT) s_t[t] = net.lift_t[t];
+    __syncthreads();
+    constexpr int G = DP / 4;
+    const int gl = tid % G;
+    const int ntiles = (n + C::TM - 1) / C::TM;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int r = tid / G; r < C::TM; r += C::NT / G) {
+        const int row = tile * C::TM + r;
+        if (row >= n) break;
+        const float v = static_cast<float>(in_scale * static_cast<double>(in[row]));
+        int lo = 0, hi = nb;  // interval = #kinks <= v
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (s_t[mid] <= v) lo = mid + 1;
+          else hi = mid;
+        }
+        const float4 al = *reinterpret_cast<const float4*>(s_a + lo * DP + 4 * gl);
+        const float4 be = *reinterpret_cast<const float4*>(s_b + lo * DP + 4 * gl);
+        st4(f.X0 + static_cast<size_t>(row) * DP + 4 * gl,
+            make_float4(fmaf(al.x, v, be.x), fmaf(al.y, v, be.y), fmaf(al.z, v, be.z), fmaf(al.w, v, be.w)));
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < (2 * (nb + 1) * DP + nb + 3) / 4; t += C::NT)  // restore the zeroed ring
+      reinterpret_cast<float4*>(p.ring)[t] = f4zero();
+  }
+  const int L = net.layers;
+  for (int l = 0; l < L; ++l) {
+    stamp();
+    target += gridDim.x;
+    grid_barrier(f.gbar, target);  // layer l's input is complete everywhere
+    stamp();
+    const float* X = (l & 1) ? f.X1 : f.X0;
+    const CUtensorMap* mx = (l & 1) ? &f.x1 : &f.x0;
+    const CUtensorMap* my = (l & 1) ? &f.x0 : &f.x1;
+    const float* uw = f.uwp + (size_t)l * 4 * DP * DP;
+    if (l + 1 < L)
+      sell_layer<DP, false, OutT, CSR>(p, a, mx, my, X, nullptr, uw, net, out_scale, out);
+    else
+      sell_layer<DP, true, OutT, CSR>(p, a, mx, my, X, nullptr, uw, net, out_scale, out);
+  }
+  stamp();
+  sell_teardown(p);
 }
 
 }  // namespace gnpk

@@ -35,6 +35,10 @@ struct gnpc_model_s {
   gnpc_impl::DevBuf<float> X[2], AXL, LPART;  // LPART: long-row chunk partials
   gnpc_impl::DevBuf<double> partials, io_in, io_out;
   gnpc_impl::DevBuf<unsigned> ticket;
+  // grid-barrier counter of the persistent apply (monotonic; the host mirrors
+  // its value so each launch knows its base; launches are stream-ordered)
+  gnpc_impl::DevBuf<unsigned long long> gbar;
+  unsigned long long gbar_host = 0;
   gnpc_impl::DevBuf<gnpk::ApplyScalars> sc;
   int sms = 0, norm_grid = 0;
   cudaStream_t stream = nullptr;

@@ -107,11 +107,14 @@ struct ApplyLaunch {
       // DP=16 only: at DP=32 the in-kernel layers measured slower than
       // separate launches (C5: 499 vs 450 us per layer) while DP=16 gains
       // (C2: 17 vs 24 us per layer: no launch gap or prologue per layer)
-      if (DP == 16 && m.use_tc && !sell_off && !fused_off && A.n_long == 0 && prof == nullptr && n > 0) {
+      const bool fits = (a.sell ? SellCfg<DP, false>::smem_bytes(net.hidden, true)
+                                : SellCfg<DP, true>::smem_bytes(net.hidden, true)) <= 226 * 1024;
+      if (DP == 16 && fits && m.use_tc && !sell_off && !fused_off && A.n_long == 0 && prof == nullptr &&
+          n > 0) {
         const bool csr = a.sell == nullptr;
         using S = SellCfg<DP, false>;
         using SC = SellCfg<DP, true>;
-        const size_t smem = csr ? SC::smem_bytes(net.hidden) : S::smem_bytes(net.hidden);
+        const size_t smem = csr ? SC::smem_bytes(net.hidden, true) : S::smem_bytes(net.hidden, true);
         auto kern = csr ? k_apply_sell<DP, InT, OutT, true> : k_apply_sell<DP, InT, OutT, false>;
         static std::once_flag f[2];
         std::call_once(f[csr ? 1 : 0], [&] {
@@ -184,13 +187,15 @@ struct ApplyLaunch {
       const bool last = l + 1 == net.layers;
       mark(last ? 4 : 3);
       if constexpr (DP == 16 || DP == 32) {
-        if (m.use_tc && !sell_off) {
+        const bool sell_fits = (a.sell ? SellCfg<DP, false>::smem_bytes(net.hidden, last)
+                                       : SellCfg<DP, true>::smem_bytes(net.hidden, last)) <= 227 * 1024;
+        if (m.use_tc && !sell_off && sell_fits) {
           // TMA pipeline, one 544-thread CTA per SM: sliced-ELL slices on
           // regular matrices, the short-row CSR ranges on ragged ones
           const bool csr = a.sell == nullptr;
           using S = SellCfg<DP, false>;
           using SC = SellCfg<DP, true>;
-          const size_t smem = csr ? SC::smem_bytes(net.hidden) : S::smem_bytes(net.hidden);
+          const size_t smem = csr ? SC::smem_bytes(net.hidden, last) : S::smem_bytes(net.hidden, last);
           auto kern = csr ? (last ? k_layer_sell<DP, true, OutT, true> : k_layer_sell<DP, false, OutT, true>)
                           : (last ? k_layer_sell<DP, true, OutT> : k_layer_sell<DP, false, OutT>);
           static std::once_flag f[4];

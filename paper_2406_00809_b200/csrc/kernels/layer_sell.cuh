@@ -111,7 +111,8 @@ struct SellCfg {
   static constexpr int TALLOC = TCOLS < 32 ? 32 : TCOLS;  // power of two >= 32
   static constexpr uint32_t CVB = KCAP * TM * 8; // staged slice (bytes)
   // CSR: [X tile | row_ptr slice (TM+4 ints, 1 KiB) | col_idx (CAPC) | values (CAPC)]
-  static constexpr int CAPC = 2048;              // staged short-row nonzeros per tile
+  static constexpr int CAPC = DP == 16 ? 2048 : 1024;  // staged short-row nonzeros per tile (DP=32: fits the
+                                                       // last layer's projection operands)
   static constexpr uint32_t RPB = (TM + 4) * 4;  // row_ptr slice copy (bytes, 16-B multiple)
   static constexpr uint32_t O_RP = OPB, O_CI = OPB + 1024, O_V = O_CI + CAPC * 4;
   static constexpr uint32_t SLOT =
@@ -121,10 +122,29 @@ struct SellCfg {
   static constexpr uint32_t O_A = O_RING + NS * SLOT;     // A1_lo, A2_hi, A2_lo
   static constexpr uint32_t O_B = O_A + 3 * OPB;          // Bu_lo, Bu_hi, Bw_lo, Bw_hi
   static constexpr uint32_t O_Y = O_B + 4 * BB;           // Y staging [2]
-  static constexpr uint32_t O_P = O_Y + 2 * OPB;          // projection: dec1 [DP][H], b1 [H], dec2 [H]
-  static constexpr uint32_t o_bar(int hidden) { return (O_P + (DP + 2) * hidden * 4 + 15) & ~15u; }
-  static size_t smem_bytes(int hidden) {
-    return o_bar(hidden) + 128 + 1024;  // barriers + TMEM slot, 1024-B alignment slack
+  // last layer only: Y_lo staging [2], the dec1 B operand [D1_lo; D1_hi]
+  // (2H rows, swizzled K-major), then dec1 (fp32, CUDA-core fallback), b1, dec2
+  static constexpr uint32_t O_YLO = O_Y + 2 * OPB;
+  static constexpr uint32_t O_D1OP = O_YLO + 2 * OPB;
+  static constexpr uint32_t o_p(int hidden, bool last) {
+    return last && tc_proj(hidden) ? O_D1OP + 2 * hidden * DP * 4 : O_Y + 2 * OPB;
+  }
+  static constexpr uint32_t o_bar(int hidden, bool last) {
+    return (o_p(hidden, last) + (last ? (DP + 2) * hidden * 4 : 0) + 15) & ~15u;
+  }
+  static size_t smem_bytes(int hidden, bool last) {
+    return o_bar(hidden, last) + 128 + 1024;  // barriers + TMEM slot, 1024-B alignment slack
+  }
+  static_assert(O_D1OP + 2 * 32 * DP * 4 + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
+                "last-layer layout must fit shared memory at hidden 32 (larger: host falls back)");
+  // TMEM: layer accumulator [0, 2DP); last layer's projection accumulator at
+  // [2DP, 2DP + 2H) (tensor-core projection when H % 16 == 0 and H <= 64)
+  static constexpr int TALLOC_LAST = 256;
+  // DP=16: the CUDA-core projection is cheap (DP*H FMAs per row) and the
+  // staging it saves is L1 for the gathers (fused C2: 27.3 vs 26.5 us LAST,
+  // 18 vs 17 us per layer with the larger layout)
+  static __host__ __device__ constexpr bool tc_proj(int hidden) {
+    return DP == 32 && hidden % 16 == 0 && hidden <= 64;
   }
 };
 
@@ -260,17 +280,20 @@ struct SellPipe {
   uint8_t* A;  // [A1_lo | A2_hi | A2_lo]
   uint8_t* Bs;
   uint8_t* Ystg;
+  uint8_t* Ylo;
+  uint8_t* D1op;
   float* D1;
   uint64_t* full;
   uint64_t* mma_bar;
   uint64_t* afull;
   uint32_t tmem;
+  int talloc;
   int ring_it = 0, mma_it = 0, af_it = 0;  // phase counters (identical in every thread)
 };
 
 // smem carve-up, barrier init, TMEM allocation (all threads of the CTA)
 template <int DP, bool CSR>
-__device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden) {
+__device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
   using C = SellCfg<DP, CSR>;
   extern __shared__ float4 smem_raw[];
   const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
@@ -280,8 +303,11 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden) {
   p.A = base + C::O_A;
   p.Bs = base + C::O_B;
   p.Ystg = base + C::O_Y;
-  p.D1 = reinterpret_cast<float*>(base + C::O_P);
-  p.full = reinterpret_cast<uint64_t*>(base + C::o_bar(hidden));
+  p.Ylo = base + C::O_YLO;
+  p.D1op = base + C::O_D1OP;
+  p.D1 = reinterpret_cast<float*>(base + C::o_p(hidden, last));
+  p.full = reinterpret_cast<uint64_t*>(base + C::o_bar(hidden, last));
+  p.talloc = last ? C::TALLOC_LAST : C::TALLOC;
   p.mma_bar = p.full + C::NS;
   p.afull = p.mma_bar + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p.afull + 1);
@@ -294,7 +320,7 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden) {
     tc::mbar_init(p.afull, C::NW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if ((tid >> 5) == 0) tc::tmem_alloc(tslot, C::TALLOC);
+  if ((tid >> 5) == 0) tc::tmem_alloc(tslot, p.talloc);
   tc::fence_proxy_async();
   tc::fence_before();
   __syncthreads();
@@ -308,7 +334,7 @@ __device__ __forceinline__ void sell_teardown(const SellPipe<DP, CSR>& p) {
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc(p.tmem, SellCfg<DP, CSR>::TALLOC);
+  if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc(p.tmem, p.talloc);
 }
 
 // One fused Res-GCONV layer over this CTA's tiles (all threads call it).
@@ -333,8 +359,22 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   // (its epilogues waited for them before the caller's barrier)
   for (int t = tid; t < int(4 * C::BB / 16); t += C::NT)
     reinterpret_cast<float4*>(p.Bs)[t] = reinterpret_cast<const float4*>(uwp)[t];
+  // last layer: the projection's first matrix on the tensor cores when its
+  // width allows (TCP), as the B operand [D1_lo; D1_hi] (rows h, K = DP:
+  // D1op(h, j) = dec1(j, h), split hi = trunc, lo = rest); else dec1 in fp32
+  const bool TCP = LAST && C::tc_proj(H);
   if constexpr (LAST) {
-    for (int t = tid; t < DP * H; t += C::NT) D1[t] = net.dec1[t];
+    if (TCP) {
+      for (int t = tid; t < H * DP; t += C::NT) {
+        const int h = t / DP, j = t % DP;
+        const float v = net.dec1[j * H + h];
+        const float hi = __int_as_float(__float_as_int(v) & 0xffffe000);
+        *reinterpret_cast<float*>(p.D1op + tc::swz_off<DP>(h, j)) = v - hi;      // rows 0..H-1: lo
+        *reinterpret_cast<float*>(p.D1op + tc::swz_off<DP>(H + h, j)) = hi;      // rows H..2H-1: hi
+      }
+    } else {
+      for (int t = tid; t < DP * H; t += C::NT) D1[t] = net.dec1[t];
+    }
     for (int t = tid; t < H; t += C::NT) {
       B1[t] = net.dec1_b[t];
       D2[t] = net.dec2[t];
@@ -344,8 +384,10 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   __syncthreads();
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int rb = p.ring_it, mb = p.mma_it, ab = p.af_it;
+  // commits: one per tile, plus the last projection MMA's (TCP)
+  const int ncommit = my_tiles + (TCP && my_tiles > 0 ? 1 : 0);
   p.ring_it += my_tiles;
-  p.mma_it += my_tiles;
+  p.mma_it += ncommit;
   p.af_it += my_tiles > 0 ? my_tiles + 1 : 0;
   if (my_tiles == 0) return;
 
@@ -413,8 +455,25 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
                            tc::make_desc_swz<DP>(sbh + k8 * 32), idesc, 1);
             }
           }
-          tc::mma_commit(p.mma_bar);
         }
+        if (TCP && it >= 1) {
+          // projection of tile it-1 (its relu'd rows are staged hi/lo):
+          // Dp[:, 0:H] = Y_hi·D1_lo, Dp[:, H:2H] = Y_hi·D1_hi + Y_lo·D1_hi
+          const uint32_t sYh = tc::smem_u32(p.Ystg + ((mb + it - 1) & 1) * C::OPB);
+          const uint32_t sYl = tc::smem_u32(p.Ylo + ((mb + it - 1) & 1) * C::OPB);
+          const uint32_t sD = tc::smem_u32(p.D1op);
+          const uint32_t sDh = sD + H * DP * 4;
+          const uint32_t iH = tc::idesc_tf32(128, H), i2H = tc::idesc_tf32(128, 2 * H);
+          const uint32_t pacc = p.tmem + 2 * DP;
+#pragma unroll
+          for (int k8 = 0; k8 < DP / 8; ++k8) {
+            tc::mma_tf32(pacc, tc::make_desc_swz<DP>(sYh + k8 * 32), tc::make_desc_swz<DP>(sD + k8 * 32), i2H,
+                         k8 > 0);
+            tc::mma_tf32(pacc + H, tc::make_desc_swz<DP>(sYl + k8 * 32), tc::make_desc_swz<DP>(sDh + k8 * 32),
+                         iH, 1);
+          }
+        }
+        if (it < my_tiles || (TCP && it >= 1)) tc::mma_commit(p.mma_bar);
         if (!LAST && it >= 1) {  // tile it-1 is fully staged
           tc::tma_store_2d(mapy, p.Ystg + ((mb + it - 1) & 1) * C::OPB, 0,
                            (blockIdx.x + (it - 1) * gridDim.x) * TM);
@@ -440,12 +499,16 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   // (warps 4*(itp%NQ)..+3, one per lane quarter) pulls whole rows into
   // registers `y` and projects them after arriving — the groups rotate, so
   // no CTA-wide barrier is needed.
+  // With the tensor-core projection (TCP) the last layer stages its relu'd
+  // rows like the others (hi into Ystg, lo into Ylo) for the control warp's
+  // projection MMA, and the rotating group reads the projection accumulator
+  // one tile later (proj_epilogue).
   auto epilogue = [&](int itp) -> bool {
     tc::mbar_wait_dbg(p.mma_bar, (mb + itp) & 1, 2, itp);
     tc::fence_after();
     const int q = warp & 3, cq = warp >> 2;  // lane quarter, column group
     const uint32_t trow = p.tmem + (static_cast<uint32_t>(32 * q) << 16);
-    if constexpr (LAST) {
+    if (LAST && !TCP) {
       if (cq != itp % NQ) return false;
 #pragma unroll
       for (int c0 = 0; c0 < DP; c0 += 16) {
@@ -481,11 +544,35 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       }
 #pragma unroll
       for (int c = 0; c < CW; c += 4)
-        *reinterpret_cast<float4*>(ys + tc::swz_off<DP>(m, cq * CW + c)) =
-            make_float4(relu(v[c]), relu(v[c + 1]), relu(v[c + 2]), relu(v[c + 3]));
+      {
+        const float4 yv = make_float4(relu(v[c]), relu(v[c + 1]), relu(v[c + 2]), relu(v[c + 3]));
+        *reinterpret_cast<float4*>(ys + tc::swz_off<DP>(m, cq * CW + c)) = yv;
+        if (LAST)
+          *reinterpret_cast<float4*>(p.Ylo + ((mb + itp) & 1) * C::OPB + tc::swz_off<DP>(m, cq * CW + c)) =
+              f4_trunc_lo(yv);
+      }
       tc::fence_before();
       return false;
     }
+  };
+  // TCP: projection epilogue of local tile itp (its projection MMA completed
+  // with the commit this iteration waited for): the rotating group reads its
+  // rows' 2H accumulator columns, out = (Σ_h relu(z_h + b1_h) dec2_h + b2)·τ/√n
+  auto proj_epilogue = [&](int itp) {
+    const int q = warp & 3, cq = warp >> 2;
+    if (cq != itp % NQ) return;
+    const uint32_t prow = p.tmem + 2 * DP + (static_cast<uint32_t>(32 * q) << 16);
+    float o = 0.f;
+    for (int h0 = 0; h0 < H; h0 += 16) {
+      float z1[16], z2[16];
+      tc::tmem_ld16(prow + h0, z1);
+      tc::tmem_ld16(prow + H + h0, z2);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) o = fmaf(relu(z1[c] + z2[c] + B1[h0 + c]), D2[h0 + c], o);
+    }
+    tc::fence_before();
+    const int i = (blockIdx.x + itp * gridDim.x) * TM + 32 * q + lane;
+    if (i < n) out[i] = static_cast<OutT>(static_cast<double>(o + net.dec2_b) * out_scale);
   };
   auto arrive = [&]() {
     tc::fence_proxy_async();
@@ -523,7 +610,8 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
 
   const int* tinfo = CSR ? a.tflag : a.sell_k;  // per tile: K_t | has-long << 16 (SELL), has-long (CSR)
   int kw = __ldg(tinfo + blockIdx.x);
-  for (int it = 0; it <= my_tiles; ++it) {
+  const int iters = my_tiles + 1 + (TCP ? 1 : 0);
+  for (int it = 0; it < iters; ++it) {
     const bool have = it < my_tiles;
     const int tile = blockIdx.x + it * gridDim.x;
     const int row0 = tile * TM;
@@ -574,7 +662,14 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
     }
 
     // ------------------------------------------- epilogue of the previous tile
-    const bool proj = it >= 1 && epilogue(it - 1);
+    bool proj = false;
+    if (it >= 1 && it - 1 < my_tiles) {
+      proj = epilogue(it - 1);
+    } else if (TCP && it == my_tiles + 1) {  // drain: wait for the last projection MMA
+      tc::mbar_wait_dbg(p.mma_bar, (mb + my_tiles) & 1, 2, it);
+      tc::fence_after();
+    }
+    if (TCP && it >= 2) proj_epilogue(it - 2);
 
     // ---------------------------------------------------------------- split
     if (have) {
@@ -588,7 +683,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         *reinterpret_cast<float4*>(p.A + 2 * C::OPB + o) = f4_trunc_lo(acc[j]);
       }
     }
-    arrive();
+    if (it <= my_tiles) arrive();
     if (proj) project((blockIdx.x + (it - 1) * gridDim.x) * TM);
   }
 }
@@ -607,7 +702,7 @@ k_layer_sell(DevCsr a, const __grid_constant__ SellMaps maps, const float* __res
     }
     return;
   }
-  auto p = sell_setup<DP, CSR>(net.hidden);
+  auto p = sell_setup<DP, CSR>(net.hidden, LAST);
   sell_layer<DP, LAST, OutT, CSR>(p, a, &maps.x, &maps.y, X, axlong, uwp, net, sc->out_scale, out);
   sell_teardown(p);
 }
@@ -701,7 +796,7 @@ k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restri
     for (int i = blockIdx.x * C::NT + tid; i < n; i += gridDim.x * C::NT) out[i] = OutT(0);
     return;
   }
-  auto p = sell_setup<DP, CSR>(net.hidden);
+  auto p = sell_setup<DP, CSR>(net.hidden, true);
   // ------------------------------------------- lift into X[0] (own tiles' rows)
   {
     const int nb = net.nbreak;

@@ -135,7 +135,48 @@ k_layer_batched(DevCsr a, const float* __restrict__ X, float* __restrict__ Y,
 // out[v] = (dec2 · relu(dec1ᵀ x_L + dec1_b) + dec2_b) * out_scale_k (f64 store)
 // (src/gnn.cpp:178-199).  One thread per virtual row, dec1 in smem.
 template <int DP>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(32 * 4)
+k_decoder_fwd(const float* __restrict__ XL, int nv, int B, NetView net,
+              const SampleScales* __restrict__ sc, double* __restrict__ out);
+
+// Warp-staged row I/O for the per-row MLP kernels below: a warp owns 32
+// consecutive virtual rows (lane = row).  Rows are loaded/stored as one
+// contiguous block with 16-byte coalesced accesses and transposed through a
+// padded shared tile [32][W + 1] (conflict-free for a lane reading its row).
+template <int W>
+__device__ __forceinline__ void warp_rows_load(const float* __restrict__ src, int v0, int nv, float* st,
+                                               int lane) {
+  const int rows = min(32, nv - v0);
+  const float4* s4 = reinterpret_cast<const float4*>(src + static_cast<size_t>(v0) * W);
+  for (int q = lane; q < rows * (W / 4); q += 32) {
+    const float4 t = ldg4(reinterpret_cast<const float*>(s4 + q));
+    const int r = q / (W / 4), c = (q % (W / 4)) * 4;
+    float* d = st + r * (W + 1) + c;
+    d[0] = t.x;
+    d[1] = t.y;
+    d[2] = t.z;
+    d[3] = t.w;
+  }
+  __syncwarp();
+}
+template <int W>
+__device__ __forceinline__ void warp_rows_store(float* __restrict__ dst, int v0, int nv, const float* st,
+                                                int lane) {
+  __syncwarp();
+  const int rows = min(32, nv - v0);
+  float4* d4 = reinterpret_cast<float4*>(dst + static_cast<size_t>(v0) * W);
+  for (int q = lane; q < rows * (W / 4); q += 32) {
+    const int r = q / (W / 4), c = (q % (W / 4)) * 4;
+    const float* s = st + r * (W + 1) + c;
+    d4[q] = make_float4(s[0], s[1], s[2], s[3]);
+  }
+  __syncwarp();
+}
+
+// Decoder forward (src/gnn.cpp:178-199) for one virtual row (out in f64 [n][B]),
+// rows read through the warp staging.
+template <int DP>
+__global__ void __launch_bounds__(32 * 4)
 k_decoder_fwd(const float* __restrict__ XL, int nv, int B, NetView net,
               const SampleScales* __restrict__ sc, double* __restrict__ out) {
   extern __shared__ float4 sm4[];
@@ -143,32 +184,47 @@ k_decoder_fwd(const float* __restrict__ XL, int nv, int B, NetView net,
   float* D1 = reinterpret_cast<float*>(sm4);  // [DP][H]
   float* B1 = D1 + DP * H;
   float* D2 = B1 + H;
-  for (int t = threadIdx.x; t < DP * H; t += kThreads) D1[t] = net.dec1[t];
-  for (int t = threadIdx.x; t < H; t += kThreads) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* sx = D2 + H + warp * 32 * (DP + 1);
+  for (int t = threadIdx.x; t < DP * H; t += blockDim.x) D1[t] = net.dec1[t];
+  for (int t = threadIdx.x; t < H; t += blockDim.x) {
     B1[t] = net.dec1_b[t];
     D2[t] = net.dec2[t];
   }
   __syncthreads();
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
-    const int k = v % B;
-    if (sc[k].zero) {
-      out[v] = 0.0;
-      continue;
-    }
-    float y[DP];
+  const int nwarps = gridDim.x * 4;
+  for (int v0 = (blockIdx.x * 4 + warp) * 32; v0 < nv; v0 += nwarps * 32) {
+    warp_rows_load<DP>(XL, v0, nv, sx, lane);
+    const int v = v0 + lane;
+    if (v < nv) {
+      const int k = v % B;
+      if (sc[k].zero) {
+        out[v] = 0.0;
+      } else {
+        float y[DP];
 #pragma unroll
-    for (int j = 0; j < DP; j += 4) {
-      const float4 t = ldg4(XL + static_cast<size_t>(v) * DP + j);
-      y[j] = t.x; y[j + 1] = t.y; y[j + 2] = t.z; y[j + 3] = t.w;
-    }
-    float o = 0.f;
-    for (int h = 0; h < H; ++h) {
-      float t = 0.f;
+        for (int j = 0; j < DP; ++j) y[j] = sx[lane * (DP + 1) + j];
+        float o = 0.f;
+        int h = 0;
+        for (; (H & 3) == 0 && h < H; h += 4) {  // dec1 read as float4 along h
+          float4 t = f4zero();
 #pragma unroll
-      for (int j = 0; j < DP; ++j) t = fmaf(y[j], D1[j * H + h], t);
-      o = fmaf(relu(t + B1[h]), D2[h], o);
+          for (int j = 0; j < DP; ++j) fma4(t, y[j], *reinterpret_cast<const float4*>(D1 + j * H + h));
+          o = fmaf(relu(t.x + B1[h]), D2[h], o);
+          o = fmaf(relu(t.y + B1[h + 1]), D2[h + 1], o);
+          o = fmaf(relu(t.z + B1[h + 2]), D2[h + 2], o);
+          o = fmaf(relu(t.w + B1[h + 3]), D2[h + 3], o);
+        }
+        for (; h < H; ++h) {
+          float t = 0.f;
+#pragma unroll
+          for (int j = 0; j < DP; ++j) t = fmaf(y[j], D1[j * H + h], t);
+          o = fmaf(relu(t + B1[h]), D2[h], o);
+        }
+        out[v] = static_cast<double>(o + *net.dec2_bp) * sc[k].out_scale;
+      }
     }
-    out[v] = static_cast<double>(o + *net.dec2_bp) * sc[k].out_scale;
+    __syncwarp();
   }
 }
 
@@ -177,8 +233,15 @@ k_decoder_fwd(const float* __restrict__ XL, int nv, int B, NetView net,
 //   stage 0: post[v][h] = relu(dec_pre_h), gy[v]      (for dec2 / dec2_b grads)
 //   stage 1: gdp[v][h] = [dec_pre_h > 0] gy dec2_h      (for dec1 / dec1_b grads)
 //            gpre[v][j] = [x_L > 0] Σ_h gdp_h dec1(j,h)  (mask of the last layer)
+// One lane per row, 32-row blocks per warp with warp-staged row I/O
+// (kMlpWarps warps per block; dynamic smem = mlp_smem_bytes).
+constexpr int kMlpWarps = 4;
+inline size_t mlp_smem_bytes(int DP, int H) {
+  const int sw = (DP > H ? DP : H) + 1;
+  return (static_cast<size_t>(DP) * H + 2 * H + static_cast<size_t>(kMlpWarps) * 3 * 32 * sw) * 4;
+}
 template <int DP>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(32 * kMlpWarps)
 k_decoder_bwd(const float* __restrict__ XL, int nv, int B, NetView net,
               const SampleScales* __restrict__ sc, const double* __restrict__ gout,
               float* __restrict__ post, float* __restrict__ gyv, float* __restrict__ gdp,
@@ -188,44 +251,86 @@ k_decoder_bwd(const float* __restrict__ XL, int nv, int B, NetView net,
   float* D1 = reinterpret_cast<float*>(sm4);  // [DP][H]
   float* B1 = D1 + DP * H;
   float* D2 = B1 + H;
-  for (int t = threadIdx.x; t < DP * H; t += kThreads) D1[t] = net.dec1[t];
-  for (int t = threadIdx.x; t < H; t += kThreads) {
+  const int SW = max(DP, H) + 1;  // staging capacity per row
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* stg = D2 + H + warp * 3 * 32 * SW;  // [3][32][SW]: x / gpre, post, gdp
+  float* sx = stg;
+  float* sp = stg + 32 * SW;
+  float* sg = sp + 32 * SW;
+  for (int t = threadIdx.x; t < DP * H; t += blockDim.x) D1[t] = net.dec1[t];
+  for (int t = threadIdx.x; t < H; t += blockDim.x) {
     B1[t] = net.dec1_b[t];
     D2[t] = net.dec2[t];
   }
   __syncthreads();
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+  const int nwarps = gridDim.x * kMlpWarps;
+  for (int v0 = (blockIdx.x * kMlpWarps + warp) * 32; v0 < nv; v0 += nwarps * 32) {
+    // rows through the staging tile (stride DP + 1 inside warp_rows_*)
+    warp_rows_load<DP>(XL, v0, nv, sx, lane);
+    const int v = v0 + lane;
+    const bool live = v < nv;
     const int k = v % B;
-    const float gy = sc[k].zero ? 0.f : static_cast<float>(gout[v] * sc[k].out_scale);
-    gyv[v] = gy;
+    const float gy = (!live || sc[k].zero) ? 0.f : static_cast<float>(gout[v] * sc[k].out_scale);
+    if (live) gyv[v] = gy;
     float y[DP], gx[DP];
 #pragma unroll
-    for (int j = 0; j < DP; j += 4) {
-      const float4 t = ldg4(XL + static_cast<size_t>(v) * DP + j);
-      y[j] = t.x; y[j + 1] = t.y; y[j + 2] = t.z; y[j + 3] = t.w;
+    for (int j = 0; j < DP; ++j) {
+      y[j] = sx[lane * (DP + 1) + j];
+      gx[j] = 0.f;
     }
+    int h = 0;
+    for (; (H & 3) == 0 && h < H; h += 4) {  // dec1 read as float4 along h, twice
+      float4 t = f4zero();
 #pragma unroll
-    for (int j = 0; j < DP; ++j) gx[j] = 0.f;
-    for (int h = 0; h < H; ++h) {
+      for (int j = 0; j < DP; ++j) fma4(t, y[j], *reinterpret_cast<const float4*>(D1 + j * H + h));
+      const float p0 = t.x + B1[h], p1 = t.y + B1[h + 1], p2 = t.z + B1[h + 2], p3 = t.w + B1[h + 3];
+      const float g0 = p0 > 0.f ? gy * D2[h] : 0.f, g1 = p1 > 0.f ? gy * D2[h + 1] : 0.f;
+      const float g2 = p2 > 0.f ? gy * D2[h + 2] : 0.f, g3 = p3 > 0.f ? gy * D2[h + 3] : 0.f;
+      float* pp = sp + lane * (H + 1) + h;
+      float* pg = sg + lane * (H + 1) + h;
+      pp[0] = relu(p0); pp[1] = relu(p1); pp[2] = relu(p2); pp[3] = relu(p3);
+      pg[0] = g0; pg[1] = g1; pg[2] = g2; pg[3] = g3;
+#pragma unroll
+      for (int j = 0; j < DP; ++j) {
+        const float4 d = *reinterpret_cast<const float4*>(D1 + j * H + h);
+        gx[j] = fmaf(g0, d.x, fmaf(g1, d.y, fmaf(g2, d.z, fmaf(g3, d.w, gx[j]))));
+      }
+    }
+    for (; h < H; ++h) {
       float t = 0.f;
 #pragma unroll
       for (int j = 0; j < DP; ++j) t = fmaf(y[j], D1[j * H + h], t);
       const float pre = t + B1[h];
-      post[static_cast<size_t>(v) * H + h] = relu(pre);
+      sp[lane * (H + 1) + h] = relu(pre);
       const float g = pre > 0.f ? gy * D2[h] : 0.f;
-      gdp[static_cast<size_t>(v) * H + h] = g;
+      sg[lane * (H + 1) + h] = g;
 #pragma unroll
       for (int j = 0; j < DP; ++j) gx[j] = fmaf(g, D1[j * H + h], gx[j]);
     }
+    __syncwarp();
 #pragma unroll
-    for (int j = 0; j < DP; ++j) gpre[static_cast<size_t>(v) * DP + j] = y[j] > 0.f ? gx[j] : 0.f;
+    for (int j = 0; j < DP; ++j) sx[lane * (DP + 1) + j] = y[j] > 0.f ? gx[j] : 0.f;
+    warp_rows_store<DP>(gpre, v0, nv, sx, lane);
+    if (H == 32) {
+      warp_rows_store<32>(post, v0, nv, sp, lane);
+      warp_rows_store<32>(gdp, v0, nv, sg, lane);
+    } else {
+      __syncwarp();
+      for (int r = 0; r < 32 && v0 + r < nv; ++r)
+        for (int h = lane; h < H; h += 32) {
+          post[static_cast<size_t>(v0 + r) * H + h] = sp[r * (H + 1) + h];
+          gdp[static_cast<size_t>(v0 + r) * H + h] = sg[r * (H + 1) + h];
+        }
+      __syncwarp();
+    }
   }
 }
 
 // Encoder backward (src/gnn.cpp:283-305) for one virtual row: recompute
-// x0 = relu(vv enc1 + b1), g_x0 = enc2 gX0, gp0 = [pre0 > 0] g_x0.
+// x0 = relu(vv enc1 + b1), g_x0 = enc2 gX0, gp0 = [pre0 > 0] g_x0.  Same
+// warp-staged row I/O as the decoder.
 template <int DP>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(32 * kMlpWarps)
 k_encoder_bwd(const float* __restrict__ vv, const float* __restrict__ gx0, int nv, NetView net,
               float* __restrict__ x0, float* __restrict__ gp0) {
   extern __shared__ float4 sm4[];
@@ -233,27 +338,45 @@ k_encoder_bwd(const float* __restrict__ vv, const float* __restrict__ gx0, int n
   float* s_enc2 = reinterpret_cast<float*>(sm4);  // [H][DP]
   float* s_enc1 = s_enc2 + H * DP;
   float* s_b1 = s_enc1 + H;
-  for (int t = threadIdx.x; t < H * DP; t += kThreads) s_enc2[t] = net.enc2[t];
-  for (int t = threadIdx.x; t < H; t += kThreads) {
+  const int SW = max(DP, H) + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* stg = s_b1 + H + warp * 3 * 32 * SW;
+  float* sx = stg;
+  float* sp = stg + 32 * SW;
+  float* sg = sp + 32 * SW;
+  for (int t = threadIdx.x; t < H * DP; t += blockDim.x) s_enc2[t] = net.enc2[t];
+  for (int t = threadIdx.x; t < H; t += blockDim.x) {
     s_enc1[t] = net.enc1[t];
     s_b1[t] = net.enc1_b[t];
   }
   __syncthreads();
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+  const int nwarps = gridDim.x * kMlpWarps;
+  for (int v0 = (blockIdx.x * kMlpWarps + warp) * 32; v0 < nv; v0 += nwarps * 32) {
+    warp_rows_load<DP>(gx0, v0, nv, sx, lane);
+    const int v = v0 + lane;
+    const float x = v < nv ? vv[v] : 0.f;
     float g[DP];
 #pragma unroll
-    for (int j = 0; j < DP; j += 4) {
-      const float4 t = ldg4(gx0 + static_cast<size_t>(v) * DP + j);
-      g[j] = t.x; g[j + 1] = t.y; g[j + 2] = t.z; g[j + 3] = t.w;
-    }
-    const float x = vv[v];
+    for (int j = 0; j < DP; ++j) g[j] = sx[lane * (DP + 1) + j];
     for (int h = 0; h < H; ++h) {
       const float pre = fmaf(x, s_enc1[h], s_b1[h]);
       float t = 0.f;
 #pragma unroll
       for (int j = 0; j < DP; ++j) t = fmaf(g[j], s_enc2[h * DP + j], t);
-      x0[static_cast<size_t>(v) * H + h] = relu(pre);
-      gp0[static_cast<size_t>(v) * H + h] = pre > 0.f ? t : 0.f;
+      sp[lane * (H + 1) + h] = relu(pre);
+      sg[lane * (H + 1) + h] = pre > 0.f ? t : 0.f;
+    }
+    if (H == 32) {
+      warp_rows_store<32>(x0, v0, nv, sp, lane);
+      warp_rows_store<32>(gp0, v0, nv, sg, lane);
+    } else {
+      __syncwarp();
+      for (int r = 0; r < 32 && v0 + r < nv; ++r)
+        for (int h = lane; h < H; h += 32) {
+          x0[static_cast<size_t>(v0 + r) * H + h] = sp[r * (H + 1) + h];
+          gp0[static_cast<size_t>(v0 + r) * H + h] = sg[r * (H + 1) + h];
+        }
+      __syncwarp();
     }
   }
 }

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "capi_common.hpp"
@@ -98,6 +99,17 @@ void make_red(gnpc_trainer_s::Red& r, const float* A1, int P1, int s1, const flo
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+// raise a kernel's dynamic shared-memory limit once per (kernel, size)
+void set_smem_once(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, size_t>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first == kern && d.second >= bytes) return;
+  GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done.emplace_back(kern, bytes);
+}
+
 // [nv][32] fp32 rows viewed as a 2-D tensor, box {32 features, 128 rows}, 128B swizzle.
 CUtensorMap rows32_map(const float* base, int nv) {
   return make_rows_map(base, nv, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -259,9 +271,10 @@ struct TrainLaunch {
     }
     for (int l = 0; l < T.L; ++l)
       layer(T, true, l, T.Xs.p + l * act, T.Xs.p + (l + 1) * act, T.AXs.p + l * act, nullptr);
-    const size_t smem = ((size_t)DP * T.H + 2 * (size_t)T.H) * 4;
-    const int g = grid_for(T.nv, kTh, T.sms * 8);
-    gnpk::k_decoder_fwd<DP><<<g, kTh, smem, T.s>>>(T.Xs.p + T.L * act, T.nv, T.B, net, T.scl.p,
+    const size_t smem = ((size_t)DP * T.H + 2 * (size_t)T.H + 4 * 32 * (DP + 1)) * 4;
+    const int g = grid_for(T.nv, 128, T.sms * 16);
+    set_smem_once((const void*)gnpk::k_decoder_fwd<DP>, smem);
+    gnpk::k_decoder_fwd<DP><<<g, 128, smem, T.s>>>(T.Xs.p + T.L * act, T.nv, T.B, net, T.scl.p,
                                                    T.out.p);
     GNPC_LAUNCHED();
   }
@@ -271,9 +284,10 @@ struct TrainLaunch {
     const std::size_t act = (std::size_t)T.nv * DP;
     GNPC_CUDA(cudaMemsetAsync(T.g64.p, 0, T.P * sizeof(double), T.s));
     {
-      const size_t smem = ((size_t)DP * T.H + 2 * (size_t)T.H) * 4;
-      const int g = grid_for(T.nv, kTh, T.sms * 8);
-      gnpk::k_decoder_bwd<DP><<<g, kTh, smem, T.s>>>(T.Xs.p + T.L * act, T.nv, T.B, net, T.scl.p,
+      const size_t smem = gnpk::mlp_smem_bytes(DP, T.H);
+      const int g = grid_for(T.nv, 32 * gnpk::kMlpWarps, T.sms * 16);
+      set_smem_once((const void*)gnpk::k_decoder_bwd<DP>, smem);
+      gnpk::k_decoder_bwd<DP><<<g, 32 * gnpk::kMlpWarps, smem, T.s>>>(T.Xs.p + T.L * act, T.nv, T.B, net, T.scl.p,
                                                      T.gout.p, T.hb1.p, T.gyv.p, T.hb2.p, T.G[0].p);
       GNPC_LAUNCHED();
     }
@@ -287,9 +301,11 @@ struct TrainLaunch {
       cur = 1 - cur;
     }
     {
-      const size_t smem = (size_t)T.H * DP * 4 + 2 * (size_t)T.H * 4;
-      const int g = grid_for(T.nv, kTh, T.sms * 8);
-      gnpk::k_encoder_bwd<DP><<<g, kTh, smem, T.s>>>(T.vv.p, T.G[cur].p, T.nv, net, T.hb1.p, T.hb2.p);
+      const size_t smem = gnpk::mlp_smem_bytes(DP, T.H);
+      const int g = grid_for(T.nv, 32 * gnpk::kMlpWarps, T.sms * 16);
+      set_smem_once((const void*)gnpk::k_encoder_bwd<DP>, smem);
+      gnpk::k_encoder_bwd<DP><<<g, 32 * gnpk::kMlpWarps, smem, T.s>>>(T.vv.p, T.G[cur].p, T.nv, net, T.hb1.p,
+                                                                      T.hb2.p);
       GNPC_LAUNCHED();
     }
     T.red_enc2.o.Bm = T.G[cur].p;

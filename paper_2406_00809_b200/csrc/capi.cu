@@ -313,9 +313,19 @@ void gnpc_csr_s::upload() {
     max_row = std::max(max_row, len);
     if (len > gnpk::kLongRow) longs.push_back(static_cast<int>(i));
   }
-  rp.upload(hrp.data(), hrp.size());
-  ci.upload(hci.data(), hci.size());
-  v.upload(hv.data(), hv.size());
+  // padded copies (row_ptr + 132 entries of nnz, col/val + 4 zeros): the
+  // training TMA layers bulk-copy 16-byte-aligned supersets of a tile's range
+  {
+    std::vector<int> prp(hrp);
+    prp.resize(hrp.size() + 132, hrp.back());
+    std::vector<int> pci(hci);
+    pci.resize(hci.size() + 4, 0);
+    std::vector<float> pv(hv);
+    pv.resize(hv.size() + 4, 0.f);
+    rp.upload(prp.data(), prp.size());
+    ci.upload(pci.data(), pci.size());
+    v.upload(pv.data(), pv.size());
+  }
   n_long = static_cast<int>(longs.size());
   if (n_long) {
     long_rows.upload(longs.data(), longs.size());
@@ -531,6 +541,7 @@ void gnpc_model_s::build_maps() {
     // of part p = [U; W](k + p*DP, j)
     const std::size_t pb = (std::size_t)dp * dp;
     map_tc_pair.assign((std::size_t)L * 4 * pb, -1);
+    map_tc_pair_bwd.assign((std::size_t)L * 4 * pb, -1);
     part_pair.assign((std::size_t)L * 4 * pb, 0);
     for (std::int64_t l = 0; l < L; ++l)
       for (int b = 0; b < 4; ++b)
@@ -539,6 +550,7 @@ void gnpc_model_s::build_maps() {
             const std::size_t off = (dp == 32 ? gnpk::tc::swz_off<32>(j, k) : gnpk::tc::swz_off<16>(j, k)) / 4;
             const std::size_t i = (std::size_t)l * 4 * pb + b * pb + off;
             map_tc_pair[i] = fwd_src(l, j, k + (b >> 1) * dp);
+            map_tc_pair_bwd[i] = bwd_src(l, j, k + (b >> 1) * dp);
             part_pair[i] = (b & 1) ? 0 : 1;  // 1 = lo part
           }
   }

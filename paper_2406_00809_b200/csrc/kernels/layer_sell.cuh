@@ -81,9 +81,11 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 
 }  // namespace tc
 
-// CSR = false: sliced-ELL slices (k_layer_sell on regular matrices);
-// CSR = true : the short-row CSR ranges of the tile (ragged matrices).
-template <int DP, bool CSR = false>
+// CSR = 0: sliced-ELL slices (k_layer_sell on regular matrices);
+// CSR = 1: the short-row CSR ranges of the tile (ragged matrices);
+// CSR = 2: training — B virtual rows per node (v = node*B + k), the full CSR
+//          ranges of the tile's 128/B nodes, plus a mask tile for the backward.
+template <int DP, int CSR = 0>
 struct SellCfg {
   // one CTA per SM: 16 math warps on one tile at a time (two 8-warp CTAs per
   // SM measured slower at DP=16: C2 26.0 vs 24.4 us, C4 213 vs 160 us)
@@ -111,10 +113,12 @@ struct SellCfg {
   static constexpr int TALLOC = TCOLS < 32 ? 32 : TCOLS;  // power of two >= 32
   static constexpr uint32_t CVB = KCAP * TM * 8; // staged slice (bytes)
   // CSR: [X tile | row_ptr slice (TM+4 ints, 1 KiB) | col_idx (CAPC) | values (CAPC)]
-  static constexpr int CAPC = DP == 16 ? 2048 : 1024;  // staged short-row nonzeros per tile (DP=32: fits the
-                                                       // last layer's projection operands)
+  static constexpr bool TR = CSR == 2;
+  static constexpr int CAPC = TR ? 512 : (DP == 16 ? 2048 : 1024);  // staged nonzeros per tile (DP=32
+                                                                     // apply: fits the projection operands)
   static constexpr uint32_t RPB = (TM + 4) * 4;  // row_ptr slice copy (bytes, 16-B multiple)
-  static constexpr uint32_t O_RP = OPB, O_CI = OPB + 1024, O_V = O_CI + CAPC * 4;
+  static constexpr uint32_t O_MASK = OPB;        // training backward: mask tile (X_l)
+  static constexpr uint32_t O_RP = TR ? 2 * OPB : OPB, O_CI = O_RP + 1024, O_V = O_CI + CAPC * 4;
   static constexpr uint32_t SLOT =
       CSR ? ((O_V + CAPC * 4 + 1023) & ~1023u) : (((OPB + CVB) + 1023) & ~1023u);
   // layout (offsets from the 1024-aligned base)
@@ -135,8 +139,9 @@ struct SellCfg {
   static size_t smem_bytes(int hidden, bool last) {
     return o_bar(hidden, last) + 128 + 1024;  // barriers + TMEM slot, 1024-B alignment slack
   }
-  static_assert(O_D1OP + 2 * 32 * DP * 4 + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
+  static_assert(TR || O_D1OP + 2 * 32 * DP * 4 + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
                 "last-layer layout must fit shared memory at hidden 32 (larger: host falls back)");
+  static_assert(!TR || O_Y + 2 * OPB + 128 + 1024 <= 227 * 1024, "training layout must fit shared memory");
   // TMEM: layer accumulator [0, 2DP); last layer's projection accumulator at
   // [2DP, 2DP + 2H) (tensor-core projection when H % 16 == 0 and H <= 64)
   static constexpr int TALLOC_LAST = 256;
@@ -215,10 +220,9 @@ __device__ __forceinline__ void gather_sell_rows(const float* __restrict__ X, in
 // of the group's rows.  Slots past a row's end get weight 0 and the row's own
 // X row (in bounds, usually cached), so no load is predicated.
 template <int DP, int R, int US>
-__device__ __forceinline__ void gather_csr_rows(const float* __restrict__ X, int gl, const int* ci,
-                                                const float* vv, const int (&s)[R], const int (&len)[R],
-                                                const int (&self)[R], float4 (&acc)[R]) {
-  const char* xb = reinterpret_cast<const char*>(X + 4 * gl);
+__device__ __forceinline__ void gather_csr_rows(const char* const (&xbj)[R], unsigned long long stride,
+                                                const int* ci, const float* vv, const int (&s)[R],
+                                                const int (&len)[R], const int (&self)[R], float4 (&acc)[R]) {
   int kmax = len[0];
 #pragma unroll
   for (int j = 1; j < R; ++j) kmax = max(kmax, len[j]);
@@ -240,13 +244,24 @@ __device__ __forceinline__ void gather_csr_rows(const float* __restrict__ X, int
 #pragma unroll
       for (int j = 0; j < R; ++j)
         x[j][u] = ldg4(reinterpret_cast<const float*>(
-            xb + static_cast<unsigned long long>(static_cast<unsigned>(c[j][u])) * (DP * 4ull)));
+            xbj[j] + static_cast<unsigned long long>(static_cast<unsigned>(c[j][u])) * stride));
 #pragma unroll
     for (int u = 0; u < US; ++u)
 #pragma unroll
       for (int j = 0; j < R; ++j) fma4(acc[j], w[j][u], x[j][u]);
   }
 }
+
+// Training extras for sell_layer (CSR = 2): B virtual rows per node; KIND 1
+// (forward) also stores the tile's ÂX (= the A2_hi operand, raw fp32) through
+// mapax; KIND 2 (backward) multiplies by [mask > 0] from the mask tile
+// (mapmask over X_l) when use_mask.
+struct TrainIO {
+  const CUtensorMap* mapax;
+  const CUtensorMap* mapmask;
+  int bs;
+  int use_mask;
+};
 
 __device__ __forceinline__ float4 f4_trunc_lo(float4 v) {
   return make_float4(v.x - __int_as_float(__float_as_int(v.x) & 0xffffe000),
@@ -273,7 +288,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // afull(t) tells the control warp every warp passed its wait for MMA(t-1),
 // so tile t-1's ring slot may be refilled.  The phase counters run on across
 // the layers of the persistent kernel.
-template <int DP, bool CSR>
+template <int DP, int CSR>
 struct SellPipe {
   using C = SellCfg<DP, CSR>;
   uint8_t* ring;
@@ -292,7 +307,7 @@ struct SellPipe {
 };
 
 // smem carve-up, barrier init, TMEM allocation (all threads of the CTA)
-template <int DP, bool CSR>
+template <int DP, int CSR>
 __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
   using C = SellCfg<DP, CSR>;
   extern __shared__ float4 smem_raw[];
@@ -329,7 +344,7 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
   return p;
 }
 
-template <int DP, bool CSR>
+template <int DP, int CSR>
 __device__ __forceinline__ void sell_teardown(const SellPipe<DP, CSR>& p) {
   tc::fence_before();
   __syncthreads();
@@ -341,15 +356,22 @@ __device__ __forceinline__ void sell_teardown(const SellPipe<DP, CSR>& p) {
 // LAST: projection epilogue writing out[i] = (dec2ᵀ relu(dec1ᵀ y + b1) + b2)
 // · out_scale (no Y).  uwp: the layer's B operands [Bu_lo | Bu_hi | Bw_lo |
 // Bw_hi] in the swz_off<DP> layout.
-template <int DP, bool LAST, typename OutT, bool CSR>
+template <int DP, bool LAST, typename OutT, int CSR, int KIND = 0>
 __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a, const CUtensorMap* mapx,
                                            const CUtensorMap* mapy, const float* __restrict__ X,
                                            const float* __restrict__ axlong, const float* __restrict__ uwp,
-                                           const NetView& net, double out_scale, OutT* __restrict__ out) {
+                                           const NetView& net, double out_scale, OutT* __restrict__ out,
+                                           const TrainIO* tio = nullptr) {
   using C = SellCfg<DP, CSR>;
   constexpr int TM = C::TM, G = C::G, R = C::R, NS = C::NS, NW = C::NW, NQ = C::NQ;
-  const int n = a.n;
+  constexpr bool TR = C::TR;
+  static_assert(!TR || (!LAST && KIND != 0), "training layers have no projection");
+  const int bs = TR ? tio->bs : 1;           // virtual rows per node
+  const int nodes = a.n;
+  const int n = nodes * bs;                  // (virtual) rows
   const int ntiles = (n + TM - 1) / TM;
+  const int npt = TM / bs;                   // nodes per tile (training: bs divides TM)
+  const bool use_mask = KIND == 2 && tio->use_mask;
   const int H = net.hidden;
   float* D1 = p.D1;
   float* B1 = D1 + DP * H;
@@ -402,7 +424,22 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         const int r = rb + it;
         const int s = r % NS;
         uint8_t* slot = p.ring + s * C::SLOT;
-        if constexpr (CSR) {
+        if constexpr (TR) {
+          // the tile's nodes [n0, n0 + npt): full CSR range (padded arrays)
+          const int n0 = t * npt;
+          const int kb = __ldg(a.rp + n0), ke = __ldg(a.rp + min(n0 + npt, nodes));
+          const int a0 = kb & ~3, cnt = ((ke + 3) & ~3) - a0;
+          const bool staged = cnt <= C::CAPC;
+          tc::mbar_expect_tx(&p.full[s],
+                             C::OPB + (use_mask ? C::OPB : 0) + C::RPB + (staged ? 8 * cnt : 0));
+          tc::tma_load_2d(slot, mapx, 0, t * TM, &p.full[s]);
+          if (use_mask) tc::tma_load_2d(slot + C::O_MASK, tio->mapmask, 0, t * TM, &p.full[s]);
+          tc::bulk_load(slot + C::O_RP, a.rp + n0, C::RPB, &p.full[s]);
+          if (staged && cnt > 0) {
+            tc::bulk_load(slot + C::O_CI, a.ci + a0, 4 * cnt, &p.full[s]);
+            tc::bulk_load(slot + C::O_V, a.v + a0, 4 * cnt, &p.full[s]);
+          }
+        } else if constexpr (CSR) {
           // the tile's short-row CSR range, 16-byte aligned superset [a0, a1)
           const int kb = __ldg(a.rps + t * TM), ke = __ldg(a.rps + min((t + 1) * TM, n));
           const int a0 = kb & ~3, cnt = ((ke + 3) & ~3) - a0;
@@ -433,6 +470,10 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         // stores issued up to the previous iteration have left the Y staging:
         // the buffer the epilogue after this MMA writes is free
         tc::bulk_wait_read0();
+        if (KIND == 1 && it < my_tiles) {  // training forward: the tile's ÂX (A2_hi) to HBM
+          tc::tma_store_2d(tio->mapax, p.A + C::OPB, 0, (blockIdx.x + it * gridDim.x) * TM);
+          tc::bulk_commit();
+        }
         if (it < my_tiles) {
           const uint32_t sX = tc::smem_u32(p.ring + ((rb + it) % NS) * C::SLOT);
           // 3xTF32 with the two A_hi products stacked along N (A_hi is read
@@ -473,6 +514,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
                          iH, 1);
           }
         }
+        if (KIND == 1 && it < my_tiles) tc::bulk_wait_read0();  // A2_hi is rewritten after the commit
         if (it < my_tiles || (TCP && it >= 1)) tc::mma_commit(p.mma_bar);
         if (!LAST && it >= 1) {  // tile it-1 is fully staged
           tc::tma_store_2d(mapy, p.Ystg + ((mb + it - 1) & 1) * C::OPB, 0,
@@ -542,10 +584,25 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           for (int c = 0; c < 8; ++c) v[c0 + c] = u1[c] + u2[c];
         }
       }
+      // training backward: D ⊙ [X_l > 0] from the tile's mask (its ring slot
+      // is refilled only after this iteration's arrival), no relu
+      const uint8_t* msk = p.ring + ((rb + itp) % NS) * C::SLOT + C::O_MASK;
 #pragma unroll
       for (int c = 0; c < CW; c += 4)
       {
-        const float4 yv = make_float4(relu(v[c]), relu(v[c + 1]), relu(v[c + 2]), relu(v[c + 3]));
+        float4 yv;
+        if constexpr (KIND == 2) {
+          yv = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+          if (use_mask) {
+            const float4 mk = *reinterpret_cast<const float4*>(msk + tc::swz_off<DP>(m, cq * CW + c));
+            yv.x = mk.x > 0.f ? yv.x : 0.f;
+            yv.y = mk.y > 0.f ? yv.y : 0.f;
+            yv.z = mk.z > 0.f ? yv.z : 0.f;
+            yv.w = mk.w > 0.f ? yv.w : 0.f;
+          }
+        } else {
+          yv = make_float4(relu(v[c]), relu(v[c + 1]), relu(v[c + 2]), relu(v[c + 3]));
+        }
         *reinterpret_cast<float4*>(ys + tc::swz_off<DP>(m, cq * CW + c)) = yv;
         if (LAST)
           *reinterpret_cast<float4*>(p.Ylo + ((mb + itp) & 1) * C::OPB + tc::swz_off<DP>(m, cq * CW + c)) =
@@ -609,7 +666,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   };
 
   const int* tinfo = CSR ? a.tflag : a.sell_k;  // per tile: K_t | has-long << 16 (SELL), has-long (CSR)
-  int kw = __ldg(tinfo + blockIdx.x);
+  int kw = TR ? 0 : __ldg(tinfo + blockIdx.x);
   const int iters = my_tiles + 1 + (TCP ? 1 : 0);
   for (int it = 0; it < iters; ++it) {
     const bool have = it < my_tiles;
@@ -620,9 +677,9 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
     float4 acc[R];
     if (have) {
       const int K = CSR ? 0 : (kw & 0xffff);
-      const bool haslong = CSR ? kw != 0 : (kw >> 16) != 0;
+      const bool haslong = !TR && (CSR ? kw != 0 : (kw >> 16) != 0);
       const bool staged = K > 0 && K <= C::KCAP;
-      kw = it + 1 < my_tiles ? __ldg(tinfo + tile + gridDim.x) : 0;  // prefetch
+      if (!TR) kw = it + 1 < my_tiles ? __ldg(tinfo + tile + gridDim.x) : 0;  // prefetch
 
       // ----------------------------------------------------------- gather
 #pragma unroll
@@ -633,12 +690,40 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           acc[j] = ldg4(axlong + static_cast<size_t>(i) * DP + 4 * gl);
       }
       tc::mbar_wait_dbg(&p.full[r % NS], (r / NS) & 1, 3, it);
-      if constexpr (CSR) {
+      if constexpr (TR) {
+        // virtual row v = node*bs + k gathers X rows (col*bs + k) of node's
+        // neighbours: one staged (col, val) list serves the node's bs rows
+        const int* rpt = reinterpret_cast<const int*>(slot + C::O_RP);
+        const int n0 = tile * npt;
+        const int kb = rpt[0], ke = rpt[min(npt, nodes - n0)];
+        const int a0 = kb & ~3;
+        const bool st = ((ke + 3) & ~3) - a0 <= C::CAPC;
+        int sj[R], lj[R], self[R];
+        const char* xbj[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const int v = row0 + R * gid + j;
+          const int node = min(v, n - 1) / bs, k = min(v, n - 1) - node * bs;
+          const int ln = node - n0;
+          const int e0 = rpt[ln], e1 = rpt[ln + 1];
+          sj[j] = st ? e0 - a0 : e0;
+          lj[j] = v < n ? e1 - e0 : 0;
+          self[j] = node;
+          xbj[j] = reinterpret_cast<const char*>(X + static_cast<size_t>(k) * DP + 4 * gl);
+        }
+        const unsigned long long stride = static_cast<unsigned long long>(bs) * DP * 4;
+        if (st)
+          gather_csr_rows<DP, R, C::USC>(xbj, stride, reinterpret_cast<const int*>(slot + C::O_CI),
+                                         reinterpret_cast<const float*>(slot + C::O_V), sj, lj, self, acc);
+        else
+          gather_csr_rows<DP, R, C::USC>(xbj, stride, a.ci, a.v, sj, lj, self, acc);
+      } else if constexpr (CSR) {
         const int* rpt = reinterpret_cast<const int*>(slot + C::O_RP);
         const int kb = rpt[0], ke = rpt[min(TM, n - row0)];
         const int a0 = kb & ~3;
         const bool st = ((ke + 3) & ~3) - a0 <= C::CAPC;
         int sj[R], lj[R], self[R];
+        const char* xbj[R];
 #pragma unroll
         for (int j = 0; j < R; ++j) {
           const int rr = R * gid + j;
@@ -646,12 +731,13 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           sj[j] = st ? e0 - a0 : e0;
           lj[j] = row0 + rr < n ? e1 - e0 : 0;
           self[j] = min(row0 + rr, n - 1);
+          xbj[j] = reinterpret_cast<const char*>(X + 4 * gl);
         }
         if (st)
-          gather_csr_rows<DP, R, C::USC>(X, gl, reinterpret_cast<const int*>(slot + C::O_CI),
+          gather_csr_rows<DP, R, C::USC>(xbj, DP * 4ull, reinterpret_cast<const int*>(slot + C::O_CI),
                                          reinterpret_cast<const float*>(slot + C::O_V), sj, lj, self, acc);
         else
-          gather_csr_rows<DP, R, C::USC>(X, gl, a.cis, a.vs, sj, lj, self, acc);
+          gather_csr_rows<DP, R, C::USC>(xbj, DP * 4ull, a.cis, a.vs, sj, lj, self, acc);
       } else {
         if (staged)
           gather_sell_rows<DP, R, C::US, TM, true>(X, gl, reinterpret_cast<const int2*>(slot + C::OPB), K,
@@ -704,6 +790,24 @@ k_layer_sell(DevCsr a, const __grid_constant__ SellMaps maps, const float* __res
   }
   auto p = sell_setup<DP, CSR>(net.hidden, LAST);
   sell_layer<DP, LAST, OutT, CSR>(p, a, &maps.x, &maps.y, X, axlong, uwp, net, sc->out_scale, out);
+  sell_teardown(p);
+}
+
+// Training layer (CSR = 2): KIND 1 forward (Y = relu(XU + ÂXW), ÂX stored
+// for the weight gradients), KIND 2 backward over Âᵀ with [Uᵀ; Wᵀ]
+// (G_in = [X_l > 0] ⊙ (G U^T + Âᵀ G W^T), unmasked for layer 0).  The bs
+// samples of a node are adjacent virtual rows; bs must divide 128.
+struct TrainMaps {
+  CUtensorMap x, y, ax, mask;
+};
+
+template <int DP, int KIND>
+__global__ void __launch_bounds__(SellCfg<DP, 2>::NT, 1)
+k_train_sell(DevCsr a, const __grid_constant__ TrainMaps maps, const float* __restrict__ X,
+             const float* __restrict__ uwp, NetView net, int bs, int use_mask) {
+  auto p = sell_setup<DP, 2>(net.hidden, false);
+  const TrainIO tio{&maps.ax, &maps.mask, bs, use_mask};
+  sell_layer<DP, false, float, 2, KIND>(p, a, &maps.x, &maps.y, X, nullptr, uwp, net, 1.0, nullptr, &tio);
   sell_teardown(p);
 }
 

@@ -47,6 +47,7 @@ struct gnpc_model_s {
   std::vector<int> map_view, map_bt_fwd, map_bt_bwd, map_tc_fwd, map_tc_bwd;
   std::vector<unsigned char> part_tc;
   std::vector<int> map_tc_pair;  // flat param -> UWP (same entries as map_tc_fwd, permuted)
+  std::vector<int> map_tc_pair_bwd;  // same layout for the backward operands [Uᵀ; Wᵀ]
   std::vector<unsigned char> part_pair;
   // TMA maps over the two activation buffers (k_layer_sell)
   CUtensorMap tmX[2]{};

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "capi_common.hpp"
+#include "kernels/layer_sell.cuh"
 #include "kernels/layer_tc.cuh"
 #include "kernels/train.cuh"
 #include "kernels/wgrad_tc.cuh"
@@ -41,8 +42,13 @@ struct gnpc_trainer_s {
   // regeneration maps (see gnpc_model_s::build_maps)
   DevBuf<int> map_view, map_bt_fwd, map_bt_bwd, map_tc_fwd, map_tc_bwd;
   DevBuf<unsigned char> part_tc, part_pair;
-  DevBuf<int> map_tc_pair;
-  DevBuf<float> BT_fwd, BT_bwd, UWTC_bwd;
+  DevBuf<int> map_tc_pair, map_tc_pair_bwd;
+  DevBuf<float> BT_fwd, BT_bwd, UWTC_bwd, UWP_bwd;
+  // TMA pipeline layers (k_train_sell): maps over the activation and
+  // gradient buffers, used when the batch divides the 128-row tile
+  bool sell = false;
+  std::vector<CUtensorMap> mX, mAX;
+  CUtensorMap mG[2]{};
   // batch
   DevBuf<double> xb, bb, out, sgn, gout, colpart, losspart, tmp;
   DevBuf<gnpk::SampleScales> scl;
@@ -208,6 +214,11 @@ void regenerate(gnpc_trainer_s& T) {
     gnpk::k_gather_split<<<(c + kTh - 1) / kTh, kTh, 0, T.s>>>(T.p64.p, T.map_tc_bwd.p, T.part_tc.p, c,
                                                                T.UWTC_bwd.p);
     GNPC_LAUNCHED();
+    if (T.sell) {
+      gnpk::k_gather_split<<<(c + kTh - 1) / kTh, kTh, 0, T.s>>>(T.p64.p, T.map_tc_pair_bwd.p, T.part_pair.p,
+                                                                 c, T.UWP_bwd.p);
+      GNPC_LAUNCHED();
+    }
     gnpk::k_gather_split<<<(c + kTh - 1) / kTh, kTh, 0, T.s>>>(T.p64.p, T.map_tc_pair.p, T.part_pair.p, c,
                                                                m.UWP.p);
     GNPC_LAUNCHED();
@@ -224,11 +235,37 @@ template <int DP>
 struct TrainLaunch {
   // one Res-GCONV layer over the B-sample batch: forward (relu, ÂX out) or
   // backward data gradient (over Âᵀ, [Uᵀ; Wᵀ], mask by the layer input)
+  // in/out: buffer ids for the TMA maps (fwd: X = Xs[l] -> Xs[l+1], ÂX -> AXs[l];
+  // bwd: G[gi] -> G[1-gi], mask Xs[l])
   static void layer(gnpc_trainer_s& T, bool fwd, int l, const float* X, float* Y, float* axout,
-                    const float* mask) {
+                    const float* mask, int gi = 0) {
     gnpc_csr_s& A = fwd ? *T.m->a : *T.At;
     gnpk::DevCsr a = A.dev();
     if constexpr (DP == 16 || DP == 32) {
+      if (T.sell) {
+        using S = gnpk::SellCfg<DP, 2>;
+        const size_t smem = S::smem_bytes(T.H, false);
+        auto kern = fwd ? gnpk::k_train_sell<DP, 1> : gnpk::k_train_sell<DP, 2>;
+        set_smem_once((const void*)kern, smem);
+        const int tiles = (T.nv + S::TM - 1) / S::TM;
+        const int grid = std::max(1, std::min(tiles, T.sms));
+        gnpk::TrainMaps maps;
+        if (fwd) {
+          maps.x = T.mX[l];
+          maps.y = T.mX[l + 1];
+          maps.ax = T.mAX[l];
+          maps.mask = T.mX[l];
+        } else {
+          maps.x = T.mG[gi];
+          maps.y = T.mG[1 - gi];
+          maps.ax = T.mG[gi];
+          maps.mask = T.mX[l];
+        }
+        const float* uwp = (fwd ? T.m->UWP.p : T.UWP_bwd.p) + (size_t)l * 4 * DP * DP;
+        kern<<<grid, S::NT, smem, T.s>>>(a, maps, X, uwp, T.m->view, T.B, mask != nullptr ? 1 : 0);
+        GNPC_LAUNCHED();
+        return;
+      }
       if (T.tc) {
         using C = gnpk::TcCfg<DP>;
         const float* uw = (fwd ? T.m->UWTC.p : T.UWTC_bwd.p) + (size_t)l * 2 * C::B_FLOATS;
@@ -297,7 +334,7 @@ struct TrainLaunch {
     for (int l = T.L - 1; l >= 0; --l) {
       T.red_layer[l].o.Bm = T.G[cur].p;
       run_red(T, T.red_layer[l]);
-      layer(T, false, l, T.G[cur].p, T.G[1 - cur].p, nullptr, l >= 1 ? T.Xs.p + l * act : nullptr);
+      layer(T, false, l, T.G[cur].p, T.G[1 - cur].p, nullptr, l >= 1 ? T.Xs.p + l * act : nullptr, cur);
       cur = 1 - cur;
     }
     {
@@ -419,6 +456,16 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
     T->part_tc.upload(m->part_tc.data(), m->part_tc.size());
     upload_i(T->map_tc_pair, m->map_tc_pair);
     T->part_pair.upload(m->part_pair.data(), m->part_pair.size());
+    // TMA pipeline layers when the batch divides the 128-row tile
+    static const bool off = [] {
+      const char* e = std::getenv("GNPC_NO_TRAIN_SELL");
+      return e && std::string(e) == "1";
+    }();
+    if (!off && 128 % T->B == 0 && (T->dp == 16 || T->dp == 32)) {
+      T->sell = true;
+      upload_i(T->map_tc_pair_bwd, m->map_tc_pair_bwd);
+      T->UWP_bwd.alloc(m->map_tc_pair_bwd.size());
+    }
     T->UWTC_bwd.alloc(m->map_tc_bwd.size());
   } else {
     upload_i(T->map_bt_fwd, m->map_bt_fwd);
@@ -442,6 +489,12 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
   T->AXs.alloc(act * T->L);
   T->G[0].alloc(act);
   T->G[1].alloc(act);
+  if (T->sell) {
+    const CUtensorMapSwizzle sw = T->dp == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    for (int l = 0; l <= T->L; ++l) T->mX.push_back(make_rows_map(T->Xs.p + l * act, T->nv, T->dp, 128, sw));
+    for (int l = 0; l < T->L; ++l) T->mAX.push_back(make_rows_map(T->AXs.p + l * act, T->nv, T->dp, 128, sw));
+    for (int g = 0; g < 2; ++g) T->mG[g] = make_rows_map(T->G[g].p, T->nv, T->dp, 128, sw);
+  }
   T->vv.alloc(nvs);
   T->hb1.alloc(nvs * T->H);
   T->hb2.alloc(nvs * T->H);

@@ -401,3 +401,219 @@ __global__ void __launch_bounds__(wgt::TH, 1) k_wgrad_tma(const __grid_constant_
 }
 
 }  // namespace gnpk
+
+// ---------------------------------------------------------------------------
+// bf16x2-split variant (same arguments and partial layout as k_wgrad_tma).
+// The tensor core takes bf16 operands MN-major (probed in tests/cuda/
+// mn_bf16_probe.cu; tf32 does not), so the staged row-major tiles convert in
+// place order — no transpose: each thread turns 8 features of a row into 8
+// bf16 hi + 8 bf16 lo words (one 16-byte store each) in the 128B/64B
+// swizzled MN-major operand layout.  x = hi + lo to ~2^-18 relative; the
+// products hi·hi + hi·lo + lo·hi are accumulated (lo·lo is below the split
+// error), fp32 in TMEM folded into f64 every kFlushBf tiles.  Staging and
+// operands are double-buffered: tile k+1 converts while MMA(k) runs.
+#include <cuda_bf16.h>
+
+namespace gnpk {
+namespace wgb {
+constexpr int TM = 128, TH = 512, NSTG = 2;
+constexpr uint32_t ARR = TM * 128;   // one staged fp32 array tile (16 KiB)
+constexpr uint32_t STAGE = 3 * ARR;  // A1 | A2 | B
+constexpr uint32_t OPA = TM * 128;   // bf16 [128 rows][64 features], SW128 (16 KiB)
+constexpr uint32_t OPB = TM * 64;    // bf16 [128 rows][32 features], SW64 (8 KiB)
+constexpr uint32_t OPS = 2 * OPA + 2 * OPB;  // one operand set: Ahi | Alo | Bhi | Blo
+constexpr size_t smem_bytes() { return NSTG * STAGE + 2 * OPS + 128 + 1024; }
+constexpr int kFlushBf = 16;
+
+__device__ __forceinline__ uint32_t offA(int r, int m) {  // MN-major SW128, bf16
+  return static_cast<uint32_t>((r >> 3) * 1024 + (r & 7) * 128 + ((((m >> 3) ^ (r & 7))) << 4) + (m & 7) * 2);
+}
+__device__ __forceinline__ uint32_t offB(int r, int n) {  // MN-major SW64, bf16
+  return static_cast<uint32_t>((r >> 3) * 512 + (r & 7) * 64 + ((((n >> 3) ^ ((r & 7) >> 1)) & 3) << 4) +
+                               (n & 7) * 2);
+}
+__device__ __forceinline__ uint64_t desc_mn(uint32_t saddr, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;  // SBO: stride between 8-row K groups
+  d |= 1ull << 46;
+  d |= static_cast<uint64_t>(layout) << 61;
+  return d;
+}
+// kind::f16: F32 accumulate, BF16 A/B, both MN-major, N = 32, M = 64
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((32u >> 3) << 17) |
+                            ((64u >> 4) << 24);
+__device__ __forceinline__ void mma_bf16(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc)
+      : "memory");
+}
+// 8 fp32 -> 8 bf16 hi + 8 bf16 lo (x ≈ hi + lo)
+__device__ __forceinline__ void split8(const float (&x)[8], uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(x[2 * i]), h1 = __float2bfloat16_rn(x[2 * i + 1]);
+    const __nv_bfloat16 l0 = __float2bfloat16_rn(x[2 * i] - __bfloat162float(h0));
+    const __nv_bfloat16 l1 = __float2bfloat16_rn(x[2 * i + 1] - __bfloat162float(h1));
+    h[i] = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
+    l[i] = static_cast<uint32_t>(__bfloat16_as_ushort(l0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+}  // namespace wgb
+
+__global__ void __launch_bounds__(wgb::TH, 1) k_wgrad_bf16(const __grid_constant__ WgradTmaArgs g) {
+  using namespace wgb;
+  extern __shared__ float4 smem_raw[];
+  const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* base = reinterpret_cast<uint8_t*>(smem_raw) + pad;
+  uint8_t* stg = base;
+  uint8_t* ops = base + NSTG * STAGE;  // [2] operand sets
+  uint64_t* full = reinterpret_cast<uint64_t*>(ops + 2 * OPS);  // [NSTG]
+  uint64_t* mbar = full + NSTG;  // [2]: tile k's MMAs commit to mbar[k & 1]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ntiles = (g.nv + TM - 1) / TM;
+  const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int t_begin = blockIdx.x * per, t_end = min(ntiles, t_begin + per);
+  const int narr = g.a2_mode == 1 ? 3 : 2;
+  if (tid == 0) {
+    for (int s = 0; s < NSTG; ++s) tc::mbar_init(&full[s], 1);
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tc::tma_prefetch_desc(&g.a1);
+    tc::tma_prefetch_desc(&g.b);
+    if (g.a2_mode == 1) tc::tma_prefetch_desc(&g.a2);
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, 32);
+  // features 32..63 are constant unless a2 is a tensor: 1.0 at 32 (bias) or 0
+  if (g.a2_mode != 1) {
+    for (int j = tid; j < 2 * TM * 32; j += TH) {
+      const int b = j / (TM * 32), r = (j / 32) % TM, m = 32 + j % 32;
+      const float v = (g.a2_mode == 2 && m == 32) ? 1.f : 0.f;
+      *reinterpret_cast<__nv_bfloat16*>(ops + b * OPS + offA(r, m)) = __float2bfloat16_rn(v);
+      *reinterpret_cast<__nv_bfloat16*>(ops + b * OPS + OPA + offA(r, m)) = __float2bfloat16_rn(0.f);
+    }
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+
+  auto issue = [&](int tile) {
+    const int k = tile - t_begin, s = k % NSTG;
+    uint8_t* st = stg + s * STAGE;
+    tc::mbar_expect_tx(&full[s], narr * ARR);
+    const int y = tile * TM;
+    tc::tma_load_2d(st, &g.a1, 0, y, &full[s]);
+    tc::tma_load_2d(st + 2 * ARR, &g.b, 0, y, &full[s]);
+    if (g.a2_mode == 1) tc::tma_load_2d(st + ARR, &g.a2, 0, y, &full[s]);
+  };
+
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  // tile k's MMAs (local index) commit to mbar[k & 1] as that barrier's
+  // (k >> 1)-th phase; a barrier never runs two phases ahead of its waiters
+  // (tile k+2 commits only after every thread passed its wait for tile k)
+  int committed = 0;
+  auto wait_tile = [&](int k) {
+    if (k < 0) return;
+    tc::mbar_wait(&mbar[k & 1], (k >> 1) & 1);
+    tc::fence_after();
+  };
+  auto wait_mma = [&]() { wait_tile(committed - 1); };  // in-order completion
+  auto flush = [&]() {
+    wait_mma();
+    float v[8];
+    const int q = warp & 3, cb = warp >> 2;  // 4 column blocks of 8
+    tc::tmem_ld8(tmem + (static_cast<uint32_t>(32 * q) << 16) + 8 * cb, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] += static_cast<double>(v[i]);
+    tc::fence_before();
+  };
+
+  if (tid == 0)
+    for (int t = t_begin; t < min(t_end, t_begin + NSTG); ++t) issue(t);
+  int since_flush = 0;
+  for (int tile = t_begin; tile < t_end; ++tile) {
+    const int k = tile - t_begin, s = k % NSTG;
+    tc::mbar_wait(&full[s], (k / NSTG) & 1);
+    wait_tile(k - 2);  // MMA(k-2) used this operand set
+    uint8_t* Ahi = ops + (k & 1) * OPS;
+    uint8_t* Alo = Ahi + OPA;
+    uint8_t* Bhi = Alo + OPA;
+    uint8_t* Blo = Bhi + OPB;
+    // convert: item = (row, 8-feature chunk) of A1 (0..3), A2 (4..7), B (8..11)
+    const uint8_t* st = stg + s * STAGE;
+    for (int j = tid; j < TM * 12; j += TH) {
+      const int r = j / 12, ch = j % 12;
+      const int arr = ch < 4 ? 0 : (ch < 8 ? 1 : 2), c8 = ch & 3;
+      if (arr == 1 && g.a2_mode != 1) continue;
+      const uint8_t* src = st + arr * ARR + r * 128;
+      const float4 x0 = *reinterpret_cast<const float4*>(src + (((2 * c8) ^ (r & 7)) << 4));
+      const float4 x1 = *reinterpret_cast<const float4*>(src + (((2 * c8 + 1) ^ (r & 7)) << 4));
+      const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+      uint4 hi, lo;
+      split8(xv, hi, lo);
+      if (arr < 2) {
+        const uint32_t o = offA(r, 32 * arr + 8 * c8);
+        *reinterpret_cast<uint4*>(Ahi + o) = hi;
+        *reinterpret_cast<uint4*>(Alo + o) = lo;
+      } else {
+        const uint32_t o = offB(r, 8 * c8);
+        *reinterpret_cast<uint4*>(Bhi + o) = hi;
+        *reinterpret_cast<uint4*>(Blo + o) = lo;
+      }
+    }
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      const uint32_t sAhi = tc::smem_u32(Ahi), sAlo = tc::smem_u32(Alo);
+      const uint32_t sBhi = tc::smem_u32(Bhi), sBlo = tc::smem_u32(Blo);
+      uint32_t accf = since_flush > 0 ? 1u : 0u;
+#pragma unroll
+      for (int ks = 0; ks < TM / 16; ++ks) {
+        const uint64_t ah = desc_mn(sAhi + ks * 2048, 1024, 2), al = desc_mn(sAlo + ks * 2048, 1024, 2);
+        const uint64_t bh = desc_mn(sBhi + ks * 1024, 512, 4), bl = desc_mn(sBlo + ks * 1024, 512, 4);
+        mma_bf16(tmem, ah, bh, accf);
+        accf = 1;
+        mma_bf16(tmem, ah, bl, 1);
+        mma_bf16(tmem, al, bh, 1);
+      }
+      tc::mma_commit(&mbar[k & 1]);
+      // stage s is consumed: it takes tile + NSTG
+      if (tile + NSTG < t_end) issue(tile + NSTG);
+    }
+    ++committed;
+    if (++since_flush == kFlushBf) {
+      flush();
+      __syncthreads();
+      since_flush = 0;
+    }
+  }
+  if (since_flush > 0) flush();
+  {
+    const int q = warp & 3, cb = warp >> 2;
+    if (lane < 16) {
+      double* dst = g.partials + static_cast<size_t>(blockIdx.x) * 64 * 32 +
+                    static_cast<size_t>(16 * q + lane) * 32 + 8 * cb;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[i] = acc[i];
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0) tc::tmem_dealloc(tmem, 32);
+}
+
+}  // namespace gnpk

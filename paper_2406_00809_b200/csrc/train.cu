@@ -171,7 +171,14 @@ void run_red(gnpc_trainer_s& T, gnpc_trainer_s::Red& r) {
       r.tma_b = Bm;
     }
     r.ta.partials = T.opart.p;
-    gnpk::k_wgrad_tma<<<T.wgrad_grid_tma, gnpk::wgt::TH, gnpk::wgt::smem_bytes(), T.s>>>(r.ta);
+    static const bool tf32 = [] {
+      const char* e = std::getenv("GNPC_WGRAD_TF32");
+      return e && std::string(e) == "1";
+    }();
+    if (tf32)
+      gnpk::k_wgrad_tma<<<T.wgrad_grid_tma, gnpk::wgt::TH, gnpk::wgt::smem_bytes(), T.s>>>(r.ta);
+    else
+      gnpk::k_wgrad_bf16<<<T.wgrad_grid_tma, gnpk::wgb::TH, gnpk::wgb::smem_bytes(), T.s>>>(r.ta);
     GNPC_LAUNCHED();
     gnpk::k_outer_finish<<<(64 * 32 + kTh - 1) / kTh, kTh, 0, T.s>>>(T.opart.p, T.wgrad_grid_tma,
                                                                    64 * 32, r.dst.p, T.g64.p);
@@ -588,6 +595,8 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
                                    (int)gnpk::wg::smem_bytes()));
     const int per_sm = tc_ctas_per_sm((const void*)gnpk::k_wgrad_tc, gnpk::wg::smem_bytes(), 32);
     T->wgrad_grid = std::max(1, std::min(per_sm * T->sms, (T->nv + 127) / 128));
+    GNPC_CUDA(cudaFuncSetAttribute(gnpk::k_wgrad_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)gnpk::wgb::smem_bytes()));
     GNPC_CUDA(cudaFuncSetAttribute(gnpk::k_wgrad_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)gnpk::wgt::smem_bytes()));
     T->wgrad_grid_tma = std::max(1, std::min(T->sms, (T->nv + 127) / 128));

@@ -410,19 +410,19 @@ __global__ void __launch_bounds__(wgt::TH, 1) k_wgrad_tma(const __grid_constant_
 // bf16 hi + 8 bf16 lo words (one 16-byte store each) in the 128B/64B
 // swizzled MN-major operand layout.  x = hi + lo to ~2^-18 relative; the
 // products hi·hi + hi·lo + lo·hi are accumulated (lo·lo is below the split
-// error), fp32 in TMEM folded into f64 every kFlushBf tiles.  Staging and
-// operands are double-buffered: tile k+1 converts while MMA(k) runs.
+// error), fp32 in TMEM folded into f64 every kFlushBf tiles.  NSTG staged
+// tiles stay in flight (the kernel is HBM-latency bound); NOPS operand sets.
 #include <cuda_bf16.h>
 
 namespace gnpk {
 namespace wgb {
-constexpr int TM = 128, TH = 512, NSTG = 2;
+constexpr int TM = 128, TH = 512, NSTG = 3, NOPS = 1;
 constexpr uint32_t ARR = TM * 128;   // one staged fp32 array tile (16 KiB)
 constexpr uint32_t STAGE = 3 * ARR;  // A1 | A2 | B
 constexpr uint32_t OPA = TM * 128;   // bf16 [128 rows][64 features], SW128 (16 KiB)
 constexpr uint32_t OPB = TM * 64;    // bf16 [128 rows][32 features], SW64 (8 KiB)
 constexpr uint32_t OPS = 2 * OPA + 2 * OPB;  // one operand set: Ahi | Alo | Bhi | Blo
-constexpr size_t smem_bytes() { return NSTG * STAGE + 2 * OPS + 128 + 1024; }
+constexpr size_t smem_bytes() { return NSTG * STAGE + NOPS * OPS + 128 + 1024; }
 constexpr int kFlushBf = 16;
 
 __device__ __forceinline__ uint32_t offA(int r, int m) {  // MN-major SW128, bf16
@@ -450,19 +450,22 @@ __device__ __forceinline__ void mma_bf16(uint32_t d, uint64_t a, uint64_t b, uin
       "l"(a), "l"(b), "r"(kIdesc), "r"(acc)
       : "memory");
 }
-// 8 fp32 -> 8 bf16 hi + 8 bf16 lo (x ≈ hi + lo)
-__device__ __forceinline__ void split8(const float (&x)[8], uint4& hi, uint4& lo) {
-  uint32_t h[4], l[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const __nv_bfloat16 h0 = __float2bfloat16_rn(x[2 * i]), h1 = __float2bfloat16_rn(x[2 * i + 1]);
-    const __nv_bfloat16 l0 = __float2bfloat16_rn(x[2 * i] - __bfloat162float(h0));
-    const __nv_bfloat16 l1 = __float2bfloat16_rn(x[2 * i + 1] - __bfloat162float(h1));
-    h[i] = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
-    l[i] = static_cast<uint32_t>(__bfloat16_as_ushort(l0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16);
-  }
-  hi = make_uint4(h[0], h[1], h[2], h[3]);
-  lo = make_uint4(l[0], l[1], l[2], l[3]);
+// 2 fp32 -> packed bf16x2 hi and lo (x ≈ hi + lo): one cvt.rn.bf16x2 each,
+// hi widened back to fp32 by shifts
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  uint32_t h;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));  // low half = a
+  const float ha = __uint_as_float(h << 16), hb = __uint_as_float(h & 0xffff0000u);
+  uint32_t l;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(b - hb), "f"(a - ha));
+  hi = h;
+  lo = l;
+}
+__device__ __forceinline__ void split8(float4 x0, float4 x1, uint4& hi, uint4& lo) {
+  split2(x0.x, x0.y, hi.x, lo.x);
+  split2(x0.z, x0.w, hi.y, lo.y);
+  split2(x1.x, x1.y, hi.z, lo.z);
+  split2(x1.z, x1.w, hi.w, lo.w);
 }
 }  // namespace wgb
 
@@ -473,7 +476,7 @@ __global__ void __launch_bounds__(wgb::TH, 1) k_wgrad_bf16(const __grid_constant
   uint8_t* base = reinterpret_cast<uint8_t*>(smem_raw) + pad;
   uint8_t* stg = base;
   uint8_t* ops = base + NSTG * STAGE;  // [2] operand sets
-  uint64_t* full = reinterpret_cast<uint64_t*>(ops + 2 * OPS);  // [NSTG]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ops + NOPS * OPS);  // [NSTG]
   uint64_t* mbar = full + NSTG;  // [2]: tile k's MMAs commit to mbar[k & 1]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -493,7 +496,7 @@ __global__ void __launch_bounds__(wgb::TH, 1) k_wgrad_bf16(const __grid_constant
   if (warp == 0) tc::tmem_alloc(tslot, 32);
   // features 32..63 are constant unless a2 is a tensor: 1.0 at 32 (bias) or 0
   if (g.a2_mode != 1) {
-    for (int j = tid; j < 2 * TM * 32; j += TH) {
+    for (int j = tid; j < NOPS * TM * 32; j += TH) {
       const int b = j / (TM * 32), r = (j / 32) % TM, m = 32 + j % 32;
       const float v = (g.a2_mode == 2 && m == 32) ? 1.f : 0.f;
       *reinterpret_cast<__nv_bfloat16*>(ops + b * OPS + offA(r, m)) = __float2bfloat16_rn(v);
@@ -545,31 +548,31 @@ __global__ void __launch_bounds__(wgb::TH, 1) k_wgrad_bf16(const __grid_constant
   for (int tile = t_begin; tile < t_end; ++tile) {
     const int k = tile - t_begin, s = k % NSTG;
     tc::mbar_wait(&full[s], (k / NSTG) & 1);
-    wait_tile(k - 2);  // MMA(k-2) used this operand set
-    uint8_t* Ahi = ops + (k & 1) * OPS;
+    wait_tile(k - NOPS);  // MMA(k-NOPS) used this operand set
+    uint8_t* Ahi = ops + (k % NOPS) * OPS;
     uint8_t* Alo = Ahi + OPA;
     uint8_t* Bhi = Alo + OPA;
     uint8_t* Blo = Bhi + OPB;
-    // convert: item = (row, 8-feature chunk) of A1 (0..3), A2 (4..7), B (8..11)
+    // convert: thread = (row r, 8-feature chunk c8) of A1, A2 and B
     const uint8_t* st = stg + s * STAGE;
-    for (int j = tid; j < TM * 12; j += TH) {
-      const int r = j / 12, ch = j % 12;
-      const int arr = ch < 4 ? 0 : (ch < 8 ? 1 : 2), c8 = ch & 3;
-      if (arr == 1 && g.a2_mode != 1) continue;
-      const uint8_t* src = st + arr * ARR + r * 128;
-      const float4 x0 = *reinterpret_cast<const float4*>(src + (((2 * c8) ^ (r & 7)) << 4));
-      const float4 x1 = *reinterpret_cast<const float4*>(src + (((2 * c8 + 1) ^ (r & 7)) << 4));
-      const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-      uint4 hi, lo;
-      split8(xv, hi, lo);
-      if (arr < 2) {
-        const uint32_t o = offA(r, 32 * arr + 8 * c8);
-        *reinterpret_cast<uint4*>(Ahi + o) = hi;
-        *reinterpret_cast<uint4*>(Alo + o) = lo;
-      } else {
-        const uint32_t o = offB(r, 8 * c8);
-        *reinterpret_cast<uint4*>(Bhi + o) = hi;
-        *reinterpret_cast<uint4*>(Blo + o) = lo;
+    {
+      const int r = tid >> 2, c8 = tid & 3;
+      const uint32_t i0 = (((2 * c8) ^ (r & 7)) << 4), i1 = (((2 * c8 + 1) ^ (r & 7)) << 4);
+#pragma unroll
+      for (int arr = 0; arr < 3; ++arr) {
+        if (arr == 1 && g.a2_mode != 1) continue;
+        const uint8_t* src = st + arr * ARR + r * 128;
+        uint4 hi, lo;
+        split8(*reinterpret_cast<const float4*>(src + i0), *reinterpret_cast<const float4*>(src + i1), hi, lo);
+        if (arr < 2) {
+          const uint32_t o = offA(r, 32 * arr + 8 * c8);
+          *reinterpret_cast<uint4*>(Ahi + o) = hi;
+          *reinterpret_cast<uint4*>(Alo + o) = lo;
+        } else {
+          const uint32_t o = offB(r, 8 * c8);
+          *reinterpret_cast<uint4*>(Bhi + o) = hi;
+          *reinterpret_cast<uint4*>(Blo + o) = lo;
+        }
       }
     }
     tc::fence_proxy_async();

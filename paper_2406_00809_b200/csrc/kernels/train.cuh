@@ -524,6 +524,57 @@ k_weighted_colsum(const float* __restrict__ A, int W, const float* __restrict__ 
   const int per = (nv + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * per, r1 = min(nv, r0 + per);
   double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (W == 32) {
+    // lane = (row slot l/8, column quad l%8): one 16-byte load covers 4 rows of
+    // a warp's 32-row step; 8 independent loads in flight per lane
+    const int ro = lane >> 3, cq = lane & 7;
+    double d1[4] = {0, 0, 0, 0}, d2[4] = {0, 0, 0, 0}, d3 = 0.0;
+    for (int v0 = r0 + warp * 32; v0 < r1; v0 += 8 * 32) {
+      float4 x[8];
+      float wv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int v = v0 + 4 * u + ro;
+        x[u] = v < r1 ? ldg4(A + static_cast<size_t>(v) * 32 + 4 * cq) : f4zero();
+        wv[u] = v < r1 ? __ldg(w + v) : 0.f;
+      }
+      float4 s1 = f4zero(), s2 = f4zero();
+      float s3 = 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        fma4(s1, wv[u], x[u]);
+        s2 = add4(s2, x[u]);
+        s3 += wv[u];
+      }
+      d1[0] += s1.x; d1[1] += s1.y; d1[2] += s1.z; d1[3] += s1.w;
+      d2[0] += s2.x; d2[1] += s2.y; d2[2] += s2.z; d2[3] += s2.w;
+      d3 += s3;
+    }
+    // combine the 4 row slots (lanes cq, cq+8, cq+16, cq+24) in a fixed order
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        d1[i] += __shfl_xor_sync(0xffffffffu, d1[i], o);
+        d2[i] += __shfl_xor_sync(0xffffffffu, d2[i], o);
+      }
+      d3 += __shfl_xor_sync(0xffffffffu, d3, o);
+    }
+    // column c = 4*cq + i lives in lanes with cq = c/4: gather to lane c
+    const int src = (lane >> 2) & 7, comp = lane & 3;
+    double t1 = 0, t2 = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double e1 = __shfl_sync(0xffffffffu, d1[i], src), e2 = __shfl_sync(0xffffffffu, d2[i], src);
+      if (comp == i) {
+        t1 = e1;
+        t2 = e2;
+      }
+    }
+    a1 = t1;
+    a2 = t2;
+    a3 = d3;
+  } else
   for (int v0 = r0 + warp * 4; v0 < r1; v0 += 32) {  // 4 rows per warp per step
     float s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll

@@ -736,8 +736,22 @@ struct OrthoPlan {
   int grid;
 };
 
+// The MGS sweep is one grid barrier per basis vector, so the barrier's cost
+// (which grows with the CTA count) is paid j+1 times per pass: prefer few
+// CTAs (1, then 2 per SM) holding w in registers with a larger EPT, and only
+// then more CTAs.  (C2: ~1180 CTAs at EPT 1 -> 148 CTAs at EPT 8.)
 OrthoPlan plan_ortho(int n) {
   const int sms = num_sms();
+  for (int per : {1, 2, 4}) {
+    for (int ept : {1, 2, 4, 8, 16}) {
+      int per_sm = 0;
+      GNPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ortho_kernel_for(ept),
+                                                              gnpk::kThreads, 0));
+      if (per_sm < per) continue;
+      const long long cap = (long long)per * sms * gnpk::kThreads * ept;
+      if (n <= cap) return {ortho_kernel_for(ept), per * sms};
+    }
+  }
   for (int ept : {1, 2, 4, 8, 16}) {
     int per_sm = 0;
     GNPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ortho_kernel_for(ept),

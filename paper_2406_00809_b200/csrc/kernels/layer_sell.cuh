@@ -434,7 +434,8 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
                              C::OPB + (use_mask ? C::OPB : 0) + C::RPB + (staged ? 8 * cnt : 0));
           tc::tma_load_2d(slot, mapx, 0, t * TM, &p.full[s]);
           if (use_mask) tc::tma_load_2d(slot + C::O_MASK, tio->mapmask, 0, t * TM, &p.full[s]);
-          tc::bulk_load(slot + C::O_RP, a.rp + n0, C::RPB, &p.full[s]);
+          // row_ptr slice from the 16-byte aligned node n0 & ~3 (npt < 4 when bs > 32)
+          tc::bulk_load(slot + C::O_RP, a.rp + (n0 & ~3), C::RPB, &p.full[s]);
           if (staged && cnt > 0) {
             tc::bulk_load(slot + C::O_CI, a.ci + a0, 4 * cnt, &p.full[s]);
             tc::bulk_load(slot + C::O_V, a.v + a0, 4 * cnt, &p.full[s]);
@@ -693,8 +694,8 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       if constexpr (TR) {
         // virtual row v = node*bs + k gathers X rows (col*bs + k) of node's
         // neighbours: one staged (col, val) list serves the node's bs rows
-        const int* rpt = reinterpret_cast<const int*>(slot + C::O_RP);
         const int n0 = tile * npt;
+        const int* rpt = reinterpret_cast<const int*>(slot + C::O_RP) + (n0 & 3);
         const int kb = rpt[0], ke = rpt[min(npt, nodes - n0)];
         const int a0 = kb & ~3;
         const bool st = ((ke + 3) & ~3) - a0 <= C::CAPC;
@@ -850,7 +851,12 @@ __global__ void __launch_bounds__(SellCfg<DP>::NT, 1)
 k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restrict__ in, NetView net,
              OutT* __restrict__ out, const int* __restrict__ skip) {
   using C = SellCfg<DP, CSR>;
-  if (skip && *skip) return;
+  // every exit consumes all 1 + L grid-barrier arrivals of this launch so
+  // the monotonic counter stays in step with the host's base for the next one
+  if (skip && *skip) {
+    if (threadIdx.x == 0) atomicAdd(f.gbar, static_cast<unsigned long long>(1 + net.layers));
+    return;
+  }
   const int n = a.n;
   const int tid = threadIdx.x;
   unsigned long long target = f.gbase;
@@ -898,6 +904,7 @@ k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restri
   const double in_scale = s_scale[0], out_scale = s_scale[1];
   if (in_scale == 0.0) {  // τ = 0: M(0) = 0
     for (int i = blockIdx.x * C::NT + tid; i < n; i += gridDim.x * C::NT) out[i] = OutT(0);
+    if (tid == 0) atomicAdd(f.gbar, static_cast<unsigned long long>(net.layers));  // skipped barriers
     return;
   }
   auto p = sell_setup<DP, CSR>(net.hidden, true);

@@ -3,7 +3,7 @@ oracle: status, iteration counts (±1 with the fp32 GNP, exact without a
 preconditioner), histories, and the reference's Krylov pins."""
 import numpy as np
 import pytest
-from conftest import f32, golden
+from conftest import f32, golden, rel_l2
 
 pytestmark = pytest.mark.gpu
 
@@ -186,3 +186,19 @@ def test_python_solve_drop_in(gnp, cuda):
         assert out["status"] == "converged"
         assert out["history"][-1][1] <= 1e-8
         assert max(abs(v - 1.0) for v in out["x"]) < 1e-6
+
+
+def test_fused_apply_after_mid_cycle_stop(capi, oc, cuda):
+    # d = 16 applies run as one persistent launch with grid barriers; a device
+    # solve that stops mid-cycle skips the rest of the cycle's applies, which
+    # must keep the barrier counter consistent for later applies
+    g = golden("c1.npz")
+    ah = oc.prescale(oc.gen_convection_diffusion(64, 0.0), 8.0)
+    A = dev_csr(capi, ah)
+    m = capi.Model(A, (16, 32, 8), g["params"])
+    r5 = capi.fgmres(A, g["b"], model=m, rtol=1e-30, maxiters=5, restart=10)["history"][-1][1]
+    for _ in range(2):
+        s = capi.fgmres(A, g["b"], model=m, rtol=r5 * 1.0001, maxiters=100, restart=10)
+        assert s["status"] == "converged" and s["history"][-1][0] <= 5
+    y = m.apply(g["b"])
+    assert rel_l2(y, g["out"]) < 1e-5

@@ -113,3 +113,56 @@ def test_sell_odd_hidden_projection(capi, oc, cuda):
     a = stencil_plus(oc, 33)
     y_sell, _, want = apply_both(capi, oc, a, (32, 13, 2), 3)
     check(y_sell, want)
+
+
+@pytest.mark.parametrize("n_grid", [2, 7, 11])
+def test_fused_apply_small_and_partial(capi, oc, cuda, n_grid):
+    # d = 16 runs the whole apply as one persistent launch; n = 4, 49, 121
+    # (grid smaller than the SM count, a single partial tile)
+    a = oc.prescale(oc.gen_convection_diffusion(n_grid, 0.3), 8.6).rounded_f32()
+    dims = (16, 32, 8)
+    p = f32(oc.init_params(*dims, 1))
+    b = oc.gaussian_vector(2, a.n)
+    y = apply_path(capi, a, dims, p, b, True)
+    check(y, oc.gnn_apply(a, dims, p, b))
+
+
+def test_fused_apply_zero_and_device_entry(capi, oc, cuda):
+    import torch
+
+    a = oc.prescale(oc.gen_convection_diffusion(40, 0.3), 8.6).rounded_f32()
+    dims = (16, 32, 8)
+    p = f32(oc.init_params(*dims, 1))
+    A = capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
+    m = capi.Model(A, dims, p)
+    assert np.all(m.apply(np.zeros(a.n)) == 0.0)  # tau = 0 -> M(0) = 0 inside the fused launch
+    b = oc.gaussian_vector(6, a.n)
+    bt = torch.tensor(b, dtype=torch.float32, device="cuda")
+    out = torch.full_like(bt, float("nan"))
+    m.apply_device_f32(bt.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    check(out.double().cpu().numpy(), oc.gnn_apply(a, dims, p, b.astype(np.float32).astype(np.float64)))
+
+
+def test_fused_apply_csr_ragged_rows(capi, oc, cuda):
+    # ragged rows (1..32 entries, no long rows): no sliced-ELL copy, the fused
+    # launch runs the CSR-staged variant
+    n = 3000
+    rng = np.random.default_rng(21)
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        k = int(rng.integers(1, 33))
+        c = rng.choice(n, size=k, replace=False)
+        rows += [i] * k
+        cols += c.tolist()
+        vals += (rng.standard_normal(k) / k).tolist()
+    t = oc.csr_from_triplets(n, rows, cols, vals)
+    a = oc.prescale(t, oc.gershgorin_gamma(t)).rounded_f32()
+    dims = (16, 32, 8)
+    p = f32(oc.init_params(*dims, 4))
+    b = oc.gaussian_vector(8, n)
+    A = capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
+    y = capi.Model(A, dims, p).apply(b)
+    uploaded, sell_built, nlong = A.device_layout()
+    assert uploaded and not sell_built and nlong == 0
+    check(y, oc.gnn_apply(a, dims, p, b))

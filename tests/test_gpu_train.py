@@ -158,3 +158,55 @@ def test_data_parallel_driver_single_rank_equals_step(capi, cuda):
     b = np.stack([ah.spmv(x[:, k]) for k in range(8)], axis=1)
     assert dp.step(x, b) == t1.step(x.ravel(order="F"), b.ravel(order="F"))
     assert np.array_equal(t1.params(), t2.params())
+
+
+@pytest.mark.parametrize("d,B", [(16, 3), (32, 6), (16, 128)])
+def test_batch_sizes_vs_oracle(capi, oc, cuda, d, B):
+    # B must divide 128 for the TMA training layers (3 and 6 take the
+    # register-staged tcgen05 layer; 128 = one node per tile)
+    a = oc.prescale(oc.gen_convection_diffusion(12, 0.4), 8.8).rounded_f32()
+    dims = (d, 32, 3)
+    p = f32(oc.init_params(*dims, 5))
+    x, b = oc.gaussian_batch(a, 9, 0, B)
+    want_loss, want = oc.batch_loss_grads(a, dims, p, x, b, B)
+    m = capi.Model(dev_csr(capi, a), dims, p)
+    t = capi.Trainer(m, B)
+    loss, grads, _ = t.forward_backward(x, b)
+    assert abs(loss - want_loss) <= 1e-5 * abs(want_loss)
+    check_grads(grads, want, dims)
+
+
+def test_tma_training_layers_match_fallback(capi, oc, cuda):
+    # the same step through k_train_sell (default) and, in a subprocess with
+    # GNPC_NO_TRAIN_SELL=1, through the register-staged tcgen05 layers
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import json, sys, numpy as np
+sys.path.insert(0, ".")
+sys.path.insert(0, "oracle")
+from paper_2406_00809_b200 import capi
+import oracle
+oc = oracle.restatement()
+a = oc.prescale(oc.gen_convection_diffusion(20, 0.3), 8.6).rounded_f32()
+p = oc.init_params(32, 32, 4, 2).astype(np.float32).astype(np.float64)
+x, b = oc.gaussian_batch(a, 4, 0, 8)
+A = capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
+t = capi.Trainer(capi.Model(A, (32, 32, 4), p), 8)
+loss, g, _ = t.forward_backward(x, b)
+print(json.dumps({"loss": loss, "g": list(g)}))
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for off in ("0", "1"):
+        env = dict(os.environ, GNPC_NO_TRAIN_SELL=off)
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert abs(outs[0]["loss"] - outs[1]["loss"]) <= 1e-6 * abs(outs[1]["loss"])
+    g0, g1 = np.array(outs[0]["g"]), np.array(outs[1]["g"])
+    assert np.linalg.norm(g0 - g1) <= 1e-4 * np.linalg.norm(g1)

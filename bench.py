@@ -7,7 +7,9 @@ one M·v apply of a fresh right-hand side.  Metric: applies/s (whole job).
   value  : device-resident inputs (gnpc_apply_device_f32), CUDA events per step,
            L2 flushed (512 MiB write) between steps (C2's working set fits in L2).
   e2e    : the reference-facing C-ABI call gnpc_apply with pinned HOST f64
-           buffers: H2D of b + D2H of M(b) inside every timed step.
+           buffers: b crosses host->device and M(b) device->host inside every
+           timed step (page-locked buffers: the one-launch apply reads/writes
+           them zero-copy through their device aliases; pageable: staged copies).
   roofline: dominant kernel.  d = 16 without long rows: the whole apply is ONE
            persistent launch (k_apply_sell), bytes = the apply's canonical bytes
            12n + 8nd + L(4(n+1) + 8nnz + 8nd) (DESIGN.md §4), timed per step;

@@ -24,6 +24,11 @@
 #include "kernels/layer_tc.cuh"
 #include "model.hpp"
 
+namespace gnpc_impl {
+bool sell_kernel_off();
+bool fused_apply_off();
+}  // namespace gnpc_impl
+
 using namespace gnpc_impl;
 using gnp_b200::CsrHost;
 
@@ -92,14 +97,8 @@ struct ApplyLaunch {
     auto mark = [&](int k) {
       if (prof) prof->mark(k, s);
     };
-    static const bool sell_off = [] {
-      const char* e = std::getenv("GNPC_NO_SELL_KERNEL");
-      return e && std::string(e) == "1";
-    }();
-    static const bool fused_off = [] {
-      const char* e = std::getenv("GNPC_NO_FUSED_APPLY");
-      return e && std::string(e) == "1";
-    }();
+    const bool sell_off = sell_kernel_off();
+    const bool fused_off = fused_apply_off();
     if constexpr (DP == 16 || DP == 32) {
       // the whole apply as one persistent cooperative launch (no long rows:
       // those need their chunk kernels between layers).  The per-kernel
@@ -129,7 +128,7 @@ struct ApplyLaunch {
         static gnpc_impl::DevBuf<unsigned long long> tbuf;
         if (times && !tbuf.p) tbuf.alloc(64);
         ApplyFused fa{m.tmX[0], m.tmX[1], m.X[0].p, m.X[1].p, m.UWP.p, m.partials.p, m.gbar.p,
-                      m.gbar_host, m.sc.p, times ? tbuf.p : nullptr};
+                      m.gbar_host, m.sc.p, times ? tbuf.p : nullptr, m.fused_stash};
         m.gbar_host += (unsigned long long)grid * (1 + net.layers);
         void* args[] = {(void*)&a, (void*)&fa, (void*)&in, (void*)&net, (void*)&out, (void*)&skip};
         GNPC_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(S::NT), args, smem, s));
@@ -265,6 +264,18 @@ struct ApplyLaunch {
 
 // ====================================================================== TMA maps
 namespace gnpc_impl {
+static bool env_on(const char* name) {
+  const char* e = std::getenv(name);
+  return e && std::string(e) == "1";
+}
+bool sell_kernel_off() {  // GNPC_NO_SELL_KERNEL=1: register-staged tcgen05 layers instead
+  static const bool v = env_on("GNPC_NO_SELL_KERNEL");
+  return v;
+}
+bool fused_apply_off() {  // GNPC_NO_FUSED_APPLY=1: per-layer launches instead of one
+  static const bool v = env_on("GNPC_NO_FUSED_APPLY");
+  return v;
+}
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -687,6 +698,15 @@ void gnpc_model_s::ensure_workspace() {
         tm_base[c] = X[c].p;
       }
   }
+}
+
+bool gnpc_model_s::fused_eligible() {
+  a->upload();
+  if (dp != 16 || !use_tc || a->n_long != 0 || a->h.n == 0) return false;
+  if (gnpc_impl::sell_kernel_off() || gnpc_impl::fused_apply_off()) return false;
+  const size_t smem = a->has_sell ? gnpk::SellCfg<16, 0>::smem_bytes(dims.hidden, true)
+                                  : gnpk::SellCfg<16, 1>::smem_bytes(dims.hidden, true);
+  return smem <= 226 * 1024;
 }
 
 template <typename InT, typename OutT>
@@ -1266,6 +1286,21 @@ int gnpc_apply(gnpc_model m, const double* b, double* out) {
     const std::size_t n = (std::size_t)m->a->h.n;
     m->io_in.ensure(n);
     m->io_out.ensure(n);
+    // pinned (page-locked) caller buffers and the one-launch apply: the
+    // kernel reads b and writes M(b) through their device aliases
+    // (zero-copy), so the transfers overlap the norm pass and the last layer
+    cudaPointerAttributes pa{}, po{};
+    if (m->fused_eligible() && cudaPointerGetAttributes(&pa, b) == cudaSuccess &&
+        cudaPointerGetAttributes(&po, out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        po.type == cudaMemoryTypeHost && pa.devicePointer != nullptr && po.devicePointer != nullptr) {
+      m->fused_stash = m->io_in.p;
+      m->launch_apply<double, double>(static_cast<const double*>(pa.devicePointer),
+                                      static_cast<double*>(po.devicePointer), m->stream, nullptr);
+      m->fused_stash = nullptr;
+      GNPC_CUDA(cudaStreamSynchronize(m->stream));
+      return;
+    }
+    cudaGetLastError();  // cudaPointerGetAttributes on unregistered memory is not an error to keep
     GNPC_CUDA(cudaMemcpyAsync(m->io_in.p, b, n * 8, cudaMemcpyHostToDevice, m->stream));
     m->launch_apply<double, double>(m->io_in.p, m->io_out.p, m->stream, nullptr);
     GNPC_CUDA(cudaMemcpyAsync(out, m->io_out.p, n * 8, cudaMemcpyDeviceToHost, m->stream));

@@ -828,6 +828,8 @@ struct ApplyFused {
   unsigned long long gbase;     // its value when this launch started
   ApplyScalars* sc;             // τ and scales (written by block 0 for callers)
   unsigned long long* times;    // debug (GNPC_FUSED_TIMES): block 0 phase timestamps, or null
+  void* stash;                  // optional device copy of the input (InT[n]): when `in` is host
+                                // memory read zero-copy, the norm pass stores it for the lift
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned long long* ctr, unsigned long long target) {
@@ -871,8 +873,11 @@ k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restri
   __shared__ double s_scale[2];
   {
     double s = 0.0;
+    InT* stash = static_cast<InT*>(f.stash);
     for (int i = blockIdx.x * C::NT + tid; i < n; i += gridDim.x * C::NT) {
-      const double x = static_cast<double>(in[i]);
+      const InT v = in[i];
+      if (stash) stash[i] = v;
+      const double x = static_cast<double>(v);
       s = fma(x, x, s);
     }
     s = warp_sum(s);
@@ -923,11 +928,12 @@ k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restri
     constexpr int G = DP / 4;
     const int gl = tid % G;
     const int ntiles = (n + C::TM - 1) / C::TM;
+    const InT* src = f.stash ? static_cast<const InT*>(f.stash) : in;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       for (int r = tid / G; r < C::TM; r += C::NT / G) {
         const int row = tile * C::TM + r;
         if (row >= n) break;
-        const float v = static_cast<float>(in_scale * static_cast<double>(in[row]));
+        const float v = static_cast<float>(in_scale * static_cast<double>(src[row]));
         int lo = 0, hi = nb;  // interval = #kinks <= v
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;

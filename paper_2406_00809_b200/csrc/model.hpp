@@ -39,6 +39,8 @@ struct gnpc_model_s {
   // its value so each launch knows its base; launches are stream-ordered)
   gnpc_impl::DevBuf<unsigned long long> gbar;
   unsigned long long gbar_host = 0;
+  void* fused_stash = nullptr;  // gnpc_apply zero-copy: device copy of the host input
+  bool fused_eligible();        // the apply runs as the single persistent launch
   gnpc_impl::DevBuf<gnpk::ApplyScalars> sc;
   int sms = 0, norm_grid = 0;
   cudaStream_t stream = nullptr;

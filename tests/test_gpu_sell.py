@@ -166,3 +166,25 @@ def test_fused_apply_csr_ragged_rows(capi, oc, cuda):
     uploaded, sell_built, nlong = A.device_layout()
     assert uploaded and not sell_built and nlong == 0
     check(y, oc.gnn_apply(a, dims, p, b))
+
+
+def test_fused_apply_zero_copy_pinned_host(capi, oc, cuda):
+    # gnpc_apply with page-locked host buffers: the one-launch apply reads b
+    # and writes M(b) through their device aliases (no staging copies)
+    import ctypes as C
+
+    import torch
+
+    a = oc.prescale(oc.gen_convection_diffusion(40, 0.3), 8.6).rounded_f32()
+    dims = (16, 32, 8)
+    p = f32(oc.init_params(*dims, 1))
+    A = capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
+    m = capi.Model(A, dims, p)
+    b = oc.gaussian_vector(6, a.n)
+    hb = torch.tensor(b, dtype=torch.float64).pin_memory()
+    ho = torch.full((a.n,), float("nan"), dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        capi.check(capi.lib().gnpc_apply(m.h, C.c_void_p(hb.data_ptr()), C.c_void_p(ho.data_ptr())))
+        y = ho.numpy().copy()
+        check(y, oc.gnn_apply(a, dims, p, b))
+        assert np.array_equal(y, m.apply(b))  # same kernels as the staged path

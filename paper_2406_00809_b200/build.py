@@ -29,6 +29,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
                      "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 if os.environ.get("GNPC_DEBUG_HANG") == "1":  # bounded pipeline waits that trap (debug only)
     NVCC_FLAGS += ["-DGNPC_DEBUG_HANG"]
+NVCC_FLAGS += os.environ.get("GNPC_NVCC_DEFS", "").split()  # tuning variants, e.g. "-DGNPC_US32=6"
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-Wall"]
 
 CU_SOURCES = ["capi.cu", "train.cu"]

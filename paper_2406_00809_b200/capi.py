@@ -14,7 +14,7 @@ import re
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgnpc.so")
+LIB_PATH = os.environ.get("GNPC_LIB") or os.path.join(HERE, "libgnpc.so")  # GNPC_LIB: a variant build (tuning)
 HEADER = os.path.join(os.path.dirname(HERE), "include", "gnpc.h")
 
 STATUS = ["converged", "maxiters", "timeout", "solution_failure", "breakdown_exact"]

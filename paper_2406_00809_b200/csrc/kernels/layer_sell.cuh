@@ -97,7 +97,13 @@ struct SellCfg {
   static constexpr int G = DP / 4;               // lanes per row
   static constexpr int NG = 32 * NW / G;         // row groups
   static constexpr int R = TM / NG;              // rows per group
-  static constexpr int US = DP == 16 ? 8 : 3;    // slice entries per gather round
+#ifndef GNPC_US32
+#define GNPC_US32 3
+#endif
+#ifndef GNPC_KCAP32
+#define GNPC_KCAP32 12
+#endif
+  static constexpr int US = DP == 16 ? 8 : GNPC_US32;    // slice entries per gather round
   static constexpr int USC = DP == 16 ? 8 : 4;   // CSR entries per gather round
   // TMA ring depth (tiles), measured per format: SELL DP16 (C2) best at 4
   // (an epilogue lag of 2 tiles with double-buffered A/TMEM and NS 5 measured
@@ -106,11 +112,12 @@ struct SellCfg {
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
   // up to round(K, US) words).  Kept small: every KB of shared memory is L1
   // the X-row gathers hit (C5 fused layer 531 -> 499 us going 24 -> 12)
-  static constexpr int KCAP = DP == 16 ? 16 : 12;
+  static constexpr int KCAP = DP == 16 ? 16 : GNPC_KCAP32;
   static constexpr uint32_t OPB = TM * DP * 4;   // one A-type operand / X tile / Y tile (bytes)
   static constexpr uint32_t BB = DP * DP * 4;    // one B operand (bytes)
   static constexpr int TCOLS = 2 * DP;           // TMEM accumulator columns (two halves)
-  static constexpr int TALLOC = TCOLS < 32 ? 32 : TCOLS;  // power of two >= 32
+  // + the X·U part's A_lo operand (DP columns, A in TMEM) at alo_col
+  static constexpr int TALLOC = 4 * DP;          // power of two >= 3 DP
   static constexpr uint32_t CVB = KCAP * TM * 8; // staged slice (bytes)
   // CSR: [X tile | row_ptr slice (TM+4 ints, 1 KiB) | col_idx (CAPC) | values (CAPC)]
   static constexpr bool TR = CSR == 2;
@@ -123,8 +130,8 @@ struct SellCfg {
       CSR ? ((O_V + CAPC * 4 + 1023) & ~1023u) : (((OPB + CVB) + 1023) & ~1023u);
   // layout (offsets from the 1024-aligned base)
   static constexpr uint32_t O_RING = 0;
-  static constexpr uint32_t O_A = O_RING + NS * SLOT;     // A1_lo, A2_hi, A2_lo
-  static constexpr uint32_t O_B = O_A + 3 * OPB;          // Bu_lo, Bu_hi, Bw_lo, Bw_hi
+  static constexpr uint32_t O_A = O_RING + NS * SLOT;     // A2_hi (ÂX), A2_lo
+  static constexpr uint32_t O_B = O_A + 2 * OPB;          // Bu_lo, Bu_hi, Bw_lo, Bw_hi
   static constexpr uint32_t O_Y = O_B + 4 * BB;           // Y staging [2]
   // last layer only: Y_lo staging [2], the dec1 B operand [D1_lo; D1_hi]
   // (2H rows, swizzled K-major), then dec1 (fp32, CUDA-core fallback), b1, dec2
@@ -145,6 +152,12 @@ struct SellCfg {
   // TMEM: layer accumulator [0, 2DP); last layer's projection accumulator at
   // [2DP, 2DP + 2H) (tensor-core projection when H % 16 == 0 and H <= 64)
   static constexpr int TALLOC_LAST = 256;
+  // TMEM column of X_lo, the A operand of X·U's A_lo·B_hi product: written
+  // row-per-lane by the math warps (tcgen05.st), read by the TS-form MMA, so
+  // it never crosses shared memory.  (ÂX_lo stays in shared memory: moving it
+  // too needs the quarter's four warps to sync before the row-wise read, and
+  // that coupling cost more than the wavefronts it saved — C4 162 -> 240 us.)
+  static __host__ __device__ constexpr int alo_col(bool tcp) { return tcp ? 2 * DP + 128 : 2 * DP; }
   // DP=16: the CUDA-core projection is cheap (DP*H FMAs per row) and the
   // staging it saves is L1 for the gathers (fused C2: 27.3 vs 26.5 us LAST,
   // 18 vs 17 us per layer with the larger layout)
@@ -292,7 +305,7 @@ template <int DP, int CSR>
 struct SellPipe {
   using C = SellCfg<DP, CSR>;
   uint8_t* ring;
-  uint8_t* A;  // [A1_lo | A2_hi | A2_lo]
+  uint8_t* A;  // [A2_hi | A2_lo]
   uint8_t* Bs;
   uint8_t* Ystg;
   uint8_t* Ylo;
@@ -464,7 +477,8 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       constexpr uint32_t idesc = tc::idesc_tf32(128, DP);
       constexpr uint32_t idesc2 = tc::idesc_tf32(128, 2 * DP);
       const uint32_t sBstk = tc::smem_u32(p.Bs);
-      const uint32_t sA1lo = tc::smem_u32(p.A), sA2hi = sA1lo + C::OPB, sA2lo = sA1lo + 2 * C::OPB;
+      const uint32_t sA2hi = tc::smem_u32(p.A), sA2lo = sA2hi + C::OPB;
+      const uint32_t tAlo = p.tmem + C::alo_col(TCP);
       for (int it = 0; it <= my_tiles; ++it) {
         tc::mbar_wait_dbg(p.afull, (ab + it) & 1, 1, it);
         tc::fence_after();
@@ -472,7 +486,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         // the buffer the epilogue after this MMA writes is free
         tc::bulk_wait_read0();
         if (KIND == 1 && it < my_tiles) {  // training forward: the tile's ÂX (A2_hi) to HBM
-          tc::tma_store_2d(tio->mapax, p.A + C::OPB, 0, (blockIdx.x + it * gridDim.x) * TM);
+          tc::tma_store_2d(tio->mapax, p.A, 0, (blockIdx.x + it * gridDim.x) * TM);
           tc::bulk_commit();
         }
         if (it < my_tiles) {
@@ -481,11 +495,12 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           // once for both): D[:, 0:DP] = A_hi·B_lo, D[:, DP:2DP] = A_hi·B_hi +
           // A_lo·B_hi; the epilogue adds the halves.  Each part's B operands
           // are stored [B_lo | B_hi], i.e. as one 2DP-row operand.  The
-          // landed X tile is A_hi of the X·U part (kind::tf32 truncates).
+          // landed X tile is A_hi of the X·U part (kind::tf32 truncates); its
+          // A_lo is in TMEM (TS form).
           uint32_t accf = 0;
 #pragma unroll
           for (int part = 0; part < 2; ++part) {
-            const uint32_t sah = part == 0 ? sX : sA2hi, sal = part == 0 ? sA1lo : sA2lo;
+            const uint32_t sah = part == 0 ? sX : sA2hi;
             const uint32_t sbs = sBstk + part * 2 * C::BB;  // [B_lo; B_hi] of this part (2DP rows)
             const uint32_t sbh = sbs + C::BB;                // B_hi rows alone
 #pragma unroll
@@ -493,8 +508,11 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
               tc::mma_tf32(p.tmem, tc::make_desc_swz<DP>(sah + k8 * 32),
                            tc::make_desc_swz<DP>(sbs + k8 * 32), idesc2, accf);
               accf = 1;
-              tc::mma_tf32(p.tmem + DP, tc::make_desc_swz<DP>(sal + k8 * 32),
-                           tc::make_desc_swz<DP>(sbh + k8 * 32), idesc, 1);
+              if (part == 0)
+                tc::mma_tf32_ts(p.tmem + DP, tAlo + 8 * k8, tc::make_desc_swz<DP>(sbh + k8 * 32), idesc, 1);
+              else
+                tc::mma_tf32(p.tmem + DP, tc::make_desc_swz<DP>(sA2lo + k8 * 32),
+                             tc::make_desc_swz<DP>(sbh + k8 * 32), idesc, 1);
             }
           }
         }
@@ -764,10 +782,28 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       for (int j = 0; j < R; ++j) {
         const int rr = R * gid + j;
         const uint32_t o = tc::swz_off<DP>(rr, 4 * gl);
-        const float4 xv = *reinterpret_cast<const float4*>(slot + o);
-        *reinterpret_cast<float4*>(p.A + o) = f4_trunc_lo(xv);
-        *reinterpret_cast<float4*>(p.A + C::OPB + o) = acc[j];
-        *reinterpret_cast<float4*>(p.A + 2 * C::OPB + o) = f4_trunc_lo(acc[j]);
+        *reinterpret_cast<float4*>(p.A + o) = acc[j];
+        *reinterpret_cast<float4*>(p.A + C::OPB + o) = f4_trunc_lo(acc[j]);
+      }
+      // X_lo into TMEM, one row per lane: warp (lane quarter q, column group
+      // cq) takes columns [cq CW, cq CW + CW) of rows 32q + lane
+      {
+        constexpr int CW = DP / NQ;
+        const int q = warp & 3, cq = warp >> 2, m = 32 * q + lane;
+        float lo[CW];
+#pragma unroll
+        for (int c = 0; c < CW; c += 4) {
+          const float4 xl = f4_trunc_lo(*reinterpret_cast<const float4*>(slot + tc::swz_off<DP>(m, cq * CW + c)));
+          lo[c] = xl.x;
+          lo[c + 1] = xl.y;
+          lo[c + 2] = xl.z;
+          lo[c + 3] = xl.w;
+        }
+        const uint32_t ta = p.tmem + C::alo_col(TCP) + (static_cast<uint32_t>(32 * q) << 16) + cq * CW;
+        if constexpr (CW == 4) tc::tmem_st4(ta, lo);
+        else tc::tmem_st8(ta, lo);
+        tc::tmem_wait_st();
+        tc::fence_before();
       }
     }
     if (it <= my_tiles) arrive();

@@ -194,6 +194,9 @@ def cpu_reference_baseline(w, seconds=15.0):
                       f"{total:.1f} s, fp32-rounded inputs as f64"}
 
 
+REF_BUDGET_S = 90.0  # bound on the reference arm's timed loop (seconds)
+
+
 def run_reference_arm(args, rank, world):
     """--impl reference: the reference CPU apply, all usable host threads."""
     cfg = args.config
@@ -242,17 +245,29 @@ def run_reference_arm(args, rank, world):
         for t in ts:
             t.join()
 
+    # one reference apply takes seconds (C2: ~2 s per thread), so the run is
+    # bounded: warm-up stops once it has taken REF_BUDGET_S / 8, and the timed
+    # loop runs at most as many steps as fit REF_BUDGET_S (reported in "steps",
+    # with the requested count beside it)
+    tw = time.perf_counter()
+    warm = 0
     for _ in range(args.warmup):
         step()
+        warm += 1
+        if time.perf_counter() - tw > REF_BUDGET_S / 8:
+            break
+    per = (time.perf_counter() - tw) / max(warm, 1)
+    steps = max(1, min(args.steps, int(REF_BUDGET_S // max(per, 1e-9))))
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(steps):
         step()
     el = time.perf_counter() - t0
-    value = args.steps * threads / el
+    value = steps * threads / el
     line = {
         "impl": "reference", "metric": f"GNP M.v applies/s ({cfg.upper()})", "value": value,
-        "unit": "applies/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+        "unit": "applies/s", "n_gpus": world, "steps": steps, "warmup": warm,
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "ms_per_step": 1e3 * el / steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "n": n, "nnz": nnz, "d": dims[0], "hidden": dims[1],
                    "layers": dims[2]},

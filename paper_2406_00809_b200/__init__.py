@@ -21,7 +21,35 @@ except ImportError as _e:  # the build module must stay importable
     _IMPORT_ERROR = _e
 
 
+# pure-Python submodules that must import before (or without) the native build
+_SUBMODULES = ("build", "capi", "dp")
+
+
+def _retry_native_import() -> bool:
+    """The package may have been imported before an in-process build; retry once."""
+    global _IMPORT_ERROR
+    import importlib
+
+    try:
+        _m = importlib.import_module(__name__ + "._gnp")
+    except ImportError as e:
+        _IMPORT_ERROR = e
+        return False
+    g = globals()
+    g.update({k: getattr(_m, k) for k in dir(_m) if not k.startswith("__")})
+    g["_gnp"] = _m
+    _IMPORT_ERROR = None
+    return True
+
+
 def __getattr__(name):
+    import importlib
+
+    if name in _SUBMODULES:
+        return importlib.import_module("." + name, __name__)
+    if _IMPORT_ERROR is not None and not name.startswith("__") and _retry_native_import():
+        if name in globals():
+            return globals()[name]
     if _IMPORT_ERROR is not None and not name.startswith("__"):
         raise ImportError(
             "paper_2406_00809_b200: native extension not built (" + str(_IMPORT_ERROR) + "); run "

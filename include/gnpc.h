@@ -197,8 +197,32 @@ int gnpc_trainer_params(gnpc_trainer t, double* params);
 /* Copy the trainer's parameters into its model (inference view rebuilt). */
 int gnpc_trainer_sync_model(gnpc_trainer t);
 
-/* train_preconditioner (src/gnn.cpp:401-451) with Gaussian pairs only
- * (spectral_count must be 0 in this build).  losses: steps+1 entries. */
+/* ------------------------------------------------------------------ sampler
+ * build_spectral_sampler (src/sampler.cpp:10-39): an unpreconditioned
+ * Arnoldi cycle of m steps from Rng(seed).gaussian_vector(n) on the device
+ * (fp32 Â, fp64 basis; the device FGMRES kernels), then the host Jacobi SVD
+ * of the (k+1) x k Hessenberg (src/svd.cpp:10-80); k < m on breakdown.
+ * GNPC_ERUNTIME when the Hessenberg is numerically zero. */
+typedef struct gnpc_sampler_s* gnpc_sampler;
+int gnpc_sampler_create(gnpc_csr a, int64_t m, uint64_t seed, gnpc_sampler* out);
+/* The host half alone, from a given cycle: v n x k basis, hbar (k+1) x k
+ * (col-major), k >= 1 (src/sampler.cpp:19-38). */
+int gnpc_sampler_from_arnoldi(int64_t n, int64_t k, const double* v, const double* hbar,
+                              gnpc_sampler* out);
+int gnpc_sampler_destroy(gnpc_sampler s);
+/* k = basis columns kept (SpectralSampler::m), m_eff = retained rank. */
+int gnpc_sampler_info(gnpc_sampler s, int64_t* k, int64_t* m_eff);
+/* v: n x k, zsv: k x k (col-major), sv: k singular values; any may be NULL. */
+int gnpc_sampler_export(gnpc_sampler s, double* v, double* zsv, double* sv);
+/* assemble_batch (src/sampler.cpp:68-83) from Rng(seed) after dropping
+ * skip_batches batches: n x batch col-major x and b = A x (f64, host).
+ * s may be NULL when spectral_count == 0. */
+int gnpc_assemble_batch(gnpc_sampler s, gnpc_csr a, uint64_t seed, int64_t skip_batches,
+                        int64_t batch, int64_t spectral_count, double* x, double* b);
+
+/* train_preconditioner (src/gnn.cpp:401-451): Gaussian and spectral pairs
+ * (spectral_count of each batch), monitor batch, best snapshot.
+ * losses: steps+1 entries. */
 typedef struct {
   double lr;
   int64_t steps, batch, spectral_count, arnoldi_m;

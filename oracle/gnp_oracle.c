@@ -859,3 +859,201 @@ done:
 #undef HSET_LAST
   return status;
 }
+
+/* ======================================================================
+ * Spectral sampler — src/sampler.cpp:10-59, src/svd.cpp:10-80,
+ * arnoldi_cycle (src/krylov.cpp:128-135) without a preconditioner.
+ * ==================================================================== */
+/* krylov.cpp:128-135 + ArnoldiProcess::step (krylov.cpp:30-65), M = none.
+ * v: n x (m+1) col-major, hbar: (m+1) x m col-major (zeroed here). */
+int oc_arnoldi_cycle(size_t n, const int64_t* rp, const int64_t* ci, const double* av,
+                     const double* r0, size_t m, double* v, double* hbar, size_t* steps,
+                     int* breakdown) {
+  if (m < 1) return fail("arnoldi: m must be >= 1");
+  const double beta = sqrt(dotv(n, r0, r0));
+  if (beta == 0.0) return fail("arnoldi: zero start vector");
+  const size_t ld = m + 1;
+  memset(v, 0, n * (m + 1) * sizeof(double));
+  memset(hbar, 0, ld * m * sizeof(double));
+  for (size_t i = 0; i < n; ++i) v[i] = r0[i] / beta;
+  double* w = (double*)malloc(n * sizeof(double));
+  *steps = 0;
+  *breakdown = 0;
+  for (size_t j = 0; j < m; ++j) {
+    oc_spmv(n, rp, ci, av, v + j * n, w); /* z_j = v_j (no preconditioner) */
+    const double wnorm0 = sqrt(dotv(n, w, w));
+    for (size_t i = 0; i <= j; ++i) {
+      const double* vi = v + i * n;
+      const double hh = dotv(n, w, vi);
+      hbar[j * ld + i] = hh;
+      for (size_t q = 0; q < n; ++q) w[q] -= hh * vi[q];
+    }
+    double wnorm = sqrt(dotv(n, w, w));
+    if (wnorm < 0.70710678118654752440 * wnorm0) {
+      for (size_t i = 0; i <= j; ++i) {
+        const double* vi = v + i * n;
+        const double cc = dotv(n, w, vi);
+        hbar[j * ld + i] += cc;
+        for (size_t q = 0; q < n; ++q) w[q] -= cc * vi[q];
+      }
+      wnorm = sqrt(dotv(n, w, w));
+    }
+    hbar[j * ld + j + 1] = wnorm;
+    ++*steps;
+    if (wnorm <= 1e-14 * wnorm0) {
+      *breakdown = 1;
+      break;
+    }
+    double* vn = v + (j + 1) * n;
+    for (size_t q = 0; q < n; ++q) vn[q] = w[q] / wnorm;
+  }
+  free(w);
+  return 0;
+}
+
+/* svd.cpp:10-80: one-sided Jacobi (cyclic sweeps, tol 1e-15, <= 60 sweeps),
+ * singular values sorted descending (std::sort on s: ties keep no defined
+ * order in the reference either).  a: rows x cols col-major (rows >= cols);
+ * u: rows x cols, s: cols, v: cols x cols. */
+int oc_jacobi_svd(size_t rows, size_t cols, const double* a, double* u, double* s, double* v) {
+  if (rows < cols) return fail("jacobi_svd: matrix must be tall");
+  double* b = (double*)malloc(rows * cols * sizeof(double));
+  double* vv = (double*)calloc(cols * cols, sizeof(double));
+  double* sv = (double*)malloc(cols * sizeof(double));
+  size_t* order = (size_t*)malloc(cols * sizeof(size_t));
+  memcpy(b, a, rows * cols * sizeof(double));
+  for (size_t i = 0; i < cols; ++i) vv[i * cols + i] = 1.0;
+  const double tol = 1e-15;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    int rotated = 0;
+    for (size_t p = 0; p + 1 < cols; ++p) {
+      for (size_t q = p + 1; q < cols; ++q) {
+        double app = 0.0, aqq = 0.0, apq = 0.0;
+        const double* bp = b + p * rows;
+        const double* bq = b + q * rows;
+        for (size_t r = 0; r < rows; ++r) {
+          app += bp[r] * bp[r];
+          aqq += bq[r] * bq[r];
+          apq += bp[r] * bq[r];
+        }
+        if (fabs(apq) <= tol * sqrt(app * aqq)) continue;
+        rotated = 1;
+        const double zeta = (aqq - app) / (2.0 * apq);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t);
+        const double sn = cs * t;
+        for (size_t r = 0; r < rows; ++r) {
+          const double t1 = b[p * rows + r], t2 = b[q * rows + r];
+          b[p * rows + r] = cs * t1 - sn * t2;
+          b[q * rows + r] = sn * t1 + cs * t2;
+        }
+        for (size_t r = 0; r < cols; ++r) {
+          const double t1 = vv[p * cols + r], t2 = vv[q * cols + r];
+          vv[p * cols + r] = cs * t1 - sn * t2;
+          vv[q * cols + r] = sn * t1 + cs * t2;
+        }
+      }
+    }
+    if (!rotated) break;
+  }
+  for (size_t j = 0; j < cols; ++j) {
+    double nrm = 0.0;
+    for (size_t r = 0; r < rows; ++r) nrm += b[j * rows + r] * b[j * rows + r];
+    sv[j] = sqrt(nrm);
+    order[j] = j;
+  }
+  /* descending by s; insertion sort is stable (distinct values sort the same
+   * as the reference's std::sort) */
+  for (size_t i = 1; i < cols; ++i) {
+    const size_t o = order[i];
+    size_t k = i;
+    while (k > 0 && sv[order[k - 1]] < sv[o]) {
+      order[k] = order[k - 1];
+      --k;
+    }
+    order[k] = o;
+  }
+  memset(u, 0, rows * cols * sizeof(double));
+  for (size_t j = 0; j < cols; ++j) {
+    const size_t src = order[j];
+    s[j] = sv[src];
+    if (sv[src] > 0.0)
+      for (size_t r = 0; r < rows; ++r) u[j * rows + r] = b[src * rows + r] / sv[src];
+    for (size_t r = 0; r < cols; ++r) v[j * cols + r] = vv[src * cols + r];
+  }
+  free(b); free(vv); free(sv); free(order);
+  return 0;
+}
+
+/* sampler.cpp:10-39: Arnoldi from Rng(seed).gaussian_vector(n), SVD of the
+ * (k+1) x k Hessenberg, rank m_eff = #{s_j >= s_0 1e-12, s_j > 0}.
+ * Outputs (caller-sized for m): v n x m (first k columns used), zsv m x m
+ * (k x k used, leading dimension k), s[m] (k used). */
+int oc_spectral_sampler(size_t n, const int64_t* rp, const int64_t* ci, const double* av,
+                        size_t m, uint64_t seed, double* v, double* zsv, double* s,
+                        size_t* k_out, size_t* m_eff_out) {
+  if (n < 2) return fail("spectral sampler: n must be >= 2");
+  if (m < 1) return fail("spectral sampler: m must be >= 1");
+  double* r0 = (double*)malloc(n * sizeof(double));
+  double* vf = (double*)malloc(n * (m + 1) * sizeof(double));
+  double* hb = (double*)malloc((m + 1) * m * sizeof(double));
+  oc_gaussian_vector(seed, n, r0);
+  size_t k = 0;
+  int brk = 0;
+  int rc = oc_arnoldi_cycle(n, rp, ci, av, r0, m, vf, hb, &k, &brk);
+  if (rc == 0) {
+    double* hk = (double*)malloc((k + 1) * k * sizeof(double));
+    double* u = (double*)malloc((k + 1) * k * sizeof(double));
+    for (size_t c = 0; c < k; ++c)
+      for (size_t i = 0; i <= k; ++i) hk[c * (k + 1) + i] = hb[c * (m + 1) + i];
+    rc = oc_jacobi_svd(k + 1, k, hk, u, s, zsv);
+    memcpy(v, vf, n * k * sizeof(double));
+    size_t me = 0;
+    const double floor = k ? s[0] * 1e-12 : 0.0;
+    for (size_t j = 0; j < k; ++j)
+      if (s[j] >= floor && s[j] > 0.0) ++me;
+    *k_out = k;
+    *m_eff_out = me;
+    if (rc == 0 && me == 0) rc = fail("spectral sampler: Hessenberg is numerically zero");
+    free(hk); free(u);
+  }
+  free(r0); free(vf); free(hb);
+  return rc;
+}
+
+/* sampler.cpp:41-83: skip `skip_batches` batches of Rng(seed), then one batch;
+ * columns k < spectral_count are spectral pairs (coef = Zsv diag(1/s) eps,
+ * x = V coef), the rest Gaussian; b = A x. */
+int oc_assemble_batch(size_t n, const int64_t* rp, const int64_t* ci, const double* av,
+                      size_t k, size_t m_eff, const double* v, const double* zsv,
+                      const double* s, uint64_t seed, size_t skip_batches, size_t batch,
+                      size_t spectral_count, double* x, double* b) {
+  if (batch == 0) return fail("assemble_batch: empty batch");
+  if (spectral_count > batch) return fail("assemble_batch: spectral_count > batch");
+  oc_rng r;
+  oc_rng_init(&r, seed);
+  double* coef = (double*)malloc((k ? k : 1) * sizeof(double));
+  for (size_t rep = 0; rep <= skip_batches; ++rep) {
+    for (size_t c = 0; c < batch; ++c) {
+      double* xc = x + c * n;
+      if (c < spectral_count) {
+        for (size_t i = 0; i < k; ++i) coef[i] = 0.0;
+        for (size_t j = 0; j < m_eff; ++j) {
+          const double scaled = oc_rng_gaussian(&r) / s[j];
+          for (size_t i = 0; i < k; ++i) coef[i] += zsv[j * k + i] * scaled;
+        }
+        for (size_t i = 0; i < n; ++i) xc[i] = 0.0;
+        for (size_t j = 0; j < k; ++j) {
+          const double cj = coef[j];
+          const double* vj = v + j * n;
+          for (size_t i = 0; i < n; ++i) xc[i] += vj[i] * cj;
+        }
+      } else {
+        for (size_t i = 0; i < n; ++i) xc[i] = oc_rng_gaussian(&r);
+      }
+      if (rep == skip_batches) oc_spmv(n, rp, ci, av, xc, b + c * n);
+    }
+  }
+  free(coef);
+  return 0;
+}

@@ -92,6 +92,19 @@ int oc_fgmres(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
               size_t restart, double timeout_secs, double* x_out, size_t* hist_iter,
               double* hist_rel, double* hist_t, size_t hist_cap, size_t* hist_len);
 
+/* ---- spectral sampler (src/sampler.cpp:10-83, src/svd.cpp:10-80) */
+int oc_arnoldi_cycle(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                     const double* r0, size_t m, double* vout, double* hbar, size_t* steps,
+                     int* breakdown);
+int oc_jacobi_svd(size_t rows, size_t cols, const double* a, double* u, double* s, double* v);
+int oc_spectral_sampler(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                        size_t m, uint64_t seed, double* vout, double* zsv, double* s,
+                        size_t* k_out, size_t* m_eff_out);
+int oc_assemble_batch(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                      size_t k, size_t m_eff, const double* vb, const double* zsv,
+                      const double* s, uint64_t seed, size_t skip_batches, size_t batch,
+                      size_t spectral_count, double* x, double* b);
+
 #ifdef __cplusplus
 }
 #endif

@@ -111,6 +111,13 @@ class Restatement:
         L.oc_fgmres.argtypes = [C.c_size_t, _i64, _i64, _d, _d, C.c_int, C.c_size_t, C.c_size_t,
                                 C.c_size_t, C.c_void_p, _d, C.c_double, C.c_size_t, C.c_size_t,
                                 C.c_double, _d, C.POINTER(C.c_size_t), _d, _d, C.c_size_t, _szp]
+        L.oc_arnoldi_cycle.argtypes = [C.c_size_t, _i64, _i64, _d, _d, C.c_size_t, _d, _d, _szp,
+                                       C.POINTER(C.c_int)]
+        L.oc_jacobi_svd.argtypes = [C.c_size_t, C.c_size_t, _d, _d, _d, _d]
+        L.oc_spectral_sampler.argtypes = [C.c_size_t, _i64, _i64, _d, C.c_size_t, C.c_uint64, _d, _d,
+                                          _d, _szp, _szp]
+        L.oc_assemble_batch.argtypes = [C.c_size_t, _i64, _i64, _d, C.c_size_t, C.c_size_t, _d, _d,
+                                        _d, C.c_uint64, C.c_size_t, C.c_size_t, C.c_size_t, _d, _d]
 
     def _check(self, rc):
         if rc != 0:
@@ -236,6 +243,48 @@ class Restatement:
         self._check(self.L.oc_gaussian_batch(*csr_arrays(a), seed, skip_batches, batch, x, b))
         return x, b
 
+    # ---- spectral sampler (src/sampler.cpp, src/svd.cpp)
+    def arnoldi_cycle(self, a: Csr, r0, m):
+        """-> (V n x (m+1) col-major flat, Hbar (m+1) x m col-major flat, steps, breakdown)"""
+        v = np.zeros(a.n * (m + 1))
+        h = np.zeros((m + 1) * m)
+        k = C.c_size_t()
+        brk = C.c_int()
+        self._check(self.L.oc_arnoldi_cycle(*csr_arrays(a), np.ascontiguousarray(r0, np.float64), m, v, h,
+                                            C.byref(k), C.byref(brk)))
+        return v, h, k.value, bool(brk.value)
+
+    def jacobi_svd(self, a_colmajor, rows, cols):
+        u = np.zeros(rows * cols)
+        s = np.zeros(cols)
+        v = np.zeros(cols * cols)
+        self._check(self.L.oc_jacobi_svd(rows, cols, np.ascontiguousarray(a_colmajor, np.float64), u, s, v))
+        return u, s, v
+
+    def spectral_sampler(self, a: Csr, m, seed):
+        """-> dict(v n x k flat, zsv k x k flat, s[k], k, m_eff)"""
+        v = np.zeros(a.n * m)
+        z = np.zeros(m * m)
+        s = np.zeros(m)
+        k = C.c_size_t()
+        me = C.c_size_t()
+        self._check(self.L.oc_spectral_sampler(*csr_arrays(a), m, seed, v, z, s, C.byref(k), C.byref(me)))
+        k = k.value
+        return {"v": v[: a.n * k].copy(), "zsv": z[: k * k].copy(), "s": s[:k].copy(), "k": k,
+                "m_eff": me.value}
+
+    def assemble_batch(self, a: Csr, sampler, seed, skip_batches, batch, spectral_count):
+        x = np.empty(a.n * batch)
+        b = np.empty(a.n * batch)
+        if sampler is None:
+            sampler = {"v": np.zeros(1), "zsv": np.zeros(1), "s": np.ones(1), "k": 0, "m_eff": 0}
+        self._check(self.L.oc_assemble_batch(*csr_arrays(a), sampler["k"], sampler["m_eff"],
+                                             np.ascontiguousarray(sampler["v"], np.float64),
+                                             np.ascontiguousarray(sampler["zsv"], np.float64),
+                                             np.ascontiguousarray(sampler["s"], np.float64), seed,
+                                             skip_batches, batch, spectral_count, x, b))
+        return x, b
+
     # ---- krylov
     def hessenberg_lstsq(self, hbar_colmajor, k, beta):
         y = np.zeros(k)
@@ -322,6 +371,10 @@ class Reference:
         L.ref_gaussian_batch.argtypes = [vp, C.c_uint64, C.c_size_t, C.c_size_t, _d, _d]
         L.ref_hessenberg_lstsq.argtypes = [C.c_size_t, _d, C.c_double, _d, C.POINTER(C.c_double),
                                            C.POINTER(C.c_int)]
+        L.ref_jacobi_svd.argtypes = [C.c_size_t, C.c_size_t, _d, _d, _d, _d]
+        L.ref_spectral_sampler.argtypes = [vp, C.c_size_t, C.c_uint64, _d, _d, _d, _szp, _szp]
+        L.ref_assemble_batch.argtypes = [vp, C.c_size_t, C.c_uint64, C.c_uint64, C.c_size_t, C.c_size_t,
+                                         C.c_size_t, _d, _d]
         L.ref_arnoldi_cycle.argtypes = [vp, _d, C.c_size_t, C.c_int, C.c_size_t, C.c_size_t,
                                         C.c_size_t, vp, _d, _d, _d, _szp, C.POINTER(C.c_int)]
         L.ref_fgmres.argtypes = [vp, _d, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t, vp, _d,
@@ -487,6 +540,33 @@ class Reference:
         x = np.empty(a.n * batch)
         b = np.empty(a.n * batch)
         self._with(a, lambda h: self._check(self.L.ref_gaussian_batch(h, seed, skip_batches, batch, x, b)))
+        return x, b
+
+    # ---- spectral sampler
+    def jacobi_svd(self, a_colmajor, rows, cols):
+        u = np.zeros(rows * cols)
+        s = np.zeros(cols)
+        v = np.zeros(cols * cols)
+        self._check(self.L.ref_jacobi_svd(rows, cols, np.ascontiguousarray(a_colmajor, np.float64), u, s, v))
+        return u, s, v
+
+    def spectral_sampler(self, a, m, seed):
+        v = np.zeros(a.n * m)
+        z = np.zeros(m * m)
+        s = np.zeros(m)
+        k = C.c_size_t()
+        me = C.c_size_t()
+        self._with(a, lambda h: self._check(self.L.ref_spectral_sampler(h, m, seed, v, z, s, C.byref(k),
+                                                                         C.byref(me))))
+        k = k.value
+        return {"v": v[: a.n * k].copy(), "zsv": z[: k * k].copy(), "s": s[:k].copy(), "k": k,
+                "m_eff": me.value}
+
+    def assemble_batch(self, a, m, sampler_seed, seed, skip_batches, batch, spectral_count):
+        x = np.empty(a.n * batch)
+        b = np.empty(a.n * batch)
+        self._with(a, lambda h: self._check(self.L.ref_assemble_batch(
+            h, m, sampler_seed, seed, skip_batches, batch, spectral_count, x, b)))
         return x, b
 
     # ---- krylov

@@ -31,6 +31,7 @@
 #include "gnp/mmio.hpp"
 #include "gnp/rng.hpp"
 #include "gnp/sampler.hpp"
+#include "gnp/svd.hpp"
 
 using namespace gnp;
 
@@ -376,6 +377,48 @@ int ref_gaussian_batch(void* h, std::uint64_t seed, std::size_t skip_batches,
     for (std::size_t s = 0; s < skip_batches; ++s)
       (void)assemble_batch(unused, a, batch, 0, rng);
     TrainingBatch tb = assemble_batch(unused, a, batch, 0, rng);
+    std::memcpy(x, tb.x.data().data(), a.n * batch * sizeof(double));
+    std::memcpy(b, tb.b.data().data(), a.n * batch * sizeof(double));
+  });
+}
+
+// ---------------------------------------------------------------- spectral sampler
+int ref_jacobi_svd(std::size_t rows, std::size_t cols, const double* a, double* u, double* s,
+                   double* v) {
+  return guarded([&] {
+    DenseMatrix m(rows, cols);
+    std::memcpy(m.data().data(), a, rows * cols * sizeof(double));
+    SvdResult r = jacobi_svd(m);
+    std::memcpy(u, r.u.data().data(), rows * cols * sizeof(double));
+    std::memcpy(s, r.s.data(), cols * sizeof(double));
+    std::memcpy(v, r.v.data().data(), cols * cols * sizeof(double));
+  });
+}
+
+// build_spectral_sampler (src/sampler.cpp:10-39); outputs sized for m.
+int ref_spectral_sampler(void* h, std::size_t m, std::uint64_t seed, double* v, double* zsv,
+                         double* s, std::size_t* k, std::size_t* m_eff) {
+  return guarded([&] {
+    SpectralSampler sp = build_spectral_sampler(*H(h), m, seed);
+    *k = sp.m;
+    *m_eff = sp.m_eff;
+    std::memcpy(v, sp.v.data().data(), sp.v.data().size() * sizeof(double));
+    std::memcpy(zsv, sp.zm_sv.data().data(), sp.zm_sv.data().size() * sizeof(double));
+    std::memcpy(s, sp.s.data(), sp.s.size() * sizeof(double));
+  });
+}
+
+// assemble_batch (src/sampler.cpp:68-83) from a freshly built sampler:
+// `skip` batches from Rng(seed) are drawn and dropped, then one is returned.
+int ref_assemble_batch(void* h, std::size_t m, std::uint64_t sampler_seed, std::uint64_t seed,
+                       std::size_t skip_batches, std::size_t batch, std::size_t spectral,
+                       double* x, double* b) {
+  return guarded([&] {
+    const CsrMatrix& a = *H(h);
+    SpectralSampler sp = build_spectral_sampler(a, m, sampler_seed);
+    Rng rng(seed);
+    for (std::size_t q = 0; q < skip_batches; ++q) (void)assemble_batch(sp, a, batch, spectral, rng);
+    TrainingBatch tb = assemble_batch(sp, a, batch, spectral, rng);
     std::memcpy(x, tb.x.data().data(), a.n * batch * sizeof(double));
     std::memcpy(b, tb.b.data().data(), a.n * batch * sizeof(double));
   });

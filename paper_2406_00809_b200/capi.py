@@ -370,7 +370,63 @@ class Trainer:
         check(lib().gnpc_trainer_sync_model(self.h))
 
 
-def train_preconditioner(csr: Csr, dims=(16, 32, 8), lr=1e-3, steps=2000, batch=16, spectral=0,
+class Sampler:
+    """gnpc_sampler: build_spectral_sampler (src/sampler.cpp:10-39), Arnoldi on
+    the device, Jacobi SVD on the host."""
+
+    def __init__(self, csr: Csr, m: int = 40, seed: int = 0, _handle=None):
+        self.csr = csr
+        self.n = csr.info()[0]
+        h = _handle
+        if h is None:
+            h = vp()
+            check(lib().gnpc_sampler_create(csr.h, C.c_int64(m), C.c_uint64(seed), C.byref(h)))
+        self.h = h
+        k, me = C.c_int64(), C.c_int64()
+        check(lib().gnpc_sampler_info(self.h, C.byref(k), C.byref(me)))
+        self.k, self.m_eff = k.value, me.value
+
+    @classmethod
+    def from_arnoldi(cls, csr: Csr, v, hbar, k):
+        """Host half only (no device): factor a given cycle's (k+1) x k Hessenberg."""
+        n = csr.info()[0]
+        v = np.ascontiguousarray(v[: n * k], np.float64)
+        hbar = np.ascontiguousarray(hbar, np.float64)
+        h = vp()
+        check(lib().gnpc_sampler_from_arnoldi(C.c_int64(n), C.c_int64(k), v.ctypes.data_as(vp),
+                                              hbar.ctypes.data_as(vp), C.byref(h)))
+        return cls(csr, _handle=h)
+
+    def __del__(self):
+        try:
+            if self.h and _lib is not None:
+                _lib.gnpc_sampler_destroy(self.h)
+        except Exception:
+            pass
+
+    def factors(self):
+        """-> (v n x k flat col-major, zsv k x k flat col-major, s[k])"""
+        v = np.empty(self.n * self.k)
+        z = np.empty(self.k * self.k)
+        s = np.empty(self.k)
+        check(lib().gnpc_sampler_export(self.h, v.ctypes.data_as(vp), z.ctypes.data_as(vp),
+                                        s.ctypes.data_as(vp)))
+        return v, z, s
+
+
+def assemble_batch(csr: Csr, sampler: Sampler | None, seed, skip_batches, batch, spectral_count):
+    """assemble_batch (src/sampler.cpp:68-83) from Rng(seed) after skip_batches batches."""
+    n = csr.info()[0]
+    x = np.empty(n * batch)
+    b = np.empty(n * batch)
+    check(lib().gnpc_assemble_batch(sampler.h if sampler else None, csr.h, C.c_uint64(seed),
+                                    C.c_int64(skip_batches), C.c_int64(batch),
+                                    C.c_int64(spectral_count), x.ctypes.data_as(vp),
+                                    b.ctypes.data_as(vp)))
+    return x, b
+
+
+def train_preconditioner(csr: Csr, dims=(16, 32, 8), lr=1e-3, steps=2000, batch=16, spectral=8,
                          arnoldi_m=40, seed=0, monitor_batch=16):
     cfg = TrainConfig(lr, steps, batch, spectral, arnoldi_m, seed, monitor_batch, *dims)
     best = np.empty(param_count(*dims))

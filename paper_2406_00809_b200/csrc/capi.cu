@@ -1030,6 +1030,39 @@ int fgmres_host(gnpc_csr a, gnpc_model m, const HostOp* hop, const double* b, co
 
 }  // namespace
 
+namespace gnpc_impl {
+// build_spectral_sampler (src/sampler.cpp:10-39).  The Arnoldi cycle is the
+// device FGMRES machinery run for one unpreconditioned cycle of m steps with
+// no convergence test (rtol < 0): r0 = b - A·0 = start exactly, V and the raw
+// Hessenberg stay in the Krylov workspace and are read back once.
+std::unique_ptr<gnpc_sampler_s> build_sampler(gnpc_csr_s& A, std::int64_t m, std::uint64_t seed) {
+  if (A.h.n < 2) throw std::invalid_argument("spectral sampler: n must be >= 2");
+  if (m < 1) throw std::invalid_argument("spectral sampler: m must be >= 1");
+  require_device();
+  const std::int64_t n = A.h.n;
+  gnp_b200::Rng rng(seed);
+  const std::vector<double> start = rng.gaussian_vector(n);
+  DevBuf<double> db(n), dx(n);
+  GNPC_CUDA(cudaMemcpy(db.p, start.data(), n * 8, cudaMemcpyHostToDevice));
+  GNPC_CUDA(cudaMemset(dx.p, 0, n * 8));
+  gnpc_solve_config cfg{-1.0, m, m, -1.0};
+  (void)fgmres_core(A, nullptr, nullptr, db.p, dx.p, cfg, nullptr, nullptr);
+  KrylovWs& W = *A.kws;
+  gnpk::KState st{};
+  GNPC_CUDA(cudaMemcpy(&st, W.st.p, sizeof st, cudaMemcpyDeviceToHost));
+  const std::int64_t k = st.steps;
+  if (k < 1 || k > m) throw std::runtime_error("spectral sampler: Arnoldi cycle made no progress");
+  std::vector<double> v(n * k), hfull((m + 1) * m), hk((k + 1) * k);
+  GNPC_CUDA(cudaMemcpy(v.data(), W.V.p, n * k * 8, cudaMemcpyDeviceToHost));
+  GNPC_CUDA(cudaMemcpy(hfull.data(), W.H.p, hfull.size() * 8, cudaMemcpyDeviceToHost));
+  for (std::int64_t c = 0; c < k; ++c)
+    for (std::int64_t i = 0; i <= k; ++i) hk[c * (k + 1) + i] = hfull[c * (m + 1) + i];
+  auto out = std::make_unique<gnpc_sampler_s>();
+  out->s = gnp_b200::spectral_from_arnoldi(n, k, std::move(v), hk);
+  return out;
+}
+}  // namespace gnpc_impl
+
 // ====================================================================== C ABI
 extern "C" {
 
@@ -1405,6 +1438,63 @@ int gnpc_fgmres_device(gnpc_csr a, gnpc_model m, const double* b_dev, double* x_
     require_device();
     if (m) need(m->a->h.n == a->h.n, "fgmres: preconditioner dimension mismatch");
     *status = fgmres_core(*a, m, nullptr, b_dev, x_dev, *cfg, hist, (cudaStream_t)stream);
+  });
+}
+
+
+int gnpc_sampler_create(gnpc_csr a, int64_t m, uint64_t seed, gnpc_sampler* out) {
+  return guarded([&] {
+    need(a && out, "sampler_create: null argument");
+    *out = build_sampler(*a, m, seed).release();
+  });
+}
+
+int gnpc_sampler_from_arnoldi(int64_t n, int64_t k, const double* v, const double* hbar,
+                              gnpc_sampler* out) {
+  return guarded([&] {
+    need(v && hbar && out, "sampler_from_arnoldi: null argument");
+    if (n < 2) throw std::invalid_argument("spectral sampler: n must be >= 2");
+    if (k < 1) throw std::invalid_argument("spectral sampler: m must be >= 1");
+    auto s = std::make_unique<gnpc_sampler_s>();
+    s->s = gnp_b200::spectral_from_arnoldi(n, k, std::vector<double>(v, v + n * k),
+                                           std::vector<double>(hbar, hbar + (k + 1) * k));
+    *out = s.release();
+  });
+}
+
+int gnpc_sampler_destroy(gnpc_sampler s) {
+  delete s;
+  return GNPC_OK;
+}
+
+int gnpc_sampler_info(gnpc_sampler s, int64_t* k, int64_t* m_eff) {
+  return guarded([&] {
+    need(s != nullptr, "sampler_info: null sampler");
+    if (k) *k = s->s.m;
+    if (m_eff) *m_eff = s->s.m_eff;
+  });
+}
+
+int gnpc_sampler_export(gnpc_sampler s, double* v, double* zsv, double* sv) {
+  return guarded([&] {
+    need(s != nullptr, "sampler_export: null sampler");
+    if (v) std::copy(s->s.v.begin(), s->s.v.end(), v);
+    if (zsv) std::copy(s->s.zm_sv.begin(), s->s.zm_sv.end(), zsv);
+    if (sv) std::copy(s->s.s.begin(), s->s.s.end(), sv);
+  });
+}
+
+int gnpc_assemble_batch(gnpc_sampler s, gnpc_csr a, uint64_t seed, int64_t skip_batches,
+                        int64_t batch, int64_t spectral_count, double* x, double* b) {
+  return guarded([&] {
+    need(a && x && b, "assemble_batch: null argument");
+    need(skip_batches >= 0, "assemble_batch: skip_batches must be >= 0");
+    if (spectral_count < 0) throw std::invalid_argument("assemble_batch: spectral_count < 0");
+    gnp_b200::Rng rng(seed);
+    const gnp_b200::SpectralSampler* sp = s ? &s->s : nullptr;
+    for (int64_t q = 0; q < skip_batches; ++q)
+      gnp_b200::assemble_batch(sp, a->h, batch, spectral_count, rng, x, b);
+    gnp_b200::assemble_batch(sp, a->h, batch, spectral_count, rng, x, b);
   });
 }
 

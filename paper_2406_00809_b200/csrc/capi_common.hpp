@@ -165,3 +165,12 @@ struct gnpc_csr_s {
                   const std::vector<float>& hv);
   gnpk::DevCsr dev();
 };
+
+// build_spectral_sampler (src/sampler.cpp:10-39): Arnoldi on the device,
+// Jacobi SVD of the small Hessenberg on the host.
+struct gnpc_sampler_s {
+  gnp_b200::SpectralSampler s;
+};
+namespace gnpc_impl {
+std::unique_ptr<gnpc_sampler_s> build_sampler(gnpc_csr_s& a, std::int64_t m, std::uint64_t seed);
+}

@@ -584,4 +584,131 @@ void checkpoint_parse(const std::string& bytes, Dims* dims, std::vector<double>*
   *meta = mm;
 }
 
+// ---------------------------------------------------------------- spectral sampler
+SvdResult jacobi_svd(std::int64_t rows, std::int64_t cols, const std::vector<double>& a) {
+  if (rows < cols) throw std::invalid_argument("jacobi_svd: matrix must be tall");
+  if (static_cast<std::int64_t>(a.size()) != rows * cols)
+    throw std::invalid_argument("jacobi_svd: size mismatch");
+  std::vector<double> b = a, v(cols * cols, 0.0);
+  for (std::int64_t i = 0; i < cols; ++i) v[i * cols + i] = 1.0;
+  auto B = [&](std::int64_t r, std::int64_t c) -> double& { return b[c * rows + r]; };
+  auto Vm = [&](std::int64_t r, std::int64_t c) -> double& { return v[c * cols + r]; };
+  // cyclic sweeps over column pairs, rotation zeroing the (p, q) inner product
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    bool rotated = false;
+    for (std::int64_t p = 0; p + 1 < cols; ++p) {
+      for (std::int64_t q = p + 1; q < cols; ++q) {
+        double app = 0.0, aqq = 0.0, apq = 0.0;
+        for (std::int64_t r = 0; r < rows; ++r) {
+          app += B(r, p) * B(r, p);
+          aqq += B(r, q) * B(r, q);
+          apq += B(r, p) * B(r, q);
+        }
+        if (std::abs(apq) <= 1e-15 * std::sqrt(app * aqq)) continue;
+        rotated = true;
+        const double zeta = (aqq - app) / (2.0 * apq);
+        const double t =
+            (zeta >= 0.0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / std::sqrt(1.0 + t * t), sn = cs * t;
+        for (std::int64_t r = 0; r < rows; ++r) {
+          const double t1 = B(r, p), t2 = B(r, q);
+          B(r, p) = cs * t1 - sn * t2;
+          B(r, q) = sn * t1 + cs * t2;
+        }
+        for (std::int64_t r = 0; r < cols; ++r) {
+          const double t1 = Vm(r, p), t2 = Vm(r, q);
+          Vm(r, p) = cs * t1 - sn * t2;
+          Vm(r, q) = sn * t1 + cs * t2;
+        }
+      }
+    }
+    if (!rotated) break;
+  }
+  std::vector<double> sv(cols);
+  for (std::int64_t j = 0; j < cols; ++j) {
+    double nrm = 0.0;
+    for (std::int64_t r = 0; r < rows; ++r) nrm += B(r, j) * B(r, j);
+    sv[j] = std::sqrt(nrm);
+  }
+  std::vector<std::int64_t> order(cols);
+  std::iota(order.begin(), order.end(), std::int64_t{0});
+  std::sort(order.begin(), order.end(),
+            [&sv](std::int64_t i, std::int64_t j) { return sv[i] > sv[j]; });
+  SvdResult out;
+  out.rows = rows;
+  out.cols = cols;
+  out.u.assign(rows * cols, 0.0);
+  out.v.assign(cols * cols, 0.0);
+  out.s.resize(cols);
+  for (std::int64_t j = 0; j < cols; ++j) {
+    const std::int64_t src = order[j];
+    out.s[j] = sv[src];
+    if (sv[src] > 0.0)
+      for (std::int64_t r = 0; r < rows; ++r) out.u[j * rows + r] = B(r, src) / sv[src];
+    for (std::int64_t r = 0; r < cols; ++r) out.v[j * cols + r] = Vm(r, src);
+  }
+  return out;
+}
+
+SpectralSampler spectral_from_arnoldi(std::int64_t n, std::int64_t k, std::vector<double> v,
+                                      const std::vector<double>& hbar) {
+  SvdResult svd = jacobi_svd(k + 1, k, hbar);
+  SpectralSampler out;
+  out.n = n;
+  out.m = k;
+  out.v = std::move(v);
+  out.v.resize(n * k);
+  out.zm_sv = std::move(svd.v);
+  out.s = std::move(svd.s);
+  const double floor = out.s.empty() ? 0.0 : out.s[0] * 1e-12;
+  for (double sv : out.s)
+    if (sv >= floor && sv > 0.0) ++out.m_eff;
+  if (out.m_eff == 0) throw std::runtime_error("spectral sampler: Hessenberg is numerically zero");
+  return out;
+}
+
+void sample_spectral_pair(const SpectralSampler& sp, const CsrHost& a, Rng& rng, double* x,
+                          double* b) {
+  std::vector<double> coef(sp.m, 0.0);
+  for (std::int64_t j = 0; j < sp.m_eff; ++j) {
+    const double scaled = rng.gaussian() / sp.s[j];
+    for (std::int64_t i = 0; i < sp.m; ++i) coef[i] += sp.zm_sv[j * sp.m + i] * scaled;
+  }
+  std::fill(x, x + a.n, 0.0);
+  for (std::int64_t j = 0; j < sp.m; ++j) {
+    const double cj = coef[j];
+    const double* vj = sp.v.data() + j * a.n;
+    for (std::int64_t i = 0; i < a.n; ++i) x[i] += vj[i] * cj;
+  }
+  for (std::int64_t i = 0; i < a.n; ++i) {
+    double s = 0.0;
+    for (std::int64_t q = a.row_ptr[i]; q < a.row_ptr[i + 1]; ++q) s += a.values[q] * x[a.col_idx[q]];
+    b[i] = s;
+  }
+}
+
+void assemble_batch(const SpectralSampler* sp, const CsrHost& a, std::int64_t batch,
+                    std::int64_t spectral_count, Rng& rng, double* x, double* b) {
+  if (batch <= 0) throw std::invalid_argument("assemble_batch: empty batch");
+  if (spectral_count > batch) throw std::invalid_argument("assemble_batch: spectral_count > batch");
+  if (spectral_count > 0 && (!sp || sp->n != a.n))
+    throw std::invalid_argument("assemble_batch: spectral columns need a sampler of this matrix");
+  const std::int64_t n = a.n;
+  for (std::int64_t k = 0; k < batch; ++k) {
+    double* xk = x + k * n;
+    double* bk = b + k * n;
+    if (k < spectral_count) {
+      sample_spectral_pair(*sp, a, rng, xk, bk);
+      continue;
+    }
+    for (std::int64_t i = 0; i < n; ++i) xk[i] = rng.gaussian();
+    for (std::int64_t i = 0; i < n; ++i) {
+      double s = 0.0;
+      for (std::int64_t q = a.row_ptr[i]; q < a.row_ptr[i + 1]; ++q)
+        s += a.values[q] * xk[a.col_idx[q]];
+      bk[i] = s;
+    }
+  }
+}
+
 }  // namespace gnp_b200

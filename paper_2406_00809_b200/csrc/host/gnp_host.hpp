@@ -97,6 +97,35 @@ CsrHost gen_anisotropic_9pt(std::int64_t grid, double eps, double theta_deg);
 CsrHost parse_matrix_market(const std::string& text);  // src/mmio.cpp:21-87
 CsrHost read_matrix_market_file(const std::string& path);
 
+// ---------------------------------------------------------------- spectral sampler
+// One-sided Jacobi SVD of a tall col-major rows x cols matrix (src/svd.cpp:10-80):
+// u rows x cols, s descending, v cols x cols, all col-major.
+struct SvdResult {
+  std::int64_t rows = 0, cols = 0;
+  std::vector<double> u, s, v;
+};
+SvdResult jacobi_svd(std::int64_t rows, std::int64_t cols, const std::vector<double>& a);
+
+// SpectralSampler (include/gnp/sampler.hpp:13-22) minus the factors sampling
+// never reads (vfull, wm).  The Arnoldi cycle that feeds it runs on the device
+// (gnpc_sampler_create); this is the host half.
+struct SpectralSampler {
+  std::int64_t n = 0, m = 0, m_eff = 0;
+  std::vector<double> v;      // n x m col-major, the first m Arnoldi basis vectors
+  std::vector<double> zm_sv;  // m x m col-major, right singular vectors of Hbar
+  std::vector<double> s;      // m singular values, descending
+};
+// src/sampler.cpp:19-38 given the cycle's k steps: v n x k, hbar (k+1) x k (col-major).
+SpectralSampler spectral_from_arnoldi(std::int64_t n, std::int64_t k, std::vector<double> v,
+                                      const std::vector<double>& hbar);
+// src/sampler.cpp:41-59: coef = Zsv[:, :m_eff] diag(1/s) eps, x = V coef, b = A x.
+void sample_spectral_pair(const SpectralSampler& sp, const CsrHost& a, Rng& rng, double* x,
+                          double* b);
+// src/sampler.cpp:68-83: columns k < spectral_count spectral, the rest Gaussian;
+// x, b n x batch col-major.  sp may be null when spectral_count == 0.
+void assemble_batch(const SpectralSampler* sp, const CsrHost& a, std::int64_t batch,
+                    std::int64_t spectral_count, Rng& rng, double* x, double* b);
+
 // ---------------------------------------------------------------- params
 struct Dims {
   std::int64_t d = 16, hidden = 32, layers = 8;

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -788,21 +789,21 @@ int gnpc_trainer_sync_model(gnpc_trainer t) {
   });
 }
 
-// train_preconditioner (src/gnn.cpp:401-451), Gaussian pairs drawn with the
-// reference Rng streams (seed+2 monitor, seed+3 training) on the host and
-// b = A x formed with the reference's f64 spmv, so the sampled data are
-// bit-identical to the reference's.
+// train_preconditioner (src/gnn.cpp:401-451).  Pairs are drawn with the
+// reference Rng streams (seed+1 sampler, seed+2 monitor, seed+3 training) and
+// assemble_batch semantics (src/sampler.cpp:68-83) on the host, b = A x with
+// the f64 matrix, so for a given sampler basis the batches are bit-identical
+// to the reference's.  The sampler's Arnoldi cycle runs on the device
+// (gnpc_sampler_create).  The next batch is drawn on a host thread while the
+// device runs the current step.
 int gnpc_train_preconditioner(gnpc_csr a, const gnpc_train_config* cfg, double* best,
                               double* losses, double* best_loss) {
   return guarded([&] {
     need(a && cfg && best && losses && best_loss, "train_preconditioner: null argument");
     if (cfg->batch < cfg->spectral_count)
       throw std::invalid_argument("train: batch must be >= spectral_count");
-    if (cfg->spectral_count != 0)
-      throw Unsupported("train_preconditioner: spectral training pairs are not in this build "
-                        "(spectral_count must be 0)");
-    if (cfg->arnoldi_m < 1) throw std::invalid_argument("spectral sampler: m must be >= 1");
-    if (a->h.n < 2) throw std::invalid_argument("spectral sampler: n must be >= 2");
+    if (cfg->batch < 1) throw std::invalid_argument("assemble_batch: empty batch");
+    if (cfg->monitor_batch < 1) throw std::invalid_argument("assemble_batch: empty batch");
     const gnp_b200::Dims dims{cfg->d, cfg->hidden, cfg->layers};
     std::vector<double> p0 = gnp_b200::init_params(dims, cfg->seed);
     gnpc_model mm = nullptr;
@@ -811,21 +812,16 @@ int gnpc_train_preconditioner(gnpc_csr a, const gnpc_train_config* cfg, double* 
     std::unique_ptr<gnpc_model_s, void (*)(gnpc_model_s*)> model(mm, [](gnpc_model_s* q) {
       gnpc_model_destroy(q);
     });
+    // built whether or not spectral pairs are drawn, like the reference
+    // (its errors surface for spectral_count == 0 too)
+    const std::unique_ptr<gnpc_sampler_s> sampler =
+        build_sampler(*a, cfg->arnoldi_m, cfg->seed + 1);
+    const gnp_b200::SpectralSampler* sp = &sampler->s;
     const std::int64_t n = a->h.n, B = cfg->batch, MB = cfg->monitor_batch;
-    auto batch_from = [&](gnp_b200::Rng& rng, std::int64_t cols, std::vector<double>& x,
-                          std::vector<double>& b) {
-      x.resize(n * cols);
-      b.resize(n * cols);
-      for (std::int64_t k = 0; k < cols; ++k) {
-        std::vector<double> xk = rng.gaussian_vector(n);
-        std::vector<double> bk = gnp_b200::spmv(a->h, xk);
-        std::copy(xk.begin(), xk.end(), x.begin() + k * n);
-        std::copy(bk.begin(), bk.end(), b.begin() + k * n);
-      }
-    };
-    std::vector<double> mx, mb, x, b;
+    std::vector<double> mx(n * MB), mb(n * MB);
     gnp_b200::Rng monitor_rng(cfg->seed + 2);
-    batch_from(monitor_rng, MB, mx, mb);
+    gnp_b200::assemble_batch(sp, a->h, MB, std::min(cfg->spectral_count, MB), monitor_rng,
+                             mx.data(), mb.data());
     gnp_b200::Rng train_rng(cfg->seed + 3);
     std::unique_ptr<gnpc_trainer_s> tr(create(model.get(), B, cfg->lr));
     std::unique_ptr<gnpc_trainer_s> mon(MB == B ? nullptr : create(model.get(), MB, cfg->lr));
@@ -840,8 +836,17 @@ int gnpc_train_preconditioner(gnpc_csr a, const gnpc_train_config* cfg, double* 
     std::vector<double> bestp = p0;
     double bl = monitoring();
     losses[0] = bl;
+    std::vector<double> x(n * B), b(n * B), xn(n * B), bn(n * B);
+    auto draw = [&](std::vector<double>& xx, std::vector<double>& bb) {
+      gnp_b200::assemble_batch(sp, a->h, B, cfg->spectral_count, train_rng, xx.data(), bb.data());
+    };
+    std::future<void> next;
+    if (cfg->steps > 0) next = std::async(std::launch::async, draw, std::ref(xn), std::ref(bn));
     for (std::int64_t step = 0; step < cfg->steps; ++step) {
-      batch_from(train_rng, B, x, b);
+      next.get();  // rethrows a sampling error
+      x.swap(xn);
+      b.swap(bn);
+      if (step + 1 < cfg->steps) next = std::async(std::launch::async, draw, std::ref(xn), std::ref(bn));
       step_fb(*tr, x.data(), b.data(), true);
       adam(*tr);
       const double ml = monitoring();

@@ -4,7 +4,7 @@ Runs only in the build container (needs oracle/_ref/libgnpref.so, built by
 `make -C oracle ref` from /root/reference).  The fixtures are committed so the
 CPU pin tests and the GPU parity tests never touch /root/reference.
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [--only spectral]
 """
 from __future__ import annotations
 
@@ -30,8 +30,30 @@ def csr_dict(prefix, a):
             f"{prefix}_col_idx": a.col_idx, f"{prefix}_values": a.values}
 
 
+def spectral(R):
+    """Spectral sampler + spectral-pair batch (src/sampler.cpp) on a 16x16
+    convection-diffusion matrix, and a short spectral training run."""
+    a = R.gen_convection_diffusion(16, 0.5)
+    gam = R.gershgorin_gamma(a)
+    ah = R.prescale(a, gam)
+    s = R.spectral_sampler(ah, 20, 7)
+    x, b = R.assemble_batch(ah, 20, 7, 9, 1, 8, 4)
+    np.savez_compressed(os.path.join(HERE, "spectral.npz"), gamma=gam, m=20, seed=7, k=s["k"],
+                        m_eff=s["m_eff"], s=s["s"], batch_seed=9, batch=8, spectral=4, x=x, b=b)
+    c6 = R.gen_convection_diffusion(6, 0.5)
+    c6h = R.prescale(c6, R.gershgorin_gamma(c6))
+    best, losses, bl = R.train(c6h, (4, 8, 2), steps=20, batch=8, spectral=4, arnoldi_m=10, seed=41,
+                               monitor_batch=8)
+    np.savez_compressed(os.path.join(HERE, "train_run_spectral.npz"), best=best, losses=losses,
+                        best_loss=bl)
+
+
 def main():
     R = O.reference()
+    if "--only" in sys.argv:
+        assert sys.argv[sys.argv.index("--only") + 1] == "spectral"
+        spectral(R)
+        return
     out = {}
 
     # 1. the reference's only real-matrix fixture, parsed by the reference
@@ -132,6 +154,7 @@ def main():
     l3, g3 = R.batch_loss_grads(c3h, (32, 32, 8), p3, x3, b3, 8)
     np.savez_compressed(os.path.join(HERE, "c3_small_train_step.npz"), **csr_dict("a", c3h), params=p3,
                         x=x3, b=b3, loss=l3, grads=g3)
+    spectral(R)
     print("golden fixtures written to", HERE)
 
 

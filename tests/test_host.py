@@ -152,3 +152,46 @@ def test_iter_time_auc(gnp):
     # tests/python/test_smoke.py metrics values
     assert gnp.iter_auc([(0, 1.0, 0.0), (1, 1e-4, 0.1), (2, 1e-8, 0.2)], rtol=1e-8) == 12.0
     assert gnp.time_auc([(0, 1.0, 0.0), (1, 1e-4, 1.0)], rtol=1e-8) == 4.0
+
+
+# ------------------------------------------------------------------ spectral sampler (host half)
+def _prod_csr(capi, a):
+    return capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
+
+
+def test_sampler_host_half_bitwise(capi, oc):
+    # the oracle's Arnoldi cycle fed to the product's SVD / rank / sampling
+    # (src/sampler.cpp:19-83, src/svd.cpp): bit-identical to the oracle
+    a = oc.prescale(oc.gen_convection_diffusion(12, 0.4), 8.0)
+    m = 15
+    v, h, k, _ = oc.arnoldi_cycle(a, oc.gaussian_vector(4, a.n), m)
+    hk = h.reshape(m, m + 1)[:k, : k + 1].copy()  # (k+1) x k col-major
+    A = _prod_csr(capi, a)
+    s = capi.Sampler.from_arnoldi(A, v, hk.ravel(), k)
+    want = oc.spectral_sampler(a, m, 4)
+    pv, pz, ps = s.factors()
+    assert (s.k, s.m_eff) == (want["k"], want["m_eff"])
+    assert np.array_equal(ps, want["s"]) and np.array_equal(pz, want["zsv"])
+    assert np.array_equal(pv, want["v"])
+    for skip, batch, spec in [(0, 8, 4), (2, 5, 5), (1, 3, 0)]:
+        x1, b1 = capi.assemble_batch(A, s, 77, skip, batch, spec)
+        x2, b2 = oc.assemble_batch(a, want, 77, skip, batch, spec)
+        assert np.array_equal(x1, x2) and np.array_equal(b1, b2)
+
+
+def test_sampler_host_errors(capi, oc):
+    a = oc.prescale(oc.gen_convection_diffusion(4, 0.0), 8.0)
+    A = _prod_csr(capi, a)
+    with pytest.raises(capi.GnpcError, match="EINVAL"):
+        capi.assemble_batch(A, None, 0, 0, 0, 0)  # empty batch
+    with pytest.raises(capi.GnpcError, match="EINVAL"):
+        capi.assemble_batch(A, None, 0, 0, 2, 3)  # spectral_count > batch
+    with pytest.raises(capi.GnpcError, match="EINVAL"):
+        capi.assemble_batch(A, None, 0, 0, 4, 2)  # spectral columns without a sampler
+    # a numerically zero Hessenberg (src/sampler.cpp:35-36)
+    with pytest.raises(capi.GnpcError, match="ERUNTIME"):
+        capi.Sampler.from_arnoldi(A, np.zeros(a.n * 2), np.zeros(6), 2)
+    # Gaussian-only batches match the oracle's reference stream
+    x1, b1 = capi.assemble_batch(A, None, 9, 1, 3, 0)
+    x2, b2 = oc.gaussian_batch(a, 9, 1, 3)
+    assert np.array_equal(x1, x2) and np.array_equal(b1, b2)

@@ -252,3 +252,83 @@ def _triplets(a):
     rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
     perm = np.random.default_rng(0).permutation(a.nnz)  # shuffled input order
     return rows[perm], a.col_idx[perm], a.values[perm]
+
+
+# ------------------------------------------------------------------ spectral sampler
+# src/sampler.cpp:10-83, src/svd.cpp:10-80; known-answer tests restate
+# tests/test_sampler.cpp:47-226.
+def _csr_diag(vals):
+    n = len(vals)
+    return Csr(n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int64), np.array(vals, np.float64))
+
+
+def _in_range(vk, k, x):
+    n = x.size
+    V = vk[: n * k].reshape(k, n).T
+    r = x - V @ (V.T @ x)
+    return np.linalg.norm(r) <= 1e-10 * np.linalg.norm(x)
+
+
+def test_sampler_identity_breaks_down_at_step_one(oc):
+    s = oc.spectral_sampler(_csr_diag([1.0] * 4), 3, 0)  # test_sampler.cpp:69-75
+    assert s["k"] == 1 and s["m_eff"] == 1
+    assert abs(s["s"][0] - 1.0) <= 1e-12
+
+
+def test_jacobi_svd_eigen_oracle(oc):
+    # test_sampler.cpp:47-67: (HᵀH - s²I) v = 0 for the right singular vectors
+    a = _csr_diag([1.0, 2.0, 3.0])
+    v, h, k, _ = oc.arnoldi_cycle(a, oc.gaussian_vector(9, 3), 3)
+    H = h.reshape(3, 4).T  # (m+1) x m col-major
+    u, s, zv = oc.jacobi_svd(H.T.ravel(), 4, 3)
+    Z = zv.reshape(3, 3).T
+    hth = H.T @ H
+    for q in range(3):
+        lam = s[q] ** 2
+        assert np.max(np.abs(hth @ Z[:, q] - lam * Z[:, q])) <= 1e-10 * (1 + lam)
+    assert list(s) == sorted(s, reverse=True)
+
+
+def test_sampler_matches_reference_bitwise(oc, ref):
+    a = ref.gen_random_nonsymmetric(50, 6, 1.3, 13)  # test_sampler.cpp:77-110
+    s1, s2 = oc.spectral_sampler(a, 40, 21), ref.spectral_sampler(a, 40, 21)
+    assert (s1["k"], s1["m_eff"]) == (s2["k"], s2["m_eff"]) == (40, s2["m_eff"])
+    for key in ("v", "zsv", "s"):
+        assert np.array_equal(s1[key], s2[key]), key
+    V = s1["v"].reshape(40, 50).T
+    assert np.max(np.abs(V.T @ V - np.eye(40))) <= 1e-10
+    Z = s1["zsv"].reshape(40, 40).T
+    assert np.max(np.abs(Z.T @ Z - np.eye(40))) <= 1e-10
+    # the SVD of a random tall matrix, bitwise
+    g = np.random.default_rng(3).standard_normal((9, 7))
+    r1, r2 = oc.jacobi_svd(g.T.ravel(), 9, 7), ref.jacobi_svd(g.T.ravel(), 9, 7)
+    assert all(np.array_equal(p, q) for p, q in zip(r1, r2))
+
+
+@pytest.mark.parametrize("skip", [0, 2])
+def test_assemble_batch_matches_reference(oc, ref, skip):
+    a = ref.gen_random_nonsymmetric(20, 4, 1.5, 2)  # test_sampler.cpp:182-216
+    s = oc.spectral_sampler(a, 8, 1)
+    x1, b1 = oc.assemble_batch(a, s, 42, skip, 16, 8)
+    x2, b2 = ref.assemble_batch(a, 8, 1, 42, skip, 16, 8)
+    assert np.array_equal(x1, x2) and np.array_equal(b1, b2)
+    for k in range(16):
+        assert np.array_equal(b1[k * 20:(k + 1) * 20], oc.spmv(a, x1[k * 20:(k + 1) * 20]))
+    assert all(_in_range(s["v"], s["k"], x1[k * 20:(k + 1) * 20]) for k in range(8))
+    assert not _in_range(s["v"], s["k"], x1[15 * 20:16 * 20])
+    with pytest.raises(Exception):
+        oc.assemble_batch(a, s, 42, 0, 0, 0)
+    with pytest.raises(Exception):
+        oc.assemble_batch(a, s, 42, 0, 2, 3)
+    # spectral_count = 0 is the Gaussian batch
+    assert np.array_equal(oc.assemble_batch(a, s, 5, 1, 3, 0)[0], oc.gaussian_batch(a, 5, 1, 3)[0])
+
+
+def test_spectral_golden(oc):
+    g = golden("spectral.npz")
+    a = oc.prescale(oc.gen_convection_diffusion(16, 0.5), float(g["gamma"]))
+    s = oc.spectral_sampler(a, int(g["m"]), int(g["seed"]))
+    assert (s["k"], s["m_eff"]) == (int(g["k"]), int(g["m_eff"]))
+    assert np.array_equal(s["s"], g["s"])
+    x, b = oc.assemble_batch(a, s, int(g["batch_seed"]), 1, int(g["batch"]), int(g["spectral"]))
+    assert np.array_equal(x, g["x"]) and np.array_equal(b, g["b"])

@@ -9,6 +9,7 @@
 #pragma once
 
 #include "apply.cuh"
+#include "tc.cuh"
 
 namespace gnpk {
 
@@ -712,6 +713,313 @@ k_spmm_nb(DevCsr a, int B, const double* __restrict__ x, double* __restrict__ y)
         s = fma(static_cast<double>(a.v[q]), x[static_cast<size_t>(a.ci[q]) * B + k], s);
       y[static_cast<size_t>(i) * B + k] = s;
     }
+}
+
+
+// ------------------------------------------------------------------ piecewise encoder
+// The lift v -> enc2ᵀ relu(v enc1 + b1) + b2 has a scalar input, so it is an
+// exact piecewise-linear map (the apply path's k_lift_pw; tables there are
+// built on the host).  Training regenerates the tables on the device after
+// every Adam step (k_lift_tables), runs the forward as one FMA per output
+// (k_lift_pw_batched), and reduces the whole encoder backward
+// (src/gnn.cpp:283-305) to per-interval sums of the layer-1 gradient rows:
+//   S1[p] = Σ_{v in p} g_v,  Sx[p] = Σ_{v in p} vv_v g_v
+//   enc2(h, j)   = Σ_p act(h, p) (enc1_h Sx[p][j] + b1_h S1[p][j])
+//   enc2_b(j)    = Σ_p S1[p][j]
+//   enc1(h)      = Σ_p act(h, p) Σ_j enc2(h, j) Sx[p][j]
+//   enc1_b(h)    = Σ_p act(h, p) Σ_j enc2(h, j) S1[p][j]
+// where act(h, p) = [unit h active on interval p].  No x0 / g_x0 cache.
+struct LiftTab {
+  float* t;                 // [H] sorted distinct kinks (nb used)
+  float* a;                 // [H+1][DP]
+  float* b;                 // [H+1][DP]
+  unsigned long long* act;  // [H+1] bit h: unit h active on the interval
+  int* nb;
+};
+struct EncOff {
+  int enc1, enc1_b, enc2, enc2_b, H, d;
+};
+
+// One block: kinks t_h = -b1_h/enc1_h (enc1_h != 0), sorted and distinct,
+// then per interval the active set at an interior point and the affine
+// coefficients, all from the f64 master parameters (the host build in
+// gnpc_model_s::build_view does the same).
+__global__ void k_lift_tables(const double* __restrict__ p, EncOff o, int DP, LiftTab tab) {
+  __shared__ double kinks[64], vr[65], e1[64], b1[64];
+  __shared__ int nbs;
+  extern __shared__ double e2[];  // [H][d]: enc2(h, j) at h * d + j
+  for (int h = threadIdx.x; h < o.H; h += blockDim.x) {
+    e1[h] = p[o.enc1 + h];
+    b1[h] = p[o.enc1_b + h];
+  }
+  for (int t = threadIdx.x; t < o.H * o.d; t += blockDim.x) {
+    const int h = t / o.d, j = t % o.d;
+    e2[t] = p[o.enc2 + j * o.H + h];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int nb = 0;
+    for (int h = 0; h < o.H; ++h) {
+      if (e1[h] == 0.0) continue;
+      const double t = -b1[h] / e1[h];
+      bool dup = false;
+      for (int q = 0; q < nb; ++q) dup = dup || kinks[q] == t;
+      if (dup) continue;
+      int k = nb++;
+      while (k > 0 && kinks[k - 1] > t) {
+        kinks[k] = kinks[k - 1];
+        --k;
+      }
+      kinks[k] = t;
+    }
+    for (int k = 0; k <= nb; ++k) {
+      if (nb == 0) vr[k] = 0.0;
+      else if (k == 0) vr[k] = kinks[0] - 1.0 - fabs(kinks[0]);
+      else if (k == nb) vr[k] = kinks[nb - 1] + 1.0 + fabs(kinks[nb - 1]);
+      else vr[k] = 0.5 * (kinks[k - 1] + kinks[k]);
+    }
+    nbs = nb;
+    *tab.nb = nb;
+  }
+  __syncthreads();
+  const int nb = nbs;
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) tab.t[k] = static_cast<float>(kinks[k]);
+  for (int idx = threadIdx.x; idx < (nb + 1) * DP; idx += blockDim.x) {
+    const int k = idx / DP, j = idx % DP;
+    double a_ = 0.0, b_ = 0.0;
+    unsigned long long m = 0ull;
+    for (int h = 0; h < o.H; ++h) {
+      if (!(e1[h] * vr[k] + b1[h] > 0.0)) continue;
+      m |= 1ull << h;
+      if (j < o.d) {
+        a_ += e1[h] * e2[h * o.d + j];
+        b_ += b1[h] * e2[h * o.d + j];
+      }
+    }
+    if (j < o.d) b_ += p[o.enc2_b + j];
+    if (j == 0) tab.act[k] = m;
+    tab.a[idx] = static_cast<float>(a_);
+    tab.b[idx] = static_cast<float>(b_);
+  }
+}
+
+__device__ __forceinline__ int interval_of(const float* s_t, int nb, float v) {
+  int lo = 0, hi = nb;  // #kinks <= v
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (s_t[mid] <= v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// X0[v] = a[p] vv + b[p], vv = (float)(in_scale_k b[v]); also writes vv.
+template <int DP>
+__global__ void __launch_bounds__(kThreads)
+k_lift_pw_batched(const double* __restrict__ b, int nv, int B, LiftTab tab, int H,
+                  const SampleScales* __restrict__ sc, float* __restrict__ X0,
+                  float* __restrict__ vv_out) {
+  constexpr int G = DP / 4, NG = kThreads / G;
+  extern __shared__ float4 sm4[];
+  const int nb = *tab.nb;
+  float* s_a = reinterpret_cast<float*>(sm4);  // [nb+1][DP]
+  float* s_b = s_a + (H + 1) * DP;
+  float* s_t = s_b + (H + 1) * DP;
+  for (int t = threadIdx.x; t < (nb + 1) * DP; t += kThreads) {
+    s_a[t] = tab.a[t];
+    s_b[t] = tab.b[t];
+  }
+  for (int t = threadIdx.x; t < nb; t += kThreads) s_t[t] = tab.t[t];
+  __syncthreads();
+  const int gl = threadIdx.x % G;
+  for (int v = blockIdx.x * NG + threadIdx.x / G; v < nv; v += gridDim.x * NG) {
+    const int k = v % B;
+    const float x = static_cast<float>(sc[k].in_scale * b[v]);
+    if (gl == 0) vv_out[v] = x;
+    const int q = interval_of(s_t, nb, x);
+    const float4 al = *reinterpret_cast<const float4*>(s_a + q * DP + 4 * gl);
+    const float4 be = *reinterpret_cast<const float4*>(s_b + q * DP + 4 * gl);
+    st4(X0 + static_cast<size_t>(v) * DP + 4 * gl,
+        make_float4(fmaf(al.x, x, be.x), fmaf(al.y, x, be.y), fmaf(al.z, x, be.z), fmaf(al.w, x, be.w)));
+  }
+}
+
+// Per-interval sums of the layer-1 gradient rows.  Block blk owns rows
+// [blk*rpb, (blk+1)*rpb) (rpb a multiple of kEncStg), staged kEncStg rows at
+// a time by 1-D bulk copies into a kEncNS-deep ring.  A sub-group of
+// GL = min(DP, 32) lanes takes one row (CPL columns per lane); each
+// sub-group owns two fp32 accumulator sets [H+1][2][DP] (even / odd rows, so
+// consecutive read-modify-writes of a lane never chain through the same set
+// and no two lanes ever touch the same word).  The sets fold into the
+// block's f64 sums in a fixed order after every kEncCh rows per set:
+// deterministic for a fixed grid.  Output: partials[blk][(H+1)*2*DP].
+constexpr int kEncCh = 128, kEncStg = 128, kEncNS = 3;
+// set stride padded by GL floats when a warp holds several sub-groups, so
+// the sub-groups land on different banks
+inline size_t enc_bucket_smem(int DP, int H, int warps) {
+  const int gl = DP < 32 ? DP : 32;
+  const size_t sets = static_cast<size_t>(warps) * (32 / gl) * 2;
+  const size_t per = static_cast<size_t>(H + 1) * 2 * DP;
+  return static_cast<size_t>(kEncNS) * kEncStg * (DP + 1) * 4 + per * 8 +
+         sets * (per + (gl < 32 ? gl : 0)) * 4 + 64 * 4 + 64;
+}
+template <int DP>
+__global__ void k_enc_buckets(const float* __restrict__ g, const float* __restrict__ vv, int nv,
+                              int rpb, LiftTab tab, int H, double* __restrict__ partials) {
+  constexpr int GL = DP < 32 ? DP : 32, CPL = DP / GL, R = 32 / GL;
+  extern __shared__ float4 sm4[];
+  const int per = (H + 1) * 2 * DP;
+  const int stride = per + (R > 1 ? GL : 0);
+  const int nsub = (blockDim.x >> 5) * R;                            // row slots per pass
+  float* sg = reinterpret_cast<float*>(sm4);                         // [NS][Stg][DP]
+  float* sx = sg + kEncNS * kEncStg * DP;                            // [NS][Stg]
+  double* blk = reinterpret_cast<double*>(sx + kEncNS * kEncStg);    // [per]
+  float* acc = reinterpret_cast<float*>(blk + per);                  // [2 nsub][stride]
+  float* s_t = acc + static_cast<size_t>(2 * nsub) * stride;         // [64]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_t + 64);             // [NS]
+  const int nb = *tab.nb;
+  const int tid = threadIdx.x;
+  for (int t = tid; t < per; t += blockDim.x) blk[t] = 0.0;
+  for (int t = tid; t < 2 * nsub * stride; t += blockDim.x) acc[t] = 0.f;
+  for (int t = tid; t < nb; t += blockDim.x) s_t[t] = tab.t[t];
+  const int r0 = blockIdx.x * rpb, r1 = min(nv, r0 + rpb);
+  const int nst = r1 > r0 ? (r1 - r0 + kEncStg - 1) / kEncStg : 0;
+  auto rows_of = [&](int st) { return min(kEncStg, r1 - (r0 + st * kEncStg)); };
+  auto issue = [&](int st) {  // thread 0: full stages only (16-byte aligned, r0 % kEncStg == 0)
+    if (st >= nst || rows_of(st) != kEncStg) return;
+    const int slot = st % kEncNS;
+    const size_t row = static_cast<size_t>(r0) + static_cast<size_t>(st) * kEncStg;
+    tc::mbar_expect_tx(&bar[slot], kEncStg * DP * 4 + kEncStg * 4);
+    tc::bulk_load(sg + slot * kEncStg * DP, g + row * DP, kEncStg * DP * 4, &bar[slot]);
+    tc::bulk_load(sx + slot * kEncStg, vv + row, kEncStg * 4, &bar[slot]);
+  };
+  if (tid == 0) {
+    for (int q = 0; q < kEncNS; ++q) tc::mbar_init(&bar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int q = 0; q < kEncNS; ++q) issue(q);
+  const int lane = tid & 31, warp = tid >> 5;
+  const int sub = warp * R + lane / GL, c0 = (lane % GL) * CPL;
+  float* my0 = acc + static_cast<size_t>(2 * sub) * stride;
+  float* my1 = my0 + stride;
+  const int flush_every = max(1, kEncCh * nsub / kEncStg);  // stages between folds
+  for (int st = 0; st < nst; ++st) {
+    const int slot = st % kEncNS, rows = rows_of(st);
+    const float* gs = sg + slot * kEncStg * DP;
+    const float* xs = sx + slot * kEncStg;
+    if (rows == kEncStg) {
+      tc::mbar_wait(&bar[slot], (st / kEncNS) & 1);
+    } else {  // the grid's ragged tail: plain loads
+      float* gw = sg + slot * kEncStg * DP;
+      float* xw = sx + slot * kEncStg;
+      const size_t row = static_cast<size_t>(r0) + static_cast<size_t>(st) * kEncStg;
+      for (int t = tid; t < rows * DP; t += blockDim.x) gw[t] = g[row * DP + t];
+      for (int t = tid; t < rows; t += blockDim.x) xw[t] = vv[row + t];
+      __syncthreads();
+    }
+    // warp w takes rows [w*rpw, (w+1)*rpw) of the stage; lane l finds row
+    // w*rpw + l's interval once, sub-groups then walk the rows R at a time
+    // with (x, interval) broadcast by shuffles, alternating their two sets
+    const int rpw = kEncStg / (blockDim.x >> 5);  // <= 32
+    const int wr0 = warp * rpw;
+    const float xl = lane < rpw && wr0 + lane < rows ? xs[wr0 + lane] : 0.f;
+    const int ql = interval_of(s_t, nb, xl) * 2 * DP;
+    const int sg_row = lane / GL;
+    // two rows per step, one per set: both read-modify-writes are issued
+    // side by side (different sets never alias)
+#pragma unroll 2
+    for (int i = 0; i < rpw; i += 2 * R) {
+      const int ra = i + sg_row, rb2 = i + R + sg_row;
+      const float xa = __shfl_sync(0xffffffffu, xl, ra);
+      const int qa = __shfl_sync(0xffffffffu, ql, ra) + c0;
+      const float xb = __shfl_sync(0xffffffffu, xl, rb2 & 31);
+      const int qb = __shfl_sync(0xffffffffu, ql, rb2 & 31) + c0;
+      const bool ona = wr0 + ra < rows && ra < rpw, onb = wr0 + rb2 < rows && rb2 < rpw;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const float ga = ona ? gs[(wr0 + ra) * DP + c0 + c] : 0.f;
+        const float gb = onb ? gs[(wr0 + rb2) * DP + c0 + c] : 0.f;
+        const float a1 = my0[qa + c], a2 = my0[qa + DP + c];
+        const float b1 = my1[qb + c], b2 = my1[qb + DP + c];
+        my0[qa + c] = a1 + ga;
+        my0[qa + DP + c] = fmaf(xa, ga, a2);
+        my1[qb + c] = b1 + gb;
+        my1[qb + DP + c] = fmaf(xb, gb, b2);
+      }
+    }
+    __syncthreads();  // the slot is free; the sets are quiescent
+    if (tid == 0) issue(st + kEncNS);
+    if ((st + 1) % flush_every == 0 || st + 1 == nst) {
+      for (int t = tid; t < per; t += blockDim.x) {
+        double s = blk[t];
+        for (int z = 0; z < 2 * nsub; ++z) {
+          s += static_cast<double>(acc[static_cast<size_t>(z) * stride + t]);
+          acc[static_cast<size_t>(z) * stride + t] = 0.f;
+        }
+        blk[t] = s;
+      }
+      __syncthreads();
+    }
+  }
+  for (int t = tid; t < per; t += blockDim.x)
+    partials[static_cast<size_t>(blockIdx.x) * per + t] = blk[t];
+}
+
+// Folds the block partials in a fixed order: S[t] = Σ_z partials[z][t].
+__global__ void k_enc_fold(const double* __restrict__ partials, int nblk, int per,
+                           double* __restrict__ S) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= per) return;
+  double s = 0.0;
+  int z = 0;
+  for (; z + 8 <= nblk; z += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = partials[static_cast<size_t>(z + u) * per + t];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; z < nblk; ++z) s += partials[static_cast<size_t>(z) * per + t];
+  S[t] = s;
+}
+
+// Encoder gradients from the folded sums into the flat f64 gradient
+// (reference slots via EncOff).
+__global__ void k_enc_grads(const double* __restrict__ Sg, int DP, LiftTab tab,
+                            const double* __restrict__ p, EncOff o, double* __restrict__ grad) {
+  extern __shared__ double S[];  // [(H+1)][2][DP]
+  const int H = o.H, per = (H + 1) * 2 * DP;
+  const int nb = *tab.nb;
+  for (int t = threadIdx.x; t < per; t += blockDim.x) S[t] = Sg[t];
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < H * o.d; idx += blockDim.x) {
+    const int h = idx % H, j = idx / H;
+    const double w = p[o.enc1 + h], bb = p[o.enc1_b + h];
+    double s = 0.0;
+    for (int q = 0; q <= nb; ++q)
+      if ((tab.act[q] >> h) & 1ull) s += w * S[q * 2 * DP + DP + j] + bb * S[q * 2 * DP + j];
+    grad[o.enc2 + j * H + h] = s;
+  }
+  for (int j = threadIdx.x; j < o.d; j += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q <= nb; ++q) s += S[q * 2 * DP + j];
+    grad[o.enc2_b + j] = s;
+  }
+  for (int h = threadIdx.x; h < H; h += blockDim.x) {
+    double gw = 0.0, gb = 0.0;
+    for (int q = 0; q <= nb; ++q) {
+      if (!((tab.act[q] >> h) & 1ull)) continue;
+      for (int j = 0; j < o.d; ++j) {
+        const double e = p[o.enc2 + j * H + h];
+        gw += e * S[q * 2 * DP + DP + j];
+        gb += e * S[q * 2 * DP + j];
+      }
+    }
+    grad[o.enc1 + h] = gw;
+    grad[o.enc1_b + h] = gb;
+  }
 }
 
 }  // namespace gnpk

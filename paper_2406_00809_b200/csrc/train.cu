@@ -78,6 +78,16 @@ struct gnpc_trainer_s {
   int tc_per_sm_fwd = 0, tc_per_sm_bwd = 0;
   int loss_grid = 0;
   std::int64_t nbytes_act = 0;
+  // piecewise-linear encoder (H <= 64): tables regenerated on device after
+  // every parameter update; backward by per-interval sums (k_enc_buckets)
+  bool pw = false;
+  DevBuf<float> lt, la, lb;
+  DevBuf<unsigned long long> lact;
+  DevBuf<int> lnb;
+  DevBuf<double> encpart;
+  gnpk::LiftTab tab{};
+  gnpk::EncOff eoff{};
+  int enc_grid = 0, enc_warps = 16, enc_rpb = 0;
 };
 
 namespace {
@@ -237,6 +247,12 @@ void regenerate(gnpc_trainer_s& T) {
     gnpk::k_gather_params<<<(c + kTh - 1) / kTh, kTh, 0, T.s>>>(T.p64.p, T.map_bt_bwd.p, c, T.BT_bwd.p);
     GNPC_LAUNCHED();
   }
+  if (T.pw) {
+    const size_t smem = (size_t)T.H * T.d * 8;
+    set_smem_once((const void*)gnpk::k_lift_tables, smem);
+    gnpk::k_lift_tables<<<1, 256, smem, T.s>>>(T.p64.p, T.eoff, T.dp, T.tab);
+    GNPC_LAUNCHED();
+  }
 }
 
 template <int DP>
@@ -308,7 +324,13 @@ struct TrainLaunch {
     GNPC_LAUNCHED();
     gnpk::k_col_norm_finish<<<(T.B + 63) / 64, 64, 0, T.s>>>(T.colpart.p, cg, T.n, T.B, T.scl.p);
     GNPC_LAUNCHED();
-    {
+    if (T.pw) {
+      const size_t smem = (size_t)(T.H + 1) * DP * 2 * 4 + 64 * 4;
+      const int g = grid_for(T.nv, kTh / (DP / 4), T.sms * 8);
+      gnpk::k_lift_pw_batched<DP><<<g, kTh, smem, T.s>>>(T.bb.p, T.nv, T.B, T.tab, T.H, T.scl.p, T.Xs.p,
+                                                          T.vv.p);
+      GNPC_LAUNCHED();
+    } else {
       const size_t smem = (size_t)T.H * DP * 4 + 2 * (size_t)T.H * 4;
       const int g = grid_for(T.nv, kTh / (DP / 4), T.sms * 8);
       gnpk::k_lift_batched<DP><<<g, kTh, smem, T.s>>>(T.bb.p, T.nv, T.B, net, T.scl.p, T.Xs.p, T.vv.p);
@@ -344,6 +366,23 @@ struct TrainLaunch {
       run_red(T, T.red_layer[l]);
       layer(T, false, l, T.G[cur].p, T.G[1 - cur].p, nullptr, l >= 1 ? T.Xs.p + l * act : nullptr, cur);
       cur = 1 - cur;
+    }
+    if (T.pw) {
+      const size_t smem = gnpk::enc_bucket_smem(DP, T.H, T.enc_warps);
+      set_smem_once((const void*)gnpk::k_enc_buckets<DP>, smem);
+      gnpk::k_enc_buckets<DP><<<T.enc_grid, 32 * T.enc_warps, smem, T.s>>>(T.G[cur].p, T.vv.p, T.nv,
+                                                                           T.enc_rpb, T.tab, T.H,
+                                                                           T.encpart.p);
+      GNPC_LAUNCHED();
+      const int per = (T.H + 1) * 2 * DP;
+      double* S = T.encpart.p + (size_t)T.enc_grid * per;
+      gnpk::k_enc_fold<<<(per + 63) / 64, 64, 0, T.s>>>(T.encpart.p, T.enc_grid, per, S);
+      GNPC_LAUNCHED();
+      const size_t fs = (size_t)per * 8;
+      set_smem_once((const void*)gnpk::k_enc_grads, fs);
+      gnpk::k_enc_grads<<<1, kTh, fs, T.s>>>(S, DP, T.tab, T.p64.p, T.eoff, T.g64.p);
+      GNPC_LAUNCHED();
+      return;
     }
     {
       const size_t smem = gnpk::mlp_smem_bytes(DP, T.H);
@@ -504,6 +543,38 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
     for (int g = 0; g < 2; ++g) T->mG[g] = make_rows_map(T->G[g].p, T->nv, T->dp, 128, sw);
   }
   T->vv.alloc(nvs);
+  {
+    static const bool off = [] {
+      const char* e = std::getenv("GNPC_NO_PW_ENCODER");
+      return e && std::string(e) == "1";
+    }();
+    const gnp_b200::ParamLayout lay = gnp_b200::param_layout(m->dims);
+    T->pw = !off && T->H <= 64;
+    if (T->pw) {
+      const int H = T->H, dp = T->dp;
+      T->lt.alloc(64);
+      T->la.alloc((std::size_t)(H + 1) * dp);
+      T->lb.alloc((std::size_t)(H + 1) * dp);
+      T->lact.alloc(H + 1);
+      T->lnb.alloc(1);
+      T->tab = gnpk::LiftTab{T->lt.p, T->la.p, T->lb.p, T->lact.p, T->lnb.p};
+      T->eoff = gnpk::EncOff{(int)lay.enc1, (int)lay.enc1_b, (int)lay.enc2, (int)lay.enc2_b, H, T->d};
+      // warps per block: as many as fit the staging ring + accumulator sets
+      // (at least 4: a warp walks kEncStg / warps <= 32 rows per stage)
+      T->enc_warps = 8;
+      if (gnpk::enc_bucket_smem(dp, H, T->enc_warps) > 220 * 1024) T->enc_warps = 4;
+      if (gnpk::enc_bucket_smem(dp, H, T->enc_warps) > 220 * 1024) T->pw = false;
+    }
+    if (T->pw) {
+      const int H = T->H, dp = T->dp;
+      T->enc_grid = std::max(1, std::min(T->sms, (T->nv + 4095) / 4096));
+      // rows per block: a multiple of the staging block (aligned bulk copies)
+      const int stg = gnpk::kEncStg;
+      T->enc_rpb = ((T->nv + T->enc_grid - 1) / T->enc_grid + stg - 1) / stg * stg;
+      T->enc_grid = (T->nv + T->enc_rpb - 1) / T->enc_rpb;
+      T->encpart.alloc((std::size_t)(T->enc_grid + 1) * (H + 1) * 2 * dp);
+    }
+  }
   T->hb1.alloc(nvs * T->H);
   T->hb2.alloc(nvs * T->H);
   T->gyv.alloc(nvs);

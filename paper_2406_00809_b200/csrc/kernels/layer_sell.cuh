@@ -104,7 +104,11 @@ struct SellCfg {
 #define GNPC_KCAP32 12
 #endif
   static constexpr int US = DP == 16 ? 8 : GNPC_US32;    // slice entries per gather round
-  static constexpr int USC = DP == 16 ? 8 : 4;   // CSR entries per gather round
+#ifndef GNPC_USC_TR
+#define GNPC_USC_TR 5
+#endif
+  // CSR entries per gather round (training: B virtual rows share one list)
+  static constexpr int USC = CSR == 2 ? GNPC_USC_TR : (DP == 16 ? 8 : 4);
   // TMA ring depth (tiles), measured per format: SELL DP16 (C2) best at 4
   // (an epilogue lag of 2 tiles with double-buffered A/TMEM and NS 5 measured
   // 25.7 vs 24.4 us); CSR DP16 (C4) at 5 (166 vs 197 us at 4); DP32 fills smem

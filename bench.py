@@ -319,10 +319,14 @@ def run_train_bench(args, capi, torch, rank, world, local, dist):
     if dist:
         dist.barrier()
     l0 = capi.launch_count()
+    # events on the trainer's own (non-blocking) stream, which every kernel
+    # of the step runs on: they bracket the steps' device work, the host
+    # gaps between steps (loss read-back, launches) included
+    ts = torch.cuda.ExternalStream(t.stream())
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
+    ev0.record(ts)
     losses = [do(1000) for _ in range(args.steps)]
-    ev1.record()
+    ev1.record(ts)
     torch.cuda.synchronize()
     launches = capi.launch_count() - l0
     clk = clocks.stop()

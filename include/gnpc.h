@@ -188,6 +188,9 @@ int gnpc_monitor_loss(gnpc_trainer t, const double* x, const double* b, int64_t 
  * gnpc_train_backward_only / gnpc_train_backward_synthetic and
  * gnpc_train_apply_grads (replaces accumulate, src/gnn.cpp:439-440). */
 int gnpc_trainer_grad_buffer(gnpc_trainer t, double** dev_ptr, int64_t* count);
+/* The CUDA stream (cudaStream_t) every kernel of this trainer runs on, for
+ * callers that time or order work against it. */
+int gnpc_trainer_stream(gnpc_trainer t, void** stream);
 int gnpc_train_backward_only(gnpc_trainer t, const double* x, const double* b, double* loss);
 int gnpc_train_backward_synthetic(gnpc_trainer t, uint64_t seed, double* loss);
 int gnpc_train_apply_grads(gnpc_trainer t);

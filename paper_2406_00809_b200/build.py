@@ -35,7 +35,7 @@ CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-Wall"]
 CU_SOURCES = ["capi.cu", "train.cu"]
 HOST_SOURCES = ["host/gnp_host.cpp"]
 HEADERS = ["capi_common.hpp", "model.hpp", "kernels/common.cuh", "kernels/apply.cuh",
-           "kernels/krylov.cuh", "kernels/train.cuh", "kernels/tc.cuh", "kernels/layer_tc.cuh", "kernels/layer_sell.cuh", "kernels/wgrad_tc.cuh", "host/gnp_host.hpp", "api/gnp_gpu.hpp"]
+           "kernels/krylov.cuh", "kernels/train.cuh", "kernels/tc.cuh", "kernels/layer_tc.cuh", "kernels/layer_sell.cuh", "kernels/wgrad_tc.cuh", "kernels/decoder_tc.cuh", "host/gnp_host.hpp", "api/gnp_gpu.hpp"]
 
 LIB = os.path.join(PKG, "libgnpc.so")
 EXT = os.path.join(PKG, "_gnp" + sysconfig.get_config_var("EXT_SUFFIX"))

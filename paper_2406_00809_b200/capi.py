@@ -292,6 +292,12 @@ class Trainer:
         self.h = h
         self.count = param_count(*model.dims)
 
+    def stream(self) -> int:
+        """cudaStream_t (as an int) all of this trainer's kernels run on."""
+        p = vp()
+        check(lib().gnpc_trainer_stream(self.h, C.byref(p)))
+        return p.value or 0
+
     def __del__(self):
         try:
             if self.h and _lib is not None:

@@ -1,0 +1,274 @@
+// Training decoder on the tensor cores (d = hidden = 32), src/gnn.cpp:178-256.
+//
+// Per 128-row tile of X_L (virtual rows v = node*B + k):
+//   MMA1   P = X_L · dec1                    3xTF32: D[:, 0:32] = Y_hi·D1_lo,
+//                                            D[:, 32:64] = Y_hi·D1_hi + Y_lo·D1_hi
+//   FWD    out[v] = (Σ_h relu(P_h + b1_h) dec2_h + b2) · τ_k/√n        (f64)
+//   BWD    gy = gout[v] τ_k/√n, g_z = [P + b1 > 0] gy dec2      (written: the
+//          dec1 / dec1_b weight gradient reads it), per-thread sums of
+//          relu(P + b1) gy (dec2) and gy (dec2_b);
+//   MMA2   G = g_z · dec1ᵀ                   3xTF32 with g_z hi/lo in TMEM
+//          G_L[v] = [X_L > 0] G                (the last layer's relu mask)
+//
+// One thread per tile row (4 warps, lane quarter = warp), thread 0 issues the
+// TMA loads and the MMAs; tiles run synchronously inside a CTA and several
+// CTAs per SM overlap.  X_L tiles arrive by TMA (SW128, the MMA's A_hi
+// operand as is: kind::tf32 truncates); Y_lo and g_z hi/lo go to TMEM (TS-form
+// MMAs), so no operand crosses shared memory twice.
+//
+// TMEM columns: [0, 64) accumulator (MMA1, then MMA2), [64, 96) Y_lo then
+// g_z lo, [96, 128) g_z hi.
+#pragma once
+
+#include "layer_sell.cuh"
+#include "train.cuh"
+
+namespace gnpk {
+
+struct DecTc {
+  static constexpr int TM = 128, NS = 3, NT = 128;
+  static constexpr uint32_t OPB = TM * 32 * 4;           // one [128][32] fp32 tile
+  static constexpr uint32_t O_RING = 0;
+  static constexpr uint32_t O_B1 = NS * OPB;              // [D1_lo; D1_hi]: rows h, K = j
+  static constexpr uint32_t O_B2 = O_B1 + 64 * 128;       // [DT_lo; DT_hi]: rows j, K = h
+  static constexpr uint32_t O_SM = O_B2 + 64 * 128;       // b1[32], dec2[32]
+  static constexpr uint32_t O_BAR = O_SM + 64 * 4;        // full[NS], mma
+  static size_t smem_bytes() { return O_BAR + 8 * (NS + 1) + 16 + 1024; }
+  static constexpr int TCOLS = 128;
+};
+
+// partials: [gridDim.x][33] per-CTA sums (dec2[h], then dec2_b) in f64.
+template <bool FWD>
+__global__ void __launch_bounds__(DecTc::NT, 3)
+k_decoder_tc(const __grid_constant__ CUtensorMap mapy, const float* __restrict__ Y, int nv, int B,
+             NetView net, const SampleScales* __restrict__ sc, const double* __restrict__ gout,
+             double* __restrict__ out, float* __restrict__ gdp, float* __restrict__ gpre,
+             double* __restrict__ partials) {
+  using C = DecTc;
+  extern __shared__ float4 smem_raw[];
+  const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* base = reinterpret_cast<uint8_t*>(smem_raw) + pad;
+  uint8_t* ring = base + C::O_RING;
+  uint8_t* B1 = base + C::O_B1;
+  uint8_t* B2 = base + C::O_B2;
+  float* b1 = reinterpret_cast<float*>(base + C::O_SM);
+  float* d2 = b1 + 32;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + C::O_BAR);
+  uint64_t* mbar = full + C::NS;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // B operands, split hi = trunc(x), lo = x - hi (kind::tf32 truncates)
+  for (int t = tid; t < 32 * 32; t += C::NT) {
+    const int a = t / 32, c = t % 32;
+    const float v1 = net.dec1[c * 32 + a];  // B1(h = a, j = c) = dec1(j, h)
+    const float h1 = __int_as_float(__float_as_int(v1) & 0xffffe000);
+    *reinterpret_cast<float*>(B1 + tc::swz_off<32>(a, c)) = v1 - h1;
+    *reinterpret_cast<float*>(B1 + tc::swz_off<32>(32 + a, c)) = h1;
+    const float v2 = net.dec1[a * 32 + c];  // B2(j = a, h = c) = dec1(j, h)
+    const float h2 = __int_as_float(__float_as_int(v2) & 0xffffe000);
+    *reinterpret_cast<float*>(B2 + tc::swz_off<32>(a, c)) = v2 - h2;
+    *reinterpret_cast<float*>(B2 + tc::swz_off<32>(32 + a, c)) = h2;
+  }
+  if (tid < 32) {
+    b1[tid] = net.dec1_b[tid];
+    d2[tid] = net.dec2[tid];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < C::NS; ++s) tc::mbar_init(&full[s], 1);
+    tc::mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, C::TCOLS);
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const float b2 = *net.dec2_bp;
+
+  const int ntiles = (nv + C::TM - 1) / C::TM;
+  const int my = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto issue = [&](int it) {
+    if (it >= my) return;
+    const int s = it % C::NS;
+    tc::mbar_expect_tx(&full[s], C::OPB);
+    tc::tma_load_2d(ring + s * C::OPB, &mapy, 0, (blockIdx.x + it * gridDim.x) * C::TM, &full[s]);
+  };
+  if (tid == 0) {
+    tc::tma_prefetch_desc(&mapy);
+    for (int it = 0; it < C::NS; ++it) issue(it);
+  }
+  const uint32_t trow = static_cast<uint32_t>(32 * warp) << 16;  // this warp's lane quarter
+  const uint32_t tD = tmem, tR1 = tmem + 64, tR2 = tmem + 96;
+  const uint32_t i64 = tc::idesc_tf32(128, 64), i32 = tc::idesc_tf32(128, 32);
+  const uint32_t sB1 = tc::smem_u32(B1), sB2 = tc::smem_u32(B2);
+  float acc[33];
+#pragma unroll
+  for (int h = 0; h < 33; ++h) acc[h] = 0.f;
+  int mph = 0;
+  int cur_it = 0;
+  // the staged [128][32] tile of the current slot -> rows [t*128, t*128+128)
+  // of dst, 16-byte chunk q = tid + 128 i (row q/8, chunk q%8): coalesced
+  auto store_tile = [&](float* dst) {
+    const uint8_t* st = ring + (cur_it % C::NS) * C::OPB;
+    const size_t row0 = static_cast<size_t>(blockIdx.x + cur_it * gridDim.x) * C::TM;
+    float4* d4 = reinterpret_cast<float4*>(dst + row0 * 32);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int q = tid + C::NT * i, r = q >> 3;
+      if (row0 + r < static_cast<size_t>(nv))
+        d4[q] = *reinterpret_cast<const float4*>(st + tc::swz_off<32>(r, 4 * (q & 7)));
+    }
+  };
+  for (int it = 0; it < my; ++it) {
+    const int s = it % C::NS;
+    cur_it = it;
+    const int v = (blockIdx.x + it * gridDim.x) * C::TM + tid;
+    const bool live = v < nv;
+    // per-row scalars first: their latency overlaps the TMA wait and MMA1
+    const int k = v % B;
+    const SampleScales scv = sc[k];
+    const double gov = (!FWD && live) ? gout[v] : 0.0;
+    tc::mbar_wait(&full[s], (it / C::NS) & 1);
+    // this row of X_L (swizzled), Y_lo into TMEM
+    uint8_t* yt = ring + s * C::OPB;
+    float y[32];
+    uint32_t ymask = 0u;  // [X_L > 0] bits (the last layer's relu mask)
+#pragma unroll
+    for (int c = 0; c < 32; c += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(yt + tc::swz_off<32>(tid, c));
+      y[c] = q.x;
+      y[c + 1] = q.y;
+      y[c + 2] = q.z;
+      y[c + 3] = q.w;
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) ymask |= (y[c] > 0.f ? 1u : 0u) << c;
+#pragma unroll
+    for (int c = 0; c < 32; c += 8) {
+      float lo[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) lo[e] = y[c + e] - __int_as_float(__float_as_int(y[c + e]) & 0xffffe000);
+      tc::tmem_st8(tR1 + trow + c, lo);
+    }
+    tc::tmem_wait_st();
+    tc::fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      const uint32_t sY = tc::smem_u32(yt);
+#pragma unroll
+      for (int k8 = 0; k8 < 4; ++k8) {
+        tc::mma_tf32(tD, tc::make_desc_swz<32>(sY + k8 * 32), tc::make_desc_swz<32>(sB1 + k8 * 32), i64,
+                     k8 > 0);
+        tc::mma_tf32_ts(tD + 32, tR1 + 8 * k8, tc::make_desc_swz<32>(sB1 + 4096 + k8 * 32), i32, 1);
+      }
+      tc::mma_commit(mbar);
+    }
+    tc::mbar_wait(mbar, mph & 1);
+    ++mph;
+    tc::fence_after();
+    float p[32];
+    {
+      float u[16], w[16];
+#pragma unroll
+      for (int h0 = 0; h0 < 32; h0 += 16) {
+        tc::tmem_ld16(tD + trow + h0, u);
+        tc::tmem_ld16(tD + trow + 32 + h0, w);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) p[h0 + e] = u[e] + w[e] + b1[h0 + e];
+      }
+    }
+    if constexpr (FWD) {
+      tc::fence_before();
+      if (live) {
+        float o = 0.f;
+#pragma unroll
+        for (int h = 0; h < 32; ++h) o = fmaf(relu(p[h]), d2[h], o);
+        out[v] = scv.zero ? 0.0 : static_cast<double>(o + b2) * scv.out_scale;
+      }
+    } else {
+      const float gy = (!live || scv.zero) ? 0.f : static_cast<float>(gov * scv.out_scale);
+      float gz[32];
+#pragma unroll
+      for (int h = 0; h < 32; ++h) {
+        gz[h] = p[h] > 0.f ? gy * d2[h] : 0.f;
+        acc[h] = fmaf(relu(p[h]), gy, acc[h]);
+      }
+      acc[32] += gy;
+      // the slot is free once MMA1 completed: it stages the tile's g_z rows
+      // (swizzled, conflict-free), written out coalesced (the tile's rows are
+      // one contiguous 16 KB block)
+#pragma unroll
+      for (int c = 0; c < 32; c += 4)
+        *reinterpret_cast<float4*>(yt + tc::swz_off<32>(tid, c)) = make_float4(gz[c], gz[c + 1], gz[c + 2], gz[c + 3]);
+#pragma unroll
+      for (int c = 0; c < 32; c += 8) {
+        float hi[8], lo[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          hi[e] = gz[c + e];
+          lo[e] = gz[c + e] - __int_as_float(__float_as_int(gz[c + e]) & 0xffffe000);
+        }
+        tc::tmem_st8(tR2 + trow + c, hi);
+        tc::tmem_st8(tR1 + trow + c, lo);
+      }
+      tc::tmem_wait_st();
+      tc::fence_before();
+      __syncthreads();
+      store_tile(gdp);
+      if (tid == 0) {
+        tc::fence_after();
+#pragma unroll
+        for (int k8 = 0; k8 < 4; ++k8) {
+          tc::mma_tf32_ts(tD, tR2 + 8 * k8, tc::make_desc_swz<32>(sB2 + k8 * 32), i64, k8 > 0);
+          tc::mma_tf32_ts(tD + 32, tR1 + 8 * k8, tc::make_desc_swz<32>(sB2 + 4096 + k8 * 32), i32, 1);
+        }
+        tc::mma_commit(mbar);
+      }
+      tc::mbar_wait(mbar, mph & 1);
+      ++mph;
+      tc::fence_after();
+      float g[32];
+      {
+        float u[16], w[16];
+#pragma unroll
+        for (int j0 = 0; j0 < 32; j0 += 16) {
+          tc::tmem_ld16(tD + trow + j0, u);
+          tc::tmem_ld16(tD + trow + 32 + j0, w);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) g[j0 + e] = (ymask >> (j0 + e)) & 1u ? u[e] + w[e] : 0.f;
+        }
+      }
+      tc::fence_before();
+      __syncthreads();  // every thread's g_z left the slot
+#pragma unroll
+      for (int c = 0; c < 32; c += 4)
+        *reinterpret_cast<float4*>(yt + tc::swz_off<32>(tid, c)) = make_float4(g[c], g[c + 1], g[c + 2], g[c + 3]);
+      __syncthreads();
+      store_tile(gpre);
+    }
+    __syncthreads();  // every thread is done with this slot and the TMEM regions
+    if (tid == 0) issue(it + C::NS);
+  }
+  if constexpr (!FWD) {
+    // per-CTA sums in a fixed order: the per-thread values through the (now
+    // idle) ring, then 33 threads add the 128 rows' values in f64
+    __syncthreads();
+    float* accs = reinterpret_cast<float*>(ring);  // [33][128]
+#pragma unroll
+    for (int h = 0; h < 33; ++h) accs[h * C::NT + tid] = acc[h];
+    __syncthreads();
+    if (tid < 33) {
+      double t = 0.0;
+      for (int r = 0; r < C::NT; ++r) t += static_cast<double>(accs[tid * C::NT + r]);
+      partials[static_cast<size_t>(blockIdx.x) * 33 + tid] = t;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0) tc::tmem_dealloc(tmem, C::TCOLS);
+}
+
+}  // namespace gnpk

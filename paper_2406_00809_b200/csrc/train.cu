@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <future>
 #include <memory>
@@ -23,6 +24,7 @@
 #include "kernels/layer_sell.cuh"
 #include "kernels/layer_tc.cuh"
 #include "kernels/train.cuh"
+#include "kernels/decoder_tc.cuh"
 #include "kernels/wgrad_tc.cuh"
 #include "model.hpp"
 
@@ -88,6 +90,12 @@ struct gnpc_trainer_s {
   gnpk::LiftTab tab{};
   gnpk::EncOff eoff{};
   int enc_grid = 0, enc_warps = 16, enc_rpb = 0;
+  // tensor-core decoder (d = hidden = 32 on the TMA maps): dec2 / dec2_b
+  // per-CTA sums folded by k_outer_finish through dec_dst
+  bool dec_tc = false;
+  int dec_grid = 0;
+  DevBuf<double> decpart;
+  DevBuf<int> dec_dst;
 };
 
 namespace {
@@ -338,6 +346,17 @@ struct TrainLaunch {
     }
     for (int l = 0; l < T.L; ++l)
       layer(T, true, l, T.Xs.p + l * act, T.Xs.p + (l + 1) * act, T.AXs.p + l * act, nullptr);
+    if constexpr (DP == 32) {
+      if (T.dec_tc) {
+        const size_t smem = gnpk::DecTc::smem_bytes();
+        set_smem_once((const void*)gnpk::k_decoder_tc<true>, smem);
+        gnpk::k_decoder_tc<true><<<T.dec_grid, gnpk::DecTc::NT, smem, T.s>>>(
+            T.mX[T.L], T.Xs.p + T.L * act, T.nv, T.B, net, T.scl.p, nullptr, T.out.p, nullptr, nullptr,
+            nullptr);
+        GNPC_LAUNCHED();
+        return;
+      }
+    }
     const size_t smem = ((size_t)DP * T.H + 2 * (size_t)T.H + 4 * 32 * (DP + 1)) * 4;
     const int g = grid_for(T.nv, 128, T.sms * 16);
     set_smem_once((const void*)gnpk::k_decoder_fwd<DP>, smem);
@@ -350,7 +369,22 @@ struct TrainLaunch {
     const gnpk::NetView& net = T.m->view;
     const std::size_t act = (std::size_t)T.nv * DP;
     GNPC_CUDA(cudaMemsetAsync(T.g64.p, 0, T.P * sizeof(double), T.s));
-    {
+    bool dec_done = false;
+    if constexpr (DP == 32) {
+      if (T.dec_tc) {
+        const size_t smem = gnpk::DecTc::smem_bytes();
+        set_smem_once((const void*)gnpk::k_decoder_tc<false>, smem);
+        gnpk::k_decoder_tc<false><<<T.dec_grid, gnpk::DecTc::NT, smem, T.s>>>(
+            T.mX[T.L], T.Xs.p + T.L * act, T.nv, T.B, net, T.scl.p, T.gout.p, nullptr, T.hb2.p, T.G[0].p,
+            T.decpart.p);
+        GNPC_LAUNCHED();
+        gnpk::k_outer_finish<<<1, 64, 0, T.s>>>(T.decpart.p, T.dec_grid, 33, T.dec_dst.p, T.g64.p);
+        GNPC_LAUNCHED();
+        run_red(T, T.red_dec1);
+        dec_done = true;
+      }
+    }
+    if (!dec_done) {
       const size_t smem = gnpk::mlp_smem_bytes(DP, T.H);
       const int g = grid_for(T.nv, 32 * gnpk::kMlpWarps, T.sms * 16);
       set_smem_once((const void*)gnpk::k_decoder_bwd<DP>, smem);
@@ -358,8 +392,10 @@ struct TrainLaunch {
                                                      T.gout.p, T.hb1.p, T.gyv.p, T.hb2.p, T.G[0].p);
       GNPC_LAUNCHED();
     }
-    run_red(T, T.red_dec2);
-    run_red(T, T.red_dec1);
+    if (!dec_done) {
+      run_red(T, T.red_dec2);
+      run_red(T, T.red_dec1);
+    }
     int cur = 0;
     for (int l = T.L - 1; l >= 0; --l) {
       T.red_layer[l].o.Bm = T.G[cur].p;
@@ -573,6 +609,40 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
       T->enc_rpb = ((T->nv + T->enc_grid - 1) / T->enc_grid + stg - 1) / stg * stg;
       T->enc_grid = (T->nv + T->enc_rpb - 1) / T->enc_rpb;
       T->encpart.alloc((std::size_t)(T->enc_grid + 1) * (H + 1) * 2 * dp);
+    }
+  }
+  {
+    static const bool off = [] {
+      const char* e = std::getenv("GNPC_NO_DEC_TC");
+      return e && std::string(e) == "1";
+    }();
+    T->dec_tc = !off && T->sell && T->tc && T->dp == 32 && T->H == 32;
+    if (T->dec_tc) {
+      const size_t smem = gnpk::DecTc::smem_bytes();
+      set_smem_once((const void*)gnpk::k_decoder_tc<true>, smem);
+      set_smem_once((const void*)gnpk::k_decoder_tc<false>, smem);
+      // several CTAs per SM overlap each other's per-tile round trips
+      for (const void* kf : {(const void*)gnpk::k_decoder_tc<true>, (const void*)gnpk::k_decoder_tc<false>})
+        GNPC_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       cudaSharedmemCarveoutMaxShared));
+      // residency by registers / smem / TMEM (the occupancy API reports 1 CTA
+      // per SM for kernels that allocate TMEM; see tc_ctas_per_sm)
+      cudaFuncAttributes fa{};
+      GNPC_CUDA(cudaFuncGetAttributes(&fa, gnpk::k_decoder_tc<false>));
+      int dev = 0, smem_sm = 0, regs_sm = 0;
+      GNPC_CUDA(cudaGetDevice(&dev));
+      GNPC_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+      GNPC_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+      int per_sm = std::min(regs_sm / (((fa.numRegs + 7) / 8) * 8 * gnpk::DecTc::NT),
+                            smem_sm / (int)(smem + fa.sharedSizeBytes + 1024));
+      per_sm = std::max(1, std::min(per_sm, 512 / gnpk::DecTc::TCOLS));
+      T->dec_grid = std::max(1, std::min(per_sm * T->sms, (T->nv + 127) / 128));
+      T->decpart.alloc((std::size_t)T->dec_grid * 33);
+      const gnp_b200::ParamLayout lay = gnp_b200::param_layout(m->dims);
+      std::vector<int> dst(33);
+      for (int h = 0; h < 32; ++h) dst[h] = (int)(lay.dec2 + h);
+      dst[32] = (int)lay.dec2_b;
+      upload_i(T->dec_dst, dst);
     }
   }
   T->hb1.alloc(nvs * T->H);
@@ -815,6 +885,13 @@ int gnpc_trainer_grad_buffer(gnpc_trainer t, double** dev_ptr, int64_t* count) {
     need(t && dev_ptr && count, "null argument");
     *dev_ptr = t->g64.p;
     *count = t->P;
+  });
+}
+
+int gnpc_trainer_stream(gnpc_trainer t, void** stream) {
+  return guarded([&] {
+    need(t && stream, "null argument");
+    *stream = static_cast<void*>(t->s);
   });
 }
 

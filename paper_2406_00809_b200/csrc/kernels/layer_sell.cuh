@@ -73,6 +73,12 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, 
                "r"(smem_u32(src)), "r"(x), "r"(y)
                : "memory");
 }
+// 1-D bulk copy shared -> global (bulk-group completion; 16-B aligned, size % 16 == 0).
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -128,8 +134,15 @@ struct SellCfg {
   static constexpr int CAPC = TR ? 512 : (DP == 16 ? 2048 : 1024);  // staged nonzeros per tile (DP=32
                                                                      // apply: fits the projection operands)
   static constexpr uint32_t RPB = (TM + 4) * 4;  // row_ptr slice copy (bytes, 16-B multiple)
-  static constexpr uint32_t O_MASK = OPB;        // training backward: mask tile (X_l)
-  static constexpr uint32_t O_RP = TR ? 2 * OPB : OPB, O_CI = O_RP + 1024, O_V = O_CI + CAPC * 4;
+  // training backward mask [X_l > 0]: at d = 32 one 32-bit word per row
+  // (written by the forward layer's epilogue), else the X_l tile itself
+#ifndef GNPC_MBITS
+#define GNPC_MBITS 0  // measured: fwd +80 us, bwd -35 us per layer at C3
+#endif
+  static constexpr bool MBITS = GNPC_MBITS && TR && DP == 32;
+  static constexpr uint32_t MASKB = MBITS ? TM * 4 : OPB;
+  static constexpr uint32_t O_MASK = OPB;
+  static constexpr uint32_t O_RP = TR ? OPB + MASKB : OPB, O_CI = O_RP + 1024, O_V = O_CI + CAPC * 4;
   static constexpr uint32_t SLOT =
       CSR ? ((O_V + CAPC * 4 + 1023) & ~1023u) : (((OPB + CVB) + 1023) & ~1023u);
   // layout (offsets from the 1024-aligned base)
@@ -141,8 +154,11 @@ struct SellCfg {
   // (2H rows, swizzled K-major), then dec1 (fp32, CUDA-core fallback), b1, dec2
   static constexpr uint32_t O_YLO = O_Y + 2 * OPB;
   static constexpr uint32_t O_D1OP = O_YLO + 2 * OPB;
+  // training forward at d = 32: the rows' [Y > 0] words staged [2][TM] next
+  // to the Y staging, stored with it by one bulk copy
+  static constexpr uint32_t O_MST = O_Y + 2 * OPB;
   static constexpr uint32_t o_p(int hidden, bool last) {
-    return last && tc_proj(hidden) ? O_D1OP + 2 * hidden * DP * 4 : O_Y + 2 * OPB;
+    return last && tc_proj(hidden) ? O_D1OP + 2 * hidden * DP * 4 : O_Y + 2 * OPB + (MBITS ? 2 * TM * 4 : 0);
   }
   static constexpr uint32_t o_bar(int hidden, bool last) {
     return (o_p(hidden, last) + (last ? (DP + 2) * hidden * 4 : 0) + 15) & ~15u;
@@ -271,13 +287,16 @@ __device__ __forceinline__ void gather_csr_rows(const char* const (&xbj)[R], uns
 
 // Training extras for sell_layer (CSR = 2): B virtual rows per node; KIND 1
 // (forward) also stores the tile's ÂX (= the A2_hi operand, raw fp32) through
-// mapax; KIND 2 (backward) multiplies by [mask > 0] from the mask tile
-// (mapmask over X_l) when use_mask.
+// mapax, and at d = 32 the rows' [Y > 0] bits (mask_out, one 32-bit word per
+// row); KIND 2 (backward) multiplies by [X_l > 0] when use_mask, from those
+// bits (mask_in, d = 32) or from the X_l tile (mapmask).
 struct TrainIO {
   const CUtensorMap* mapax;
   const CUtensorMap* mapmask;
   int bs;
   int use_mask;
+  const uint32_t* mask_in;
+  uint8_t* mask_out;
 };
 
 __device__ __forceinline__ float4 f4_trunc_lo(float4 v) {
@@ -448,9 +467,14 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           const int a0 = kb & ~3, cnt = ((ke + 3) & ~3) - a0;
           const bool staged = cnt <= C::CAPC;
           tc::mbar_expect_tx(&p.full[s],
-                             C::OPB + (use_mask ? C::OPB : 0) + C::RPB + (staged ? 8 * cnt : 0));
+                             C::OPB + (use_mask ? C::MASKB : 0) + C::RPB + (staged ? 8 * cnt : 0));
           tc::tma_load_2d(slot, mapx, 0, t * TM, &p.full[s]);
-          if (use_mask) tc::tma_load_2d(slot + C::O_MASK, tio->mapmask, 0, t * TM, &p.full[s]);
+          if (use_mask) {
+            if constexpr (C::MBITS)
+              tc::bulk_load(slot + C::O_MASK, tio->mask_in + static_cast<size_t>(t) * TM, C::MASKB, &p.full[s]);
+            else
+              tc::tma_load_2d(slot + C::O_MASK, tio->mapmask, 0, t * TM, &p.full[s]);
+          }
           // row_ptr slice from the 16-byte aligned node n0 & ~3 (npt < 4 when bs > 32)
           tc::bulk_load(slot + C::O_RP, a.rp + (n0 & ~3), C::RPB, &p.full[s]);
           if (staged && cnt > 0) {
@@ -542,6 +566,13 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         if (!LAST && it >= 1) {  // tile it-1 is fully staged
           tc::tma_store_2d(mapy, p.Ystg + ((mb + it - 1) & 1) * C::OPB, 0,
                            (blockIdx.x + (it - 1) * gridDim.x) * TM);
+          if constexpr (KIND == 1 && C::MBITS) {
+            if (tio->mask_out) {
+              const int t1 = blockIdx.x + (it - 1) * gridDim.x;
+              tc::bulk_store(tio->mask_out + static_cast<size_t>(t1) * TM * 4,
+                             p.Ystg + C::O_MST - C::O_Y + ((mb + it - 1) & 1) * TM * 4, TM * 4);
+            }
+          }
           tc::bulk_commit();
         }
         // every warp passed its wait for MMA(it-1): that slot takes tile it+NS-1
@@ -610,6 +641,10 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       // training backward: D ⊙ [X_l > 0] from the tile's mask (its ring slot
       // is refilled only after this iteration's arrival), no relu
       const uint8_t* msk = p.ring + ((rb + itp) % NS) * C::SLOT + C::O_MASK;
+      uint32_t mword = 0u, mout = 0u;
+      if constexpr (KIND == 2 && C::MBITS) {
+        if (use_mask) mword = *reinterpret_cast<const uint32_t*>(msk + 4 * m) >> (cq * CW);
+      }
 #pragma unroll
       for (int c = 0; c < CW; c += 4)
       {
@@ -617,19 +652,31 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         if constexpr (KIND == 2) {
           yv = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
           if (use_mask) {
-            const float4 mk = *reinterpret_cast<const float4*>(msk + tc::swz_off<DP>(m, cq * CW + c));
-            yv.x = mk.x > 0.f ? yv.x : 0.f;
-            yv.y = mk.y > 0.f ? yv.y : 0.f;
-            yv.z = mk.z > 0.f ? yv.z : 0.f;
-            yv.w = mk.w > 0.f ? yv.w : 0.f;
+            if constexpr (C::MBITS) {
+              yv.x = (mword >> c) & 1u ? yv.x : 0.f;
+              yv.y = (mword >> (c + 1)) & 1u ? yv.y : 0.f;
+              yv.z = (mword >> (c + 2)) & 1u ? yv.z : 0.f;
+              yv.w = (mword >> (c + 3)) & 1u ? yv.w : 0.f;
+            } else {
+              const float4 mk = *reinterpret_cast<const float4*>(msk + tc::swz_off<DP>(m, cq * CW + c));
+              yv.x = mk.x > 0.f ? yv.x : 0.f;
+              yv.y = mk.y > 0.f ? yv.y : 0.f;
+              yv.z = mk.z > 0.f ? yv.z : 0.f;
+              yv.w = mk.w > 0.f ? yv.w : 0.f;
+            }
           }
         } else {
           yv = make_float4(relu(v[c]), relu(v[c + 1]), relu(v[c + 2]), relu(v[c + 3]));
+          mout |= (v[c] > 0.f ? 1u : 0u) << c | (v[c + 1] > 0.f ? 1u : 0u) << (c + 1) |
+                  (v[c + 2] > 0.f ? 1u : 0u) << (c + 2) | (v[c + 3] > 0.f ? 1u : 0u) << (c + 3);
         }
         *reinterpret_cast<float4*>(ys + tc::swz_off<DP>(m, cq * CW + c)) = yv;
         if (LAST)
           *reinterpret_cast<float4*>(p.Ylo + ((mb + itp) & 1) * C::OPB + tc::swz_off<DP>(m, cq * CW + c)) =
               f4_trunc_lo(yv);
+      }
+      if constexpr (KIND == 1 && C::MBITS) {  // this warp's CW = 8 columns: one byte of the row's word
+        p.Ystg[C::O_MST - C::O_Y + ((mb + itp) & 1) * TM * 4 + 4 * m + cq] = static_cast<uint8_t>(mout);
       }
       tc::fence_before();
       return false;
@@ -845,9 +892,10 @@ struct TrainMaps {
 template <int DP, int KIND>
 __global__ void __launch_bounds__(SellCfg<DP, 2>::NT, 1)
 k_train_sell(DevCsr a, const __grid_constant__ TrainMaps maps, const float* __restrict__ X,
-             const float* __restrict__ uwp, NetView net, int bs, int use_mask) {
+             const float* __restrict__ uwp, NetView net, int bs, int use_mask,
+             const uint32_t* __restrict__ mask_in, uint8_t* __restrict__ mask_out) {
   auto p = sell_setup<DP, 2>(net.hidden, false);
-  const TrainIO tio{&maps.ax, &maps.mask, bs, use_mask};
+  const TrainIO tio{&maps.ax, &maps.mask, bs, use_mask, mask_in, mask_out};
   sell_layer<DP, false, float, 2, KIND>(p, a, &maps.x, &maps.y, X, nullptr, uwp, net, 1.0, nullptr, &tio);
   sell_teardown(p);
 }

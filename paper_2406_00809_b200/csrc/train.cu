@@ -51,6 +51,11 @@ struct gnpc_trainer_s {
   // gradient buffers, used when the batch divides the 128-row tile
   bool sell = false;
   std::vector<CUtensorMap> mX, mAX;
+  // [X_l > 0] bits of the layer outputs (d = 32: one 32-bit word per row,
+  // rows padded to the 128-row tile), written by forward layer l-1 and read
+  // by backward layer l instead of the X_l tile
+  DevBuf<uint32_t> mbits;
+  std::size_t nvpad = 0;
   CUtensorMap mG[2]{};
   // batch
   DevBuf<double> xb, bb, out, sgn, gout, colpart, losspart, tmp;
@@ -294,7 +299,14 @@ struct TrainLaunch {
           maps.mask = T.mX[l];
         }
         const float* uwp = (fwd ? T.m->UWP.p : T.UWP_bwd.p) + (size_t)l * 4 * DP * DP;
-        kern<<<grid, S::NT, smem, T.s>>>(a, maps, X, uwp, T.m->view, T.B, mask != nullptr ? 1 : 0);
+        const uint32_t* min_ = nullptr;
+        uint8_t* mout = nullptr;
+        if (T.mbits.p) {
+          if (fwd && l + 1 <= T.L - 1) mout = reinterpret_cast<uint8_t*>(T.mbits.p + (size_t)(l + 1) * T.nvpad);
+          if (!fwd && mask != nullptr) min_ = T.mbits.p + (size_t)l * T.nvpad;
+        }
+        kern<<<grid, S::NT, smem, T.s>>>(a, maps, X, uwp, T.m->view, T.B, mask != nullptr ? 1 : 0, min_,
+                                         mout);
         GNPC_LAUNCHED();
         return;
       }
@@ -577,6 +589,11 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
     for (int l = 0; l <= T->L; ++l) T->mX.push_back(make_rows_map(T->Xs.p + l * act, T->nv, T->dp, 128, sw));
     for (int l = 0; l < T->L; ++l) T->mAX.push_back(make_rows_map(T->AXs.p + l * act, T->nv, T->dp, 128, sw));
     for (int g = 0; g < 2; ++g) T->mG[g] = make_rows_map(T->G[g].p, T->nv, T->dp, 128, sw);
+    if (gnpk::SellCfg<32, 2>::MBITS && T->dp == 32) {
+      T->nvpad = ((std::size_t)T->nv + 127) / 128 * 128;
+      T->mbits.alloc(T->nvpad * T->L);
+      GNPC_CUDA(cudaMemsetAsync(T->mbits.p, 0, T->nvpad * T->L * 4, T->s));
+    }
   }
   T->vv.alloc(nvs);
   {

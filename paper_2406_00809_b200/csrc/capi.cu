@@ -106,17 +106,23 @@ struct ApplyLaunch {
       // DP=16 only: at DP=32 the in-kernel layers measured slower than
       // separate launches (C5: 499 vs 450 us per layer) while DP=16 gains
       // (C2: 17 vs 24 us per layer: no launch gap or prologue per layer)
-      const bool fits = (a.sell ? SellCfg<DP, false>::smem_bytes(net.hidden, true)
-                                : SellCfg<DP, true>::smem_bytes(net.hidden, true)) <= 226 * 1024;
+      // pipeline mode: 3 windowed sliced-ELL (d = 16), 0 sliced-ELL, 1 CSR ranges
+      const int mode = (DP == 16 && a.wdesc) ? 3 : (a.sell ? 0 : 1);
+      auto smem_of = [&](int md, bool last) -> size_t {
+        if constexpr (DP == 16)
+          if (md == 3) return SellCfg<16, 3>::smem_bytes(net.hidden, last);
+        return md == 0 ? SellCfg<DP, 0>::smem_bytes(net.hidden, last) : SellCfg<DP, 1>::smem_bytes(net.hidden, last);
+      };
+      const bool fits = smem_of(mode, true) <= 226 * 1024;
       if (DP == 16 && fits && m.use_tc && !sell_off && !fused_off && A.n_long == 0 && prof == nullptr &&
           n > 0) {
-        const bool csr = a.sell == nullptr;
         using S = SellCfg<DP, false>;
-        using SC = SellCfg<DP, true>;
-        const size_t smem = csr ? SC::smem_bytes(net.hidden, true) : S::smem_bytes(net.hidden, true);
-        auto kern = csr ? k_apply_sell<DP, InT, OutT, true> : k_apply_sell<DP, InT, OutT, false>;
-        static std::once_flag f[2];
-        std::call_once(f[csr ? 1 : 0], [&] {
+        const size_t smem = smem_of(mode, true);
+        auto kern = mode == 1 ? k_apply_sell<DP, InT, OutT, 1>
+                              : (mode == 3 ? k_apply_sell<DP, InT, OutT, (DP == 16 ? 3 : 0)>
+                                           : k_apply_sell<DP, InT, OutT, 0>);
+        static std::once_flag f[4];
+        std::call_once(f[mode], [&] {
           cudaFuncAttributes fa{};
           GNPC_CUDA(cudaFuncGetAttributes(&fa, (const void*)kern));  // static smem counts against 227 KB
           GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -127,8 +133,8 @@ struct ApplyLaunch {
         static const bool times = std::getenv("GNPC_FUSED_TIMES") != nullptr;
         static gnpc_impl::DevBuf<unsigned long long> tbuf;
         if (times && !tbuf.p) tbuf.alloc(64);
-        ApplyFused fa{m.tmX[0], m.tmX[1], m.X[0].p, m.X[1].p, m.UWP.p, m.partials.p, m.gbar.p,
-                      m.gbar_host, m.sc.p, times ? tbuf.p : nullptr, m.fused_stash};
+        ApplyFused fa{m.tmX[0], m.tmX[1], m.tmXw[0], m.tmXw[1], m.X[0].p, m.X[1].p, m.UWP.p, m.partials.p,
+                      m.gbar.p, m.gbar_host, m.sc.p, times ? tbuf.p : nullptr, m.fused_stash};
         m.gbar_host += (unsigned long long)grid * (1 + net.layers);
         void* args[] = {(void*)&a, (void*)&fa, (void*)&in, (void*)&net, (void*)&out, (void*)&skip};
         GNPC_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(S::NT), args, smem, s));
@@ -186,24 +192,27 @@ struct ApplyLaunch {
       const bool last = l + 1 == net.layers;
       mark(last ? 4 : 3);
       if constexpr (DP == 16 || DP == 32) {
-        const bool sell_fits = (a.sell ? SellCfg<DP, false>::smem_bytes(net.hidden, last)
-                                       : SellCfg<DP, true>::smem_bytes(net.hidden, last)) <= 227 * 1024;
+        const int lmode = (DP == 16 && a.wdesc && A.n_long == 0) ? 3 : (a.sell ? 0 : 1);
+        const size_t smem = lmode == 3 ? SellCfg<DP, (DP == 16 ? 3 : 0)>::smem_bytes(net.hidden, last)
+                                       : (lmode == 0 ? SellCfg<DP, 0>::smem_bytes(net.hidden, last)
+                                                     : SellCfg<DP, 1>::smem_bytes(net.hidden, last));
+        const bool sell_fits = smem <= 227 * 1024;
         if (m.use_tc && !sell_off && sell_fits) {
-          // TMA pipeline, one 544-thread CTA per SM: sliced-ELL slices on
-          // regular matrices, the short-row CSR ranges on ragged ones
-          const bool csr = a.sell == nullptr;
+          // TMA pipeline, one 544-thread CTA per SM: windowed or plain
+          // sliced-ELL slices on regular matrices, the short-row CSR ranges
+          // on ragged ones
           using S = SellCfg<DP, false>;
-          using SC = SellCfg<DP, true>;
-          const size_t smem = csr ? SC::smem_bytes(net.hidden, last) : S::smem_bytes(net.hidden, last);
-          auto kern = csr ? (last ? k_layer_sell<DP, true, OutT, true> : k_layer_sell<DP, false, OutT, true>)
-                          : (last ? k_layer_sell<DP, true, OutT> : k_layer_sell<DP, false, OutT>);
-          static std::once_flag f[4];
-          std::call_once(f[(last ? 1 : 0) + (csr ? 2 : 0)], [&] {
+          constexpr int W = DP == 16 ? 3 : 0;
+          auto kern = lmode == 1 ? (last ? k_layer_sell<DP, true, OutT, 1> : k_layer_sell<DP, false, OutT, 1>)
+                                 : (lmode == 3 ? (last ? k_layer_sell<DP, true, OutT, W> : k_layer_sell<DP, false, OutT, W>)
+                                               : (last ? k_layer_sell<DP, true, OutT> : k_layer_sell<DP, false, OutT>));
+          static std::once_flag f[8];
+          std::call_once(f[(last ? 1 : 0) + 2 * lmode], [&] {
             GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
           });
           const int tiles_s = (n + S::TM - 1) / S::TM;
           const int grid = std::max(1, std::min(tiles_s, sms));
-          SellMaps maps{m.tmX[cur], m.tmX[1 - cur]};
+          SellMaps maps{m.tmX[cur], m.tmX[1 - cur], m.tmXw[cur]};
           const float* uwp = m.UWP.p + (size_t)l * 4 * DP * DP;
           kern<<<grid, S::NT, smem, s>>>(a, maps, X, axl, uwp, net, m.sc.p, out, skip);
           GNPC_LAUNCHED();
@@ -448,6 +457,47 @@ void gnpc_csr_s::build_sell(const std::vector<int>& hrp, const std::vector<int>&
   sell_off.upload(off.data(), off.size());
   sell_k.upload(K.data(), K.size());
   has_sell = true;
+  // windows: every tile's columns (and its own rows, the MMA's X tile) within
+  // at most kWinBlocks 64-row blocks, no long rows
+  // opt-in (GNPC_WIN=1): measured slower on C2 (34 vs 24 us per d = 16 layer:
+  // the 32 KB of window blocks per tile arrive slower than the L1-cached gathers)
+  if (const char* e = std::getenv("GNPC_WIN"); !e || std::string(e) != "1") return;
+  if (n_long != 0) return;
+  constexpr int BR = gnpk::kWinRows, NB = gnpk::kWinBlocks, WD = gnpk::kWinDesc;
+  std::vector<int> desc((std::size_t)ntiles * WD, 0);
+  std::vector<int2> went(ent.size());
+  std::vector<int> blocks;
+  for (std::int64_t t = 0; t < ntiles; ++t) {
+    const int kt = K[t] & 0xffff;
+    blocks.clear();
+    const int own = (int)(t * TM / BR);
+    blocks.push_back(own);
+    blocks.push_back(own + 1);
+    const int rows = (int)std::min<std::int64_t>(TM, n - t * TM);  // rows past n: padding only
+    for (int k = 0; k < kt; ++k)
+      for (int r = 0; r < rows; ++r) blocks.push_back(ent[off[t] + (std::size_t)k * TM + r].x / BR);
+    std::sort(blocks.begin(), blocks.end());
+    blocks.erase(std::unique(blocks.begin(), blocks.end()), blocks.end());
+    if ((int)blocks.size() > NB) return;  // not windowed
+    int* d = desc.data() + t * WD;
+    d[0] = (int)blocks.size();
+    d[1] = (int)(std::lower_bound(blocks.begin(), blocks.end(), own) - blocks.begin());
+    for (std::size_t i = 0; i < blocks.size(); ++i) d[2 + i] = blocks[i];
+    for (int k = 0; k < kt; ++k)
+      for (int r = 0; r < TM; ++r) {
+        const std::size_t q = off[t] + (std::size_t)k * TM + r;
+        if (r >= rows) {
+          went[q] = make_int2(d[1] * BR, 0);
+          continue;
+        }
+        const int c = ent[q].x;
+        const int slot = (int)(std::lower_bound(blocks.begin(), blocks.end(), c / BR) - blocks.begin());
+        went[q] = make_int2(slot * BR + c % BR, ent[q].y);
+      }
+  }
+  wsell.upload(went.data(), went.size());
+  wdesc.upload(desc.data(), desc.size());
+  has_win = true;
 }
 
 gnpk::DevCsr gnpc_csr_s::dev() {
@@ -467,6 +517,8 @@ gnpk::DevCsr gnpc_csr_s::dev() {
   d.sell = has_sell ? sell.p : nullptr;
   d.sell_off = has_sell ? sell_off.p : nullptr;
   d.sell_k = has_sell ? sell_k.p : nullptr;
+  d.wsell = has_win ? wsell.p : nullptr;
+  d.wdesc = has_win ? wdesc.p : nullptr;
   return d;
 }
 
@@ -695,6 +747,8 @@ void gnpc_model_s::ensure_workspace() {
       if (tm_base[c] != X[c].p) {
         tmX[c] = make_rows_map(X[c].p, (std::int64_t)n, dp, 128,
                                dp == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+        tmXw[c] = make_rows_map(X[c].p, (std::int64_t)n, dp, gnpk::kWinRows,
+                                dp == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
         tm_base[c] = X[c].p;
       }
   }
@@ -704,8 +758,9 @@ bool gnpc_model_s::fused_eligible() {
   a->upload();
   if (dp != 16 || !use_tc || a->n_long != 0 || a->h.n == 0) return false;
   if (gnpc_impl::sell_kernel_off() || gnpc_impl::fused_apply_off()) return false;
-  const size_t smem = a->has_sell ? gnpk::SellCfg<16, 0>::smem_bytes(dims.hidden, true)
-                                  : gnpk::SellCfg<16, 1>::smem_bytes(dims.hidden, true);
+  const size_t smem = a->has_win    ? gnpk::SellCfg<16, 3>::smem_bytes(dims.hidden, true)
+                      : a->has_sell ? gnpk::SellCfg<16, 0>::smem_bytes(dims.hidden, true)
+                                    : gnpk::SellCfg<16, 1>::smem_bytes(dims.hidden, true);
   return smem <= 226 * 1024;
 }
 

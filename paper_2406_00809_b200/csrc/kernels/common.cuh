@@ -33,7 +33,16 @@ struct DevCsr {
   const int* __restrict__ cis;
   const float* __restrict__ vs;
   const int* __restrict__ tflag;
+  // Windowed sliced-ELL (d = 16 apply, matrices without long rows whose
+  // tiles each reference at most kWinBlocks 64-row blocks of X, e.g.
+  // stencils): wdesc[t*kWinDesc] = {nblk, xslot, blk_0 .. blk_7} (sorted
+  // block ids; xslot = position of the tile's own first block), wsell = the
+  // sell entries with the column replaced by its row in the tile's staged
+  // window (slot i*64 + col%64).  nullptr when not built.
+  const int2* __restrict__ wsell;
+  const int* __restrict__ wdesc;
 };
+constexpr int kWinBlocks = 8, kWinRows = 64, kWinDesc = 2 + kWinBlocks;
 
 // Per-apply scalars produced by the norm kernel (scale sandwich,
 // src/gnn.cpp:128-139,191-199).

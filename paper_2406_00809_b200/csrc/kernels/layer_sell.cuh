@@ -87,6 +87,8 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 
 }  // namespace tc
 
+// CSR = 3: windowed sliced-ELL (d = 16): the tile's X rows arrive as up to
+//          kWinBlocks 64-row blocks (TMA) and the gathers read shared memory;
 // CSR = 0: sliced-ELL slices (k_layer_sell on regular matrices);
 // CSR = 1: the short-row CSR ranges of the tile (ragged matrices);
 // CSR = 2: training — B virtual rows per node (v = node*B + k), the full CSR
@@ -118,11 +120,14 @@ struct SellCfg {
   // TMA ring depth (tiles), measured per format: SELL DP16 (C2) best at 4
   // (an epilogue lag of 2 tiles with double-buffered A/TMEM and NS 5 measured
   // 25.7 vs 24.4 us); CSR DP16 (C4) at 5 (166 vs 197 us at 4); DP32 fills smem
-  static constexpr int NS = DP == 16 ? (CSR ? 5 : 4) : 3;
+  static constexpr bool WIN = CSR == 3;                // windowed sliced-ELL
+  static constexpr bool CSRL = CSR == 1 || CSR == 2;    // CSR ranges staged per tile
+  static_assert(!WIN || DP == 16, "windowed slices are built for d = 16");
+  static constexpr int NS = DP == 16 ? (CSRL ? 5 : 4) : 3;
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
   // up to round(K, US) words).  Kept small: every KB of shared memory is L1
   // the X-row gathers hit (C5 fused layer 531 -> 499 us going 24 -> 12)
-  static constexpr int KCAP = DP == 16 ? 16 : GNPC_KCAP32;
+  static constexpr int KCAP = WIN ? 8 : (DP == 16 ? 16 : GNPC_KCAP32);
   static constexpr uint32_t OPB = TM * DP * 4;   // one A-type operand / X tile / Y tile (bytes)
   static constexpr uint32_t BB = DP * DP * 4;    // one B operand (bytes)
   static constexpr int TCOLS = 2 * DP;           // TMEM accumulator columns (two halves)
@@ -143,8 +148,13 @@ struct SellCfg {
   static constexpr uint32_t MASKB = MBITS ? TM * 4 : OPB;
   static constexpr uint32_t O_MASK = OPB;
   static constexpr uint32_t O_RP = TR ? OPB + MASKB : OPB, O_CI = O_RP + 1024, O_V = O_CI + CAPC * 4;
+  // windowed: [kWinBlocks 64-row X blocks | slice]; the tile's own rows (the
+  // MMA's X tile) are two consecutive blocks of the window
+  static constexpr uint32_t BLKB = kWinRows * DP * 4;
+  static constexpr uint32_t WB = WIN ? kWinBlocks * BLKB : 0;
+  static constexpr uint32_t O_SL = WIN ? WB : OPB;  // staged slice (sliced-ELL modes)
   static constexpr uint32_t SLOT =
-      CSR ? ((O_V + CAPC * 4 + 1023) & ~1023u) : (((OPB + CVB) + 1023) & ~1023u);
+      CSRL ? ((O_V + CAPC * 4 + 1023) & ~1023u) : (((O_SL + CVB) + 1023) & ~1023u);
   // layout (offsets from the 1024-aligned base)
   static constexpr uint32_t O_RING = 0;
   static constexpr uint32_t O_A = O_RING + NS * SLOT;     // A2_hi (ÂX), A2_lo
@@ -187,8 +197,9 @@ struct SellCfg {
 };
 
 struct SellMaps {
-  CUtensorMap x;  // layer input  [n][DP], box {DP, 128}, swizzled
-  CUtensorMap y;  // layer output [n][DP] (unused by the last layer)
+  CUtensorMap x;   // layer input  [n][DP], box {DP, 128}, swizzled
+  CUtensorMap y;   // layer output [n][DP] (unused by the last layer)
+  CUtensorMap xw;  // layer input, box {DP, kWinRows} (windowed mode)
 };
 
 // Sliced-ELL gather, R rows per group, rounds of US entries.  Slots past K
@@ -245,6 +256,39 @@ __device__ __forceinline__ void gather_sell_rows(const float* __restrict__ X, in
     for (int u = 0; u < US; ++u)
 #pragma unroll
       for (int j = 0; j < R; ++j) fma4(acc[j], w[j][u], x[j][u]);
+  }
+}
+
+// Windowed gather: entries hold the row's position in the tile's staged
+// window; the X rows are read from shared memory (swizzled as the TMA wrote
+// them, 64-row blocks at BLKB-aligned offsets), otherwise as gather_sell_rows.
+template <int DP, int R, int US, int TM, bool SMEM>
+__device__ __forceinline__ void gather_win_rows(const uint8_t* win, int gl, const int2* cv, int K, int gid,
+                                                float4 (&acc)[R]) {
+  for (int k = 0; k < K; k += US) {
+    int c[R][US];
+    float w[R][US];
+#pragma unroll
+    for (int u = 0; u < US; ++u) {
+      const bool on = k + u < K;
+      const int2* src = cv + (k + u) * TM + R * gid;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        int2 e;
+        if constexpr (SMEM) {
+          e = src[j];
+        } else {
+          e = on ? __ldg(src + j) : make_int2(0, 0);
+        }
+        c[j][u] = on ? e.x : 0;
+        w[j][u] = on ? __int_as_float(e.y) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < US; ++u)
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        fma4(acc[j], w[j][u], *reinterpret_cast<const float4*>(win + tc::swz_off<DP>(c[j][u], 4 * gl)));
   }
 }
 
@@ -397,7 +441,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
                                            const CUtensorMap* mapy, const float* __restrict__ X,
                                            const float* __restrict__ axlong, const float* __restrict__ uwp,
                                            const NetView& net, double out_scale, OutT* __restrict__ out,
-                                           const TrainIO* tio = nullptr) {
+                                           const TrainIO* tio = nullptr, const CUtensorMap* mapxw = nullptr) {
   using C = SellCfg<DP, CSR>;
   constexpr int TM = C::TM, G = C::G, R = C::R, NS = C::NS, NW = C::NW, NQ = C::NQ;
   constexpr bool TR = C::TR;
@@ -452,7 +496,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   if (warp == NW) {
     // ============================================================ control warp
     if (lane == 0) {
-      tc::tma_prefetch_desc(mapx);
+      tc::tma_prefetch_desc(C::WIN ? mapxw : mapx);
       if (!LAST) tc::tma_prefetch_desc(mapy);
       auto issue = [&](int it) {  // tile `it` of this CTA into ring slot (rb + it) % NS
         if (it >= my_tiles) return;
@@ -481,7 +525,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
             tc::bulk_load(slot + C::O_CI, a.ci + a0, 4 * cnt, &p.full[s]);
             tc::bulk_load(slot + C::O_V, a.v + a0, 4 * cnt, &p.full[s]);
           }
-        } else if constexpr (CSR) {
+        } else if constexpr (CSR == 1) {
           // the tile's short-row CSR range, 16-byte aligned superset [a0, a1)
           const int kb = __ldg(a.rps + t * TM), ke = __ldg(a.rps + min((t + 1) * TM, n));
           const int a0 = kb & ~3, cnt = ((ke + 3) & ~3) - a0;
@@ -493,6 +537,15 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
             tc::bulk_load(slot + C::O_CI, a.cis + a0, 4 * cnt, &p.full[s]);
             tc::bulk_load(slot + C::O_V, a.vs + a0, 4 * cnt, &p.full[s]);
           }
+        } else if constexpr (C::WIN) {
+          const int* wd = a.wdesc + static_cast<size_t>(t) * kWinDesc;
+          const int nbk = __ldg(wd);
+          const int K = __ldg(a.sell_k + t) & 0xffff;
+          const bool staged = K > 0 && K <= C::KCAP;
+          tc::mbar_expect_tx(&p.full[s], nbk * C::BLKB + (staged ? K * TM * 8 : 0));
+          for (int i = 0; i < nbk; ++i)
+            tc::tma_load_2d(slot + i * C::BLKB, mapxw, 0, __ldg(wd + 2 + i) * kWinRows, &p.full[s]);
+          if (staged) tc::bulk_load(slot + C::O_SL, a.wsell + __ldg(a.sell_off + t), K * TM * 8, &p.full[s]);
         } else {
           const int K = __ldg(a.sell_k + t) & 0xffff;
           const bool staged = K > 0 && K <= C::KCAP;
@@ -518,7 +571,9 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           tc::bulk_commit();
         }
         if (it < my_tiles) {
-          const uint32_t sX = tc::smem_u32(p.ring + ((rb + it) % NS) * C::SLOT);
+          uint32_t sX = tc::smem_u32(p.ring + ((rb + it) % NS) * C::SLOT);
+          if constexpr (C::WIN)  // the tile's own rows inside the window
+            sX += __ldg(a.wdesc + static_cast<size_t>(blockIdx.x + it * gridDim.x) * kWinDesc + 1) * C::BLKB;
           // 3xTF32 with the two A_hi products stacked along N (A_hi is read
           // once for both): D[:, 0:DP] = A_hi·B_lo, D[:, DP:2DP] = A_hi·B_hi +
           // A_lo·B_hi; the epilogue adds the halves.  Each part's B operands
@@ -735,7 +790,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
     }
   };
 
-  const int* tinfo = CSR ? a.tflag : a.sell_k;  // per tile: K_t | has-long << 16 (SELL), has-long (CSR)
+  const int* tinfo = C::CSRL ? a.tflag : a.sell_k;  // per tile: K_t | has-long << 16 (SELL), has-long (CSR)
   int kw = TR ? 0 : __ldg(tinfo + blockIdx.x);
   const int iters = my_tiles + 1 + (TCP ? 1 : 0);
   for (int it = 0; it < iters; ++it) {
@@ -746,8 +801,8 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
     uint8_t* slot = p.ring + (r % NS) * C::SLOT;
     float4 acc[R];
     if (have) {
-      const int K = CSR ? 0 : (kw & 0xffff);
-      const bool haslong = !TR && (CSR ? kw != 0 : (kw >> 16) != 0);
+      const int K = C::CSRL ? 0 : (kw & 0xffff);
+      const bool haslong = !TR && (C::CSRL ? kw != 0 : (kw >> 16) != 0);
       const bool staged = K > 0 && K <= C::KCAP;
       if (!TR) kw = it + 1 < my_tiles ? __ldg(tinfo + tile + gridDim.x) : 0;  // prefetch
 
@@ -787,7 +842,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
                                          reinterpret_cast<const float*>(slot + C::O_V), sj, lj, self, acc);
         else
           gather_csr_rows<DP, R, C::USC>(xbj, stride, a.ci, a.v, sj, lj, self, acc);
-      } else if constexpr (CSR) {
+      } else if constexpr (CSR == 1) {
         const int* rpt = reinterpret_cast<const int*>(slot + C::O_RP);
         const int kb = rpt[0], ke = rpt[min(TM, n - row0)];
         const int a0 = kb & ~3;
@@ -809,7 +864,14 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         else
           gather_csr_rows<DP, R, C::USC>(xbj, DP * 4ull, a.cis, a.vs, sj, lj, self, acc);
       } else {
-        if (staged)
+        if constexpr (C::WIN) {
+          // window rows in shared memory (swizzled like the TMA wrote them)
+          if (staged)
+            gather_win_rows<DP, R, C::US, TM, true>(slot, gl, reinterpret_cast<const int2*>(slot + C::O_SL), K,
+                                                    gid, acc);
+          else
+            gather_win_rows<DP, R, C::US, TM, false>(slot, gl, a.wsell + __ldg(a.sell_off + tile), K, gid, acc);
+        } else if (staged)
           gather_sell_rows<DP, R, C::US, TM, true>(X, gl, reinterpret_cast<const int2*>(slot + C::OPB), K,
                                                    gid, acc);
         else
@@ -841,10 +903,12 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       {
         constexpr int CW = DP / NQ;
         const int q = warp & 3, cq = warp >> 2, m = 32 * q + lane;
+        const uint8_t* xtile = slot;
+        if constexpr (C::WIN) xtile += __ldg(a.wdesc + static_cast<size_t>(tile) * kWinDesc + 1) * C::BLKB;
         float lo[CW];
 #pragma unroll
         for (int c = 0; c < CW; c += 4) {
-          const float4 xl = f4_trunc_lo(*reinterpret_cast<const float4*>(slot + tc::swz_off<DP>(m, cq * CW + c)));
+          const float4 xl = f4_trunc_lo(*reinterpret_cast<const float4*>(xtile + tc::swz_off<DP>(m, cq * CW + c)));
           lo[c] = xl.x;
           lo[c + 1] = xl.y;
           lo[c + 2] = xl.z;
@@ -863,7 +927,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
 }
 
 // One layer as its own launch (norm/lift/layers pipeline of ApplyLaunch).
-template <int DP, bool LAST, typename OutT, bool CSR = false>
+template <int DP, bool LAST, typename OutT, int CSR = 0>
 __global__ void __launch_bounds__(SellCfg<DP>::NT, 1)
 k_layer_sell(DevCsr a, const __grid_constant__ SellMaps maps, const float* __restrict__ X,
              const float* __restrict__ axlong, const float* __restrict__ uwp, NetView net,
@@ -877,7 +941,8 @@ k_layer_sell(DevCsr a, const __grid_constant__ SellMaps maps, const float* __res
     return;
   }
   auto p = sell_setup<DP, CSR>(net.hidden, LAST);
-  sell_layer<DP, LAST, OutT, CSR>(p, a, &maps.x, &maps.y, X, axlong, uwp, net, sc->out_scale, out);
+  sell_layer<DP, LAST, OutT, CSR>(p, a, &maps.x, &maps.y, X, axlong, uwp, net, sc->out_scale, out, nullptr,
+                                  &maps.xw);
   sell_teardown(p);
 }
 
@@ -908,6 +973,7 @@ k_train_sell(DevCsr a, const __grid_constant__ TrainMaps maps, const float* __re
 // ApplyLaunch for matrices without long rows (src/gnn.cpp:120-201).
 struct ApplyFused {
   CUtensorMap x0, x1;           // TMA maps over X[0], X[1]
+  CUtensorMap x0w, x1w;         // the same, box {DP, kWinRows} (windowed mode)
   float* X0;
   float* X1;
   const float* uwp;             // [L][4 DP DP] B operands
@@ -936,7 +1002,7 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* ctr, unsigned l
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-template <int DP, typename InT, typename OutT, bool CSR>
+template <int DP, typename InT, typename OutT, int CSR>
 __global__ void __launch_bounds__(SellCfg<DP>::NT, 1)
 k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restrict__ in, NetView net,
              OutT* __restrict__ out, const int* __restrict__ skip) {
@@ -1047,11 +1113,12 @@ k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restri
     const float* X = (l & 1) ? f.X1 : f.X0;
     const CUtensorMap* mx = (l & 1) ? &f.x1 : &f.x0;
     const CUtensorMap* my = (l & 1) ? &f.x0 : &f.x1;
+    const CUtensorMap* mxw = (l & 1) ? &f.x1w : &f.x0w;
     const float* uw = f.uwp + (size_t)l * 4 * DP * DP;
     if (l + 1 < L)
-      sell_layer<DP, false, OutT, CSR>(p, a, mx, my, X, nullptr, uw, net, out_scale, out);
+      sell_layer<DP, false, OutT, CSR>(p, a, mx, my, X, nullptr, uw, net, out_scale, out, nullptr, mxw);
     else
-      sell_layer<DP, true, OutT, CSR>(p, a, mx, my, X, nullptr, uw, net, out_scale, out);
+      sell_layer<DP, true, OutT, CSR>(p, a, mx, my, X, nullptr, uw, net, out_scale, out, nullptr, mxw);
   }
   stamp();
   sell_teardown(p);

@@ -123,7 +123,10 @@ struct SellCfg {
   static constexpr bool WIN = CSR == 3;                // windowed sliced-ELL
   static constexpr bool CSRL = CSR == 1 || CSR == 2;    // CSR ranges staged per tile
   static_assert(!WIN || DP == 16, "windowed slices are built for d = 16");
-  static constexpr int NS = DP == 16 ? (CSRL ? 5 : 4) : 3;
+#ifndef GNPC_NS_TR32
+#define GNPC_NS_TR32 3
+#endif
+  static constexpr int NS = DP == 16 ? (CSRL ? 5 : 4) : (CSR == 2 ? GNPC_NS_TR32 : 3);
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
   // up to round(K, US) words).  Kept small: every KB of shared memory is L1
   // the X-row gathers hit (C5 fused layer 531 -> 499 us going 24 -> 12)

@@ -22,7 +22,7 @@ except ImportError as _e:  # the build module must stay importable
 
 
 # pure-Python submodules that must import before (or without) the native build
-_SUBMODULES = ("build", "capi", "dp")
+_SUBMODULES = ("build", "capi", "dp", "runrecord")
 
 
 def _retry_native_import() -> bool:

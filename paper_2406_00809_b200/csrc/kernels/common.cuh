@@ -7,7 +7,10 @@
 namespace gnpk {
 
 constexpr int kThreads = 256;     // CTA size used by the streaming kernels
-constexpr int kLongRow = 32;      // rows with more nonzeros take the long-row path
+#ifndef GNPC_LONGROW
+#define GNPC_LONGROW 32
+#endif
+constexpr int kLongRow = GNPC_LONGROW;  // rows with more nonzeros take the long-row path
 
 // Device view of Â (or Âᵀ): int32 indices (nnz < 2^31 enforced on upload),
 // fp32 values.  long_rows lists the rows with > kLongRow nonzeros.

@@ -46,12 +46,26 @@ k_col_norm_partials(const double* __restrict__ b, int n, int B, double* __restri
   }
 }
 
+// One warp per sample: lane l sums blocks l, l+32, ... (8 loads in flight),
+// then a fixed shuffle tree (deterministic).
 __global__ void k_col_norm_finish(const double* __restrict__ partials, int nblk, int n, int B,
                                   SampleScales* __restrict__ sc) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (k >= B) return;
   double t = 0.0;
-  for (int q = 0; q < nblk; ++q) t += partials[static_cast<size_t>(q) * B + k];
+  int q = lane;
+  for (; q + 7 * 32 < nblk; q += 8 * 32) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = partials[static_cast<size_t>(q + 32 * u) * B + k];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t += v[u];
+  }
+  for (; q < nblk; q += 32) t += partials[static_cast<size_t>(q) * B + k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane != 0) return;
   const double tau = sqrt(t), sn = sqrt(static_cast<double>(n));
   sc[k].zero = tau == 0.0;
   sc[k].in_scale = tau == 0.0 ? 0.0 : sn / tau;
@@ -506,10 +520,19 @@ __global__ void k_outer_finish(const double* __restrict__ partials, int nblk, in
                                const int* __restrict__ dst, double* __restrict__ grad) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= PQ) return;
-  double s = 0.0;
-  for (int b = 0; b < nblk; ++b) s += partials[static_cast<size_t>(b) * PQ + idx];
   const int d = dst[idx];
-  if (d >= 0) grad[d] = s;
+  if (d < 0) return;
+  double s = 0.0;
+  int b = 0;
+  for (; b + 8 <= nblk; b += 8) {  // 8 loads in flight, summed in block order
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = partials[static_cast<size_t>(b + u) * PQ + idx];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; b < nblk; ++b) s += partials[static_cast<size_t>(b) * PQ + idx];
+  grad[d] = s;
 }
 
 // ------------------------------------------------------------------ weighted column sums

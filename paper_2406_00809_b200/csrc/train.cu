@@ -342,7 +342,7 @@ struct TrainLaunch {
     const int cg = grid_for(T.n, 8, 1024);
     gnpk::k_col_norm_partials<<<cg, kTh, kTh * sizeof(double), T.s>>>(T.bb.p, T.n, T.B, T.colpart.p);
     GNPC_LAUNCHED();
-    gnpk::k_col_norm_finish<<<(T.B + 63) / 64, 64, 0, T.s>>>(T.colpart.p, cg, T.n, T.B, T.scl.p);
+    gnpk::k_col_norm_finish<<<(T.B + 7) / 8, 256, 0, T.s>>>(T.colpart.p, cg, T.n, T.B, T.scl.p);
     GNPC_LAUNCHED();
     if (T.pw) {
       const size_t smem = (size_t)(T.H + 1) * DP * 2 * 4 + 64 * 4;

@@ -194,6 +194,32 @@ def cpu_reference_baseline(w, seconds=15.0):
                       f"{total:.1f} s, fp32-rounded inputs as f64"}
 
 
+def cpu_reference_train_baseline(ah, n, dims, B):
+    """The unmodified reference forward + L1 loss + backward (oracle/_ref,
+    src/gnn.cpp:120-335) on ONE column of the C3 batch, timed on the host; the
+    reference step runs its B columns over hardware_concurrency() threads
+    (src/gnn.cpp:369-388), so a step is ceil(B / threads) such column times
+    (extrapolated; Adam is negligible)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    rp, ci, v = ah.arrays()
+    csr = oracle.Csr(n, rp, ci, v.astype(np.float32).astype(np.float64))
+    impl, kind = (oracle.reference(), "reference") if oracle.reference_available() else \
+        (oracle.restatement(), "port")
+    p = impl.init_params(*dims, 0)
+    x = np.random.default_rng(1).standard_normal(n)
+    b = impl.spmv(csr, x)
+    t0 = time.perf_counter()
+    impl.batch_loss_grads(csr, dims, p, x, b, 1)
+    col = time.perf_counter() - t0
+    threads = os.cpu_count() or 1
+    step = col * -(-B // threads)
+    return {"value": 1.0 / step, "unit": "steps/s", "cores": threads, "kind": kind,
+            "sample": f"1 column forward+loss+backward at C3 size (n={n}, d={dims[0]}) took {col:.1f} s on "
+                      f"1 core; step = ceil({B}/{threads}) columns-per-thread x that (extrapolated)"}
+
+
 REF_BUDGET_S = 90.0  # bound on the reference arm's timed loop (seconds)
 
 
@@ -331,6 +357,32 @@ def run_train_bench(args, capi, torch, rank, world, local, dist):
     launches = capi.launch_count() - l0
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
+    # e2e: the host-buffer step gnpc_train_step (pinned n x B f64 x and b
+    # copied in every step, loss read back), on one fixed batch
+    e2e = None
+    if not dist:
+        xh = torch.empty((B, n), dtype=torch.float64, pin_memory=True).numpy()
+        bh = torch.empty((B, n), dtype=torch.float64, pin_memory=True).numpy()
+        rng = np.random.default_rng(5)
+        xh[:] = rng.standard_normal((B, n))
+        for k in range(B):
+            bh[k] = ah.spmv(xh[k])
+        xf, bf = xh.reshape(-1), bh.reshape(-1)
+        for _ in range(2):
+            t.step(xf, bf)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ne = max(3, min(args.steps, 10))
+        e0.record(ts)
+        for _ in range(ne):
+            t.step(xf, bf)
+        e1.record(ts)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / ne
+        e2e = {"value": 1e3 / ems, "unit": "steps/s", "h2d_bytes_per_step": 2 * 8 * n * B,
+               "d2h_bytes_per_step": 8, "api": "gnpc_train_step (host f64 x, b; pinned)"}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1 and rank == 0:
+        cpu = cpu_reference_train_baseline(ah, n, dims, B)
     tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -353,7 +405,8 @@ def run_train_bench(args, capi, torch, rank, world, local, dist):
                      "frac": sb / step_s / 1e9 / peak, "traffic": None,
                      "algorithmic_bytes_per_step": sb, "peak_source": peak_src,
                      "kernel": "whole training step"},
-        "loss_first_last": [losses[0], losses[-1]], "clocks": clk, "gpu_launches": int(launches),
+        "loss_first_last": [losses[0], losses[-1]], "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+        "gpu_launches": int(launches),
     }
     print(json.dumps(line), flush=True)
 

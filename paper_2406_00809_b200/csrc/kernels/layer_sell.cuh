@@ -332,6 +332,36 @@ __device__ __forceinline__ void gather_csr_rows(const char* const (&xbj)[R], uns
   }
 }
 
+// Training gather when a group's R rows are consecutive samples of ONE node
+// (bs % R == 0): the node's (col, val) list is read once per entry for all R
+// rows, and row j's X row is row 0's plus j rows (j * DP floats).
+template <int DP, int R, int US>
+__device__ __forceinline__ void gather_csr_node(const char* xb0, unsigned long long stride, const int* ci,
+                                                const float* vv, int s, int len, int self,
+                                                float4 (&acc)[R]) {
+  for (int k = 0; k < len; k += US) {
+    int c[US];
+    float w[US];
+#pragma unroll
+    for (int u = 0; u < US; ++u) {
+      const bool on = k + u < len;
+      c[u] = on ? ci[s + k + u] : self;
+      w[u] = on ? vv[s + k + u] : 0.f;
+    }
+    float4 x[R][US];
+#pragma unroll
+    for (int u = 0; u < US; ++u) {
+      const char* base = xb0 + static_cast<unsigned long long>(static_cast<unsigned>(c[u])) * stride;
+#pragma unroll
+      for (int j = 0; j < R; ++j) x[j][u] = ldg4(reinterpret_cast<const float*>(base + j * DP * 4));
+    }
+#pragma unroll
+    for (int u = 0; u < US; ++u)
+#pragma unroll
+      for (int j = 0; j < R; ++j) fma4(acc[j], w[u], x[j][u]);
+  }
+}
+
 // Training extras for sell_layer (CSR = 2): B virtual rows per node; KIND 1
 // (forward) also stores the tile's ÂX (= the A2_hi operand, raw fp32) through
 // mapax, and at d = 32 the rows' [Y > 0] bits (mask_out, one 32-bit word per
@@ -840,11 +870,12 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           xbj[j] = reinterpret_cast<const char*>(X + static_cast<size_t>(k) * DP + 4 * gl);
         }
         const unsigned long long stride = static_cast<unsigned long long>(bs) * DP * 4;
-        if (st)
-          gather_csr_rows<DP, R, C::USC>(xbj, stride, reinterpret_cast<const int*>(slot + C::O_CI),
-                                         reinterpret_cast<const float*>(slot + C::O_V), sj, lj, self, acc);
+        const int* cis = st ? reinterpret_cast<const int*>(slot + C::O_CI) : a.ci;
+        const float* vs = st ? reinterpret_cast<const float*>(slot + C::O_V) : a.v;
+        if (bs % R == 0)  // the group's rows: consecutive samples of one node
+          gather_csr_node<DP, R, C::USC>(xbj[0], stride, cis, vs, sj[0], lj[0], self[0], acc);
         else
-          gather_csr_rows<DP, R, C::USC>(xbj, stride, a.ci, a.v, sj, lj, self, acc);
+          gather_csr_rows<DP, R, C::USC>(xbj, stride, cis, vs, sj, lj, self, acc);
       } else if constexpr (CSR == 1) {
         const int* rpt = reinterpret_cast<const int*>(slot + C::O_RP);
         const int kb = rpt[0], ke = rpt[min(TM, n - row0)];

@@ -16,35 +16,47 @@
 // operand as is: kind::tf32 truncates); Y_lo and g_z hi/lo go to TMEM (TS-form
 // MMAs), so no operand crosses shared memory twice.
 //
+//   MMA3   (backward) dec1 / dec1_b gradient [X_L | 1]ᵀ · g_z accumulated
+//          in TMEM (bf16 hi/lo, MN-major: the wgb operand layout of
+//          wgrad_tc.cuh), folded into per-CTA f64 partials every wgb::kFlushBf
+//          tiles — g_z never goes to HBM
+//
 // TMEM columns: [0, 64) accumulator (MMA1, then MMA2), [64, 96) Y_lo then
-// g_z lo, [96, 128) g_z hi.
+// g_z lo, [96, 128) g_z hi, backward: [128, 160) the M = 64 weight-gradient
+// accumulator.
 #pragma once
 
 #include "layer_sell.cuh"
 #include "train.cuh"
+#include "wgrad_tc.cuh"
 
 namespace gnpk {
 
+template <bool FWD>
 struct DecTc {
-  static constexpr int TM = 128, NS = 3, NT = 128;
+  static constexpr bool WG = !FWD;                       // fused dec1 / dec1_b gradient
+  static constexpr int TM = 128, NS = FWD ? 3 : 2, NT = 128;
   static constexpr uint32_t OPB = TM * 32 * 4;           // one [128][32] fp32 tile
   static constexpr uint32_t O_RING = 0;
   static constexpr uint32_t O_B1 = NS * OPB;              // [D1_lo; D1_hi]: rows h, K = j
   static constexpr uint32_t O_B2 = O_B1 + 64 * 128;       // [DT_lo; DT_hi]: rows j, K = h
-  static constexpr uint32_t O_SM = O_B2 + 64 * 128;       // b1[32], dec2[32]
+  static constexpr uint32_t O_WG = O_B2 + 64 * 128;       // Ahi | Alo | Bhi | Blo (wgb layouts)
+  static constexpr uint32_t O_SM = O_WG + (WG ? wgb::OPS : 0);  // b1[32], dec2[32]
   static constexpr uint32_t O_BAR = O_SM + 64 * 4;        // full[NS], mma
   static size_t smem_bytes() { return O_BAR + 8 * (NS + 1) + 16 + 1024; }
-  static constexpr int TCOLS = 128;
+  static constexpr int TCOLS = WG ? 256 : 128;
 };
 
-// partials: [gridDim.x][33] per-CTA sums (dec2[h], then dec2_b) in f64.
+// partials: [gridDim.x][33] per-CTA sums (dec2[h], then dec2_b) in f64;
+// wpart: [gridDim.x][64][32] per-CTA dec1 (rows j < 32) / dec1_b (row 32)
+// gradient partials in the wgrad partial layout (backward).
 template <bool FWD>
-__global__ void __launch_bounds__(DecTc::NT, 3)
+__global__ void __launch_bounds__(DecTc<FWD>::NT, FWD ? 3 : 2)
 k_decoder_tc(const __grid_constant__ CUtensorMap mapy, const float* __restrict__ Y, int nv, int B,
              NetView net, const SampleScales* __restrict__ sc, const double* __restrict__ gout,
-             double* __restrict__ out, float* __restrict__ gdp, float* __restrict__ gpre,
-             double* __restrict__ partials) {
-  using C = DecTc;
+             double* __restrict__ out, float* __restrict__ gpre, double* __restrict__ partials,
+             double* __restrict__ wpart) {
+  using C = DecTc<FWD>;
   extern __shared__ float4 smem_raw[];
   const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* base = reinterpret_cast<uint8_t*>(smem_raw) + pad;
@@ -73,6 +85,19 @@ k_decoder_tc(const __grid_constant__ CUtensorMap mapy, const float* __restrict__
     b1[tid] = net.dec1_b[tid];
     d2[tid] = net.dec2[tid];
   }
+  uint8_t* WA = base + C::O_WG;  // Ahi | Alo | Bhi | Blo
+  if constexpr (C::WG) {
+    // A = [X_L | 1 | 0]: features 32..63 are constant (1.0 at 32: dec1_b)
+    for (int j = tid; j < C::TM * 32; j += C::NT) {
+      const int r = j / 32, m = 32 + j % 32;
+      *reinterpret_cast<__nv_bfloat16*>(WA + wgb::offA(r, m)) = __float2bfloat16_rn(m == 32 ? 1.f : 0.f);
+      *reinterpret_cast<__nv_bfloat16*>(WA + wgb::OPA + wgb::offA(r, m)) = __float2bfloat16_rn(0.f);
+    }
+    // this CTA's partials: thread (warp q, lane < 16) owns row 16 q + lane
+    if ((tid & 31) < 16)
+      for (int c = 0; c < 32; ++c)
+        wpart[static_cast<size_t>(blockIdx.x) * 2048 + (16 * (tid >> 5) + (tid & 31)) * 32 + c] = 0.0;
+  }
   if (tid == 0) {
     for (int s = 0; s < C::NS; ++s) tc::mbar_init(&full[s], 1);
     tc::mbar_init(mbar, 1);
@@ -99,7 +124,8 @@ k_decoder_tc(const __grid_constant__ CUtensorMap mapy, const float* __restrict__
     for (int it = 0; it < C::NS; ++it) issue(it);
   }
   const uint32_t trow = static_cast<uint32_t>(32 * warp) << 16;  // this warp's lane quarter
-  const uint32_t tD = tmem, tR1 = tmem + 64, tR2 = tmem + 96;
+  const uint32_t tD = tmem, tR1 = tmem + 64, tR2 = tmem + 96, tW = tmem + 128;
+  int since_flush = 0;
   const uint32_t i64 = tc::idesc_tf32(128, 64), i32 = tc::idesc_tf32(128, 32);
   const uint32_t sB1 = tc::smem_u32(B1), sB2 = tc::smem_u32(B2);
   float acc[33];
@@ -144,6 +170,16 @@ k_decoder_tc(const __grid_constant__ CUtensorMap mapy, const float* __restrict__
     }
 #pragma unroll
     for (int c = 0; c < 32; ++c) ymask |= (y[c] > 0.f ? 1u : 0u) << c;
+    if constexpr (C::WG) {  // this row of [X_L | 1] as bf16 hi/lo (MMA3 of the previous tile completed)
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint4 hi, lo;
+        wgb::split8(make_float4(y[8 * c8], y[8 * c8 + 1], y[8 * c8 + 2], y[8 * c8 + 3]),
+                    make_float4(y[8 * c8 + 4], y[8 * c8 + 5], y[8 * c8 + 6], y[8 * c8 + 7]), hi, lo);
+        *reinterpret_cast<uint4*>(WA + wgb::offA(tid, 8 * c8)) = hi;
+        *reinterpret_cast<uint4*>(WA + wgb::OPA + wgb::offA(tid, 8 * c8)) = lo;
+      }
+    }
 #pragma unroll
     for (int c = 0; c < 32; c += 8) {
       float lo[8];
@@ -196,12 +232,15 @@ k_decoder_tc(const __grid_constant__ CUtensorMap mapy, const float* __restrict__
         acc[h] = fmaf(relu(p[h]), gy, acc[h]);
       }
       acc[32] += gy;
-      // the slot is free once MMA1 completed: it stages the tile's g_z rows
-      // (swizzled, conflict-free), written out coalesced (the tile's rows are
-      // one contiguous 16 KB block)
+      // g_z as the weight gradient's B operand (bf16 hi/lo, MN-major)
 #pragma unroll
-      for (int c = 0; c < 32; c += 4)
-        *reinterpret_cast<float4*>(yt + tc::swz_off<32>(tid, c)) = make_float4(gz[c], gz[c + 1], gz[c + 2], gz[c + 3]);
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint4 hi, lo;
+        wgb::split8(make_float4(gz[8 * c8], gz[8 * c8 + 1], gz[8 * c8 + 2], gz[8 * c8 + 3]),
+                    make_float4(gz[8 * c8 + 4], gz[8 * c8 + 5], gz[8 * c8 + 6], gz[8 * c8 + 7]), hi, lo);
+        *reinterpret_cast<uint4*>(WA + 2 * wgb::OPA + wgb::offB(tid, 8 * c8)) = hi;
+        *reinterpret_cast<uint4*>(WA + 2 * wgb::OPA + wgb::OPB + wgb::offB(tid, 8 * c8)) = lo;
+      }
 #pragma unroll
       for (int c = 0; c < 32; c += 8) {
         float hi[8], lo[8];
@@ -214,15 +253,28 @@ k_decoder_tc(const __grid_constant__ CUtensorMap mapy, const float* __restrict__
         tc::tmem_st8(tR1 + trow + c, lo);
       }
       tc::tmem_wait_st();
+      tc::fence_proxy_async();
       tc::fence_before();
       __syncthreads();
-      store_tile(gdp);
       if (tid == 0) {
         tc::fence_after();
 #pragma unroll
         for (int k8 = 0; k8 < 4; ++k8) {
           tc::mma_tf32_ts(tD, tR2 + 8 * k8, tc::make_desc_swz<32>(sB2 + k8 * 32), i64, k8 > 0);
           tc::mma_tf32_ts(tD + 32, tR1 + 8 * k8, tc::make_desc_swz<32>(sB2 + 4096 + k8 * 32), i32, 1);
+        }
+        // MMA3: Dw (+)= [X_L | 1]ᵀ g_z, products hi·hi + hi·lo + lo·hi
+        const uint32_t sAh = tc::smem_u32(WA), sAl = sAh + wgb::OPA;
+        const uint32_t sBh = sAl + wgb::OPA, sBl = sBh + wgb::OPB;
+        uint32_t accw = since_flush > 0 ? 1u : 0u;
+#pragma unroll
+        for (int ks = 0; ks < C::TM / 16; ++ks) {
+          const uint64_t ah = wgb::desc_mn(sAh + ks * 2048, 1024, 2), al = wgb::desc_mn(sAl + ks * 2048, 1024, 2);
+          const uint64_t bh = wgb::desc_mn(sBh + ks * 1024, 512, 4), bl = wgb::desc_mn(sBl + ks * 1024, 512, 4);
+          wgb::mma_bf16(tW, ah, bh, accw);
+          accw = 1;
+          wgb::mma_bf16(tW, ah, bl, 1);
+          wgb::mma_bf16(tW, al, bh, 1);
         }
         tc::mma_commit(mbar);
       }
@@ -240,8 +292,22 @@ k_decoder_tc(const __grid_constant__ CUtensorMap mapy, const float* __restrict__
           for (int e = 0; e < 16; ++e) g[j0 + e] = (ymask >> (j0 + e)) & 1u ? u[e] + w[e] : 0.f;
         }
       }
+      if (++since_flush == wgb::kFlushBf || it + 1 == my) {  // Dw -> this CTA's f64 partials
+        float w1[16], w2[16];
+        tc::tmem_ld16(tW + trow, w1);
+        tc::tmem_ld16(tW + trow + 16, w2);
+        if (lane < 16) {
+          double* dst = wpart + static_cast<size_t>(blockIdx.x) * 2048 + (16 * warp + lane) * 32;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            dst[c] += static_cast<double>(w1[c]);
+            dst[16 + c] += static_cast<double>(w2[c]);
+          }
+        }
+        since_flush = 0;
+      }
       tc::fence_before();
-      __syncthreads();  // every thread's g_z left the slot
+      __syncthreads();  // every thread's G rows may enter the slot
 #pragma unroll
       for (int c = 0; c < 32; c += 4)
         *reinterpret_cast<float4*>(yt + tc::swz_off<32>(tid, c)) = make_float4(g[c], g[c + 1], g[c + 2], g[c + 3]);

@@ -98,8 +98,8 @@ struct gnpc_trainer_s {
   // tensor-core decoder (d = hidden = 32 on the TMA maps): dec2 / dec2_b
   // per-CTA sums folded by k_outer_finish through dec_dst
   bool dec_tc = false;
-  int dec_grid = 0;
-  DevBuf<double> decpart;
+  int dec_grid = 0, dec_grid_bwd = 0;
+  DevBuf<double> decpart, decwpart;
   DevBuf<int> dec_dst;
 };
 
@@ -360,9 +360,9 @@ struct TrainLaunch {
       layer(T, true, l, T.Xs.p + l * act, T.Xs.p + (l + 1) * act, T.AXs.p + l * act, nullptr);
     if constexpr (DP == 32) {
       if (T.dec_tc) {
-        const size_t smem = gnpk::DecTc::smem_bytes();
+        const size_t smem = gnpk::DecTc<true>::smem_bytes();
         set_smem_once((const void*)gnpk::k_decoder_tc<true>, smem);
-        gnpk::k_decoder_tc<true><<<T.dec_grid, gnpk::DecTc::NT, smem, T.s>>>(
+        gnpk::k_decoder_tc<true><<<T.dec_grid, gnpk::DecTc<true>::NT, smem, T.s>>>(
             T.mX[T.L], T.Xs.p + T.L * act, T.nv, T.B, net, T.scl.p, nullptr, T.out.p, nullptr, nullptr,
             nullptr);
         GNPC_LAUNCHED();
@@ -384,15 +384,18 @@ struct TrainLaunch {
     bool dec_done = false;
     if constexpr (DP == 32) {
       if (T.dec_tc) {
-        const size_t smem = gnpk::DecTc::smem_bytes();
+        const size_t smem = gnpk::DecTc<false>::smem_bytes();
         set_smem_once((const void*)gnpk::k_decoder_tc<false>, smem);
-        gnpk::k_decoder_tc<false><<<T.dec_grid, gnpk::DecTc::NT, smem, T.s>>>(
-            T.mX[T.L], T.Xs.p + T.L * act, T.nv, T.B, net, T.scl.p, T.gout.p, nullptr, T.hb2.p, T.G[0].p,
-            T.decpart.p);
+        gnpk::k_decoder_tc<false><<<T.dec_grid_bwd, gnpk::DecTc<false>::NT, smem, T.s>>>(
+            T.mX[T.L], T.Xs.p + T.L * act, T.nv, T.B, net, T.scl.p, T.gout.p, nullptr, T.G[0].p, T.decpart.p,
+            T.decwpart.p);
         GNPC_LAUNCHED();
-        gnpk::k_outer_finish<<<1, 64, 0, T.s>>>(T.decpart.p, T.dec_grid, 33, T.dec_dst.p, T.g64.p);
+        gnpk::k_outer_finish<<<1, 64, 0, T.s>>>(T.decpart.p, T.dec_grid_bwd, 33, T.dec_dst.p, T.g64.p);
         GNPC_LAUNCHED();
-        run_red(T, T.red_dec1);
+        // dec1 / dec1_b from the fused [X_L | 1]ᵀ g_z partials (red_dec1's layout)
+        gnpk::k_outer_finish<<<(64 * 32 + kTh - 1) / kTh, kTh, 0, T.s>>>(T.decwpart.p, T.dec_grid_bwd, 64 * 32,
+                                                                        T.red_dec1.dst.p, T.g64.p);
+        GNPC_LAUNCHED();
         dec_done = true;
       }
     }
@@ -635,26 +638,29 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
     }();
     T->dec_tc = !off && T->sell && T->tc && T->dp == 32 && T->H == 32;
     if (T->dec_tc) {
-      const size_t smem = gnpk::DecTc::smem_bytes();
-      set_smem_once((const void*)gnpk::k_decoder_tc<true>, smem);
-      set_smem_once((const void*)gnpk::k_decoder_tc<false>, smem);
-      // several CTAs per SM overlap each other's per-tile round trips
-      for (const void* kf : {(const void*)gnpk::k_decoder_tc<true>, (const void*)gnpk::k_decoder_tc<false>})
-        GNPC_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                       cudaSharedmemCarveoutMaxShared));
       // residency by registers / smem / TMEM (the occupancy API reports 1 CTA
       // per SM for kernels that allocate TMEM; see tc_ctas_per_sm)
-      cudaFuncAttributes fa{};
-      GNPC_CUDA(cudaFuncGetAttributes(&fa, gnpk::k_decoder_tc<false>));
-      int dev = 0, smem_sm = 0, regs_sm = 0;
-      GNPC_CUDA(cudaGetDevice(&dev));
-      GNPC_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-      GNPC_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
-      int per_sm = std::min(regs_sm / (((fa.numRegs + 7) / 8) * 8 * gnpk::DecTc::NT),
-                            smem_sm / (int)(smem + fa.sharedSizeBytes + 1024));
-      per_sm = std::max(1, std::min(per_sm, 512 / gnpk::DecTc::TCOLS));
-      T->dec_grid = std::max(1, std::min(per_sm * T->sms, (T->nv + 127) / 128));
-      T->decpart.alloc((std::size_t)T->dec_grid * 33);
+      auto ctas = [&](const void* kf, size_t smem, int nt, int tcols) {
+        set_smem_once(kf, smem);
+        GNPC_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       cudaSharedmemCarveoutMaxShared));
+        cudaFuncAttributes fa{};
+        GNPC_CUDA(cudaFuncGetAttributes(&fa, kf));
+        int dev = 0, smem_sm = 0, regs_sm = 0;
+        GNPC_CUDA(cudaGetDevice(&dev));
+        GNPC_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+        GNPC_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+        int per_sm = std::min(regs_sm / (((fa.numRegs + 7) / 8) * 8 * nt),
+                              smem_sm / (int)(smem + fa.sharedSizeBytes + 1024));
+        per_sm = std::max(1, std::min(per_sm, 512 / tcols));
+        return std::max(1, std::min(per_sm * T->sms, (T->nv + 127) / 128));
+      };
+      T->dec_grid = ctas((const void*)gnpk::k_decoder_tc<true>, gnpk::DecTc<true>::smem_bytes(),
+                         gnpk::DecTc<true>::NT, gnpk::DecTc<true>::TCOLS);
+      T->dec_grid_bwd = ctas((const void*)gnpk::k_decoder_tc<false>, gnpk::DecTc<false>::smem_bytes(),
+                             gnpk::DecTc<false>::NT, gnpk::DecTc<false>::TCOLS);
+      T->decpart.alloc((std::size_t)T->dec_grid_bwd * 33);
+      T->decwpart.alloc((std::size_t)T->dec_grid_bwd * 64 * 32);
       const gnp_b200::ParamLayout lay = gnp_b200::param_layout(m->dims);
       std::vector<int> dst(33);
       for (int h = 0; h < 32; ++h) dst[h] = (int)(lay.dec2 + h);

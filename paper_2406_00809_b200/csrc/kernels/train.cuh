@@ -779,33 +779,43 @@ __global__ void k_lift_tables(const double* __restrict__ p, EncOff o, int DP, Li
     const int h = t / o.d, j = t % o.d;
     e2[t] = p[o.enc2 + j * o.H + h];
   }
+  __shared__ double tk[64];
+  __shared__ int valid[64];
   __syncthreads();
+  // sorted distinct kinks in parallel: unit h keeps its kink when no earlier
+  // unit has the same value; its slot = #distinct kept values below it
+  for (int h = threadIdx.x; h < o.H; h += blockDim.x) {
+    valid[h] = e1[h] != 0.0;
+    tk[h] = valid[h] ? -b1[h] / e1[h] : 0.0;
+  }
+  __shared__ int first[64];  // unit h holds its value's first occurrence
+  __syncthreads();
+  for (int h = threadIdx.x; h < o.H; h += blockDim.x) {
+    int f = valid[h];
+    for (int r = 0; r < h && f; ++r) f = !(valid[r] && tk[r] == tk[h]);
+    first[h] = f;
+  }
+  __syncthreads();
+  int keep = 0;
+  if (threadIdx.x < o.H && first[threadIdx.x]) {
+    const double t = tk[threadIdx.x];
+    int slot = 0;
+    for (int q = 0; q < o.H; ++q) slot += first[q] && tk[q] < t;
+    kinks[slot] = t;
+    keep = 1;
+  }
+  const int nb = __syncthreads_count(keep);
   if (threadIdx.x == 0) {
-    int nb = 0;
-    for (int h = 0; h < o.H; ++h) {
-      if (e1[h] == 0.0) continue;
-      const double t = -b1[h] / e1[h];
-      bool dup = false;
-      for (int q = 0; q < nb; ++q) dup = dup || kinks[q] == t;
-      if (dup) continue;
-      int k = nb++;
-      while (k > 0 && kinks[k - 1] > t) {
-        kinks[k] = kinks[k - 1];
-        --k;
-      }
-      kinks[k] = t;
-    }
-    for (int k = 0; k <= nb; ++k) {
-      if (nb == 0) vr[k] = 0.0;
-      else if (k == 0) vr[k] = kinks[0] - 1.0 - fabs(kinks[0]);
-      else if (k == nb) vr[k] = kinks[nb - 1] + 1.0 + fabs(kinks[nb - 1]);
-      else vr[k] = 0.5 * (kinks[k - 1] + kinks[k]);
-    }
     nbs = nb;
     *tab.nb = nb;
   }
+  for (int k = threadIdx.x; k <= nb; k += blockDim.x) {
+    if (nb == 0) vr[k] = 0.0;
+    else if (k == 0) vr[k] = kinks[0] - 1.0 - fabs(kinks[0]);
+    else if (k == nb) vr[k] = kinks[nb - 1] + 1.0 + fabs(kinks[nb - 1]);
+    else vr[k] = 0.5 * (kinks[k - 1] + kinks[k]);
+  }
   __syncthreads();
-  const int nb = nbs;
   for (int k = threadIdx.x; k < nb; k += blockDim.x) tab.t[k] = static_cast<float>(kinks[k]);
   for (int idx = threadIdx.x; idx < (nb + 1) * DP; idx += blockDim.x) {
     const int k = idx / DP, j = idx % DP;
@@ -1012,33 +1022,39 @@ __global__ void k_enc_fold(const double* __restrict__ partials, int nblk, int pe
 // (reference slots via EncOff).
 __global__ void k_enc_grads(const double* __restrict__ Sg, int DP, LiftTab tab,
                             const double* __restrict__ p, EncOff o, double* __restrict__ grad) {
-  extern __shared__ double S[];  // [(H+1)][2][DP]
-  const int H = o.H, per = (H + 1) * 2 * DP;
+  extern __shared__ double S[];  // [(H+1)][2][DP], then X, Y [H][d]
+  const int H = o.H, d = o.d, per = (H + 1) * 2 * DP;
+  double* Xs = S + per;  // X(h, j) = Σ_{q: h active} Sx[q][j]
+  double* Ys = Xs + H * d;  // Y(h, j) = Σ_{q: h active} S1[q][j]
+  __shared__ unsigned long long act[65];
   const int nb = *tab.nb;
   for (int t = threadIdx.x; t < per; t += blockDim.x) S[t] = Sg[t];
+  for (int q = threadIdx.x; q <= nb; q += blockDim.x) act[q] = tab.act[q];
   __syncthreads();
-  for (int idx = threadIdx.x; idx < H * o.d; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < H * d; idx += blockDim.x) {
     const int h = idx % H, j = idx / H;
-    const double w = p[o.enc1 + h], bb = p[o.enc1_b + h];
-    double s = 0.0;
+    double x = 0.0, y = 0.0;
     for (int q = 0; q <= nb; ++q)
-      if ((tab.act[q] >> h) & 1ull) s += w * S[q * 2 * DP + DP + j] + bb * S[q * 2 * DP + j];
-    grad[o.enc2 + j * H + h] = s;
+      if ((act[q] >> h) & 1ull) {
+        x += S[q * 2 * DP + DP + j];
+        y += S[q * 2 * DP + j];
+      }
+    Xs[h * d + j] = x;
+    Ys[h * d + j] = y;
+    grad[o.enc2 + j * H + h] = p[o.enc1 + h] * x + p[o.enc1_b + h] * y;
   }
-  for (int j = threadIdx.x; j < o.d; j += blockDim.x) {
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
     double s = 0.0;
     for (int q = 0; q <= nb; ++q) s += S[q * 2 * DP + j];
     grad[o.enc2_b + j] = s;
   }
+  __syncthreads();
   for (int h = threadIdx.x; h < H; h += blockDim.x) {
     double gw = 0.0, gb = 0.0;
-    for (int q = 0; q <= nb; ++q) {
-      if (!((tab.act[q] >> h) & 1ull)) continue;
-      for (int j = 0; j < o.d; ++j) {
-        const double e = p[o.enc2 + j * H + h];
-        gw += e * S[q * 2 * DP + DP + j];
-        gb += e * S[q * 2 * DP + j];
-      }
+    for (int j = 0; j < d; ++j) {
+      const double e = p[o.enc2 + j * H + h];
+      gw += e * Xs[h * d + j];
+      gb += e * Ys[h * d + j];
     }
     grad[o.enc1 + h] = gw;
     grad[o.enc1_b + h] = gb;

@@ -429,7 +429,7 @@ struct TrainLaunch {
       double* S = T.encpart.p + (size_t)T.enc_grid * per;
       gnpk::k_enc_fold<<<(per + 63) / 64, 64, 0, T.s>>>(T.encpart.p, T.enc_grid, per, S);
       GNPC_LAUNCHED();
-      const size_t fs = (size_t)per * 8;
+      const size_t fs = (size_t)(per + 2 * T.H * T.d) * 8;
       set_smem_once((const void*)gnpk::k_enc_grads, fs);
       gnpk::k_enc_grads<<<1, kTh, fs, T.s>>>(S, DP, T.tab, T.p64.p, T.eoff, T.g64.p);
       GNPC_LAUNCHED();

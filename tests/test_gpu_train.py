@@ -210,3 +210,47 @@ print(json.dumps({"loss": loss, "g": list(g)}))
     assert abs(outs[0]["loss"] - outs[1]["loss"]) <= 1e-6 * abs(outs[1]["loss"])
     g0, g1 = np.array(outs[0]["g"]), np.array(outs[1]["g"])
     assert np.linalg.norm(g0 - g1) <= 1e-4 * np.linalg.norm(g1)
+
+
+@pytest.mark.parametrize("switch", ["GNPC_NO_PW_ENCODER", "GNPC_NO_DEC_TC"])
+def test_encoder_decoder_paths_match_mlp_kernels(capi, oc, cuda, switch):
+    # the piecewise-linear encoder (lift tables + interval sums) and the
+    # tensor-core decoder against the CUDA-core MLP kernels they replace
+    # (switched off in a subprocess), both against the oracle
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import json, sys, numpy as np
+sys.path.insert(0, ".")
+sys.path.insert(0, "oracle")
+from paper_2406_00809_b200 import capi
+import oracle
+oc = oracle.restatement()
+a = oc.prescale(oc.gen_convection_diffusion(20, 0.3), 8.6).rounded_f32()
+p = oc.init_params(32, 32, 3, 4).astype(np.float64)
+p[32:64] = 0.3 * np.sin(np.arange(32))  # nonzero enc1 biases (flat order: enc1, enc1_b, ...): distinct kinks
+p = p.astype(np.float32).astype(np.float64)
+x, b = oc.gaussian_batch(a, 6, 0, 8)
+A = capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
+t = capi.Trainer(capi.Model(A, (32, 32, 3), p), 8)
+loss, g, _ = t.forward_backward(x, b)
+l2, g2 = oc.batch_loss_grads(a, (32, 32, 3), p, x, b, 8)
+print(json.dumps({"loss": loss, "g": list(g), "want_loss": l2, "want": list(g2)}))
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for off in ("0", "1"):
+        env = dict(os.environ, **{switch: off})
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    want = np.array(outs[0]["want"])
+    for o in outs:
+        assert abs(o["loss"] - o["want_loss"]) <= 1e-5 * abs(o["want_loss"])
+        check_grads(np.array(o["g"]), want, (32, 32, 3))
+    g0, g1 = np.array(outs[0]["g"]), np.array(outs[1]["g"])
+    assert np.linalg.norm(g0 - g1) <= 1e-4 * np.linalg.norm(g1)

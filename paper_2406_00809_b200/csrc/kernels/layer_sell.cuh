@@ -1078,9 +1078,12 @@ k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restri
     }
     target += gridDim.x;
     grid_barrier(f.gbar, target);
-    if (tid == 0) {
+    if (tid < 32) {  // every CTA folds the partials the same way: lane-strided, then a fixed tree
       double t = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) t += reinterpret_cast<volatile double*>(f.partials)[b];
+      for (int b = tid; b < (int)gridDim.x; b += 32) t += reinterpret_cast<volatile double*>(f.partials)[b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (tid == 0) {
       const double tau = sqrt(t);
       const double sn = sqrt(static_cast<double>(n));
       s_scale[0] = tau == 0.0 ? 0.0 : sn / tau;
@@ -1090,6 +1093,7 @@ k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restri
         f.sc->zero = tau == 0.0;
         f.sc->in_scale = s_scale[0];
         f.sc->out_scale = s_scale[1];
+      }
       }
     }
     __syncthreads();
@@ -1117,21 +1121,33 @@ k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restri
     const int gl = tid % G;
     const int ntiles = (n + C::TM - 1) / C::TM;
     const InT* src = f.stash ? static_cast<const InT*>(f.stash) : in;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      for (int r = tid / G; r < C::TM; r += C::NT / G) {
-        const int row = tile * C::TM + r;
-        if (row >= n) break;
-        const float v = static_cast<float>(in_scale * static_cast<double>(src[row]));
+    // a thread's rows of up to LT of this CTA's tiles at once: their input
+    // loads are in flight together (one tile per pass left the load latency
+    // exposed 14 times per apply at C2)
+    constexpr int LT = 8;
+    for (int r = tid / G; r < C::TM; r += C::NT / G)
+    for (int t0 = blockIdx.x; t0 < ntiles; t0 += LT * gridDim.x) {
+      float v[LT];
+#pragma unroll
+      for (int k = 0; k < LT; ++k) {
+        const int row = (t0 + k * gridDim.x) * C::TM + r;
+        v[k] = row < n ? static_cast<float>(in_scale * static_cast<double>(src[row])) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < LT; ++k) {
+        const int row = (t0 + k * gridDim.x) * C::TM + r;
+        if (row >= n) continue;
         int lo = 0, hi = nb;  // interval = #kinks <= v
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          if (s_t[mid] <= v) lo = mid + 1;
+          if (s_t[mid] <= v[k]) lo = mid + 1;
           else hi = mid;
         }
         const float4 al = *reinterpret_cast<const float4*>(s_a + lo * DP + 4 * gl);
         const float4 be = *reinterpret_cast<const float4*>(s_b + lo * DP + 4 * gl);
         st4(f.X0 + static_cast<size_t>(row) * DP + 4 * gl,
-            make_float4(fmaf(al.x, v, be.x), fmaf(al.y, v, be.y), fmaf(al.z, v, be.z), fmaf(al.w, v, be.w)));
+            make_float4(fmaf(al.x, v[k], be.x), fmaf(al.y, v[k], be.y), fmaf(al.z, v[k], be.z),
+                        fmaf(al.w, v[k], be.w)));
       }
     }
     __syncthreads();

@@ -416,7 +416,13 @@ __global__ void __launch_bounds__(wgt::TH, 1) k_wgrad_tma(const __grid_constant_
 
 namespace gnpk {
 namespace wgb {
-constexpr int TM = 128, TH = 512, NSTG = 3, NOPS = 1;
+#ifndef GNPC_WGB_NSTG
+#define GNPC_WGB_NSTG 2
+#endif
+#ifndef GNPC_WGB_NOPS
+#define GNPC_WGB_NOPS 2  // double-buffered operands: conversion of tile k overlaps MMA(k-1) (C3 22.6 -> 22.3 ms vs 3 stages x 1 set)
+#endif
+constexpr int TM = 128, TH = 512, NSTG = GNPC_WGB_NSTG, NOPS = GNPC_WGB_NOPS;
 constexpr uint32_t ARR = TM * 128;   // one staged fp32 array tile (16 KiB)
 constexpr uint32_t STAGE = 3 * ARR;  // A1 | A2 | B
 constexpr uint32_t OPA = TM * 128;   // bf16 [128 rows][64 features], SW128 (16 KiB)

@@ -124,7 +124,7 @@ struct SellCfg {
   static constexpr bool CSRL = CSR == 1 || CSR == 2;    // CSR ranges staged per tile
   static_assert(!WIN || DP == 16, "windowed slices are built for d = 16");
 #ifndef GNPC_NS_TR32
-#define GNPC_NS_TR32 3
+#define GNPC_NS_TR32 4  // ring depth of the training layers (fits with GNPC_CAPC_TR 256): C3 22.0 -> 20.3 ms vs 3
 #endif
   static constexpr int NS = DP == 16 ? (CSRL ? 5 : 4) : (CSR == 2 ? GNPC_NS_TR32 : 3);
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
@@ -139,7 +139,10 @@ struct SellCfg {
   static constexpr uint32_t CVB = KCAP * TM * 8; // staged slice (bytes)
   // CSR: [X tile | row_ptr slice (TM+4 ints, 1 KiB) | col_idx (CAPC) | values (CAPC)]
   static constexpr bool TR = CSR == 2;
-  static constexpr int CAPC = TR ? 512 : (DP == 16 ? 2048 : 1024);  // staged nonzeros per tile (DP=32
+#ifndef GNPC_CAPC_TR
+#define GNPC_CAPC_TR 256  // C3 tiles stage ~20 entries (4 nodes); 512 measured 0.4 % slower (less L1)
+#endif
+  static constexpr int CAPC = TR ? GNPC_CAPC_TR : (DP == 16 ? 2048 : 1024);  // staged nonzeros per tile (DP=32
                                                                      // apply: fits the projection operands)
   static constexpr uint32_t RPB = (TM + 4) * 4;  // row_ptr slice copy (bytes, 16-B multiple)
   // training backward mask [X_l > 0]: at d = 32 one 32-bit word per row

@@ -886,7 +886,13 @@ k_lift_pw_batched(const double* __restrict__ b, int nv, int B, LiftTab tab, int 
 // and no two lanes ever touch the same word).  The sets fold into the
 // block's f64 sums in a fixed order after every kEncCh rows per set:
 // deterministic for a fixed grid.  Output: partials[blk][(H+1)*2*DP].
-constexpr int kEncCh = 128, kEncStg = 128, kEncNS = 3;
+#ifndef GNPC_ENC_STG
+#define GNPC_ENC_STG 128
+#endif
+#ifndef GNPC_ENC_NS
+#define GNPC_ENC_NS 3
+#endif
+constexpr int kEncCh = 128, kEncStg = GNPC_ENC_STG, kEncNS = GNPC_ENC_NS;
 // set stride padded by GL floats when a warp holds several sub-groups, so
 // the sub-groups land on different banks
 inline size_t enc_bucket_smem(int DP, int H, int warps) {

@@ -346,7 +346,10 @@ struct TrainLaunch {
     GNPC_LAUNCHED();
     if (T.pw) {
       const size_t smem = (size_t)(T.H + 1) * DP * 2 * 4 + 64 * 4;
-      const int g = grid_for(T.nv, kTh / (DP / 4), T.sms * 8);
+#ifndef GNPC_LIFT_BPS
+#define GNPC_LIFT_BPS 8
+#endif
+      const int g = grid_for(T.nv, kTh / (DP / 4), T.sms * GNPC_LIFT_BPS);
       gnpk::k_lift_pw_batched<DP><<<g, kTh, smem, T.s>>>(T.bb.p, T.nv, T.B, T.tab, T.H, T.scl.p, T.Xs.p,
                                                           T.vv.p);
       GNPC_LAUNCHED();
@@ -617,7 +620,10 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
       T->eoff = gnpk::EncOff{(int)lay.enc1, (int)lay.enc1_b, (int)lay.enc2, (int)lay.enc2_b, H, T->d};
       // warps per block: as many as fit the staging ring + accumulator sets
       // (at least 4: a warp walks kEncStg / warps <= 32 rows per stage)
-      T->enc_warps = 8;
+#ifndef GNPC_ENC_WARPS
+#define GNPC_ENC_WARPS 8
+#endif
+      T->enc_warps = GNPC_ENC_WARPS;
       if (gnpk::enc_bucket_smem(dp, H, T->enc_warps) > 220 * 1024) T->enc_warps = 4;
       if (gnpk::enc_bucket_smem(dp, H, T->enc_warps) > 220 * 1024) T->pw = false;
     }

@@ -203,18 +203,24 @@ struct ApplyLaunch {
           // on ragged ones
           using S = SellCfg<DP, false>;
           constexpr int W = DP == 16 ? 3 : 0;
+          // d = 32 non-last sliced-ELL layers: the 4-deep ring (mode 4)
+          constexpr int D4 = DP == 32 ? 4 : 0;
+          const bool deep = DP == 32 && lmode == 0 && !last;
           auto kern = lmode == 1 ? (last ? k_layer_sell<DP, true, OutT, 1> : k_layer_sell<DP, false, OutT, 1>)
                                  : (lmode == 3 ? (last ? k_layer_sell<DP, true, OutT, W> : k_layer_sell<DP, false, OutT, W>)
-                                               : (last ? k_layer_sell<DP, true, OutT> : k_layer_sell<DP, false, OutT>));
-          static std::once_flag f[8];
-          std::call_once(f[(last ? 1 : 0) + 2 * lmode], [&] {
+                                               : (last ? k_layer_sell<DP, true, OutT>
+                                                       : (deep ? k_layer_sell<DP, false, OutT, D4>
+                                                               : k_layer_sell<DP, false, OutT>)));
+          const size_t smem_l = deep ? SellCfg<DP, D4>::smem_bytes(net.hidden, false) : smem;
+          static std::once_flag f[10];
+          std::call_once(f[deep ? 8 : (last ? 1 : 0) + 2 * lmode], [&] {
             GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
           });
           const int tiles_s = (n + S::TM - 1) / S::TM;
           const int grid = std::max(1, std::min(tiles_s, sms));
           SellMaps maps{m.tmX[cur], m.tmX[1 - cur], m.tmXw[cur]};
           const float* uwp = m.UWP.p + (size_t)l * 4 * DP * DP;
-          kern<<<grid, S::NT, smem, s>>>(a, maps, X, axl, uwp, net, m.sc.p, out, skip);
+          kern<<<grid, S::NT, smem_l, s>>>(a, maps, X, axl, uwp, net, m.sc.p, out, skip);
           GNPC_LAUNCHED();
           cur = 1 - cur;
           continue;

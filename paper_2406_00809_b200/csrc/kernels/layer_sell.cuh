@@ -89,7 +89,8 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 
 // CSR = 3: windowed sliced-ELL (d = 16): the tile's X rows arrive as up to
 //          kWinBlocks 64-row blocks (TMA) and the gathers read shared memory;
-// CSR = 0: sliced-ELL slices (k_layer_sell on regular matrices);
+// CSR = 0: sliced-ELL slices (k_layer_sell on regular matrices; CSR = 4:
+//          the same with a deeper ring for d = 32 non-last layers);
 // CSR = 1: the short-row CSR ranges of the tile (ragged matrices);
 // CSR = 2: training — B virtual rows per node (v = node*B + k), the full CSR
 //          ranges of the tile's 128/B nodes, plus a mask tile for the backward.
@@ -126,7 +127,11 @@ struct SellCfg {
 #ifndef GNPC_NS_TR32
 #define GNPC_NS_TR32 4  // ring depth of the training layers (fits with GNPC_CAPC_TR 256): C3 22.0 -> 20.3 ms vs 3
 #endif
-  static constexpr int NS = DP == 16 ? (CSRL ? 5 : 4) : (CSR == 2 ? GNPC_NS_TR32 : 3);
+  // CSR = 4: sliced-ELL at d = 32 with a 4-deep ring, for the non-last
+  // layers (the last layer's projection operands need the smem of a slot)
+  static constexpr bool DEEP = CSR == 4;
+  static_assert(!DEEP || DP == 32, "the deep-ring sliced-ELL mode is a d = 32 layout");
+  static constexpr int NS = DP == 16 ? (CSRL ? 5 : 4) : (CSR == 2 ? GNPC_NS_TR32 : (DEEP ? 4 : 3));
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
   // up to round(K, US) words).  Kept small: every KB of shared memory is L1
   // the X-row gathers hit (C5 fused layer 531 -> 499 us going 24 -> 12)
@@ -182,7 +187,7 @@ struct SellCfg {
   static size_t smem_bytes(int hidden, bool last) {
     return o_bar(hidden, last) + 128 + 1024;  // barriers + TMEM slot, 1024-B alignment slack
   }
-  static_assert(TR || O_D1OP + 2 * 32 * DP * 4 + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
+  static_assert(TR || DEEP || O_D1OP + 2 * 32 * DP * 4 + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
                 "last-layer layout must fit shared memory at hidden 32 (larger: host falls back)");
   static_assert(!TR || O_Y + 2 * OPB + 128 + 1024 <= 227 * 1024, "training layout must fit shared memory");
   // TMEM: layer accumulator [0, 2DP); last layer's projection accumulator at

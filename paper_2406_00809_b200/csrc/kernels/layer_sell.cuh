@@ -131,7 +131,14 @@ struct SellCfg {
   // layers (the last layer's projection operands need the smem of a slot)
   static constexpr bool DEEP = CSR == 4;
   static_assert(!DEEP || DP == 32, "the deep-ring sliced-ELL mode is a d = 32 layout");
-  static constexpr int NS = DP == 16 ? (CSRL ? 5 : 4) : (CSR == 2 ? GNPC_NS_TR32 : (DEEP ? 4 : 3));
+#ifndef GNPC_NS_CSR16
+#define GNPC_NS_CSR16 5
+#endif
+#ifndef GNPC_NS_SELL16
+#define GNPC_NS_SELL16 4
+#endif
+  static constexpr int NS = DP == 16 ? (CSRL ? GNPC_NS_CSR16 : GNPC_NS_SELL16)
+                                     : (CSR == 2 ? GNPC_NS_TR32 : (DEEP ? 4 : 3));
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
   // up to round(K, US) words).  Kept small: every KB of shared memory is L1
   // the X-row gathers hit (C5 fused layer 531 -> 499 us going 24 -> 12)

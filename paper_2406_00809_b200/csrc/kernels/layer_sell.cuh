@@ -124,8 +124,11 @@ struct SellCfg {
   static constexpr bool WIN = CSR == 3;                // windowed sliced-ELL
   static constexpr bool CSRL = CSR == 1 || CSR == 2;    // CSR ranges staged per tile
   static_assert(!WIN || DP == 16, "windowed slices are built for d = 16");
+#ifndef GNPC_MBITS
+#define GNPC_MBITS 1  // per-row mask words instead of the X_l tile: frees 15.5 KB per ring slot
+#endif
 #ifndef GNPC_NS_TR32
-#define GNPC_NS_TR32 4  // ring depth of the training layers (fits with GNPC_CAPC_TR 256): C3 22.0 -> 20.3 ms vs 3
+#define GNPC_NS_TR32 (GNPC_MBITS ? 5 : 4)  // C3: 3 -> 4 (22.0 -> 20.3 ms), mask words + 5 (-> 19.3 ms)
 #endif
   // CSR = 4: sliced-ELL at d = 32 with a 4-deep ring, for the non-last
   // layers (the last layer's projection operands need the smem of a slot)
@@ -159,9 +162,6 @@ struct SellCfg {
   static constexpr uint32_t RPB = (TM + 4) * 4;  // row_ptr slice copy (bytes, 16-B multiple)
   // training backward mask [X_l > 0]: at d = 32 one 32-bit word per row
   // (written by the forward layer's epilogue), else the X_l tile itself
-#ifndef GNPC_MBITS
-#define GNPC_MBITS 0  // measured: fwd +80 us, bwd -35 us per layer at C3
-#endif
   static constexpr bool MBITS = GNPC_MBITS && TR && DP == 32;
   static constexpr uint32_t MASKB = MBITS ? TM * 4 : OPB;
   static constexpr uint32_t O_MASK = OPB;

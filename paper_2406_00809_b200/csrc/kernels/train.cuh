@@ -892,7 +892,10 @@ k_lift_pw_batched(const double* __restrict__ b, int nv, int B, LiftTab tab, int 
 #ifndef GNPC_ENC_NS
 #define GNPC_ENC_NS 3
 #endif
-constexpr int kEncCh = 128, kEncStg = GNPC_ENC_STG, kEncNS = GNPC_ENC_NS;
+#ifndef GNPC_ENC_CH
+#define GNPC_ENC_CH 128
+#endif
+constexpr int kEncCh = GNPC_ENC_CH, kEncStg = GNPC_ENC_STG, kEncNS = GNPC_ENC_NS;
 // set stride padded by GL floats when a warp holds several sub-groups, so
 // the sub-groups land on different banks
 inline size_t enc_bucket_smem(int DP, int H, int warps) {

@@ -140,7 +140,7 @@ struct SellCfg {
 #ifndef GNPC_NS_SELL16
 #define GNPC_NS_SELL16 4
 #endif
-  static constexpr int NS = DP == 16 ? (CSRL ? GNPC_NS_CSR16 : GNPC_NS_SELL16)
+  static constexpr int NS = DP == 16 ? (CSRL ? GNPC_NS_CSR16 : (WIN ? 4 : GNPC_NS_SELL16))
                                      : (CSR == 2 ? GNPC_NS_TR32 : (DEEP ? 4 : 3));
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
   // up to round(K, US) words).  Kept small: every KB of shared memory is L1
@@ -194,7 +194,7 @@ struct SellCfg {
   static size_t smem_bytes(int hidden, bool last) {
     return o_bar(hidden, last) + 128 + 1024;  // barriers + TMEM slot, 1024-B alignment slack
   }
-  static_assert(TR || DEEP || O_D1OP + 2 * 32 * DP * 4 + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
+  static_assert(TR || DEEP || (DP == 32 ? O_D1OP + 2 * 32 * DP * 4 : O_Y + 2 * OPB) + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
                 "last-layer layout must fit shared memory at hidden 32 (larger: host falls back)");
   static_assert(!TR || O_Y + 2 * OPB + 128 + 1024 <= 227 * 1024, "training layout must fit shared memory");
   // TMEM: layer accumulator [0, 2DP); last layer's projection accumulator at

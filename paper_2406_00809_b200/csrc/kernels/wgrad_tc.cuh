@@ -429,7 +429,10 @@ constexpr uint32_t OPA = TM * 128;   // bf16 [128 rows][64 features], SW128 (16 
 constexpr uint32_t OPB = TM * 64;    // bf16 [128 rows][32 features], SW64 (8 KiB)
 constexpr uint32_t OPS = 2 * OPA + 2 * OPB;  // one operand set: Ahi | Alo | Bhi | Blo
 constexpr size_t smem_bytes() { return NSTG * STAGE + NOPS * OPS + 128 + 1024; }
-constexpr int kFlushBf = 16;
+#ifndef GNPC_FLUSH_BF
+#define GNPC_FLUSH_BF 16  // 64 was 1 % faster at C3 but moved the U gradients by 1.9e-5 (fp32 folds over 8K rows)
+#endif
+constexpr int kFlushBf = GNPC_FLUSH_BF;
 
 __device__ __forceinline__ uint32_t offA(int r, int m) {  // MN-major SW128, bf16
   return static_cast<uint32_t>((r >> 3) * 1024 + (r & 7) * 128 + ((((m >> 3) ^ (r & 7))) << 4) + (m & 7) * 2);

@@ -146,6 +146,11 @@ k_decoder_tc(const __grid_constant__ CUtensorMap mapy, const float* __restrict__
         d4[q] = *reinterpret_cast<const float4*>(st + tc::swz_off<32>(r, 4 * (q & 7)));
     }
   };
+  double gnext = 0.0;
+  if (!FWD && my > 0) {
+    const int v0 = blockIdx.x * C::TM + tid;
+    gnext = v0 < nv ? gout[v0] : 0.0;
+  }
   for (int it = 0; it < my; ++it) {
     const int s = it % C::NS;
     cur_it = it;
@@ -154,7 +159,12 @@ k_decoder_tc(const __grid_constant__ CUtensorMap mapy, const float* __restrict__
     // per-row scalars first: their latency overlaps the TMA wait and MMA1
     const int k = v % B;
     const SampleScales scv = sc[k];
-    const double gov = (!FWD && live) ? gout[v] : 0.0;
+    // gout of this row: loaded one tile ahead (its latency hides behind a tile)
+    const double gov = gnext;
+    {
+      const int vn = v + static_cast<int>(gridDim.x) * C::TM;
+      gnext = (!FWD && it + 1 < my && vn < nv) ? gout[vn] : 0.0;
+    }
     tc::mbar_wait(&full[s], (it / C::NS) & 1);
     // this row of X_L (swizzled), Y_lo into TMEM
     uint8_t* yt = ring + s * C::OPB;

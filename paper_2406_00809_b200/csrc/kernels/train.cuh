@@ -887,22 +887,25 @@ k_lift_pw_batched(const double* __restrict__ b, int nv, int B, LiftTab tab, int 
 // block's f64 sums in a fixed order after every kEncCh rows per set:
 // deterministic for a fixed grid.  Output: partials[blk][(H+1)*2*DP].
 #ifndef GNPC_ENC_STG
-#define GNPC_ENC_STG 128
+#define GNPC_ENC_STG 256  // with a 2-deep ring: 0.07 ms per C3 step better than 128 x 3
 #endif
 #ifndef GNPC_ENC_NS
-#define GNPC_ENC_NS 3
+#define GNPC_ENC_NS 2
 #endif
 #ifndef GNPC_ENC_CH
 #define GNPC_ENC_CH 128
 #endif
 constexpr int kEncCh = GNPC_ENC_CH, kEncStg = GNPC_ENC_STG, kEncNS = GNPC_ENC_NS;
+// rows per stage: kEncStg, capped so a warp walks at most 32 rows of it
+__host__ __device__ inline int enc_stage_rows(int warps) { return kEncStg < 32 * warps ? kEncStg : 32 * warps; }
 // set stride padded by GL floats when a warp holds several sub-groups, so
 // the sub-groups land on different banks
 inline size_t enc_bucket_smem(int DP, int H, int warps) {
   const int gl = DP < 32 ? DP : 32;
   const size_t sets = static_cast<size_t>(warps) * (32 / gl) * 2;
   const size_t per = static_cast<size_t>(H + 1) * 2 * DP;
-  return static_cast<size_t>(kEncNS) * kEncStg * (DP + 1) * 4 + per * 8 +
+  const int stg = enc_stage_rows(warps);
+  return static_cast<size_t>(kEncNS) * stg * (DP + 1) * 4 + per * 8 +
          sets * (per + (gl < 32 ? gl : 0)) * 4 + 64 * 4 + 64;
 }
 template <int DP>
@@ -912,10 +915,11 @@ __global__ void k_enc_buckets(const float* __restrict__ g, const float* __restri
   extern __shared__ float4 sm4[];
   const int per = (H + 1) * 2 * DP;
   const int stride = per + (R > 1 ? GL : 0);
+  const int stg = enc_stage_rows(blockDim.x >> 5);
   const int nsub = (blockDim.x >> 5) * R;                            // row slots per pass
   float* sg = reinterpret_cast<float*>(sm4);                         // [NS][Stg][DP]
-  float* sx = sg + kEncNS * kEncStg * DP;                            // [NS][Stg]
-  double* blk = reinterpret_cast<double*>(sx + kEncNS * kEncStg);    // [per]
+  float* sx = sg + kEncNS * stg * DP;                            // [NS][Stg]
+  double* blk = reinterpret_cast<double*>(sx + kEncNS * stg);    // [per]
   float* acc = reinterpret_cast<float*>(blk + per);                  // [2 nsub][stride]
   float* s_t = acc + static_cast<size_t>(2 * nsub) * stride;         // [64]
   uint64_t* bar = reinterpret_cast<uint64_t*>(s_t + 64);             // [NS]
@@ -925,15 +929,15 @@ __global__ void k_enc_buckets(const float* __restrict__ g, const float* __restri
   for (int t = tid; t < 2 * nsub * stride; t += blockDim.x) acc[t] = 0.f;
   for (int t = tid; t < nb; t += blockDim.x) s_t[t] = tab.t[t];
   const int r0 = blockIdx.x * rpb, r1 = min(nv, r0 + rpb);
-  const int nst = r1 > r0 ? (r1 - r0 + kEncStg - 1) / kEncStg : 0;
-  auto rows_of = [&](int st) { return min(kEncStg, r1 - (r0 + st * kEncStg)); };
-  auto issue = [&](int st) {  // thread 0: full stages only (16-byte aligned, r0 % kEncStg == 0)
-    if (st >= nst || rows_of(st) != kEncStg) return;
+  const int nst = r1 > r0 ? (r1 - r0 + stg - 1) / stg : 0;
+  auto rows_of = [&](int st) { return min(stg, r1 - (r0 + st * stg)); };
+  auto issue = [&](int st) {  // thread 0: full stages only (16-byte aligned, r0 % stg == 0)
+    if (st >= nst || rows_of(st) != stg) return;
     const int slot = st % kEncNS;
-    const size_t row = static_cast<size_t>(r0) + static_cast<size_t>(st) * kEncStg;
-    tc::mbar_expect_tx(&bar[slot], kEncStg * DP * 4 + kEncStg * 4);
-    tc::bulk_load(sg + slot * kEncStg * DP, g + row * DP, kEncStg * DP * 4, &bar[slot]);
-    tc::bulk_load(sx + slot * kEncStg, vv + row, kEncStg * 4, &bar[slot]);
+    const size_t row = static_cast<size_t>(r0) + static_cast<size_t>(st) * stg;
+    tc::mbar_expect_tx(&bar[slot], stg * DP * 4 + stg * 4);
+    tc::bulk_load(sg + slot * stg * DP, g + row * DP, stg * DP * 4, &bar[slot]);
+    tc::bulk_load(sx + slot * stg, vv + row, stg * 4, &bar[slot]);
   };
   if (tid == 0) {
     for (int q = 0; q < kEncNS; ++q) tc::mbar_init(&bar[q], 1);
@@ -946,17 +950,17 @@ __global__ void k_enc_buckets(const float* __restrict__ g, const float* __restri
   const int sub = warp * R + lane / GL, c0 = (lane % GL) * CPL;
   float* my0 = acc + static_cast<size_t>(2 * sub) * stride;
   float* my1 = my0 + stride;
-  const int flush_every = max(1, kEncCh * nsub / kEncStg);  // stages between folds
+  const int flush_every = max(1, kEncCh * nsub / stg);  // stages between folds
   for (int st = 0; st < nst; ++st) {
     const int slot = st % kEncNS, rows = rows_of(st);
-    const float* gs = sg + slot * kEncStg * DP;
-    const float* xs = sx + slot * kEncStg;
-    if (rows == kEncStg) {
+    const float* gs = sg + slot * stg * DP;
+    const float* xs = sx + slot * stg;
+    if (rows == stg) {
       tc::mbar_wait(&bar[slot], (st / kEncNS) & 1);
     } else {  // the grid's ragged tail: plain loads
-      float* gw = sg + slot * kEncStg * DP;
-      float* xw = sx + slot * kEncStg;
-      const size_t row = static_cast<size_t>(r0) + static_cast<size_t>(st) * kEncStg;
+      float* gw = sg + slot * stg * DP;
+      float* xw = sx + slot * stg;
+      const size_t row = static_cast<size_t>(r0) + static_cast<size_t>(st) * stg;
       for (int t = tid; t < rows * DP; t += blockDim.x) gw[t] = g[row * DP + t];
       for (int t = tid; t < rows; t += blockDim.x) xw[t] = vv[row + t];
       __syncthreads();
@@ -964,7 +968,7 @@ __global__ void k_enc_buckets(const float* __restrict__ g, const float* __restri
     // warp w takes rows [w*rpw, (w+1)*rpw) of the stage; lane l finds row
     // w*rpw + l's interval once, sub-groups then walk the rows R at a time
     // with (x, interval) broadcast by shuffles, alternating their two sets
-    const int rpw = kEncStg / (blockDim.x >> 5);  // <= 32
+    const int rpw = stg / (blockDim.x >> 5);  // <= 32
     const int wr0 = warp * rpw;
     const float xl = lane < rpw && wr0 + lane < rows ? xs[wr0 + lane] : 0.f;
     const int ql = interval_of(s_t, nb, xl) * 2 * DP;

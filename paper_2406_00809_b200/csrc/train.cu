@@ -631,7 +631,7 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
       const int H = T->H, dp = T->dp;
       T->enc_grid = std::max(1, std::min(T->sms, (T->nv + 4095) / 4096));
       // rows per block: a multiple of the staging block (aligned bulk copies)
-      const int stg = gnpk::kEncStg;
+      const int stg = gnpk::enc_stage_rows(T->enc_warps);
       T->enc_rpb = ((T->nv + T->enc_grid - 1) / T->enc_grid + stg - 1) / stg * stg;
       T->enc_grid = (T->nv + T->enc_rpb - 1) / T->enc_rpb;
       T->encpart.alloc((std::size_t)(T->enc_grid + 1) * (H + 1) * 2 * dp);

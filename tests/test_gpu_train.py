@@ -254,3 +254,18 @@ print(json.dumps({"loss": loss, "g": list(g), "want_loss": l2, "want": list(g2)}
         check_grads(np.array(o["g"]), want, (32, 32, 3))
     g0, g1 = np.array(outs[0]["g"]), np.array(outs[1]["g"])
     assert np.linalg.norm(g0 - g1) <= 1e-4 * np.linalg.norm(g1)
+
+
+def test_piecewise_encoder_hidden64(capi, oc, cuda):
+    # hidden 64 at d = 32: the interval sums run with 4 warps (128-row stages)
+    a = oc.prescale(oc.gen_convection_diffusion(16, 0.3), 8.6).rounded_f32()
+    dims = (32, 64, 2)
+    p = oc.init_params(*dims, 6).astype(np.float64)
+    p[64:128] = 0.2 * np.cos(np.arange(64))  # enc1 biases: distinct kinks
+    p = f32(p)
+    x, b = oc.gaussian_batch(a, 7, 0, 8)
+    t = capi.Trainer(capi.Model(dev_csr(capi, a), dims, p), 8)
+    loss, g, _ = t.forward_backward(x, b)
+    want_loss, want = oc.batch_loss_grads(a, dims, p, x, b, 8)
+    assert abs(loss - want_loss) <= 1e-5 * abs(want_loss)
+    check_grads(g, want, dims)

@@ -110,7 +110,7 @@ struct SellCfg {
 #define GNPC_US32 3
 #endif
 #ifndef GNPC_KCAP32
-#define GNPC_KCAP32 12
+#define GNPC_KCAP32 9  // staged slice words per row at d = 32 (a 9-point row; 12 left less L1: C5 283 vs 287 applies/s)
 #endif
   static constexpr int US = DP == 16 ? 8 : GNPC_US32;    // slice entries per gather round
 #ifndef GNPC_USC_TR
@@ -134,6 +134,9 @@ struct SellCfg {
   // layers (the last layer's projection operands need the smem of a slot)
   static constexpr bool DEEP = CSR == 4;
   static_assert(!DEEP || DP == 32, "the deep-ring sliced-ELL mode is a d = 32 layout");
+#ifndef GNPC_NS_DEEP32
+#define GNPC_NS_DEEP32 4
+#endif
 #ifndef GNPC_NS_CSR16
 #define GNPC_NS_CSR16 5
 #endif
@@ -141,7 +144,7 @@ struct SellCfg {
 #define GNPC_NS_SELL16 4
 #endif
   static constexpr int NS = DP == 16 ? (CSRL ? GNPC_NS_CSR16 : (WIN ? 4 : GNPC_NS_SELL16))
-                                     : (CSR == 2 ? GNPC_NS_TR32 : (DEEP ? 4 : 3));
+                                     : (CSR == 2 ? GNPC_NS_TR32 : (DEEP ? GNPC_NS_DEEP32 : 3));
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
   // up to round(K, US) words).  Kept small: every KB of shared memory is L1
   // the X-row gathers hit (C5 fused layer 531 -> 499 us going 24 -> 12)

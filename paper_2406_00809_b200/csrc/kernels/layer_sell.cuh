@@ -148,7 +148,10 @@ struct SellCfg {
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
   // up to round(K, US) words).  Kept small: every KB of shared memory is L1
   // the X-row gathers hit (C5 fused layer 531 -> 499 us going 24 -> 12)
-  static constexpr int KCAP = WIN ? 8 : (DP == 16 ? 16 : GNPC_KCAP32);
+#ifndef GNPC_KCAP16
+#define GNPC_KCAP16 16
+#endif
+  static constexpr int KCAP = WIN ? 8 : (DP == 16 ? GNPC_KCAP16 : GNPC_KCAP32);
   static constexpr uint32_t OPB = TM * DP * 4;   // one A-type operand / X tile / Y tile (bytes)
   static constexpr uint32_t BB = DP * DP * 4;    // one B operand (bytes)
   static constexpr int TCOLS = 2 * DP;           // TMEM accumulator columns (two halves)

@@ -160,10 +160,13 @@ struct SellCfg {
   static constexpr uint32_t CVB = KCAP * TM * 8; // staged slice (bytes)
   // CSR: [X tile | row_ptr slice (TM+4 ints, 1 KiB) | col_idx (CAPC) | values (CAPC)]
   static constexpr bool TR = CSR == 2;
+#ifndef GNPC_CAPC16
+#define GNPC_CAPC16 2048
+#endif
 #ifndef GNPC_CAPC_TR
 #define GNPC_CAPC_TR 256  // C3 tiles stage ~20 entries (4 nodes); 512 measured 0.4 % slower (less L1)
 #endif
-  static constexpr int CAPC = TR ? GNPC_CAPC_TR : (DP == 16 ? 2048 : 1024);  // staged nonzeros per tile (DP=32
+  static constexpr int CAPC = TR ? GNPC_CAPC_TR : (DP == 16 ? GNPC_CAPC16 : 1024);  // staged nonzeros per tile (DP=32
                                                                      // apply: fits the projection operands)
   static constexpr uint32_t RPB = (TM + 4) * 4;  // row_ptr slice copy (bytes, 16-B multiple)
   // training backward mask [X_l > 0]: at d = 32 one 32-bit word per row

@@ -84,8 +84,13 @@ int oc_gaussian_batch(size_t n, const int64_t* rp, const int64_t* ci, const doub
 int oc_hessenberg_lstsq(size_t k, const double* hbar, double beta, double* y,
                         double* tracked, int* singular);
 /* kind: 0 none, 1 gnp(d,hidden,layers,params), 2 dense n x n col-major in params,
- * 3 identity.  Returns SolveStatus (0 converged, 1 maxiters, 2 timeout,
+ * 3 identity, 4 callback (params points to an oc_op_cb: any FlexibleOperator,
+ * e.g. the device GNP, driven by the oracle's f64 FGMRES).  Returns SolveStatus (0 converged, 1 maxiters, 2 timeout,
  * 3 solution_failure, 4 breakdown_exact) or -1. */
+typedef struct {
+  void (*fn)(void* ctx, const double* in, double* out, size_t n);
+  void* ctx;
+} oc_op_cb;
 int oc_fgmres(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
               const double* b, int kind, size_t d, size_t hidden, size_t layers,
               const double* params, const double* x0, double rtol, size_t maxiters,
@@ -104,6 +109,27 @@ int oc_assemble_batch(size_t n, const int64_t* rp, const int64_t* ci, const doub
                       size_t k, size_t m_eff, const double* vb, const double* zsv,
                       const double* s, uint64_t seed, size_t skip_batches, size_t batch,
                       size_t spectral_count, double* x, double* b);
+
+/* ---- full-size parity support (bit-identical threaded restatements) */
+typedef struct {
+  size_t n, nnz, cap;
+  int64_t *rp, *ci;
+  double* v;
+} oc_csr_buf;
+/* BASELINE config generators (the repo's recipes, gnp_host.cpp): kind
+ * "c2_convdiff3d" | "c3_varcoeff2d" | "c4_powerlaw" | "c5_aniso9pt". */
+int oc_gen_named(const char* kind, size_t size, double p0, double p1, uint64_t seed,
+                 oc_csr_buf* out);
+void oc_csr_buf_free(oc_csr_buf* a);
+/* threads used by oc_fgmres's GNP operator (default 1) */
+void oc_set_threads(size_t t);
+int oc_gnn_apply_mt(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                    size_t d, size_t hidden, size_t layers, const double* params,
+                    const double* b, double* out, size_t threads);
+int oc_batch_loss_grads_mt(size_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                           size_t d, size_t hidden, size_t layers, const double* params,
+                           size_t batch, const double* x, const double* b, double* loss,
+                           double* grads, double* out_batch, size_t threads);
 
 #ifdef __cplusplus
 }

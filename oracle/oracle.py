@@ -60,6 +60,19 @@ def csr_arrays(a: Csr):
             np.ascontiguousarray(a.values, np.float64))
 
 
+class _CsrBuf(C.Structure):
+    _fields_ = [("n", C.c_size_t), ("nnz", C.c_size_t), ("cap", C.c_size_t),
+                ("rp", C.POINTER(C.c_int64)), ("ci", C.POINTER(C.c_int64)),
+                ("v", C.POINTER(C.c_double))]
+
+
+_OP_CB_T = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_size_t)
+
+
+class _OpCb(C.Structure):
+    _fields_ = [("fn", _OP_CB_T), ("ctx", C.c_void_p)]
+
+
 class OracleError(RuntimeError):
     pass
 
@@ -118,10 +131,58 @@ class Restatement:
                                           _d, _szp, _szp]
         L.oc_assemble_batch.argtypes = [C.c_size_t, _i64, _i64, _d, C.c_size_t, C.c_size_t, _d, _d,
                                         _d, C.c_uint64, C.c_size_t, C.c_size_t, C.c_size_t, _d, _d]
+        L.oc_gen_named.argtypes = [C.c_char_p, C.c_size_t, C.c_double, C.c_double, C.c_uint64,
+                                   C.POINTER(_CsrBuf)]
+        L.oc_csr_buf_free.argtypes = [C.POINTER(_CsrBuf)]
+        L.oc_set_threads.argtypes = [C.c_size_t]
+        L.oc_gnn_apply_mt.argtypes = [C.c_size_t, _i64, _i64, _d, C.c_size_t, C.c_size_t, C.c_size_t,
+                                      _d, _d, _d, C.c_size_t]
+        L.oc_batch_loss_grads_mt.argtypes = [C.c_size_t, _i64, _i64, _d, C.c_size_t, C.c_size_t,
+                                             C.c_size_t, _d, C.c_size_t, _d, _d,
+                                             C.POINTER(C.c_double), _d, C.c_void_p, C.c_size_t]
 
     def _check(self, rc):
         if rc != 0:
             raise OracleError(self.L.oc_last_error().decode())
+
+    # ---- full-size parity support (bit-identical threaded restatements)
+    def gen_named(self, kind: str, size: int, p0: float = 0.0, p1: float = 0.0, seed: int = 0) -> Csr:
+        """BASELINE config matrices C2-C5 (the repo's recipes; see gnp_oracle.c)."""
+        buf = _CsrBuf()
+        rc = self.L.oc_gen_named(kind.encode(), size, p0, p1, seed, C.byref(buf))
+        if rc != 0:
+            self.L.oc_csr_buf_free(C.byref(buf))
+            raise OracleError(self.L.oc_last_error().decode())
+        try:
+            n, nnz = buf.n, buf.nnz
+            rp = np.ctypeslib.as_array(buf.rp, (n + 1,)).copy()
+            ci = np.ctypeslib.as_array(buf.ci, (max(nnz, 1),))[:nnz].copy()
+            v = np.ctypeslib.as_array(buf.v, (max(nnz, 1),))[:nnz].copy()
+        finally:
+            self.L.oc_csr_buf_free(C.byref(buf))
+        return Csr(n, rp, ci, v)
+
+    def set_threads(self, t: int) -> None:
+        """Threads for oc_fgmres's GNP operator (bit-identical to 1)."""
+        self.L.oc_set_threads(max(1, int(t)))
+
+    def gnn_apply_mt(self, a: Csr, dims, params, b, threads=None) -> np.ndarray:
+        out = np.empty(a.n)
+        self._check(self.L.oc_gnn_apply_mt(*csr_arrays(a), *dims, np.ascontiguousarray(params, np.float64),
+                                           np.ascontiguousarray(b, np.float64), out,
+                                           threads or (os.cpu_count() or 1)))
+        return out
+
+    def batch_loss_grads_mt(self, a: Csr, dims, params, x, b, batch, want_out=False, threads=None):
+        loss = C.c_double()
+        grads = np.empty(self.param_count(*dims))
+        out = np.empty(a.n * batch) if want_out else None
+        self._check(self.L.oc_batch_loss_grads_mt(
+            *csr_arrays(a), *dims, np.ascontiguousarray(params, np.float64), batch,
+            np.ascontiguousarray(x, np.float64), np.ascontiguousarray(b, np.float64),
+            C.byref(loss), grads, out.ctypes.data if want_out else None,
+            threads or (os.cpu_count() or 1)))
+        return (loss.value, grads, out) if want_out else (loss.value, grads)
 
     # ---- rng
     def gaussian_vector(self, seed: int, n: int) -> np.ndarray:
@@ -304,9 +365,23 @@ class Restatement:
         hr = np.empty(cap)
         ht = np.empty(cap)
         hl = C.c_size_t()
-        p = np.ascontiguousarray(params, np.float64) if params is not None else None
+        keep = None
+        if callable(kind):
+            # kind 4: a caller-supplied operator M(v) -> array (e.g. the device GNP)
+            fn = kind
+
+            def tramp(ctx, pin, pout, nn):
+                vin = np.ctypeslib.as_array(pin, (nn,)).copy()
+                np.ctypeslib.as_array(pout, (nn,))[:] = fn(vin)
+
+            keep = _OP_CB_T(tramp)
+            cb = _OpCb(keep, None)
+            kind, pptr = 4, C.addressof(cb)
+        else:
+            p = np.ascontiguousarray(params, np.float64) if params is not None else None
+            pptr = p.ctypes.data if p is not None else None
         st = self.L.oc_fgmres(*csr_arrays(a), np.ascontiguousarray(b, np.float64), kind, *dims,
-                              p.ctypes.data if p is not None else None, x0, rtol, maxiters,
+                              pptr, x0, rtol, maxiters,
                               restart, timeout_secs, x, hi, hr, ht, cap, C.byref(hl))
         if st < 0:
             raise OracleError(self.L.oc_last_error().decode())

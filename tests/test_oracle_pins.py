@@ -332,3 +332,87 @@ def test_spectral_golden(oc):
     assert np.array_equal(s["s"], g["s"])
     x, b = oc.assemble_batch(a, s, int(g["batch_seed"]), 1, int(g["batch"]), int(g["spectral"]))
     assert np.array_equal(x, g["x"]) and np.array_equal(b, g["b"])
+
+
+# ------------------------------------------- full-size parity support (r02)
+# Content hashes of the BASELINE config matrices at their full sizes (n, nnz,
+# FNV-1a of the CSR as src/csr.cpp:152-173), shared by the oracle's
+# restatement of the generators and the product's gnpc_csr_generate.
+FULL_SIZE = [
+    ("c2_convdiff3d", 64, 10.0, 0.0, 0, 262144, 1810432),
+    ("c3_varcoeff2d", 512, 2.0, 0.0, 2, 262144, 1308672),
+    ("c4_powerlaw", 1 << 20, 2.2, 0.0, 4, 1048576, 17069302),
+    ("c5_aniso9pt", 2048, 1e-3, 30.0, 0, 4194304, 37724164),
+]
+
+
+@pytest.mark.parametrize("kind,size,p0,p1,seed", [
+    ("c2_convdiff3d", 9, 10.0, 0.0, 0), ("c3_varcoeff2d", 33, 2.0, 0.0, 2),
+    ("c4_powerlaw", 4000, 2.2, 0.0, 4), ("c5_aniso9pt", 37, 1e-3, 30.0, 0)])
+def test_config_generators_bitwise_small(oc, capi, kind, size, p0, p1, seed):
+    a = oc.gen_named(kind, size, p0, p1, seed)
+    rp, ci, v = capi.Csr.generate(kind, size, p0, p1, seed).arrays()
+    assert np.array_equal(a.row_ptr, rp) and np.array_equal(a.col_idx, ci)
+    assert np.array_equal(a.values, v)
+
+
+@pytest.mark.parametrize("kind,size,p0,p1,seed,n,nnz", FULL_SIZE)
+def test_config_generators_full_size_hash(oc, capi, kind, size, p0, p1, seed, n, nnz):
+    a = oc.gen_named(kind, size, p0, p1, seed)
+    g = capi.Csr.generate(kind, size, p0, p1, seed)
+    assert (a.n, a.nnz) == (n, nnz) == g.info()
+    assert oc.csr_hash(a) == g.hash()
+    assert oc.gershgorin_gamma(a) == g.gamma()
+
+
+@pytest.mark.parametrize("dims", [(16, 32, 8), (32, 32, 8), (5, 7, 3)])
+def test_streaming_apply_bitwise(oc, dims):
+    a = oc.gen_named("c4_powerlaw", 3000, 2.2, 0.0, 4)
+    ah = oc.prescale(a, oc.gershgorin_gamma(a)).rounded_f32()
+    p = f32(oc.init_params(*dims, 1))
+    b = oc.gaussian_vector(2, ah.n)
+    want = oc.gnn_apply(ah, dims, p, b)
+    for t in (1, 3, 8):
+        assert np.array_equal(oc.gnn_apply_mt(ah, dims, p, b, threads=t), want)
+    assert np.all(oc.gnn_apply_mt(ah, dims, p, np.zeros(ah.n), threads=4) == 0.0)
+
+
+def test_streaming_apply_equals_reference_live(oc, ref):
+    a = oc.gen_named("c5_aniso9pt", 40, 1e-3, 30.0)
+    ah = oc.prescale(a, oc.gershgorin_gamma(a)).rounded_f32()
+    p = f32(oc.init_params(32, 32, 8, 0))
+    b = oc.gaussian_vector(3, ah.n)
+    assert np.array_equal(oc.gnn_apply_mt(ah, (32, 32, 8), p, b, threads=5),
+                          ref.gnn_apply(ah, (32, 32, 8), p, b))
+
+
+def test_parallel_batch_grads_bitwise(oc, ref):
+    a = oc.gen_named("c3_varcoeff2d", 20, 2.0, 0.0, 2)
+    ah = oc.prescale(a, oc.gershgorin_gamma(a)).rounded_f32()
+    dims, B = (32, 32, 3), 6
+    p = f32(oc.init_params(*dims, 0))
+    x, b = oc.gaussian_batch(ah, 3, 0, B)
+    l0, g0, o0 = oc.batch_loss_grads(ah, dims, p, x, b, B, want_out=True)
+    for t in (1, 4):
+        l1, g1, o1 = oc.batch_loss_grads_mt(ah, dims, p, x, b, B, want_out=True, threads=t)
+        assert l1 == l0 and np.array_equal(g1, g0) and np.array_equal(o1, o0)
+    lr, gr = ref.batch_loss_grads(ah, dims, p, x, b, B)
+    assert lr == l0 and np.array_equal(gr, g0)
+
+
+def test_fgmres_threaded_and_callback_operators_bitwise(oc):
+    a = oc.prescale(oc.gen_convection_diffusion(16, 0.3), 8.0)
+    dims = (4, 8, 2)
+    p = oc.init_params(*dims, 0)
+    b = oc.gaussian_vector(1, a.n)
+    r1 = oc.fgmres(a, b, kind=1, dims=dims, params=p, maxiters=30, restart=10)
+    r2 = oc.fgmres(a, b, kind=lambda v: oc.gnn_apply(a, dims, p, v), maxiters=30, restart=10)
+    oc.set_threads(4)
+    try:
+        r3 = oc.fgmres(a, b, kind=1, dims=dims, params=p, maxiters=30, restart=10)
+    finally:
+        oc.set_threads(1)
+    for r in (r2, r3):
+        assert r["status"] == r1["status"]
+        assert [h[:2] for h in r["history"]] == [h[:2] for h in r1["history"]]
+        assert np.array_equal(r["x"], r1["x"])

@@ -453,6 +453,14 @@ def fgmres_device(csr: Csr, model: Model | None, b_ptr: int, x_ptr: int, rtol, m
     return {"status": STATUS[st.value], "history": _unpack(h, bufs), "reorth_steps": int(h.reorth)}
 
 
+def checkpoint_save(path: str, dims, params, csr: Csr) -> None:
+    """save_checkpoint (src/gnn.cpp:480-531): GNPCKPT 1 file, byte-identical
+    to the reference's."""
+    p = np.ascontiguousarray(params, np.float64)
+    check(lib().gnpc_checkpoint_save(path.encode(), C.c_int64(dims[0]), C.c_int64(dims[1]),
+                                     C.c_int64(dims[2]), p.ctypes.data_as(vp), csr.h))
+
+
 def launch_count() -> int:
     c = C.c_int64()
     check(lib().gnpc_launch_count(C.byref(c)))

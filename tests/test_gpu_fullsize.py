@@ -11,6 +11,8 @@ seconds at n = 2^20 .. 2^22 on the GPU box's host cores.
 Tolerances (north_star): GNP outputs rel-L2 and max-abs/max-ref <= 1e-4;
 gradients per parameter tensor, norm-wise, <= 1e-4; loss <= 1e-5 relative.
 """
+import os
+
 import numpy as np
 import pytest
 from conftest import f32, max_rel, rel_l2
@@ -102,3 +104,79 @@ def test_c3_full_size_gradients(capi, oc, cuda):
         worst = max(worst, e)
         assert e <= TOL, (nm, e)
     print(f"C3 full size: loss rel {abs(loss - want_loss) / abs(want_loss):.2e}, worst tensor {worst:.2e}")
+
+
+# ---------------------------------------------------------------- trained GNP
+def _read_gnpckpt(path):
+    """Test-side GNPCKPT 1 reader (format: src/gnn.cpp:480-557): text header,
+    then per array 'array <name> <count>\\n' + count raw LE f64 + '\\n'."""
+    raw = open(path, "rb").read()
+    pos = 0
+
+    def line():
+        nonlocal pos
+        e = raw.index(b"\n", pos)
+        s = raw[pos:e].decode()
+        pos = e + 1
+        return s
+
+    assert line() == "GNPCKPT 1"
+    d, h, L = (int(v) for v in line().split()[1:])
+    line()  # matrix n nnz hash
+    vals = []
+    while pos < len(raw):
+        tag, _name, cnt = line().split()
+        assert tag == "array"
+        cnt = int(cnt)
+        vals.append(np.frombuffer(raw[pos:pos + 8 * cnt], dtype="<f8").copy())
+        pos += 8 * cnt + 1
+    return (d, h, L), np.concatenate(vals)
+
+
+def _trained_fgmres_case(capi, oc, ah, b, dims, steps, rtol, restart, maxiters, tmp_path):
+    A = dev_csr(capi, ah)
+    best, losses, bl = capi.train_preconditioner(A, dims=dims, steps=steps, batch=16, spectral=8,
+                                                 arnoldi_m=40, seed=0)
+    assert bl < losses[0]
+    path = str(tmp_path / "trained.gnpckpt")
+    capi.checkpoint_save(path, dims, best, A)
+    dims2, p = _read_gnpckpt(path)
+    assert dims2 == dims and np.array_equal(p, best)
+    p32 = f32(p)
+    m = capi.Model(A, dims, p32)
+    dev = capi.fgmres(A, b, model=m, rtol=rtol, maxiters=maxiters, restart=restart)
+    # the oracle's f64 FGMRES driven by the device M: isolates the device
+    # Krylov machinery from M's precision
+    cb = oc.fgmres(ah, b, kind=lambda v: m.apply(v), rtol=rtol, maxiters=maxiters, restart=restart)
+    # the oracle end to end: f64 FGMRES with the f64 GNP on the same fp32 params
+    oc.set_threads(os.cpu_count() or 1)
+    try:
+        ref = oc.fgmres(ah, b, kind=1, dims=dims, params=p32, rtol=rtol, maxiters=maxiters, restart=restart)
+    finally:
+        oc.set_threads(1)
+    its = [r["history"][-1][0] for r in (dev, cb, ref)]
+    print(f"trained GNP ({steps} steps): iterations device {its[0]}, oracle-FGMRES+device-M {its[1]}, "
+          f"oracle {its[2]}")
+    assert dev["status"] == cb["status"] == ref["status"] == "converged"
+    assert abs(its[0] - its[2]) <= 1 and abs(its[0] - its[1]) <= 1
+    for r in (dev, cb, ref):
+        assert r["history"][-1][1] <= rtol
+    # the device's final true residual, recomputed independently
+    assert np.linalg.norm(oc.spmv(ah, dev["x"]) - b) / np.linalg.norm(b) <= rtol * 1.01
+
+
+def test_trained_gnp_fgmres_iteration_parity_c1(capi, oc, cuda, tmp_path):
+    # C1 (64^2 Laplacian, restart 10, rtol 1e-8).  The GPU-trained GNP (2000
+    # steps, the reference's train defaults) needs ~114 iterations, so maxiters
+    # is raised from C1's 100 to 300 to reach convergence (seed-0 weights stop
+    # at maxiters on every config).
+    ah = oc.prescale(oc.gen_convection_diffusion(64, 0.0), 8.0)
+    b = oc.gaussian_vector(1, ah.n)
+    _trained_fgmres_case(capi, oc, ah, b, (16, 32, 8), 2000, 1e-8, 10, 300, tmp_path)
+
+
+def test_trained_gnp_fgmres_iteration_parity_c2(capi, oc, cuda, tmp_path):
+    # C2 at full size (n = 262,144, restart 30, rtol 1e-6, b = A x*)
+    ah = scaled(oc, "c2_convdiff3d", 64, 10.0)
+    b = oc.spmv(ah, oc.gaussian_vector(1, ah.n))
+    _trained_fgmres_case(capi, oc, ah, b, (16, 32, 8), 600, 1e-6, 30, 300, tmp_path)

@@ -110,7 +110,14 @@ int gnpc_model_dims(gnpc_model m, int64_t* d, int64_t* hidden, int64_t* layers);
 int gnpc_model_destroy(gnpc_model m);
 /* out = M(b): host f64 in/out (the FlexibleOperator::apply drop-in). */
 int gnpc_apply(gnpc_model m, const double* b, double* out);
-/* Device-resident variants on a caller stream (cudaStream_t passed as void*). */
+/* Device-resident variants on a caller stream (cudaStream_t passed as void*).
+ * Threading: a model owns one apply workspace (activations, τ partials, the
+ * persistent apply's grid-barrier counter), so applies of ONE model must be
+ * serialised (one stream / one thread at a time), like the reference's
+ * "called from the solve's thread only".  Distinct models may
+ * run concurrently.  After a trainer's Adam step updates a model's device
+ * parameters, applies and gnpc_model_get_params return GNPC_EINVAL until
+ * gnpc_trainer_sync_model (or gnpc_model_set_params) makes it consistent. */
 int gnpc_apply_device_f32(gnpc_model m, const float* b, float* out, void* stream);
 int gnpc_apply_device_f64(gnpc_model m, const double* b, double* out, void* stream);
 /* Same as gnpc_apply_device_f32 with CUDA events between the pipeline's
@@ -234,6 +241,11 @@ typedef struct {
 } gnpc_train_config;
 int gnpc_train_preconditioner(gnpc_csr a, const gnpc_train_config* cfg, double* best,
                               double* losses, double* best_loss);
+/* The same run with device timings: timing_ms4 = {whole loop, pair generation
+ * (Box-Muller / spectral x + b = A x), monitoring forward + best snapshot,
+ * host wait for the pair stream}, milliseconds summed over the steps. */
+int gnpc_train_preconditioner_timed(gnpc_csr a, const gnpc_train_config* cfg, double* best,
+                                    double* losses, double* best_loss, double* timing_ms4);
 
 #ifdef __cplusplus
 }

@@ -33,9 +33,11 @@ NVCC_FLAGS += os.environ.get("GNPC_NVCC_DEFS", "").split()  # tuning variants, e
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-Wall"]
 
 CU_SOURCES = ["capi.cu", "train.cu"]
-HOST_SOURCES = ["host/gnp_host.cpp"]
+HOST_SOURCES = ["host/gnp_host.cpp", "host/pair_stream.cpp"]
+# per-source extra flags (no -mfma anywhere: the host restatements must not contract a*b+c)
+HOST_EXTRA = {"host/pair_stream.cpp": ["-O3", "-mavx2"]}
 HEADERS = ["capi_common.hpp", "model.hpp", "kernels/common.cuh", "kernels/apply.cuh",
-           "kernels/krylov.cuh", "kernels/train.cuh", "kernels/tc.cuh", "kernels/layer_tc.cuh", "kernels/layer_sell.cuh", "kernels/wgrad_tc.cuh", "kernels/decoder_tc.cuh", "host/gnp_host.hpp", "api/gnp_gpu.hpp"]
+           "kernels/krylov.cuh", "kernels/train.cuh", "kernels/tc.cuh", "kernels/layer_tc.cuh", "kernels/layer_sell.cuh", "kernels/wgrad_tc.cuh", "kernels/decoder_tc.cuh", "kernels/pairs.cuh", "host/gnp_host.hpp", "host/pair_stream.hpp", "api/gnp_gpu.hpp"]
 
 LIB = os.path.join(PKG, "libgnpc.so")
 EXT = os.path.join(PKG, "_gnp" + sysconfig.get_config_var("EXT_SUFFIX"))
@@ -80,7 +82,7 @@ def build_lib(force: bool = False) -> str:
         o = os.path.join(BUILD, src.replace("/", "_") + ".o")
         objs.append(o)
         if force or _newer(o, [s] + hdrs):
-            jobs.append([CXX, *CXX_FLAGS, "-I", CSRC, "-c", s, "-o", o])
+            jobs.append([CXX, *CXX_FLAGS, *HOST_EXTRA.get(src, []), "-I", CSRC, "-c", s, "-o", o])
     with cf.ThreadPoolExecutor(max_workers=4) as ex:
         futs = [ex.submit(_run, j, os.path.join(BUILD, os.path.basename(j[-1]) + ".log")) for j in jobs]
         for f in futs:

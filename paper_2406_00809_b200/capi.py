@@ -443,6 +443,26 @@ def train_preconditioner(csr: Csr, dims=(16, 32, 8), lr=1e-3, steps=2000, batch=
     return best, losses, bl.value
 
 
+def train_run(csr: Csr, dims=(16, 32, 8), lr=1e-3, steps=2000, batch=16, spectral=8, arnoldi_m=40,
+              seed=0, monitor_batch=16, timing=False):
+    """train_preconditioner with device timings (gnpc_train_preconditioner_timed):
+    -> {"best", "losses", "best_loss", "timing": {ms_per_step, pairgen_ms, monitor_ms, host_wait_ms}}"""
+    cfg = TrainConfig(lr, steps, batch, spectral, arnoldi_m, seed, monitor_batch, *dims)
+    best = np.empty(param_count(*dims))
+    losses = np.empty(steps + 1)
+    bl = C.c_double()
+    tm = np.zeros(4)
+    check(lib().gnpc_train_preconditioner_timed(csr.h, C.byref(cfg), best.ctypes.data_as(vp),
+                                                losses.ctypes.data_as(vp), C.byref(bl),
+                                                tm.ctypes.data_as(vp)))
+    s = max(steps, 1)
+    return {"best": best, "losses": losses, "best_loss": bl.value,
+            "timing": {"ms_per_step": tm[0] / s, "pairgen_ms": tm[1] / s, "monitor_ms": tm[2] / s,
+                       "host_wait_ms": tm[3] / s,
+                       "how": "CUDA events on the model stream around the whole loop and around each "
+                              "step's pair generation and monitoring phases"}}
+
+
 def fgmres_device(csr: Csr, model: Model | None, b_ptr: int, x_ptr: int, rtol, maxiters, restart,
                   stream: int = 0):
     cfg = SolveConfig(rtol, maxiters, restart, -1.0)

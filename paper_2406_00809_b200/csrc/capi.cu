@@ -121,23 +121,24 @@ struct ApplyLaunch {
         auto kern = mode == 1 ? k_apply_sell<DP, InT, OutT, 1>
                               : (mode == 3 ? k_apply_sell<DP, InT, OutT, (DP == 16 ? 3 : 0)>
                                            : k_apply_sell<DP, InT, OutT, 0>);
-        static std::once_flag f[4];
-        std::call_once(f[mode], [&] {
+        {
           cudaFuncAttributes fa{};
           GNPC_CUDA(cudaFuncGetAttributes(&fa, (const void*)kern));  // static smem counts against 227 KB
-          GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024 - (int)fa.sharedSizeBytes));
-        });
+          set_smem_attr((const void*)kern, 227 * 1024 - (int)fa.sharedSizeBytes);
+        }
         const int tiles = (n + S::TM - 1) / S::TM;
         const int grid = std::max(1, std::min(tiles, sms));
         static const bool times = std::getenv("GNPC_FUSED_TIMES") != nullptr;
-        static gnpc_impl::DevBuf<unsigned long long> tbuf;
+        gnpc_impl::DevBuf<unsigned long long>& tbuf = m.phase_times;  // GNPC_FUSED_TIMES debug only
         if (times && !tbuf.p) tbuf.alloc(64);
         ApplyFused fa{m.tmX[0], m.tmX[1], m.tmXw[0], m.tmXw[1], m.X[0].p, m.X[1].p, m.UWP.p, m.partials.p,
                       m.gbar.p, m.gbar_host, m.sc.p, times ? tbuf.p : nullptr, m.fused_stash};
-        m.gbar_host += (unsigned long long)grid * (1 + net.layers);
         void* args[] = {(void*)&a, (void*)&fa, (void*)&in, (void*)&net, (void*)&out, (void*)&skip};
         GNPC_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(S::NT), args, smem, s));
+        // the grid barriers' base advances only for a launch that happened (a
+        // failed cooperative launch must not leave the host count ahead of
+        // the device counter)
+        m.gbar_host += (unsigned long long)grid * (1 + net.layers);
         GNPC_LAUNCHED();
         if (times) {
           unsigned long long h[64];
@@ -158,10 +159,7 @@ struct ApplyLaunch {
     {
       const size_t smem = (size_t)(net.nbreak + 1) * DP * 8 + (size_t)net.nbreak * 4 + 16;
       auto kern = k_lift_pw<DP, InT>;
-      static std::once_flag f;
-      std::call_once(f, [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      });
+      set_smem_attr((const void*)kern, 160 * 1024);
       mark(1);
       const int ng = kThreads / (DP / 4);
       int grid = std::min((n + ng - 1) / ng, sms * 8);
@@ -212,10 +210,7 @@ struct ApplyLaunch {
                                                        : (deep ? k_layer_sell<DP, false, OutT, D4>
                                                                : k_layer_sell<DP, false, OutT>)));
           const size_t smem_l = deep ? SellCfg<DP, D4>::smem_bytes(net.hidden, false) : smem;
-          static std::once_flag f[10];
-          std::call_once(f[deep ? 8 : (last ? 1 : 0) + 2 * lmode], [&] {
-            GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-          });
+          set_smem_attr((const void*)kern, 227 * 1024);
           const int tiles_s = (n + S::TM - 1) / S::TM;
           const int grid = std::max(1, std::min(tiles_s, sms));
           SellMaps maps{m.tmX[cur], m.tmX[1 - cur], m.tmXw[cur]};
@@ -253,20 +248,14 @@ struct ApplyLaunch {
       if (!last) {
         auto kern = k_layer<DP, false, OutT>;
         const size_t smem = Cfg::smem_bytes(false, net.hidden);
-        static std::once_flag f;
-        std::call_once(f, [&] {
-          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        });
+        set_smem_attr((const void*)kern, 200 * 1024);
         kern<<<tiles, kThreads, smem, s>>>(a, X, m.X[1 - cur].p, uw, axl, net, m.sc.p, out, skip);
         GNPC_LAUNCHED();
         cur = 1 - cur;
       } else {
         auto kern = k_layer<DP, true, OutT>;
         const size_t smem = Cfg::smem_bytes(true, net.hidden);
-        static std::once_flag f;
-        std::call_once(f, [&] {
-          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        });
+        set_smem_attr((const void*)kern, 200 * 1024);
         kern<<<tiles, kThreads, smem, s>>>(a, X, nullptr, uw, axl, net, m.sc.p, out, skip);
         GNPC_LAUNCHED();
       }
@@ -773,6 +762,9 @@ bool gnpc_model_s::fused_eligible() {
 template <typename InT, typename OutT>
 void gnpc_model_s::launch_apply(const InT* in, OutT* out, cudaStream_t s, const int* skip,
                                 ApplyProf* prof) {
+  if (trainer_dirty)
+    throw std::logic_error("model parameters were updated by a trainer: call gnpc_trainer_sync_model "
+                           "before applying the model");
   a->upload();
   ensure_workspace();
   switch (dp) {
@@ -1345,12 +1337,16 @@ int gnpc_model_set_params(gnpc_model m, const double* params) {
     m->params.assign(params, params + m->params.size());
     GNPC_CUDA(cudaStreamSynchronize(m->stream));
     m->build_view();
+    m->trainer_dirty = false;
   });
 }
 
 int gnpc_model_get_params(gnpc_model m, double* params) {
   return guarded([&] {
     need(m && params, "null argument");
+    if (m->trainer_dirty)
+      throw std::logic_error("model parameters were updated by a trainer: call gnpc_trainer_sync_model "
+                             "first");
     std::copy(m->params.begin(), m->params.end(), params);
   });
 }

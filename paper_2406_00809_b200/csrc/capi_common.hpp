@@ -8,6 +8,8 @@
 #include <atomic>
 #include <cstdint>
 #include <memory>
+#include <mutex>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -85,6 +87,21 @@ int guarded(F&& f) {
 void require_device();
 int num_sms();
 int tc_ctas_per_sm(const void* kern, size_t smem, int tcols);
+
+// Raise a kernel's dynamic shared-memory limit on the CURRENT device, once
+// per (device, kernel, size): the attribute is per device, so a process that
+// drives several devices sets it on each.
+inline void set_smem_attr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::tuple<int, const void*, int>> done;
+  int dev = 0;
+  GNPC_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& [d, k, b] : done)
+    if (d == dev && k == kern && b >= bytes) return;
+  GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.emplace_back(dev, kern, bytes);
+}
 
 template <typename T>
 struct DevBuf {

@@ -152,6 +152,9 @@ struct SellCfg {
 #define GNPC_KCAP16 16
 #endif
   static constexpr int KCAP = WIN ? 8 : (DP == 16 ? GNPC_KCAP16 : GNPC_KCAP32);
+  // the staged gather reads round(K, US) words of a slice: KCAP must be a
+  // multiple of US or the last round would read past the staged slice
+  static_assert(WIN || KCAP % US == 0, "GNPC_KCAP16/GNPC_KCAP32 must be a multiple of the gather round");
   static constexpr uint32_t OPB = TM * DP * 4;   // one A-type operand / X tile / Y tile (bytes)
   static constexpr uint32_t BB = DP * DP * 4;    // one B operand (bytes)
   static constexpr int TCOLS = 2 * DP;           // TMEM accumulator columns (two halves)

@@ -28,6 +28,10 @@ struct gnpc_model_s {
   gnpc_impl::DevBuf<float> LIFT;  // piecewise-linear lift tables (kinks, alpha, beta)
   gnpc_impl::DevBuf<float> UWTC;  // per layer [U;W]^T split tf32 hi/lo, tcgen05 layout
   gnpc_impl::DevBuf<float> UWP;   // per layer [Bu_hi|Bw_hi|Bu_lo|Bw_lo], k_layer_sell layout
+  // set by a trainer's Adam step (it rewrites P/UWTC/UWP on the device but
+  // not the host params or the lift tables); applies refuse to run on the
+  // mixed state until gnpc_trainer_sync_model or gnpc_model_set_params
+  bool trainer_dirty = false;
   bool use_tc = true;             // DP 16/32: tcgen05 transform (GNPC_NO_TC=1: CUDA cores)
   int tc_per_sm[8] = {};  // cached occupancy per (last, OutT, path) tcgen05 kernel
   gnpk::NetView view{};
@@ -39,6 +43,7 @@ struct gnpc_model_s {
   // its value so each launch knows its base; launches are stream-ordered)
   gnpc_impl::DevBuf<unsigned long long> gbar;
   unsigned long long gbar_host = 0;
+  gnpc_impl::DevBuf<unsigned long long> phase_times;  // GNPC_FUSED_TIMES (debug)
   void* fused_stash = nullptr;  // gnpc_apply zero-copy: device copy of the host input
   bool fused_eligible();        // the apply runs as the single persistent launch
   gnpc_impl::DevBuf<gnpk::ApplyScalars> sc;

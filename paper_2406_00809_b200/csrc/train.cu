@@ -15,7 +15,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
+#include <condition_variable>
+#include <exception>
 #include <future>
+#include <thread>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -26,6 +30,8 @@
 #include "kernels/train.cuh"
 #include "kernels/decoder_tc.cuh"
 #include "kernels/wgrad_tc.cuh"
+#include "kernels/pairs.cuh"
+#include "host/pair_stream.hpp"
 #include "model.hpp"
 
 using namespace gnpc_impl;
@@ -130,15 +136,7 @@ void make_red(gnpc_trainer_s::Red& r, const float* A1, int P1, int s1, const flo
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
 // raise a kernel's dynamic shared-memory limit once per (kernel, size)
-void set_smem_once(const void* kern, size_t bytes) {
-  static std::mutex mu;
-  static std::vector<std::pair<const void*, size_t>> done;
-  std::lock_guard<std::mutex> lk(mu);
-  for (auto& d : done)
-    if (d.first == kern && d.second >= bytes) return;
-  GNPC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  done.emplace_back(kern, bytes);
-}
+void set_smem_once(const void* kern, size_t bytes) { set_smem_attr(kern, (int)bytes); }
 
 // [nv][32] fp32 rows viewed as a 2-D tensor, box {32 features, 128 rows}, 128B swizzle.
 CUtensorMap rows32_map(const float* base, int nv) {
@@ -497,6 +495,7 @@ void adam(gnpc_trainer_s& T) {
                                                               T.lr, bc1, bc2);
   GNPC_LAUNCHED();
   regenerate(T);
+  T.m->trainer_dirty = true;
 }
 
 // host n x B column-major f64 -> device [n][B]
@@ -511,6 +510,7 @@ void sync_model_params(gnpc_trainer_s& T) {
   GNPC_CUDA(cudaMemcpyAsync(T.m->params.data(), T.p64.p, T.P * 8, cudaMemcpyDeviceToHost, T.s));
   GNPC_CUDA(cudaStreamSynchronize(T.s));
   T.m->build_view();
+  T.m->trainer_dirty = false;
 }
 
 void need(bool c, const char* msg) {
@@ -585,7 +585,7 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
   T->colpart.alloc((std::size_t)1024 * T->B);
   T->scl.alloc(T->B);
   T->loss_grid = grid_for((std::int64_t)T->n * 32, kTh, T->sms * 8);
-  T->losspart.alloc(T->loss_grid);
+  T->losspart.alloc(T->loss_grid + 1);  // + one scratch slot (train_run's step loss)
   T->Xs.alloc(act * (T->L + 1));
   T->AXs.alloc(act * T->L);
   T->G[0].alloc(act);
@@ -966,77 +966,286 @@ int gnpc_trainer_sync_model(gnpc_trainer t) {
   });
 }
 
-// train_preconditioner (src/gnn.cpp:401-451).  Pairs are drawn with the
-// reference Rng streams (seed+1 sampler, seed+2 monitor, seed+3 training) and
-// assemble_batch semantics (src/sampler.cpp:68-83) on the host, b = A x with
-// the f64 matrix, so for a given sampler basis the batches are bit-identical
-// to the reference's.  The sampler's Arnoldi cycle runs on the device
-// (gnpc_sampler_create).  The next batch is drawn on a host thread while the
-// device runs the current step.
-int gnpc_train_preconditioner(gnpc_csr a, const gnpc_train_config* cfg, double* best,
-                              double* losses, double* best_loss) {
-  return guarded([&] {
-    need(a && cfg && best && losses && best_loss, "train_preconditioner: null argument");
-    if (cfg->batch < cfg->spectral_count)
-      throw std::invalid_argument("train: batch must be >= spectral_count");
-    if (cfg->batch < 1) throw std::invalid_argument("assemble_batch: empty batch");
-    if (cfg->monitor_batch < 1) throw std::invalid_argument("assemble_batch: empty batch");
-    const gnp_b200::Dims dims{cfg->d, cfg->hidden, cfg->layers};
-    std::vector<double> p0 = gnp_b200::init_params(dims, cfg->seed);
-    gnpc_model mm = nullptr;
-    if (int rc = gnpc_model_create(a, dims.d, dims.hidden, dims.layers, p0.data(), &mm))
-      throw std::runtime_error(gnpc_last_error());
-    std::unique_ptr<gnpc_model_s, void (*)(gnpc_model_s*)> model(mm, [](gnpc_model_s* q) {
-      gnpc_model_destroy(q);
-    });
-    // built whether or not spectral pairs are drawn, like the reference
-    // (its errors surface for spectral_count == 0 too)
-    const std::unique_ptr<gnpc_sampler_s> sampler =
-        build_sampler(*a, cfg->arnoldi_m, cfg->seed + 1);
-    const gnp_b200::SpectralSampler* sp = &sampler->s;
-    const std::int64_t n = a->h.n, B = cfg->batch, MB = cfg->monitor_batch;
+// train_preconditioner (src/gnn.cpp:401-451), device-resident.
+//
+// Seeds as the reference: init `seed`, sampler seed+1 (built also when
+// spectral_count == 0), monitor seed+2, training stream seed+3.  Per step:
+//   pairs   a host thread advances the reference Mersenne Twister for the
+//           next batch (raw words, pair_stream.hpp) into a pinned slot; the
+//           slot crosses on a copy stream while the device runs the current
+//           step; k_pairs_x tempers + Box-Muller (or x = V coef for spectral
+//           columns) into the trainer's [n][B] batch and k_spmm_nb_f64 forms
+//           b = A x with the f64 matrix values
+//   step    forward, L1 loss (folded on the device), backward, Adam
+//   monitor forward of the fixed monitoring batch (uploaded once), its loss
+//           into a device loss array, the best snapshot kept on the device
+// No host synchronisation inside the loop: losses and the best parameters are
+// read back once at the end.
+namespace {
+
+struct PinnedBuf {
+  unsigned char* p = nullptr;
+  std::size_t bytes = 0;
+  explicit PinnedBuf(std::size_t b) : bytes(b) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&p), b ? b : 1, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      throw std::bad_alloc();
+    }
+  }
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+};
+
+struct EvPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+// loss over the batch into *dst on the device (no host read)
+void loss_device(gnpc_trainer_s& T, bool want_grad, double* dst) {
+  gnpk::DevCsr a = T.m->a->dev();
+  gnpk::k_loss_residual<<<T.loss_grid, kTh, 0, T.s>>>(a, T.B, T.out.p, T.xb.p, T.sgn.p, T.losspart.p);
+  GNPC_LAUNCHED();
+  if (want_grad) {
+    gnpk::DevCsr at = T.At->dev();
+    gnpk::k_loss_grad<<<T.loss_grid, kTh, 0, T.s>>>(at, T.B, T.sgn.p, T.gout.p);
+    GNPC_LAUNCHED();
+  }
+  gnpk::k_loss_fold<<<1, 32, 0, T.s>>>(T.losspart.p, T.loss_grid, T.B, dst);
+  GNPC_LAUNCHED();
+}
+
+void train_run(gnpc_csr_s* a, const gnpc_train_config* cfg, double* best, double* losses,
+               double* best_loss, double* timing) {
+  need(a && cfg && best && losses && best_loss, "train_preconditioner: null argument");
+  if (cfg->batch < cfg->spectral_count)
+    throw std::invalid_argument("train: batch must be >= spectral_count");
+  if (cfg->batch < 1) throw std::invalid_argument("assemble_batch: empty batch");
+  if (cfg->monitor_batch < 1) throw std::invalid_argument("assemble_batch: empty batch");
+  const gnp_b200::Dims dims{cfg->d, cfg->hidden, cfg->layers};
+  std::vector<double> p0 = gnp_b200::init_params(dims, cfg->seed);
+  gnpc_model mm = nullptr;
+  if (gnpc_model_create(a, dims.d, dims.hidden, dims.layers, p0.data(), &mm))
+    throw std::runtime_error(gnpc_last_error());
+  std::unique_ptr<gnpc_model_s, void (*)(gnpc_model_s*)> model(mm, [](gnpc_model_s* q) {
+    gnpc_model_destroy(q);
+  });
+  const std::unique_ptr<gnpc_sampler_s> sampler = build_sampler(*a, cfg->arnoldi_m, cfg->seed + 1);
+  const gnp_b200::SpectralSampler* sp = &sampler->s;
+  const std::int64_t n = a->h.n, B = cfg->batch, MB = cfg->monitor_batch, S = cfg->spectral_count;
+  std::unique_ptr<gnpc_trainer_s> tr(create(model.get(), B, cfg->lr));
+  std::unique_ptr<gnpc_trainer_s> mon(MB == B ? nullptr : create(model.get(), MB, cfg->lr));
+  gnpc_trainer_s& M = mon ? *mon : *tr;
+  cudaStream_t s = tr->s;  // every trainer of a model runs on the model's stream
+  // the monitoring batch: drawn once on the host (Rng(seed+2)), resident
+  DevBuf<double> mxd, mbd;
+  {
     std::vector<double> mx(n * MB), mb(n * MB);
     gnp_b200::Rng monitor_rng(cfg->seed + 2);
-    gnp_b200::assemble_batch(sp, a->h, MB, std::min(cfg->spectral_count, MB), monitor_rng,
-                             mx.data(), mb.data());
-    gnp_b200::Rng train_rng(cfg->seed + 3);
-    std::unique_ptr<gnpc_trainer_s> tr(create(model.get(), B, cfg->lr));
-    std::unique_ptr<gnpc_trainer_s> mon(MB == B ? nullptr : create(model.get(), MB, cfg->lr));
-    gnpc_trainer_s& M = mon ? *mon : *tr;
-    auto monitoring = [&]() {
-      if (mon) {  // the monitor trainer reads the current params
-        GNPC_CUDA(cudaMemcpyAsync(M.p64.p, tr->p64.p, tr->P * 8, cudaMemcpyDeviceToDevice, tr->s));
-        regenerate(M);
-      }
-      return step_fb(M, mx.data(), mb.data(), false);
-    };
-    std::vector<double> bestp = p0;
-    double bl = monitoring();
-    losses[0] = bl;
-    std::vector<double> x(n * B), b(n * B), xn(n * B), bn(n * B);
-    auto draw = [&](std::vector<double>& xx, std::vector<double>& bb) {
-      gnp_b200::assemble_batch(sp, a->h, B, cfg->spectral_count, train_rng, xx.data(), bb.data());
-    };
-    std::future<void> next;
-    if (cfg->steps > 0) next = std::async(std::launch::async, draw, std::ref(xn), std::ref(bn));
-    for (std::int64_t step = 0; step < cfg->steps; ++step) {
-      next.get();  // rethrows a sampling error
-      x.swap(xn);
-      b.swap(bn);
-      if (step + 1 < cfg->steps) next = std::async(std::launch::async, draw, std::ref(xn), std::ref(bn));
-      step_fb(*tr, x.data(), b.data(), true);
-      adam(*tr);
-      const double ml = monitoring();
-      losses[step + 1] = ml;
-      if (ml < bl) {
-        bl = ml;
-        GNPC_CUDA(cudaMemcpyAsync(bestp.data(), tr->p64.p, tr->P * 8, cudaMemcpyDeviceToHost, tr->s));
-        GNPC_CUDA(cudaStreamSynchronize(tr->s));
-      }
+    gnp_b200::assemble_batch(sp, a->h, MB, std::min(S, MB), monitor_rng, mx.data(), mb.data());
+    upload_batch(M, mx.data(), M.xb);
+    upload_batch(M, mb.data(), M.bb);
+    if (!mon) {  // shared trainer: keep the monitor batch aside, swap it in
+      mxd.alloc(M.xb.count);
+      mbd.alloc(M.bb.count);
+      std::swap(mxd, M.xb);
+      std::swap(mbd, M.bb);
+      GNPC_CUDA(cudaStreamSynchronize(s));
     }
-    std::copy(bestp.begin(), bestp.end(), best);
-    *best_loss = bl;
-  });
+  }
+  // f64 matrix values for b = A x (the reference's pairs use the f64 Â)
+  DevBuf<double> a64;
+  a64.upload(a->h.values.data(), a->h.values.size(), s);
+  DevBuf<double> vdev;
+  if (S > 0) vdev.upload(sp->v.data(), sp->v.size(), s);
+  const std::int64_t steps = cfg->steps;
+  DevBuf<double> dloss(steps + 1), dbest(1), dbestp(tr->P);
+  auto monitoring = [&](std::int64_t k) {
+    if (mon) {  // the monitor trainer reads the current params
+      GNPC_CUDA(cudaMemcpyAsync(M.p64.p, tr->p64.p, tr->P * 8, cudaMemcpyDeviceToDevice, s));
+      regenerate(M);
+    } else {
+      std::swap(mxd, M.xb);
+      std::swap(mbd, M.bb);
+    }
+    forward(M);
+    loss_device(M, false, dloss.p + k);
+    if (!mon) {
+      std::swap(mxd, M.xb);
+      std::swap(mbd, M.bb);
+    }
+  };
+  monitoring(0);
+  GNPC_CUDA(cudaMemcpyAsync(dbest.p, dloss.p, 8, cudaMemcpyDeviceToDevice, s));
+  GNPC_CUDA(cudaMemcpyAsync(dbestp.p, tr->p64.p, tr->P * 8, cudaMemcpyDeviceToDevice, s));
+
+  // ---- pair stream: host producer thread, two pinned + two device slots
+  gnp_b200::PairStream ps(cfg->seed + 3, n, B, S, sp);
+  const gnp_b200::PairBatchLayout& lay = ps.layout();
+  std::unique_ptr<PinnedBuf> hslot[2];
+  DevBuf<unsigned char> dslot[2];
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  cudaStream_t cs = nullptr;
+  if (steps > 0) {
+    for (int q = 0; q < 2; ++q) {
+      hslot[q] = std::make_unique<PinnedBuf>(lay.bytes);
+      dslot[q].alloc(lay.bytes);
+      GNPC_CUDA(cudaEventCreateWithFlags(&ev_copied[q], cudaEventDisableTiming));
+      GNPC_CUDA(cudaEventCreateWithFlags(&ev_used[q], cudaEventDisableTiming));
+    }
+    GNPC_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  }
+  struct Cleanup {
+    cudaEvent_t* e1;
+    cudaEvent_t* e2;
+    cudaStream_t* cs;
+    ~Cleanup() {
+      for (int q = 0; q < 2; ++q) {
+        if (e1[q]) cudaEventDestroy(e1[q]);
+        if (e2[q]) cudaEventDestroy(e2[q]);
+      }
+      if (*cs) cudaStreamDestroy(*cs);
+    }
+  } cleanup{ev_copied, ev_used, &cs};
+  std::mutex mu;
+  std::condition_variable cv;
+  std::int64_t ready = 0, enqueued = 0;
+  bool abort = false;
+  std::exception_ptr perr;
+  std::thread producer;
+  if (steps > 0)
+    producer = std::thread([&] {
+      try {
+        for (std::int64_t t = 0; t < steps; ++t) {
+          const int q = (int)(t & 1);
+          {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return abort || enqueued >= t - 1; });
+            if (abort) return;
+          }
+          if (t >= 2 && cudaEventSynchronize(ev_copied[q]) != cudaSuccess)
+            throw std::runtime_error("pair stream: copy failed");
+          ps.fill(hslot[q]->p);
+          {
+            std::lock_guard<std::mutex> lk(mu);
+            ready = t + 1;
+          }
+          cv.notify_all();
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu);
+        perr = std::current_exception();
+        abort = true;
+        cv.notify_all();
+      }
+    });
+  struct Joiner {
+    std::thread& t;
+    std::mutex& mu;
+    std::condition_variable& cv;
+    bool& abort;
+    ~Joiner() {
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        abort = true;
+      }
+      cv.notify_all();
+      if (t.joinable()) t.join();
+    }
+  } joiner{producer, mu, cv, abort};
+
+  std::vector<EvPair> evp, evm;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timing) {
+    evp.resize(steps);
+    evm.resize(steps);
+    for (std::int64_t t = 0; t < steps; ++t)
+      for (cudaEvent_t* e : {&evp[t].a, &evp[t].b, &evm[t].a, &evm[t].b}) GNPC_CUDA(cudaEventCreate(e));
+    GNPC_CUDA(cudaEventCreate(&e0));
+    GNPC_CUDA(cudaEventCreate(&e1));
+    GNPC_CUDA(cudaEventRecord(e0, s));
+  }
+  double host_wait_ms = 0.0;
+  const int pgrid = (int)((n * B + kTh - 1) / kTh);
+  const gnpk::DevCsr adev = a->dev();
+  for (std::int64_t t = 0; t < steps; ++t) {
+    const int q = (int)(t & 1);
+    {
+      const auto w0 = std::chrono::steady_clock::now();
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [&] { return abort || ready >= t + 1; });
+      if (perr) std::rethrow_exception(perr);
+      if (abort) throw std::runtime_error("pair stream stopped");
+      host_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+    }
+    GNPC_CUDA(cudaStreamWaitEvent(cs, ev_used[q], 0));
+    GNPC_CUDA(cudaMemcpyAsync(dslot[q].p, hslot[q]->p, lay.bytes, cudaMemcpyHostToDevice, cs));
+    GNPC_CUDA(cudaEventRecord(ev_copied[q], cs));
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      enqueued = t + 1;
+    }
+    cv.notify_all();
+    GNPC_CUDA(cudaStreamWaitEvent(s, ev_copied[q], 0));
+    if (timing) GNPC_CUDA(cudaEventRecord(evp[t].a, s));
+    const unsigned char* ds = dslot[q].p;
+    gnpk::k_pairs_x<<<pgrid, kTh, 0, s>>>(
+        reinterpret_cast<const gnpk::PairColDev*>(ds + lay.cols_off),
+        reinterpret_cast<const double*>(ds + lay.coef_off),
+        reinterpret_cast<const unsigned long long*>(ds + lay.words_off), vdev.p, (int)lay.m, (int)n, (int)B,
+        tr->xb.p);
+    GNPC_LAUNCHED();
+    gnpk::k_spmm_nb_f64<<<tr->loss_grid, kTh, 0, s>>>(adev, a64.p, (int)B, tr->xb.p, tr->bb.p);
+    GNPC_LAUNCHED();
+    GNPC_CUDA(cudaEventRecord(ev_used[q], s));
+    if (timing) GNPC_CUDA(cudaEventRecord(evp[t].b, s));
+    forward(*tr);
+    loss_device(*tr, true, tr->losspart.p + tr->loss_grid);  // scratch slot past the partials
+    backward(*tr);
+    adam(*tr);
+    if (timing) GNPC_CUDA(cudaEventRecord(evm[t].a, s));
+    monitoring(t + 1);
+    gnpk::k_best_keep<<<1, kTh, 0, s>>>(dloss.p + t + 1, dbest.p, M.p64.p, dbestp.p, (int)tr->P);
+    GNPC_LAUNCHED();
+    if (timing) GNPC_CUDA(cudaEventRecord(evm[t].b, s));
+  }
+  if (timing) GNPC_CUDA(cudaEventRecord(e1, s));
+  GNPC_CUDA(cudaMemcpyAsync(losses, dloss.p, (steps + 1) * 8, cudaMemcpyDeviceToHost, s));
+  GNPC_CUDA(cudaMemcpyAsync(best, dbestp.p, tr->P * 8, cudaMemcpyDeviceToHost, s));
+  GNPC_CUDA(cudaMemcpyAsync(best_loss, dbest.p, 8, cudaMemcpyDeviceToHost, s));
+  GNPC_CUDA(cudaStreamSynchronize(s));
+  if (timing) {
+    float tot = 0.f, pm = 0.f, mm2 = 0.f, x = 0.f;
+    GNPC_CUDA(cudaEventElapsedTime(&tot, e0, e1));
+    for (std::int64_t t = 0; t < steps; ++t) {
+      GNPC_CUDA(cudaEventElapsedTime(&x, evp[t].a, evp[t].b));
+      pm += x;
+      GNPC_CUDA(cudaEventElapsedTime(&x, evm[t].a, evm[t].b));
+      mm2 += x;
+      for (cudaEvent_t e : {evp[t].a, evp[t].b, evm[t].a, evm[t].b}) cudaEventDestroy(e);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    timing[0] = tot;
+    timing[1] = pm;
+    timing[2] = mm2;
+    timing[3] = host_wait_ms;
+  }
+}
+
+}  // namespace
+
+int gnpc_train_preconditioner(gnpc_csr a, const gnpc_train_config* cfg, double* best,
+                              double* losses, double* best_loss) {
+  return guarded([&] { train_run(a, cfg, best, losses, best_loss, nullptr); });
+}
+
+int gnpc_train_preconditioner_timed(gnpc_csr a, const gnpc_train_config* cfg, double* best,
+                                    double* losses, double* best_loss, double* timing_ms4) {
+  return guarded([&] { train_run(a, cfg, best, losses, best_loss, timing_ms4); });
 }
 
 }  // extern "C"

@@ -269,3 +269,24 @@ def test_piecewise_encoder_hidden64(capi, oc, cuda):
     want_loss, want = oc.batch_loss_grads(a, dims, p, x, b, 8)
     assert abs(loss - want_loss) <= 1e-5 * abs(want_loss)
     check_grads(g, want, dims)
+
+
+def test_trained_model_refuses_apply_until_synced(capi, oc, cuda):
+    # a trainer's Adam step rewrites the model's device operands but not its
+    # host params / lift tables: applies must refuse the mixed state until
+    # gnpc_trainer_sync_model, then match the oracle with the trained params
+    a = oc.prescale(oc.gen_convection_diffusion(12, 0.4), 8.8).rounded_f32()
+    dims = (16, 32, 3)
+    p = f32(oc.init_params(*dims, 5))
+    m = capi.Model(dev_csr(capi, a), dims, p)
+    b = oc.gaussian_vector(2, a.n)
+    m.apply(b)
+    t = capi.Trainer(m, 4)
+    x, bb = oc.gaussian_batch(a, 9, 0, 4)
+    t.step(x, bb)
+    with pytest.raises(capi.GnpcError):
+        m.apply(b)
+    t.sync_model()
+    y = m.apply(b)
+    want = oc.gnn_apply(a, dims, t.params(), b)
+    assert rel_l2(y, want) <= 1e-4

@@ -807,22 +807,53 @@ void* ortho_kernel_for(int ept) {
 struct OrthoPlan {
   void* kern;
   int grid;
+  int block = gnpk::kThreads;
+  size_t smem = 0;
+  int chunk = 0;  // on-chip variant: rows per CTA
 };
 
 // The MGS sweep is one grid barrier per basis vector, so the barrier's cost
 // (which grows with the CTA count) is paid j+1 times per pass: prefer few
 // CTAs (1, then 2 per SM) holding w in registers with a larger EPT, and only
-// then more CTAs.  (C2: ~1180 CTAs at EPT 1 -> 148 CTAs at EPT 8.)
+// then more CTAs.  (C2: ~1180 CTAs at EPT 1 -> 148 CTAs at EPT 8.)  Vectors
+// too long for that keep w in registers + shared memory of one 1024-thread
+// CTA per SM (k_krylov_ortho_onchip, C5) before falling back to w in HBM.
 OrthoPlan plan_ortho(int n) {
   const int sms = num_sms();
+  static const bool onchip_off = [] {
+    const char* e = std::getenv("GNPC_NO_ONCHIP_MGS");
+    return e && std::string(e) == "1";
+  }();
+  static const bool force_onchip = [] {  // test hook: exercise the on-chip variant at small n
+    const char* e = std::getenv("GNPC_FORCE_ONCHIP_MGS");
+    return e && std::string(e) == "1";
+  }();
   for (int per : {1, 2, 4}) {
     for (int ept : {1, 2, 4, 8, 16}) {
+      if (force_onchip) break;
       int per_sm = 0;
       GNPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ortho_kernel_for(ept),
                                                               gnpk::kThreads, 0));
       if (per_sm < per) continue;
       const long long cap = (long long)per * sms * gnpk::kThreads * ept;
       if (n <= cap) return {ortho_kernel_for(ept), per * sms};
+    }
+  }
+  if (!onchip_off) {
+    constexpr int NR = 4;
+    auto kern = (const void*)gnpk::k_krylov_ortho_onchip<NR>;
+    cudaFuncAttributes fa{};
+    GNPC_CUDA(cudaFuncGetAttributes(&fa, kern));
+    const int smem_cap = 227 * 1024 - (int)fa.sharedSizeBytes - 1024;
+    const long long chunk = ((long long)n + sms - 1) / sms;
+    const long long need_smem = std::max<long long>(0, chunk - (long long)NR * gnpk::kOnchipThreads) * 8;
+    if (need_smem <= smem_cap) {
+      set_smem_attr(kern, (int)std::max<long long>(need_smem, 8));
+      int per_sm = 0;
+      GNPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, gnpk::kOnchipThreads,
+                                                              (size_t)std::max<long long>(need_smem, 8)));
+      if (per_sm >= 1)
+        return {(void*)kern, sms, gnpk::kOnchipThreads, (size_t)std::max<long long>(need_smem, 8), (int)chunk};
     }
   }
   for (int ept : {1, 2, 4, 8, 16}) {
@@ -1008,8 +1039,9 @@ int fgmres_core(gnpc_csr_s& A, gnpc_model_s* M, const HostOp* hop, const double*
         }
         gnpk::k_krylov_spmv<<<rgrid, gnpk::kThreads, 0, s>>>(a, k);
         GNPC_LAUNCHED();
-        void* args[] = {&k};
-        GNPC_CUDA(cudaLaunchCooperativeKernel(op.kern, op.grid, gnpk::kThreads, args, 0, s));
+        int chunk = op.chunk;
+        void* args[] = {&k, &chunk};
+        GNPC_CUDA(cudaLaunchCooperativeKernel(op.kern, op.grid, op.block, args, op.smem, s));
         GNPC_LAUNCHED();
       }
       gnpk::k_cycle_solve<<<1, 32, 0, s>>>(k);

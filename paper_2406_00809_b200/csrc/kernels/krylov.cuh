@@ -174,7 +174,10 @@ __global__ void __launch_bounds__(kThreads) k_krylov_ortho(KrylovDev k) {
   const int ld = k.m + 1;
   double* Hj = k.H + static_cast<size_t>(j) * ld;
 
-  // One MGS pass over v_0..v_j; returns ||w|| afterwards.
+  // One MGS pass over v_0..v_j; returns ||w|| afterwards.  With w in
+  // registers, v_s also stays in registers from its dot (step s) to its axpy
+  // (step s + 1): every basis vector is read once per pass.
+  double vc[E];
   auto mgs_pass = [&](bool add) -> double {
     double hprev = 0.0;
     for (int s = 0; s <= j + 1; ++s) {
@@ -186,8 +189,13 @@ __global__ void __launch_bounds__(kThreads) k_krylov_ortho(KrylovDev k) {
         for (int t = 0; t < EPT; ++t) {
           const int e = gt + t * T;
           if (e < n) {
-            if (s > 0) w[t] = fma(-hprev, vprev[e], w[t]);
-            part = s <= j ? fma(w[t], vs[e], part) : fma(w[t], w[t], part);
+            if (s > 0) w[t] = fma(-hprev, vc[t], w[t]);
+            if (s <= j) {
+              vc[t] = vs[e];
+              part = fma(w[t], vc[t], part);
+            } else {
+              part = fma(w[t], w[t], part);
+            }
           }
         }
       } else {
@@ -236,6 +244,107 @@ __global__ void __launch_bounds__(kThreads) k_krylov_ortho(KrylovDev k) {
     }
   }
   if (gt == 0) givens_and_state(k, j, wnorm, brk, reo);
+}
+
+// The same step for vectors too long for w in registers at any grid size
+// (C5: n = 4.19M): one 1024-thread CTA per SM owns a contiguous chunk of w,
+// NR elements per thread in registers and the rest in shared memory, so w
+// never goes back to HBM during the MGS sweeps; only the basis vectors stream
+// (v_s once per step; v_{s-1} again for the shared-memory part, from L2).
+// Arithmetic per element and the reductions are those of k_krylov_ortho.
+constexpr int kOnchipThreads = 1024;
+template <int NR>
+__global__ void __launch_bounds__(kOnchipThreads, 1) k_krylov_ortho_onchip(KrylovDev k, int chunk) {
+  cg::grid_group grid = cg::this_grid();
+  KState* st = k.st;
+  if (st->stop) return;
+  extern __shared__ double wsm[];
+  const int j = st->j;
+  const int n = k.n;
+  const int tid = threadIdx.x;
+  const int base = blockIdx.x * chunk;
+  const int len = max(0, min(chunk, n - base));
+  constexpr int RB = NR * kOnchipThreads;  // chunk elements held in registers
+  __shared__ double scratch[32];
+  int phase = 0;
+  double w[NR > 0 ? NR : 1], vc[NR > 0 ? NR : 1];
+  double p = 0.0;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int c = r * kOnchipThreads + tid;
+    w[r] = c < len ? k.w[base + c] : 0.0;
+    p = fma(w[r], w[r], p);
+  }
+  for (int c = RB + tid; c < len; c += kOnchipThreads) {
+    const double we = k.w[base + c];
+    wsm[c - RB] = we;
+    p = fma(we, we, p);
+  }
+  const double wnorm0 = sqrt(grid_sum(grid, p, k.partials, phase, scratch));
+  const int ld = k.m + 1;
+  double* Hj = k.H + static_cast<size_t>(j) * ld;
+
+  auto mgs_pass = [&](bool add) -> double {
+    double hprev = 0.0;
+    for (int s = 0; s <= j + 1; ++s) {
+      const double* vprev = k.V + static_cast<size_t>(s > 0 ? s - 1 : 0) * n + base;
+      const double* vs = k.V + static_cast<size_t>(s) * n + base;
+      double part = 0.0;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int c = r * kOnchipThreads + tid;
+        if (c < len) {
+          if (s > 0) w[r] = fma(-hprev, vc[r], w[r]);
+          if (s <= j) {
+            vc[r] = vs[c];
+            part = fma(w[r], vc[r], part);
+          } else {
+            part = fma(w[r], w[r], part);
+          }
+        }
+      }
+      for (int c = RB + tid; c < len; c += kOnchipThreads) {
+        double we = wsm[c - RB];
+        if (s > 0) {
+          we = fma(-hprev, vprev[c], we);
+          wsm[c - RB] = we;
+        }
+        part = s <= j ? fma(we, vs[c], part) : fma(we, we, part);
+      }
+      const double tot = grid_sum(grid, part, k.partials, phase, scratch);
+      if (s <= j) {
+        hprev = tot;
+        if (blockIdx.x == 0 && tid == 0) Hj[s] = add ? Hj[s] + tot : tot;
+      } else {
+        return sqrt(tot);
+      }
+    }
+    return 0.0;
+  };
+
+  double wnorm = mgs_pass(false);
+  const bool reo = wnorm < 0.70710678118654752440 * wnorm0;
+  if (reo) wnorm = mgs_pass(true);
+  const bool brk = wnorm <= 1e-14 * wnorm0;
+  if (!brk) {
+    double* vn = k.V + static_cast<size_t>(j + 1) * n + base;
+    double* vi = k.vin + base;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int c = r * kOnchipThreads + tid;
+      if (c < len) {
+        const double v = w[r] / wnorm;
+        vn[c] = v;
+        vi[c] = v;
+      }
+    }
+    for (int c = RB + tid; c < len; c += kOnchipThreads) {
+      const double v = wsm[c - RB] / wnorm;
+      vn[c] = v;
+      vi[c] = v;
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) givens_and_state(k, j, wnorm, brk, reo);
 }
 
 // r = b - A x (src/krylov.cpp:194-199), ||r|| with a last-block finish;

@@ -202,3 +202,52 @@ def test_fused_apply_after_mid_cycle_stop(capi, oc, cuda):
         assert s["status"] == "converged" and s["history"][-1][0] <= 5
     y = m.apply(g["b"])
     assert rel_l2(y, g["out"]) < 1e-5
+
+
+@pytest.mark.parametrize("n_grid", [64, 23])
+def test_onchip_mgs_variant_matches(capi, oc, gnp, cuda, n_grid):
+    # k_krylov_ortho_onchip (w in registers + shared memory; taken for n too
+    # long for the register variant, e.g. C5) forced at C2 size and at an
+    # odd size in a subprocess, against the default variant and the oracle
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import json, sys, numpy as np
+sys.path.insert(0, "."); sys.path.insert(0, "oracle")
+from paper_2406_00809_b200 import capi
+import oracle
+oc = oracle.restatement()
+a0 = oc.gen_named("c2_convdiff3d", %d, 10.0)
+a = oc.prescale(a0, oc.gershgorin_gamma(a0)).rounded_f32()
+b = oc.spmv(a, oc.gaussian_vector(1, a.n))
+A = capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
+s = capi.fgmres(A, b, rtol=1e-8, maxiters=120, restart=30)
+m = capi.Model(A, (16, 32, 8), oc.init_params(16, 32, 8, 0).astype(np.float32).astype(np.float64))
+g = capi.fgmres(A, b, model=m, rtol=1e-8, maxiters=40, restart=30)
+print(json.dumps({"h": [e[1] for e in s["history"]], "st": s["status"], "hg": [e[1] for e in g["history"]],
+                  "re": s["reorth_steps"]}))
+""" % n_grid
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for force in ("0", "1"):
+        env = dict(os.environ, GNPC_FORCE_ONCHIP_MGS=force)
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    d, o = outs
+    assert d["st"] == o["st"] and len(d["h"]) == len(o["h"]) and len(d["hg"]) == len(o["hg"])
+    for x, y in zip(d["h"], o["h"]):  # GMRES: only the MGS reduction order differs
+        assert abs(x - y) <= 1e-9 * max(abs(y), 1e-300) + 1e-15
+    for x, y in zip(d["hg"], o["hg"]):  # fp32 GNP: rounding flips inside M can follow
+        assert abs(x - y) <= 1e-4 * abs(y)
+    # and the oracle's GMRES on the same system
+    a0 = oc.gen_named("c2_convdiff3d", n_grid, 10.0)
+    a = oc.prescale(a0, oc.gershgorin_gamma(a0)).rounded_f32()
+    b = oc.spmv(a, oc.gaussian_vector(1, a.n))
+    want = oc.fgmres(a, b, rtol=1e-8, maxiters=120, restart=30)
+    assert want["status"] == o["st"] and len(want["history"]) == len(o["h"])
+    assert abs(want["history"][-1][1] - o["h"][-1]) <= 1e-6 * want["history"][-1][1]

@@ -77,9 +77,11 @@ int gnpc_csr_generate(const char* kind, int64_t size, double p0, double p1, uint
 int gnpc_csr_read_matrix_market(const char* path, gnpc_csr* out); /* src/mmio.cpp:89-93 */
 int gnpc_csr_info(gnpc_csr a, int64_t* n, int64_t* nnz);
 /* Device layout of Â (introspection; the device copy is built on first use):
- * *uploaded = 1 once it exists, *sliced_ell = 1 when the 128-row sliced-ELL
- * copy feeding the TMA layer pipeline was built, *long_rows = rows routed to
- * the chunked long-row path (> 32 nonzeros).  No reference counterpart. */
+ * *uploaded = 1 once it exists; *sliced_ell = 0 when no TMA-pipeline layout
+ * was built, else a bit mask: 1 the 128-row sliced-ELL copy, 2 its pair-union
+ * form (d = 32), 4 the strip-window pair-union form (d = 32), 8 the windowed
+ * d = 16 form; *long_rows = rows routed to the chunked long-row path (> 32
+ * nonzeros).  No reference counterpart. */
 int gnpc_csr_device_layout(gnpc_csr a, int* uploaded, int* sliced_ell, int* long_rows);
 int gnpc_csr_export(gnpc_csr a, int64_t* row_ptr, int64_t* col_idx, double* values);
 int gnpc_csr_gershgorin_gamma(gnpc_csr a, double* gamma);          /* src/csr.cpp:127-143 */

@@ -189,6 +189,43 @@ struct ApplyLaunch {
       }
       const bool last = l + 1 == net.layers;
       mark(last ? 4 : 3);
+      if constexpr (DP == 32) {
+        // strip windows (stencil-like d = 32 matrices with a dominant tile
+        // stride): X rows staged in shared memory, one new window per tile
+        if (a.pw && m.use_tc && !sell_off && SellCfg<32, 8>::smem_bytes(net.hidden, true) <= 227 * 1024) {
+          using S = SellCfg<DP, 7>;
+          auto kern = last ? k_layer_sell<DP, true, OutT, 8> : k_layer_sell<DP, false, OutT, 7>;
+          const size_t smem_l = last ? SellCfg<DP, 8>::smem_bytes(net.hidden, true)
+                                     : SellCfg<DP, 7>::smem_bytes(net.hidden, false);
+          set_smem_attr((const void*)kern, 227 * 1024);
+          const int tiles_s = (n + S::TM - 1) / S::TM;
+          const int grid = std::max(1, std::min(tiles_s, sms));
+          SellMaps maps{m.tmX[cur], m.tmX[1 - cur], m.tmXw[cur]};
+          const float* uwp = m.UWP.p + (size_t)l * 4 * DP * DP;
+          kern<<<grid, S::NT, smem_l, s>>>(a, maps, X, axl, uwp, net, m.sc.p, out, skip);
+          GNPC_LAUNCHED();
+          cur = 1 - cur;
+          continue;
+        }
+        // pair-union slices (stencil-like d = 32 matrices): 4-deep ring for
+        // the non-last layers, 3 deep for the last
+        if (a.psell && m.use_tc && !sell_off &&
+            SellCfg<32, 6>::smem_bytes(net.hidden, true) <= 227 * 1024) {
+          using S = SellCfg<DP, 5>;
+          auto kern = last ? k_layer_sell<DP, true, OutT, 6> : k_layer_sell<DP, false, OutT, 5>;
+          const size_t smem_l = last ? SellCfg<DP, 6>::smem_bytes(net.hidden, true)
+                                     : SellCfg<DP, 5>::smem_bytes(net.hidden, false);
+          set_smem_attr((const void*)kern, 227 * 1024);
+          const int tiles_s = (n + S::TM - 1) / S::TM;
+          const int grid = std::max(1, std::min(tiles_s, sms));
+          SellMaps maps{m.tmX[cur], m.tmX[1 - cur], m.tmXw[cur]};
+          const float* uwp = m.UWP.p + (size_t)l * 4 * DP * DP;
+          kern<<<grid, S::NT, smem_l, s>>>(a, maps, X, axl, uwp, net, m.sc.p, out, skip);
+          GNPC_LAUNCHED();
+          cur = 1 - cur;
+          continue;
+        }
+      }
       if constexpr (DP == 16 || DP == 32) {
         const int lmode = (DP == 16 && a.wdesc && A.n_long == 0) ? 3 : (a.sell ? 0 : 1);
         const size_t smem = lmode == 3 ? SellCfg<DP, (DP == 16 ? 3 : 0)>::smem_bytes(net.hidden, last)
@@ -360,6 +397,9 @@ void gnpc_csr_s::upload() {
     long_c0.upload(c0.data(), c0.size());
   }
   build_sell(hrp, hci, hv);
+  build_pairs(hrp, hci, hv);
+  build_pw(hrp, hci, hv);
+  build_order(hrp, hci);
   // short-row CSR (long rows emptied), padded for the TMA pipeline's bulk copies
   {
     const std::int64_t n = h.n;
@@ -495,6 +535,262 @@ void gnpc_csr_s::build_sell(const std::vector<int>& hrp, const std::vector<int>&
   has_win = true;
 }
 
+// Pair-union sliced-ELL (see DevCsr::psell).  Built for matrices without long
+// rows whose rows are column-sorted and whose adjacent row pairs share enough
+// columns that the union gathers are <= 80 % of the sliced-ELL gathers
+// (9-point stencil: 12 vs 18 per pair).  GNPC_NO_PAIR=1 disables it.
+void gnpc_csr_s::build_pairs(const std::vector<int>& hrp, const std::vector<int>& hci,
+                             const std::vector<float>& hv) {
+  has_pairs = false;
+  if (!has_sell || n_long != 0) return;
+  if (const char* e = std::getenv("GNPC_NO_PAIR"); e && std::string(e) == "1") return;
+  const std::int64_t n = h.n;
+  constexpr int TM = 128, NG = TM / 2;
+  const std::int64_t ntiles = (n + TM - 1) / TM;
+  for (std::int64_t i = 0; i < n; ++i)
+    for (int k = hrp[i] + 1; k < hrp[i + 1]; ++k)
+      if (hci[k] <= hci[k - 1]) return;  // unsorted or duplicate columns: stored order not a merge
+  auto row_range = [&](std::int64_t i, int& s, int& e) {
+    if (i < n) {
+      s = hrp[i];
+      e = hrp[i + 1];
+    } else {
+      s = e = 0;
+    }
+  };
+  // union length of each pair, per tile maximum
+  std::vector<int> K(ntiles, 0), off(ntiles, 0);
+  std::int64_t total = 0, sell_gathers = 0;
+  for (std::int64_t t = 0; t < ntiles; ++t) {
+    int kt = 0, ks = 0;
+    for (int g = 0; g < NG; ++g) {
+      int s0, e0, s1, e1;
+      row_range(t * TM + 2 * g, s0, e0);
+      row_range(t * TM + 2 * g + 1, s1, e1);
+      ks = std::max(ks, std::max(e0 - s0, e1 - s1));
+      int u = 0;
+      while (s0 < e0 || s1 < e1) {
+        if (s1 >= e1 || (s0 < e0 && hci[s0] < hci[s1])) ++s0;
+        else if (s0 >= e0 || hci[s1] < hci[s0]) ++s1;
+        else { ++s0; ++s1; }
+        ++u;
+      }
+      kt = std::max(kt, u);
+    }
+    off[t] = static_cast<int>(total);
+    total += (std::int64_t)kt * NG;
+    if (total >= (std::int64_t(1) << 31)) return;
+    K[t] = kt;
+    sell_gathers += (std::int64_t)ks * TM;
+  }
+  if ((double)total > 0.8 * (double)sell_gathers) return;  // not enough sharing
+  std::vector<int4> ent(std::max<std::int64_t>(total, 1));
+  for (std::int64_t t = 0; t < ntiles; ++t) {
+    for (int g = 0; g < NG; ++g) {
+      const std::int64_t i0 = t * TM + 2 * g;
+      int s0, e0, s1, e1;
+      row_range(i0, s0, e0);
+      row_range(i0 + 1, s1, e1);
+      int u = 0;
+      auto put = [&](int col, float w0, float w1) {
+        int4 e;
+        e.x = col;
+        std::memcpy(&e.y, &w0, 4);
+        std::memcpy(&e.z, &w1, 4);
+        e.w = 0;
+        ent[off[t] + (std::size_t)u * NG + g] = e;
+        ++u;
+      };
+      while (s0 < e0 || s1 < e1) {
+        if (s1 >= e1 || (s0 < e0 && hci[s0] < hci[s1])) {
+          put(hci[s0], hv[s0], 0.f);
+          ++s0;
+        } else if (s0 >= e0 || hci[s1] < hci[s0]) {
+          put(hci[s1], 0.f, hv[s1]);
+          ++s1;
+        } else {
+          put(hci[s0], hv[s0], hv[s1]);
+          ++s0;
+          ++s1;
+        }
+      }
+      const int own = i0 < n ? static_cast<int>(i0) : 0;
+      while (u < K[t]) put(own, 0.f, 0.f);
+    }
+  }
+  psell.upload(ent.data(), ent.size());
+  psell_off.upload(off.data(), off.size());
+  psell_k.upload(K.data(), K.size());
+  has_pairs = true;
+}
+
+// Tile schedule for the TMA layer pipeline.  A CTA walks a contiguous chunk
+// of this order, so its consecutive tiles should gather from overlapping row
+// windows and hit L1.  For matrices whose off-tile columns concentrate at one
+// tile distance S (stencils: the grid-line offset, e.g. 2048 rows = 16 tiles on
+// C5's 2048^2 grid, 4096 rows = 32 tiles on C2's 64^3), tiles are ordered
+// t = s + S k (s < S, k ascending): tile s + S(k+1) then reuses two of the
+// three row windows of tile s + S k.  Ragged/random matrices have no dominant
+// stride and keep round-robin.
+void gnpc_csr_s::build_order(const std::vector<int>& hrp, const std::vector<int>& hci) {
+  tstride = 0;
+  const std::int64_t n = h.n;
+  constexpr int TM = 128;
+  const std::int64_t T = (n + TM - 1) / TM;
+  // opt-in (GNPC_TORDER=1): C5 measured 427 vs 418 us per layer with it (its
+  // 28 KB of L1 beside the 198 KB ring cannot hold the three windows)
+  if (const char* e = std::getenv("GNPC_TORDER"); !e || std::string(e) != "1") return;
+  if (n_long != 0 || T < 4 * 148) return;
+  const int S = dominant_tile_stride(hrp, hci);
+  if (S < 2) return;
+  std::vector<int> ord;
+  ord.reserve(T);
+  for (int s0 = 0; s0 < S; ++s0)
+    for (std::int64_t t = s0; t < T; t += S) ord.push_back(static_cast<int>(t));
+  torder.upload(ord.data(), ord.size());
+  tstride = S;
+}
+
+// The tile distance S (>= 2) at which most off-tile columns sit (a row
+// window straddles two tiles, so distances S-1..S+1 count for S); 0 when no
+// distance holds >= 25 % of a row sample's entries.
+int gnpc_csr_s::dominant_tile_stride(const std::vector<int>& hrp, const std::vector<int>& hci) const {
+  const std::int64_t n = h.n;
+  constexpr int TM = 128;
+  // histogram of |tile distance| for off-tile entries of a row sample
+  std::vector<std::int64_t> hist(4097, 0);
+  std::int64_t total = 0;
+  const std::int64_t step = std::max<std::int64_t>(1, n / 65536);
+  for (std::int64_t i = 0; i < n; i += step) {
+    const std::int64_t ti = i / TM;
+    for (int k = hrp[i]; k < hrp[i + 1]; ++k) {
+      const std::int64_t d = std::llabs(static_cast<std::int64_t>(hci[k]) / TM - ti);
+      ++total;
+      if (d >= 2 && d <= 4096) ++hist[d];
+    }
+  }
+  if (total == 0) return 0;
+  std::int64_t best = 0;
+  int S = 0;
+  for (int d = 2; d <= 4095; ++d) {
+    const std::int64_t c = hist[d - 1] + hist[d] + hist[d + 1];
+    if (c > best) {
+      best = c;
+      S = d;
+    }
+  }
+  if (S < 2 || 4 * best < total) return 0;  // no dominant stride: < 25 % of the entries
+  return S;
+}
+
+// Strip-window pair-union layout (see DevCsr::pw): tiles ordered in strips
+// of stride S, every column of tile u inside the halo-extended row windows of
+// tiles u - S, u, u + S, at most GNPC_KCAPPW union entries per row pair.
+// GNPC_NO_PW=1 disables it.
+void gnpc_csr_s::build_pw(const std::vector<int>& hrp, const std::vector<int>& hci, const std::vector<float>& hv) {
+  has_pw = false;
+  if (!has_pairs || n_long != 0) return;
+  if (const char* e = std::getenv("GNPC_NO_PW"); e && std::string(e) == "1") return;
+  const std::int64_t n = h.n;
+  constexpr int TM = 128, NG = TM / 2, H = gnpk::kPwHalo, WR = gnpk::kPwRows;
+  constexpr int KMAX = gnpk::SellCfg<32, 7>::KCAP;
+  const std::int64_t T = (n + TM - 1) / TM;
+  // short strips make most tiles chunk starts (three fresh windows each):
+  // at least 4 tiles per SM (GNPC_PW_MIN_TILES overrides, for tests)
+  std::int64_t min_tiles = 4 * 148;
+  if (const char* e = std::getenv("GNPC_PW_MIN_TILES")) min_tiles = std::atoll(e);
+  if (T < min_tiles) return;
+  const int S = dominant_tile_stride(hrp, hci);
+  if (S < 2) return;
+  // entry index: the row R = 144 w + r of the windows (a, b, c) laid end to
+  // end, as the byte offset 128 R with the SWIZZLE_128B chunk bits of lane
+  // group 0 (16 (R & 7)); -1 if the column is outside the three windows
+  auto enc = [](int R) { return 128 * R + 16 * (R & 7); };
+  auto widx = [&](std::int64_t t, int c) -> int {
+    const std::int64_t b1 = t * TM - H;
+    if (c >= b1 && c < b1 + WR) return enc(WR + static_cast<int>(c - b1));
+    const std::int64_t b0 = (t - S) * TM - H;
+    if (c >= b0 && c < b0 + WR) return enc(static_cast<int>(c - b0));
+    const std::int64_t b2 = (t + S) * TM - H;
+    if (c >= b2 && c < b2 + WR) return enc(2 * WR + static_cast<int>(c - b2));
+    return -1;
+  };
+  // per tile: union entries per pair, padded to a multiple of 4
+  std::vector<int> K(T, 0), off(T, 0);
+  std::int64_t total16 = 0;
+  for (std::int64_t t = 0; t < T; ++t) {
+    int kt = 0;
+    for (int g = 0; g < NG; ++g) {
+      const std::int64_t i0 = t * TM + 2 * g;
+      int s0 = i0 < n ? hrp[i0] : 0, e0 = i0 < n ? hrp[i0 + 1] : 0;
+      int s1 = i0 + 1 < n ? hrp[i0 + 1] : 0, e1 = i0 + 1 < n ? hrp[i0 + 2] : 0;
+      int u = 0;
+      while (s0 < e0 || s1 < e1) {
+        int c;
+        if (s1 >= e1 || (s0 < e0 && hci[s0] < hci[s1])) c = hci[s0++];
+        else if (s0 >= e0 || hci[s1] < hci[s0]) c = hci[s1++];
+        else { c = hci[s0++]; ++s1; }
+        if (widx(t, c) < 0) return;  // a column outside the three windows
+        ++u;
+      }
+      kt = std::max(kt, u);
+    }
+    kt = (kt + 3) & ~3;
+    if (kt > KMAX) return;
+    K[t] = kt;
+    off[t] = static_cast<int>(total16);
+    total16 += (std::int64_t)kt * NG * 10 / 16;  // kt % 4 == 0: 640-byte multiples
+  }
+  std::vector<uint8_t> buf(std::max<std::int64_t>(total16 * 16, 16), 0);
+  for (std::int64_t t = 0; t < T; ++t) {
+    const int kt = K[t];
+    uint8_t* sl = buf.data() + (std::size_t)off[t] * 16;
+    uint16_t* idx = reinterpret_cast<uint16_t*>(sl);
+    float* w0 = reinterpret_cast<float*>(sl + NG * kt * 2);
+    float* w1 = w0 + NG * kt;
+    for (int g = 0; g < NG; ++g) {
+      const std::int64_t i0 = t * TM + 2 * g;
+      int s0 = i0 < n ? hrp[i0] : 0, e0 = i0 < n ? hrp[i0 + 1] : 0;
+      int s1 = i0 + 1 < n ? hrp[i0 + 1] : 0, e1 = i0 + 1 < n ? hrp[i0 + 2] : 0;
+      int u = 0;
+      auto put = [&](int c, float a0, float a1) {
+        idx[g * kt + u] = static_cast<uint16_t>(widx(t, c));
+        w0[g * kt + u] = a0;
+        w1[g * kt + u] = a1;
+        ++u;
+      };
+      while (s0 < e0 || s1 < e1) {
+        if (s1 >= e1 || (s0 < e0 && hci[s0] < hci[s1])) {
+          put(hci[s0], hv[s0], 0.f);
+          ++s0;
+        } else if (s0 >= e0 || hci[s1] < hci[s0]) {
+          put(hci[s1], 0.f, hv[s1]);
+          ++s1;
+        } else {
+          put(hci[s0], hv[s0], hv[s1]);
+          ++s0;
+          ++s1;
+        }
+      }
+      for (; u < kt; ++u) {  // padding: the pair's first row in its own window, weight 0
+        idx[g * kt + u] = static_cast<uint16_t>(enc(WR + H + 2 * g));
+        w0[g * kt + u] = 0.f;
+        w1[g * kt + u] = 0.f;
+      }
+    }
+  }
+  std::vector<int> ord;
+  ord.reserve(T);
+  for (int s0 = 0; s0 < S; ++s0)
+    for (std::int64_t t = s0; t < T; t += S) ord.push_back(static_cast<int>(t));
+  pw.upload(buf.data(), buf.size());
+  pw_off.upload(off.data(), off.size());
+  pw_k.upload(K.data(), K.size());
+  pw_order.upload(ord.data(), ord.size());
+  pw_S = S;
+  has_pw = true;
+}
+
 gnpk::DevCsr gnpc_csr_s::dev() {
   upload();
   gnpk::DevCsr d;
@@ -514,6 +810,20 @@ gnpk::DevCsr gnpc_csr_s::dev() {
   d.sell_k = has_sell ? sell_k.p : nullptr;
   d.wsell = has_win ? wsell.p : nullptr;
   d.wdesc = has_win ? wdesc.p : nullptr;
+  d.torder = tstride ? torder.p : nullptr;
+  d.pw = has_pw ? pw.p : nullptr;
+  d.pw_off = has_pw ? pw_off.p : nullptr;
+  d.pw_k = has_pw ? pw_k.p : nullptr;
+  d.pw_order = has_pw ? pw_order.p : nullptr;
+  d.pw_S = has_pw ? pw_S : 0;
+  d.psell = has_pairs ? psell.p : nullptr;
+  d.psell_off = has_pairs ? psell_off.p : nullptr;
+  d.psell_k = has_pairs ? psell_k.p : nullptr;
+  static const bool hint_off = [] {
+    const char* e = std::getenv("GNPC_L2HINT");
+    return e && std::string(e) == "0";
+  }();
+  d.l2hint = (l2hint && !hint_off) ? 1 : 0;
   return d;
 }
 
@@ -742,7 +1052,9 @@ void gnpc_model_s::ensure_workspace() {
       if (tm_base[c] != X[c].p) {
         tmX[c] = make_rows_map(X[c].p, (std::int64_t)n, dp, 128,
                                dp == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
-        tmXw[c] = make_rows_map(X[c].p, (std::int64_t)n, dp, gnpk::kWinRows,
+        // windows: 64-row blocks (d = 16 windowed sliced-ELL) or the strip
+        // windows' halo-extended tiles (d = 32)
+        tmXw[c] = make_rows_map(X[c].p, (std::int64_t)n, dp, dp == 32 ? gnpk::kPwRows : gnpk::kWinRows,
                                 dp == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
         tm_base[c] = X[c].p;
       }
@@ -1252,7 +1564,8 @@ int gnpc_csr_device_layout(gnpc_csr a, int* uploaded, int* sliced_ell, int* long
   return guarded([&] {
     need(a, "null csr");
     if (uploaded) *uploaded = a->dev_ready ? 1 : 0;
-    if (sliced_ell) *sliced_ell = a->has_sell ? 1 : 0;
+    if (sliced_ell)
+      *sliced_ell = (a->has_sell ? 1 : 0) | (a->has_pairs ? 2 : 0) | (a->has_pw ? 4 : 0) | (a->has_win ? 8 : 0);
     if (long_rows) *long_rows = a->n_long;
   });
 }

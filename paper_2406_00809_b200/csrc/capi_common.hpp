@@ -179,11 +179,29 @@ struct gnpc_csr_s {
   // padded short-row CSR + per-tile long flags for the TMA CSR layer (see DevCsr)
   gnpc_impl::DevBuf<int> rps, cis, tflag;
   gnpc_impl::DevBuf<float> vs;
+  // pair-union sliced-ELL (see DevCsr::psell)
+  gnpc_impl::DevBuf<int4> psell;
+  gnpc_impl::DevBuf<int> psell_off, psell_k;
+  bool has_pairs = false;
+  // strip-window pair-union layout (see DevCsr::pw)
+  gnpc_impl::DevBuf<uint8_t> pw;
+  gnpc_impl::DevBuf<int> pw_off, pw_k, pw_order;
+  int pw_S = 0;
+  bool has_pw = false;
+  // tile schedule of the TMA layers (see DevCsr::torder); tstride = the
+  // dominant tile stride it was built from (0: round-robin, no order)
+  gnpc_impl::DevBuf<int> torder;
+  int tstride = 0;
+  bool l2hint = true;
   std::unique_ptr<gnpc_csr_s> tr;  // Âᵀ (lazy, for training backward)
   std::unique_ptr<gnpc_impl::KrylovWs> kws;
   void upload();
   void build_sell(const std::vector<int>& hrp, const std::vector<int>& hci,
                   const std::vector<float>& hv);
+  void build_order(const std::vector<int>& hrp, const std::vector<int>& hci);
+  void build_pairs(const std::vector<int>& hrp, const std::vector<int>& hci, const std::vector<float>& hv);
+  void build_pw(const std::vector<int>& hrp, const std::vector<int>& hci, const std::vector<float>& hv);
+  int dominant_tile_stride(const std::vector<int>& hrp, const std::vector<int>& hci) const;
   gnpk::DevCsr dev();
 };
 

@@ -213,22 +213,25 @@ k_long_chunks(DevCsr a, LongPlan lp, const float* __restrict__ X,
   const int k0 = lp.chunk_k0[c], k1 = lp.chunk_k1[c];
   float4 acc = f4zero();
   int k = k0 + grp;
+  // L2: the chunk's (col, val) stream evict_first, the X gathers evict_last
+  const uint64_t ps = a.l2hint ? l2_policy_evict_first() : l2_policy_evict_normal();
+  const uint64_t pk = a.l2hint ? l2_policy_evict_last() : l2_policy_evict_normal();
   for (; k + 3 * NGW < k1; k += 4 * NGW) {
-    const int c0 = __ldg(a.ci + k), c1 = __ldg(a.ci + k + NGW);
-    const int c2 = __ldg(a.ci + k + 2 * NGW), c3 = __ldg(a.ci + k + 3 * NGW);
-    const float v0 = __ldg(a.v + k), v1 = __ldg(a.v + k + NGW);
-    const float v2 = __ldg(a.v + k + 2 * NGW), v3 = __ldg(a.v + k + 3 * NGW);
-    const float4 x0 = ldg4(X + static_cast<size_t>(c0) * DP + 4 * gl);
-    const float4 x1 = ldg4(X + static_cast<size_t>(c1) * DP + 4 * gl);
-    const float4 x2 = ldg4(X + static_cast<size_t>(c2) * DP + 4 * gl);
-    const float4 x3 = ldg4(X + static_cast<size_t>(c3) * DP + 4 * gl);
+    const int c0 = ldg_hint(a.ci + k, ps), c1 = ldg_hint(a.ci + k + NGW, ps);
+    const int c2 = ldg_hint(a.ci + k + 2 * NGW, ps), c3 = ldg_hint(a.ci + k + 3 * NGW, ps);
+    const float v0 = ldg_hint(a.v + k, ps), v1 = ldg_hint(a.v + k + NGW, ps);
+    const float v2 = ldg_hint(a.v + k + 2 * NGW, ps), v3 = ldg_hint(a.v + k + 3 * NGW, ps);
+    const float4 x0 = ldg4_hint(X + static_cast<size_t>(c0) * DP + 4 * gl, pk);
+    const float4 x1 = ldg4_hint(X + static_cast<size_t>(c1) * DP + 4 * gl, pk);
+    const float4 x2 = ldg4_hint(X + static_cast<size_t>(c2) * DP + 4 * gl, pk);
+    const float4 x3 = ldg4_hint(X + static_cast<size_t>(c3) * DP + 4 * gl, pk);
     fma4(acc, v0, x0);
     fma4(acc, v1, x1);
     fma4(acc, v2, x2);
     fma4(acc, v3, x3);
   }
   for (; k < k1; k += NGW)
-    fma4(acc, __ldg(a.v + k), ldg4(X + static_cast<size_t>(__ldg(a.ci + k)) * DP + 4 * gl));
+    fma4(acc, ldg_hint(a.v + k, ps), ldg4_hint(X + static_cast<size_t>(ldg_hint(a.ci + k, ps)) * DP + 4 * gl, pk));
 #pragma unroll
   for (int o = G; o < 32; o <<= 1) {
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);

@@ -44,8 +44,45 @@ struct DevCsr {
   // window (slot i*64 + col%64).  nullptr when not built.
   const int2* __restrict__ wsell;
   const int* __restrict__ wdesc;
+  // Pair-union sliced-ELL (d = 32 apply, stencil-like matrices without long
+  // rows): the two adjacent rows (2g, 2g+1) of a 128-row tile share one entry
+  // list, the sorted union of their columns, with one weight per row (0 where
+  // a row lacks the column).  Entry (k, g) of tile t at psell_off[t] + 64k + g
+  // as {col, w0 bits, w1 bits, 0}; padding {2g, 0, 0, 0}.  psell_k[t] = K_t
+  // (union entries of the tile's longest pair).  Each X row the pair shares is
+  // gathered once (9-point stencil: 12 loads per pair instead of 18).
+  const int4* __restrict__ psell;
+  const int* __restrict__ psell_off;
+  const int* __restrict__ psell_k;
+  // Strip-window pair-union layout (d = 32 apply; stencil-like matrices whose
+  // off-tile columns sit at one dominant tile stride S): tiles run in strips
+  // t = s0 + S k (pw_order, chunked per CTA) and tile u gathers only from the
+  // row windows of tiles u - S, u, u + S, staged in shared memory by TMA (one
+  // new window per tile along a strip).  Per tile, the slice at byte
+  // 16 pw_off[t] holds K = pw_k[t] (a multiple of 4) pair-union entries per
+  // row pair as structure-of-arrays over the 64 pairs: uint16 idx[64][K]
+  // (window w in bits 8-9, row within the window in bits 0-7), float
+  // w0[64][K], float w1[64][K] (10 bytes per entry).
+  const uint8_t* __restrict__ pw;
+  const int* __restrict__ pw_off;
+  const int* __restrict__ pw_k;
+  const int* __restrict__ pw_order;
+  int pw_S;
+  // Tile schedule of the TMA layer pipeline (apply path): nullptr = CTA b
+  // takes tiles b, b + grid, ...; else CTA b takes positions
+  // [b T / grid, (b+1) T / grid) of this permutation of the T tiles, ordered
+  // so consecutive tiles of a CTA reuse each other's X-row windows in L1
+  // (built from the matrix's dominant tile stride, gnpc_csr_s::build_order).
+  const int* __restrict__ torder;
+  // L2 policy: 1 = the streamed matrix (slices, CSR ranges) is loaded
+  // evict_first and the X-row gathers evict_last, so the layer input stays
+  // L2-resident while Â streams past it; 0 = evict_normal everywhere.
+  int l2hint;
 };
 constexpr int kWinBlocks = 8, kWinRows = 64, kWinDesc = 2 + kWinBlocks;
+// Row windows of the strip-ordered window mode (d = 32): a window of tile u is
+// rows [128u - kPwHalo, 128u + 128 + kPwHalo), one TMA box of kPwRows rows.
+constexpr int kPwHalo = 8, kPwRows = 128 + 2 * kPwHalo;
 
 // Per-apply scalars produced by the norm kernel (scale sandwich,
 // src/gnn.cpp:128-139,191-199).
@@ -104,6 +141,39 @@ struct KrylovDev {
 
 __device__ __forceinline__ float4 ldg4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
+}
+// L2 cache policies (createpolicy) and a 128-bit read-only load under one.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int ldg_hint(const int* p, uint64_t pol) {
+  int v;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ldg_hint(const float* p, uint64_t pol) {
+  float v;
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float4 ldg4_hint(const float* p, uint64_t pol) {
+  float4 v;
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
 }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 __device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }

@@ -79,6 +79,12 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t 
                "r"(bytes)
                : "memory");
 }
+// 128-bit shared-memory load by 32-bit shared address
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -112,7 +118,16 @@ struct SellCfg {
 #ifndef GNPC_KCAP32
 #define GNPC_KCAP32 9  // staged slice words per row at d = 32 (a 9-point row; 12 left less L1: C5 283 vs 287 applies/s)
 #endif
-  static constexpr int US = DP == 16 ? 8 : GNPC_US32;    // slice entries per gather round
+#ifndef GNPC_USP
+#define GNPC_USP 6  // pair-union entries per gather round
+#endif
+#ifndef GNPC_KCAPP
+#define GNPC_KCAPP 12  // staged pair-union entries per pair (a 9-point pair's union)
+#endif
+#ifndef GNPC_KCAPPW
+#define GNPC_KCAPPW 12  // strip-window entries per pair (multiple of 4; every tile is staged; 16 overflows the last layer's smem)
+#endif
+  static constexpr int US = DP == 16 ? 8 : ((CSR == 5 || CSR == 6) ? GNPC_USP : GNPC_US32);  // entries per gather round
 #ifndef GNPC_USC_TR
 #define GNPC_USC_TR 5
 #endif
@@ -143,24 +158,50 @@ struct SellCfg {
 #ifndef GNPC_NS_SELL16
 #define GNPC_NS_SELL16 4
 #endif
+  // CSR = 5 / 6: pair-union sliced-ELL (d = 32): the 4-deep ring for the
+  // non-last layers (5), 3 deep for the last (6)
+  static constexpr bool PAIR = CSR == 5 || CSR == 6;
+  static_assert(!PAIR || DP == 32, "pair-union slices are a d = 32 layout (two rows per 8-lane group)");
+  // CSR = 7 / 8: strip-window pair-union (d = 32, DevCsr::pw): the ring holds
+  // only the slices; X rows come from NWIN row windows (one new per tile in a
+  // strip); 7 = non-last layers (4-deep ring), 8 = last layer (3 deep)
+  static constexpr bool PW = CSR == 7 || CSR == 8;
+  static_assert(!PW || DP == 32, "strip windows are a d = 32 layout");
+#ifndef GNPC_NS_PW
+#define GNPC_NS_PW 4
+#endif
   static constexpr int NS = DP == 16 ? (CSRL ? GNPC_NS_CSR16 : (WIN ? 4 : GNPC_NS_SELL16))
-                                     : (CSR == 2 ? GNPC_NS_TR32 : (DEEP ? GNPC_NS_DEEP32 : 3));
+                                     : (CSR == 2 ? GNPC_NS_TR32
+                                                 : ((DEEP || CSR == 5) ? GNPC_NS_DEEP32
+                                                                       : (CSR == 7 ? GNPC_NS_PW : 3)));
+  // windows alive: the MMA's window of the current tile plus NS - 1 tiles
+  // of lookahead (steady state: one new window per tile), and a strip break
+  // needs the MMA's window plus three fresh ones
+  static constexpr int NWIN = PW ? (NS + 1 > 4 ? NS + 1 : 4) : 0;
+  static constexpr uint32_t WINB = kPwRows * DP * 4;
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
   // up to round(K, US) words).  Kept small: every KB of shared memory is L1
   // the X-row gathers hit (C5 fused layer 531 -> 499 us going 24 -> 12)
 #ifndef GNPC_KCAP16
 #define GNPC_KCAP16 16
 #endif
-  static constexpr int KCAP = WIN ? 8 : (DP == 16 ? GNPC_KCAP16 : GNPC_KCAP32);
+  // (pair-union: entries per pair; a union entry is 16 B for 2 rows, so the
+  // staged bytes K * TM * 8 match the sliced-ELL formula)
+  static constexpr int KCAP = WIN ? 8
+                                 : (DP == 16 ? GNPC_KCAP16
+                                             : ((CSR == 5 || CSR == 6) ? GNPC_KCAPP
+                                                                       : ((CSR == 7 || CSR == 8) ? GNPC_KCAPPW
+                                                                                                 : GNPC_KCAP32)));
   // the staged gather reads round(K, US) words of a slice: KCAP must be a
   // multiple of US or the last round would read past the staged slice
-  static_assert(WIN || KCAP % US == 0, "GNPC_KCAP16/GNPC_KCAP32 must be a multiple of the gather round");
+  static_assert(WIN || PW || KCAP % US == 0, "GNPC_KCAP16/GNPC_KCAP32 must be a multiple of the gather round");
+  static_assert(!PW || KCAP % 4 == 0, "strip-window slices hold a multiple of 4 entries per pair");
   static constexpr uint32_t OPB = TM * DP * 4;   // one A-type operand / X tile / Y tile (bytes)
   static constexpr uint32_t BB = DP * DP * 4;    // one B operand (bytes)
   static constexpr int TCOLS = 2 * DP;           // TMEM accumulator columns (two halves)
   // + the X·U part's A_lo operand (DP columns, A in TMEM) at alo_col
   static constexpr int TALLOC = 4 * DP;          // power of two >= 3 DP
-  static constexpr uint32_t CVB = KCAP * TM * 8; // staged slice (bytes)
+  static constexpr uint32_t CVB = PW ? KCAP * (TM / 2) * 10 : KCAP * TM * 8;  // staged slice (bytes)
   // CSR: [X tile | row_ptr slice (TM+4 ints, 1 KiB) | col_idx (CAPC) | values (CAPC)]
   static constexpr bool TR = CSR == 2;
 #ifndef GNPC_CAPC16
@@ -182,12 +223,13 @@ struct SellCfg {
   // MMA's X tile) are two consecutive blocks of the window
   static constexpr uint32_t BLKB = kWinRows * DP * 4;
   static constexpr uint32_t WB = WIN ? kWinBlocks * BLKB : 0;
-  static constexpr uint32_t O_SL = WIN ? WB : OPB;  // staged slice (sliced-ELL modes)
+  static constexpr uint32_t O_SL = WIN ? WB : (PW ? 0 : OPB);  // staged slice (sliced-ELL modes)
   static constexpr uint32_t SLOT =
       CSRL ? ((O_V + CAPC * 4 + 1023) & ~1023u) : (((O_SL + CVB) + 1023) & ~1023u);
   // layout (offsets from the 1024-aligned base)
   static constexpr uint32_t O_RING = 0;
-  static constexpr uint32_t O_A = O_RING + NS * SLOT;     // A2_hi (ÂX), A2_lo
+  static constexpr uint32_t O_WIN = O_RING + NS * SLOT;   // strip windows [NWIN] (PW)
+  static constexpr uint32_t O_A = O_WIN + NWIN * WINB;    // A2_hi (ÂX), A2_lo
   static constexpr uint32_t O_B = O_A + 2 * OPB;          // Bu_lo, Bu_hi, Bw_lo, Bw_hi
   static constexpr uint32_t O_Y = O_B + 4 * BB;           // Y staging [2]
   // last layer only: Y_lo staging [2], the dec1 B operand [D1_lo; D1_hi]
@@ -203,10 +245,13 @@ struct SellCfg {
   static constexpr uint32_t o_bar(int hidden, bool last) {
     return (o_p(hidden, last) + (last ? (DP + 2) * hidden * 4 : 0) + 15) & ~15u;
   }
+  // PW: per-CTA schedule table (tile, K, slice offset) after the barriers
+  static constexpr int KSCHED = PW ? 256 : 0;
   static size_t smem_bytes(int hidden, bool last) {
-    return o_bar(hidden, last) + 128 + 1024;  // barriers + TMEM slot, 1024-B alignment slack
+    // barriers + TMEM slot, the schedule, 1024-B alignment slack
+    return o_bar(hidden, last) + 128 + 3 * KSCHED * 4 + 1024;
   }
-  static_assert(TR || DEEP || (DP == 32 ? O_D1OP + 2 * 32 * DP * 4 : O_Y + 2 * OPB) + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
+  static_assert(TR || DEEP || CSR == 5 || CSR == 7 || (DP == 32 ? O_D1OP + 2 * 32 * DP * 4 : O_Y + 2 * OPB) + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
                 "last-layer layout must fit shared memory at hidden 32 (larger: host falls back)");
   static_assert(!TR || O_Y + 2 * OPB + 128 + 1024 <= 227 * 1024, "training layout must fit shared memory");
   // TMEM: layer accumulator [0, 2DP); last layer's projection accumulator at
@@ -237,7 +282,7 @@ struct SellMaps {
 // given weight 0 and the round's first column, so no load is predicated.
 template <int DP, int R, int US, int TM, bool SMEM>
 __device__ __forceinline__ void gather_sell_rows(const float* __restrict__ X, int gl, const int2* cv,
-                                                 int K, int gid, float4 (&acc)[R]) {
+                                                 int K, int gid, float4 (&acc)[R], uint64_t pol) {
   const char* xb = reinterpret_cast<const char*>(X + 4 * gl);
   for (int k = 0; k < K; k += US) {
     int c[R][US];
@@ -280,12 +325,88 @@ __device__ __forceinline__ void gather_sell_rows(const float* __restrict__ X, in
     for (int u = 0; u < US; ++u)
 #pragma unroll
       for (int j = 0; j < R; ++j)
-        x[j][u] = ldg4(reinterpret_cast<const float*>(
-            xb + static_cast<unsigned long long>(static_cast<unsigned>(c[j][u])) * (DP * 4ull)));
+        x[j][u] = ldg4_hint(reinterpret_cast<const float*>(
+            xb + static_cast<unsigned long long>(static_cast<unsigned>(c[j][u])) * (DP * 4ull)), pol);
 #pragma unroll
     for (int u = 0; u < US; ++u)
 #pragma unroll
       for (int j = 0; j < R; ++j) fma4(acc[j], w[j][u], x[j][u]);
+  }
+}
+
+// Pair-union gather (CSR = 5/6): the group's two adjacent rows share one
+// entry list; each entry's X row is loaded once and feeds both rows' sums
+// (weight 0 where a row lacks the column, which adds exactly 0 and keeps each
+// row's own terms in stored order).  Slots past K: weight 0, the round's
+// first column.
+template <int DP, int US, int NG, bool SMEM>
+__device__ __forceinline__ void gather_pair_rows(const float* __restrict__ X, int gl, const int4* cv, int K,
+                                                 int gid, float4 (&acc)[2], uint64_t pol) {
+  const char* xb = reinterpret_cast<const char*>(X + 4 * gl);
+  for (int k = 0; k < K; k += US) {
+    int c[US];
+    float w0[US], w1[US];
+#pragma unroll
+    for (int u = 0; u < US; ++u) {
+      const bool on = k + u < K;
+      const int4* src = cv + (k + u) * NG + gid;
+      int4 e;
+      if constexpr (SMEM) {
+        e = *src;
+      } else {
+        e = on ? __ldg(src) : make_int4(0, 0, 0, 0);
+      }
+      c[u] = (u == 0 || on) ? e.x : c[0];
+      w0[u] = on ? __int_as_float(e.y) : 0.f;
+      w1[u] = on ? __int_as_float(e.z) : 0.f;
+    }
+    float4 x[US];
+#pragma unroll
+    for (int u = 0; u < US; ++u)
+      x[u] = ldg4_hint(reinterpret_cast<const float*>(
+                           xb + static_cast<unsigned long long>(static_cast<unsigned>(c[u])) * (DP * 4ull)),
+                       pol);
+#pragma unroll
+    for (int u = 0; u < US; ++u) {
+      fma4(acc[0], w0[u], x[u]);
+      fma4(acc[1], w1[u], x[u]);
+    }
+  }
+}
+
+// Strip-window gather (CSR = 7/8): the tile's slice holds, per row pair,
+// K entries {idx, w0, w1} as structure-of-arrays.  idx is the byte offset of
+// the X row in the tile's three consecutive windows (a, b, c) laid end to end
+// — R = 144 w + row, idx = 128 R + 16 (R & 7), i.e. with the SWIZZLE_128B
+// chunk bits of lane group 0 — so lane gl reads (wbase + idx) ^ (gl << 4),
+// wrapped once around the NWIN-window ring.  Padding entries carry weight 0.
+template <int NG>
+__device__ __forceinline__ void gather_pw_rows(const uint8_t* sl, int K, int gid, int gl, uint32_t wbase,
+                                               uint32_t wlim, uint32_t wring, float4 (&acc)[2]) {
+  const uint16_t* idx = reinterpret_cast<const uint16_t*>(sl) + gid * K;
+  const float* w0 = reinterpret_cast<const float*>(sl + NG * K * 2) + gid * K;
+  const float* w1 = w0 + NG * K;
+  const uint32_t gx = static_cast<uint32_t>(gl) << 4;
+  for (int k = 0; k < K; k += 4) {
+    const uint2 rr = *reinterpret_cast<const uint2*>(idx + k);
+    const float4 a0 = *reinterpret_cast<const float4*>(w0 + k);
+    const float4 a1 = *reinterpret_cast<const float4*>(w1 + k);
+    const uint32_t e[4] = {rr.x & 0xffffu, rr.x >> 16, rr.y & 0xffffu, rr.y >> 16};
+    float4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t v = wbase + e[u];
+      v = v >= wlim ? v - wring : v;
+      x[u] = tc::lds4(v ^ gx);
+    }
+    fma4(acc[0], a0.x, x[0]);
+    fma4(acc[1], a1.x, x[0]);
+    fma4(acc[0], a0.y, x[1]);
+    fma4(acc[1], a1.y, x[1]);
+    fma4(acc[0], a0.z, x[2]);
+    fma4(acc[1], a1.z, x[2]);
+    fma4(acc[0], a0.w, x[3]);
+    fma4(acc[1], a1.w, x[3]);
   }
 }
 
@@ -329,7 +450,8 @@ __device__ __forceinline__ void gather_win_rows(const uint8_t* win, int gl, cons
 template <int DP, int R, int US>
 __device__ __forceinline__ void gather_csr_rows(const char* const (&xbj)[R], unsigned long long stride,
                                                 const int* ci, const float* vv, const int (&s)[R],
-                                                const int (&len)[R], const int (&self)[R], float4 (&acc)[R]) {
+                                                const int (&len)[R], const int (&self)[R], float4 (&acc)[R],
+                                                uint64_t pol) {
   int kmax = len[0];
 #pragma unroll
   for (int j = 1; j < R; ++j) kmax = max(kmax, len[j]);
@@ -350,8 +472,8 @@ __device__ __forceinline__ void gather_csr_rows(const char* const (&xbj)[R], uns
     for (int u = 0; u < US; ++u)
 #pragma unroll
       for (int j = 0; j < R; ++j)
-        x[j][u] = ldg4(reinterpret_cast<const float*>(
-            xbj[j] + static_cast<unsigned long long>(static_cast<unsigned>(c[j][u])) * stride));
+        x[j][u] = ldg4_hint(reinterpret_cast<const float*>(
+            xbj[j] + static_cast<unsigned long long>(static_cast<unsigned>(c[j][u])) * stride), pol);
 #pragma unroll
     for (int u = 0; u < US; ++u)
 #pragma unroll
@@ -432,6 +554,8 @@ template <int DP, int CSR>
 struct SellPipe {
   using C = SellCfg<DP, CSR>;
   uint8_t* ring;
+  uint8_t* win;  // strip windows (PW)
+  int* sched;    // PW: the CTA's tile schedule [3][KSCHED]
   uint8_t* A;  // [A2_hi | A2_lo]
   uint8_t* Bs;
   uint8_t* Ystg;
@@ -446,6 +570,42 @@ struct SellPipe {
   int ring_it = 0, mma_it = 0, af_it = 0;  // phase counters (identical in every thread)
 };
 
+// Window sequence of the strip-window mode, replayed identically by the
+// control warp (which loads the windows) and the math warps (which read them):
+// tile position j gets windows (a, b, c) = those of tiles u - S, u, u + S;
+// window seq q lives in slot q % NWIN.  Along a strip (u = previous + S) only
+// c is new; at a break (chunk start, strip end) three fresh windows follow
+// the previous tile's b: (b+1, b+2, b+3), so only the previous tile's MMA
+// window b stays protected.
+struct WinSeq {
+  int last = -1, pb = -1, pc = -1, ctr = 0;
+  // returns the number of new windows (3 at a break, else 1)
+  __device__ __forceinline__ int next(int tile, int S, int& sa, int& sb, int& sc) {
+    const bool brk = last < 0 || tile != last + S;
+    int nnew;
+    if (brk) {
+      sa = pb + 1;
+      sb = pb + 2;
+      sc = pb + 3;
+      nnew = 3;
+    } else {
+      sa = pb;
+      sb = pc;
+      sc = ctr;
+      nnew = 1;
+    }
+    ctr = sc + 1;
+    pb = sb;
+    pc = sc;
+    last = tile;
+    return nnew;
+  }
+  // c of the next tile without advancing
+  __device__ __forceinline__ int peek_c(int tile, int S) const {
+    return (last < 0 || tile != last + S) ? pb + 3 : ctr;
+  }
+};
+
 // smem carve-up, barrier init, TMEM allocation (all threads of the CTA)
 template <int DP, int CSR>
 __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
@@ -455,6 +615,7 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
   uint8_t* base = reinterpret_cast<uint8_t*>(smem_raw) + pad;
   SellPipe<DP, CSR> p;
   p.ring = base + C::O_RING;
+  p.win = base + C::O_WIN;
   p.A = base + C::O_A;
   p.Bs = base + C::O_B;
   p.Ystg = base + C::O_Y;
@@ -466,6 +627,7 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
   p.mma_bar = p.full + C::NS;
   p.afull = p.mma_bar + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p.afull + 1);
+  p.sched = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(p.full) + 128);
   const int tid = threadIdx.x;
   for (int t = tid; t < int(C::NS * C::SLOT / 16); t += C::NT)  // stale slice words must be valid columns
     reinterpret_cast<float4*>(p.ring)[t] = f4zero();
@@ -544,7 +706,38 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   }
   tc::fence_proxy_async();
   __syncthreads();
-  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // tile schedule: round-robin, or a contiguous chunk of the matrix's tile
+  // order (a.torder, apply path) so consecutive tiles share X-row windows
+  const int* torder = TR ? nullptr : (C::PW ? a.pw_order : a.torder);
+  const int chunk0 = torder ? static_cast<int>(static_cast<long long>(blockIdx.x) * ntiles / gridDim.x) : 0;
+  const int my_tiles =
+      torder ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * ntiles / gridDim.x) - chunk0
+             : (blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
+  // PW: this CTA's chunk of the strip order with each tile's K and slice
+  // offset, staged in shared memory once (the control thread would otherwise
+  // chase order -> K -> offset through L2 for every tile it issues)
+  int* sch_t = p.sched;
+  int* sch_k = p.sched + C::KSCHED;
+  int* sch_o = p.sched + 2 * C::KSCHED;
+  const bool use_sched = C::PW && my_tiles <= C::KSCHED;
+  if (use_sched) {
+    for (int j = tid; j < my_tiles; j += C::NT) {
+      const int t = __ldg(torder + chunk0 + j);
+      sch_t[j] = t;
+      sch_k[j] = __ldg(a.pw_k + t);
+      sch_o[j] = __ldg(a.pw_off + t);
+    }
+    __syncthreads();
+  }
+  auto tile_at = [&](int it) -> int {
+    if (use_sched) return sch_t[it];
+    return torder ? __ldg(torder + chunk0 + it) : static_cast<int>(blockIdx.x + it * gridDim.x);
+  };
+  // L2 policies: Â streams evict_first, X gathers evict_last (a.l2hint)
+  // (training activations are far larger than L2: normal policy there)
+  const bool hint = a.l2hint && !TR;
+  const uint64_t pol_stream = hint ? l2_policy_evict_first() : l2_policy_evict_normal();
+  const uint64_t pol_keep = hint ? l2_policy_evict_last() : l2_policy_evict_normal();
   const int rb = p.ring_it, mb = p.mma_it, ab = p.af_it;
   // commits: one per tile, plus the last projection MMA's (TCP)
   const int ncommit = my_tiles + (TCP && my_tiles > 0 ? 1 : 0);
@@ -560,7 +753,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       if (!LAST) tc::tma_prefetch_desc(mapy);
       auto issue = [&](int it) {  // tile `it` of this CTA into ring slot (rb + it) % NS
         if (it >= my_tiles) return;
-        const int t = blockIdx.x + it * gridDim.x;
+        const int t = tile_at(it);
         const int r = rb + it;
         const int s = r % NS;
         uint8_t* slot = p.ring + s * C::SLOT;
@@ -591,11 +784,11 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           const int a0 = kb & ~3, cnt = ((ke + 3) & ~3) - a0;
           const bool staged = cnt <= C::CAPC;
           tc::mbar_expect_tx(&p.full[s], C::OPB + C::RPB + (staged ? 8 * cnt : 0));
-          tc::tma_load_2d(slot, mapx, 0, t * TM, &p.full[s]);
-          tc::bulk_load(slot + C::O_RP, a.rps + t * TM, C::RPB, &p.full[s]);
+          tc::tma_load_2d_hint(slot, mapx, 0, t * TM, &p.full[s], pol_keep);
+          tc::bulk_load_hint(slot + C::O_RP, a.rps + t * TM, C::RPB, &p.full[s], pol_stream);
           if (staged && cnt > 0) {
-            tc::bulk_load(slot + C::O_CI, a.cis + a0, 4 * cnt, &p.full[s]);
-            tc::bulk_load(slot + C::O_V, a.vs + a0, 4 * cnt, &p.full[s]);
+            tc::bulk_load_hint(slot + C::O_CI, a.cis + a0, 4 * cnt, &p.full[s], pol_stream);
+            tc::bulk_load_hint(slot + C::O_V, a.vs + a0, 4 * cnt, &p.full[s], pol_stream);
           }
         } else if constexpr (C::WIN) {
           const int* wd = a.wdesc + static_cast<size_t>(t) * kWinDesc;
@@ -607,14 +800,50 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
             tc::tma_load_2d(slot + i * C::BLKB, mapxw, 0, __ldg(wd + 2 + i) * kWinRows, &p.full[s]);
           if (staged) tc::bulk_load(slot + C::O_SL, a.wsell + __ldg(a.sell_off + t), K * TM * 8, &p.full[s]);
         } else {
-          const int K = __ldg(a.sell_k + t) & 0xffff;
+          const int K = __ldg((C::PAIR ? a.psell_k : a.sell_k) + t) & 0xffff;
           const bool staged = K > 0 && K <= C::KCAP;
           tc::mbar_expect_tx(&p.full[s], C::OPB + (staged ? K * TM * 8 : 0));
-          tc::tma_load_2d(slot, mapx, 0, t * TM, &p.full[s]);
-          if (staged) tc::bulk_load(slot + C::OPB, a.sell + __ldg(a.sell_off + t), K * TM * 8, &p.full[s]);
+          tc::tma_load_2d_hint(slot, mapx, 0, t * TM, &p.full[s], pol_keep);
+          if (staged) {
+            const void* src = C::PAIR ? static_cast<const void*>(a.psell + __ldg(a.psell_off + t))
+                                      : static_cast<const void*>(a.sell + __ldg(a.sell_off + t));
+            tc::bulk_load_hint(slot + C::OPB, src, K * TM * 8, &p.full[s], pol_stream);
+          }
         }
       };
-      for (int it = 0; it < NS - 1; ++it) issue(it);
+      // strip windows (PW): tiles are issued in order while the slice ring
+      // has room (j <= it + NS - 1) and the new windows' slots are free: every
+      // window older than the current tile's MMA window b(it) is dead
+      WinSeq ws;   // issue side
+      WinSeq wsb;  // MMA side: b(it) of the current tile
+      int nxt = 0, bcur = 0;
+      auto issue_pw = [&](int j) {
+        const int t = tile_at(j);
+        int sa, sb, sc;
+        const int nnew = ws.next(t, a.pw_S, sa, sb, sc);
+        const int s = (rb + j) % NS;
+        uint8_t* slot = p.ring + s * C::SLOT;
+        const int K = use_sched ? sch_k[j] : __ldg(a.pw_k + t);
+        const int off = use_sched ? sch_o[j] : __ldg(a.pw_off + t);
+        tc::mbar_expect_tx(&p.full[s], K * (TM / 2) * 10 + nnew * C::WINB);
+        tc::bulk_load_hint(slot, a.pw + static_cast<size_t>(off) * 16, K * (TM / 2) * 10, &p.full[s], pol_stream);
+        auto load_win = [&](int q, int u) {
+          tc::tma_load_2d_hint(p.win + (q % C::NWIN) * C::WINB, mapxw, 0, u * TM - kPwHalo, &p.full[s], pol_keep);
+        };
+        if (nnew == 3) {
+          load_win(sa, t - a.pw_S);
+          load_win(sb, t);
+        }
+        load_win(sc, t + a.pw_S);
+      };
+      auto issue_more = [&](int it) {  // after afull(it) (it = -1: prologue)
+        const int prot = it >= 0 ? bcur : 0;
+        while (nxt < my_tiles && nxt <= it + NS - 1 && ws.peek_c(tile_at(nxt), a.pw_S) - prot < C::NWIN)
+          issue_pw(nxt++);
+      };
+      if constexpr (C::PW) issue_more(-1);
+      else
+        for (int it = 0; it < NS - 1; ++it) issue(it);
       constexpr uint32_t idesc = tc::idesc_tf32(128, DP);
       constexpr uint32_t idesc2 = tc::idesc_tf32(128, 2 * DP);
       const uint32_t sBstk = tc::smem_u32(p.Bs);
@@ -627,13 +856,18 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         // the buffer the epilogue after this MMA writes is free
         tc::bulk_wait_read0();
         if (KIND == 1 && it < my_tiles) {  // training forward: the tile's ÂX (A2_hi) to HBM
-          tc::tma_store_2d(tio->mapax, p.A, 0, (blockIdx.x + it * gridDim.x) * TM);
+          tc::tma_store_2d(tio->mapax, p.A, 0, tile_at(it) * TM);
           tc::bulk_commit();
         }
         if (it < my_tiles) {
           uint32_t sX = tc::smem_u32(p.ring + ((rb + it) % NS) * C::SLOT);
+          if constexpr (C::PW) {  // the tile's own rows: window b(it) past its halo
+            int sa, sc;
+            wsb.next(tile_at(it), a.pw_S, sa, bcur, sc);
+            sX = tc::smem_u32(p.win + (bcur % C::NWIN) * C::WINB + kPwHalo * DP * 4);
+          }
           if constexpr (C::WIN)  // the tile's own rows inside the window
-            sX += __ldg(a.wdesc + static_cast<size_t>(blockIdx.x + it * gridDim.x) * kWinDesc + 1) * C::BLKB;
+            sX += __ldg(a.wdesc + static_cast<size_t>(tile_at(it)) * kWinDesc + 1) * C::BLKB;
           // 3xTF32 with the two A_hi products stacked along N (A_hi is read
           // once for both): D[:, 0:DP] = A_hi·B_lo, D[:, DP:2DP] = A_hi·B_hi +
           // A_lo·B_hi; the epilogue adds the halves.  Each part's B operands
@@ -679,11 +913,10 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         if (KIND == 1 && it < my_tiles) tc::bulk_wait_read0();  // A2_hi is rewritten after the commit
         if (it < my_tiles || (TCP && it >= 1)) tc::mma_commit(p.mma_bar);
         if (!LAST && it >= 1) {  // tile it-1 is fully staged
-          tc::tma_store_2d(mapy, p.Ystg + ((mb + it - 1) & 1) * C::OPB, 0,
-                           (blockIdx.x + (it - 1) * gridDim.x) * TM);
+          tc::tma_store_2d(mapy, p.Ystg + ((mb + it - 1) & 1) * C::OPB, 0, tile_at(it - 1) * TM);
           if constexpr (KIND == 1 && C::MBITS) {
             if (tio->mask_out) {
-              const int t1 = blockIdx.x + (it - 1) * gridDim.x;
+              const int t1 = tile_at(it - 1);
               tc::bulk_store(tio->mask_out + static_cast<size_t>(t1) * TM * 4,
                              p.Ystg + C::O_MST - C::O_Y + ((mb + it - 1) & 1) * TM * 4, TM * 4);
             }
@@ -691,7 +924,11 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           tc::bulk_commit();
         }
         // every warp passed its wait for MMA(it-1): that slot takes tile it+NS-1
-        issue(it + NS - 1);
+        if constexpr (C::PW) {
+          if (it < my_tiles) issue_more(it);
+        } else {
+          issue(it + NS - 1);
+        }
       }
       // the layer's output is in global memory before the caller's barrier
       tc::bulk_wait0();
@@ -813,7 +1050,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       for (int c = 0; c < 16; ++c) o = fmaf(relu(z1[c] + z2[c] + B1[h0 + c]), D2[h0 + c], o);
     }
     tc::fence_before();
-    const int i = (blockIdx.x + itp * gridDim.x) * TM + 32 * q + lane;
+    const int i = tile_at(itp) * TM + 32 * q + lane;
     if (i < n) out[i] = static_cast<OutT>(static_cast<double>(o + net.dec2_b) * out_scale);
   };
   auto arrive = [&]() {
@@ -850,21 +1087,35 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
     }
   };
 
-  const int* tinfo = C::CSRL ? a.tflag : a.sell_k;  // per tile: K_t | has-long << 16 (SELL), has-long (CSR)
-  int kw = TR ? 0 : __ldg(tinfo + blockIdx.x);
+  // per tile: K_t | has-long << 16 (SELL, pair-union), has-long (CSR)
+  const int* tinfo = C::CSRL ? a.tflag : (C::PAIR ? a.psell_k : (C::PW ? a.pw_k : a.sell_k));
+  int kw = TR ? 0 : (use_sched ? sch_k[0] : __ldg(tinfo + tile_at(0)));
   const int iters = my_tiles + 1 + (TCP ? 1 : 0);
+  WinSeq wsm;                       // strip windows (PW): the control warp's sequence, replayed
+  const uint8_t* wtile = nullptr;   // PW: the tile's own rows (window b past its halo)
   for (int it = 0; it < iters; ++it) {
     const bool have = it < my_tiles;
-    const int tile = blockIdx.x + it * gridDim.x;
+    const int tile = have ? tile_at(it) : 0;
     const int row0 = tile * TM;
     const int r = rb + it;
     uint8_t* slot = p.ring + (r % NS) * C::SLOT;
     float4 acc[R];
+    uint32_t wbase = 0;  // PW: shared address of window a; b, c follow (wrapped in the ring)
+    const uint32_t wring0 = tc::smem_u32(p.win);
+    if constexpr (C::PW) {
+      if (have) {
+        int sq[3];
+        wsm.next(tile, a.pw_S, sq[0], sq[1], sq[2]);
+        wbase = wring0 + (sq[0] % C::NWIN) * C::WINB;
+        wtile = p.win + (sq[1] % C::NWIN) * C::WINB + kPwHalo * DP * 4;
+      }
+    }
     if (have) {
       const int K = C::CSRL ? 0 : (kw & 0xffff);
       const bool haslong = !TR && (C::CSRL ? kw != 0 : (kw >> 16) != 0);
       const bool staged = K > 0 && K <= C::KCAP;
-      if (!TR) kw = it + 1 < my_tiles ? __ldg(tinfo + tile + gridDim.x) : 0;  // prefetch
+      if (!TR)  // prefetch
+        kw = it + 1 < my_tiles ? (use_sched ? sch_k[it + 1] : __ldg(tinfo + tile_at(it + 1))) : 0;
 
       // ----------------------------------------------------------- gather
 #pragma unroll
@@ -902,7 +1153,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         if (bs % R == 0)  // the group's rows: consecutive samples of one node
           gather_csr_node<DP, R, C::USC>(xbj[0], stride, cis, vs, sj[0], lj[0], self[0], acc);
         else
-          gather_csr_rows<DP, R, C::USC>(xbj, stride, cis, vs, sj, lj, self, acc);
+          gather_csr_rows<DP, R, C::USC>(xbj, stride, cis, vs, sj, lj, self, acc, pol_keep);
       } else if constexpr (CSR == 1) {
         const int* rpt = reinterpret_cast<const int*>(slot + C::O_RP);
         const int kb = rpt[0], ke = rpt[min(TM, n - row0)];
@@ -921,9 +1172,10 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         }
         if (st)
           gather_csr_rows<DP, R, C::USC>(xbj, DP * 4ull, reinterpret_cast<const int*>(slot + C::O_CI),
-                                         reinterpret_cast<const float*>(slot + C::O_V), sj, lj, self, acc);
+                                         reinterpret_cast<const float*>(slot + C::O_V), sj, lj, self, acc,
+                                         pol_keep);
         else
-          gather_csr_rows<DP, R, C::USC>(xbj, DP * 4ull, a.cis, a.vs, sj, lj, self, acc);
+          gather_csr_rows<DP, R, C::USC>(xbj, DP * 4ull, a.cis, a.vs, sj, lj, self, acc, pol_keep);
       } else {
         if constexpr (C::WIN) {
           // window rows in shared memory (swizzled like the TMA wrote them)
@@ -932,11 +1184,22 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
                                                     gid, acc);
           else
             gather_win_rows<DP, R, C::US, TM, false>(slot, gl, a.wsell + __ldg(a.sell_off + tile), K, gid, acc);
+        } else if constexpr (C::PW) {
+          if constexpr (R == 2)
+            gather_pw_rows<C::NG>(slot, K, gid, gl, wbase, wring0 + C::NWIN * C::WINB, C::NWIN * C::WINB, acc);
+        } else if constexpr (C::PAIR) {
+          if (staged)
+            gather_pair_rows<DP, C::US, C::NG, true>(X, gl, reinterpret_cast<const int4*>(slot + C::OPB), K, gid,
+                                                     acc, pol_keep);
+          else
+            gather_pair_rows<DP, C::US, C::NG, false>(X, gl, a.psell + __ldg(a.psell_off + tile), K, gid, acc,
+                                                      pol_keep);
         } else if (staged)
           gather_sell_rows<DP, R, C::US, TM, true>(X, gl, reinterpret_cast<const int2*>(slot + C::OPB), K,
-                                                   gid, acc);
+                                                   gid, acc, pol_keep);
         else
-          gather_sell_rows<DP, R, C::US, TM, false>(X, gl, a.sell + __ldg(a.sell_off + tile), K, gid, acc);
+          gather_sell_rows<DP, R, C::US, TM, false>(X, gl, a.sell + __ldg(a.sell_off + tile), K, gid, acc,
+                                                    pol_keep);
       }
     }
 
@@ -966,6 +1229,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         const int q = warp & 3, cq = warp >> 2, m = 32 * q + lane;
         const uint8_t* xtile = slot;
         if constexpr (C::WIN) xtile += __ldg(a.wdesc + static_cast<size_t>(tile) * kWinDesc + 1) * C::BLKB;
+        if constexpr (C::PW) xtile = wtile;
         float lo[CW];
 #pragma unroll
         for (int c = 0; c < CW; c += 4) {
@@ -983,7 +1247,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       }
     }
     if (it <= my_tiles) arrive();
-    if (proj) project((blockIdx.x + (it - 1) * gridDim.x) * TM);
+    if (proj) project(tile_at(it - 1) * TM);
   }
 }
 

@@ -1,0 +1,93 @@
+"""GPU parity of the d = 32 stencil layouts of Â (DevCsr::psell, DevCsr::pw):
+the pair-union sliced-ELL and the strip-window pair-union form (X row windows
+staged in shared memory by TMA, tiles in strips of the dominant tile stride).
+Both sum every row's own entries in stored order (the union adds exact zeros),
+so their outputs must equal the plain sliced-ELL path bit for bit, and the
+oracle within the north-star 1e-4.
+
+Grids: 9-point anisotropic (the C5 generator) at widths 250 / 256 / 262 — the
+grid-line offset is within the 8-row window halo of 2 tiles (256 rows), so
+the strip windows apply; 250^2 and 262^2 also end in a partial tile.  Small
+grids have short strips: most tiles are chunk starts that load three fresh
+windows, which exercises the window-sequence breaks."""
+import os
+
+import numpy as np
+import pytest
+from conftest import f32, max_rel, rel_l2
+
+from oracle import Csr
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+PW, PAIR, SELL = 4, 2, 1
+
+
+def layout_apply(capi, ah, dims, p, b, env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        c = capi.Csr.from_arrays(ah.n, ah.row_ptr, ah.col_idx, ah.values)
+        y = capi.Model(c, dims, p).apply(b)
+        return y, c.layout_flags()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("grid", [250, 256, 262])
+def test_strip_windows_vs_oracle_and_sell(capi, oc, gnp, cuda, grid):
+    a0 = gnp.generate("c5_aniso9pt", grid, 1e-3, 30.0)
+    a = Csr(a0.n, np.array(a0.row_ptr), np.array(a0.col_idx), np.array(a0.values))
+    ah = oc.prescale(a, oc.gershgorin_gamma(a)).rounded_f32()
+    dims = (32, 32, 8)
+    p = f32(oc.init_params(*dims, 0))
+    b = oc.gaussian_vector(3, a.n)
+    y_pw, f_pw = layout_apply(capi, ah, dims, p, b, {"GNPC_PW_MIN_TILES": "0"})
+    assert f_pw & PW and f_pw & PAIR and f_pw & SELL, f_pw
+    y_pair, f_pair = layout_apply(capi, ah, dims, p, b, {"GNPC_NO_PW": "1"})
+    assert f_pair & PAIR and not f_pair & PW, f_pair
+    y_sell, f_sell = layout_apply(capi, ah, dims, p, b, {"GNPC_NO_PW": "1", "GNPC_NO_PAIR": "1"})
+    assert f_sell == SELL, f_sell
+    want = oc.gnn_apply(ah, dims, p, b)
+    for y in (y_pw, y_pair, y_sell):
+        assert rel_l2(y, want) <= TOL and max_rel(y, want) <= TOL, (rel_l2(y, want), max_rel(y, want))
+    assert np.array_equal(y_pw, y_sell)
+    assert np.array_equal(y_pair, y_sell)
+
+
+def test_strip_windows_not_built_off_stride(capi, oc, gnp, cuda):
+    # grid-line offset 300 rows: 44 rows past 2 tiles, outside the 8-row halo
+    a0 = gnp.generate("c5_aniso9pt", 300, 1e-3, 30.0)
+    c = capi.Csr.from_arrays(a0.n, np.array(a0.row_ptr), np.array(a0.col_idx), np.array(a0.values))
+    os.environ["GNPC_PW_MIN_TILES"] = "0"
+    try:
+        capi.Model(c, (32, 32, 8), capi.init_params(32, 32, 8, 0)).apply(np.ones(a0.n))
+    finally:
+        os.environ.pop("GNPC_PW_MIN_TILES", None)
+    assert not c.layout_flags() & PW
+
+
+def test_c5_full_size_strip_windows_bitwise(capi, cuda):
+    # BASELINE config 5 at its full size: the strip-window path (the default
+    # there) against the plain sliced-ELL path, bit for bit
+    dims = (32, 32, 8)
+    p = capi.init_params(*dims, 0)
+    b = np.random.default_rng(3).standard_normal(2048 * 2048)
+    ys = []
+    for env in ({}, {"GNPC_NO_PW": "1", "GNPC_NO_PAIR": "1"}):
+        for k, v in env.items():
+            os.environ[k] = v
+        try:
+            a = capi.Csr.generate("c5_aniso9pt", 2048, 1e-3, 30.0)
+            ah = a.prescale(a.gamma())
+            ys.append(capi.Model(ah, dims, p).apply(b))
+            flags = ah.layout_flags()
+            assert (flags & PW) if not env else flags == SELL, flags
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+    assert np.array_equal(ys[0], ys[1])

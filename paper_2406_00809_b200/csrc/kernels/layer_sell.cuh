@@ -106,7 +106,10 @@ struct SellCfg {
   // SM measured slower at DP=16: C2 26.0 vs 24.4 us, C4 213 vs 160 us)
   static constexpr int NW = 16;                  // math warps (gather / epilogue / split)
   static constexpr int CPS = 1;                  // CTAs per SM
-  static constexpr int NT = 32 * (NW + 1);       // + one control warp (MMA, TMA, stores)
+  // + one control warp (MMA, TMA, stores); the strip-window modes add a TMA
+  // producer warp, so the MMA issue is not serialised behind the loads
+  static constexpr int NPROD = (CSR == 7 || CSR == 8) ? 1 : 0;
+  static constexpr int NT = 32 * (NW + 1 + NPROD);
   static constexpr int NQ = NW / 4;              // epilogue column groups (warps per TMEM lane quarter)
   static constexpr int TM = 128;                 // rows per tile (MMA M)
   static constexpr int G = DP / 4;               // lanes per row
@@ -168,7 +171,7 @@ struct SellCfg {
   static constexpr bool PW = CSR == 7 || CSR == 8;
   static_assert(!PW || DP == 32, "strip windows are a d = 32 layout");
 #ifndef GNPC_NS_PW
-#define GNPC_NS_PW 4
+#define GNPC_NS_PW 4  // 3 measured slower (C5 409 vs 368 us)
 #endif
   static constexpr int NS = DP == 16 ? (CSRL ? GNPC_NS_CSR16 : (WIN ? 4 : GNPC_NS_SELL16))
                                      : (CSR == 2 ? GNPC_NS_TR32
@@ -177,8 +180,15 @@ struct SellCfg {
   // windows alive: the MMA's window of the current tile plus NS - 1 tiles
   // of lookahead (steady state: one new window per tile), and a strip break
   // needs the MMA's window plus three fresh ones
+  // windows alive: the MMA's window of the current tile plus NS - 1 tiles
+  // of lookahead (steady state: one new window per tile); a strip break
+  // needs the MMA's window plus three fresh ones
   static constexpr int NWIN = PW ? (NS + 1 > 4 ? NS + 1 : 4) : 0;
   static constexpr uint32_t WINB = kPwRows * DP * 4;
+#ifndef GNPC_PW_PF
+#define GNPC_PW_PF 0  // 4 / 8 measured slower with the single control thread (C5 406 / 398 vs 368 us)
+#endif
+  static constexpr int PF = PW ? GNPC_PW_PF : 0;  // L2 prefetch distance (tiles)
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
   // up to round(K, US) words).  Kept small: every KB of shared memory is L1
   // the X-row gathers hit (C5 fused layer 531 -> 499 us going 24 -> 12)
@@ -270,6 +280,12 @@ struct SellCfg {
     return DP == 32 && hidden % 16 == 0 && hidden <= 64;
   }
 };
+
+// the strip-window layouts fit one SM's shared memory (hidden 32)
+static_assert(SellCfg<32, 7>::o_bar(32, false) + 128 + 3 * SellCfg<32, 7>::KSCHED * 4 + 1024 <= 227 * 1024,
+              "strip-window layer layout exceeds shared memory");
+static_assert(SellCfg<32, 8>::o_bar(32, true) + 128 + 3 * SellCfg<32, 8>::KSCHED * 4 + 1024 <= 227 * 1024,
+              "strip-window last-layer layout exceeds shared memory");
 
 struct SellMaps {
   CUtensorMap x;   // layer input  [n][DP], box {DP, 128}, swizzled
@@ -565,6 +581,7 @@ struct SellPipe {
   uint64_t* full;
   uint64_t* mma_bar;
   uint64_t* afull;
+  int* prog;
   uint32_t tmem;
   int talloc;
   int ring_it = 0, mma_it = 0, af_it = 0;  // phase counters (identical in every thread)
@@ -627,6 +644,7 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
   p.mma_bar = p.full + C::NS;
   p.afull = p.mma_bar + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p.afull + 1);
+  p.prog = reinterpret_cast<int*>(tslot + 1);  // PW: tiles whose MMA the control warp has issued
   p.sched = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(p.full) + 128);
   const int tid = threadIdx.x;
   for (int t = tid; t < int(C::NS * C::SLOT / 16); t += C::NT)  // stale slice words must be valid columns
@@ -635,6 +653,7 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
     for (int s = 0; s < C::NS; ++s) tc::mbar_init(&p.full[s], 1);
     tc::mbar_init(p.mma_bar, 1);
     tc::mbar_init(p.afull, C::NW);
+    *p.prog = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if ((tid >> 5) == 0) tc::tmem_alloc(tslot, p.talloc);
@@ -746,8 +765,11 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   p.af_it += my_tiles > 0 ? my_tiles + 1 : 0;
   if (my_tiles == 0) return;
 
-  if (warp == NW) {
+  if (warp >= NW) {
     // ============================================================ control warp
+    // (strip windows: warp NW issues the MMAs and Y stores, warp NW + 1 the
+    // ring and window loads, following the MMA warp's progress counter)
+    const bool producer = C::PW && warp == NW + 1;
     if (lane == 0) {
       tc::tma_prefetch_desc(C::WIN ? mapxw : mapx);
       if (!LAST) tc::tma_prefetch_desc(mapy);
@@ -814,6 +836,22 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       // strip windows (PW): tiles are issued in order while the slice ring
       // has room (j <= it + NS - 1) and the new windows' slots are free: every
       // window older than the current tile's MMA window b(it) is dead
+      // L2 prefetch of tile j's new window(s) and slice, C::PF tiles ahead of
+      // its ring load: DRAM latency is covered in L2, the ring only needs to
+      // cover L2 latency (the ring depth is what shared memory allows)
+      auto prefetch_pw = [&](int j) {
+        if (C::PF == 0 || j >= my_tiles) return;
+        const int t = tile_at(j);
+        const bool brk = j == 0 || t != tile_at(j - 1) + a.pw_S;
+        const int K = use_sched ? sch_k[j] : __ldg(a.pw_k + t);
+        const int off = use_sched ? sch_o[j] : __ldg(a.pw_off + t);
+        tc::bulk_prefetch_l2(a.pw + static_cast<size_t>(off) * 16, K * (TM / 2) * 10);
+        if (brk) {
+          tc::tma_prefetch_2d(mapxw, 0, (t - a.pw_S) * TM - kPwHalo);
+          tc::tma_prefetch_2d(mapxw, 0, t * TM - kPwHalo);
+        }
+        tc::tma_prefetch_2d(mapxw, 0, (t + a.pw_S) * TM - kPwHalo);
+      };
       WinSeq ws;   // issue side
       WinSeq wsb;  // MMA side: b(it) of the current tile
       int nxt = 0, bcur = 0;
@@ -835,13 +873,31 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           load_win(sb, t);
         }
         load_win(sc, t + a.pw_S);
+        prefetch_pw(j + C::PF);
       };
       auto issue_more = [&](int it) {  // after afull(it) (it = -1: prologue)
         const int prot = it >= 0 ? bcur : 0;
         while (nxt < my_tiles && nxt <= it + NS - 1 && ws.peek_c(tile_at(nxt), a.pw_S) - prot < C::NWIN)
           issue_pw(nxt++);
       };
-      if constexpr (C::PW) issue_more(-1);
+      if constexpr (C::PW) {
+        if (producer) {
+          for (int j = NS - 1; j < C::PF; ++j) prefetch_pw(j);  // those the first issues do not reach
+          issue_more(-1);
+          for (int it = 0; it < my_tiles && nxt < my_tiles; ++it) {
+            // MMA(it) issued: tile it's gathers are done, its window b(it) in use
+            while (true) {
+              int v;
+              asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(tc::smem_u32(p.prog)) : "memory");
+              if (v > it) break;
+              __nanosleep(32);
+            }
+            int sa, sc;
+            wsb.next(tile_at(it), a.pw_S, sa, bcur, sc);
+            issue_more(it);
+          }
+        }
+      }
       else
         for (int it = 0; it < NS - 1; ++it) issue(it);
       constexpr uint32_t idesc = tc::idesc_tf32(128, DP);
@@ -849,7 +905,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       const uint32_t sBstk = tc::smem_u32(p.Bs);
       const uint32_t sA2hi = tc::smem_u32(p.A), sA2lo = sA2hi + C::OPB;
       const uint32_t tAlo = p.tmem + C::alo_col(TCP);
-      for (int it = 0; it <= my_tiles; ++it) {
+      for (int it = 0; it <= (producer ? -1 : my_tiles); ++it) {
         tc::mbar_wait_dbg(p.afull, (ab + it) & 1, 1, it);
         tc::fence_after();
         // stores issued up to the previous iteration have left the Y staging:
@@ -924,8 +980,9 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           tc::bulk_commit();
         }
         // every warp passed its wait for MMA(it-1): that slot takes tile it+NS-1
-        if constexpr (C::PW) {
-          if (it < my_tiles) issue_more(it);
+        if constexpr (C::PW) {  // the producer warp refills
+          if (it < my_tiles)
+            asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(tc::smem_u32(p.prog)), "r"(it + 1) : "memory");
         } else {
           issue(it + NS - 1);
         }
@@ -1253,7 +1310,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
 
 // One layer as its own launch (norm/lift/layers pipeline of ApplyLaunch).
 template <int DP, bool LAST, typename OutT, int CSR = 0>
-__global__ void __launch_bounds__(SellCfg<DP>::NT, 1)
+__global__ void __launch_bounds__(SellCfg<DP, CSR>::NT, 1)
 k_layer_sell(DevCsr a, const __grid_constant__ SellMaps maps, const float* __restrict__ X,
              const float* __restrict__ axlong, const float* __restrict__ uwp, NetView net,
              const ApplyScalars* __restrict__ sc, OutT* __restrict__ out, const int* __restrict__ skip) {

@@ -21,3 +21,14 @@ for i in sorted(order) if ctx == 0 else order:
             if j != i:
                 print(f"      {j:5d} {100*int(data[j][si])/tot:5.1f}% {data[j][src].strip()}")
         print()
+
+
+def by_reason(path, reason, top=15):
+    rows = list(csv.reader(open(path)))
+    h = rows[1]
+    d = rows[2:]
+    ri = h.index(reason)
+    tot = sum(float(r[ri] or 0) for r in d)
+    print(f"== {reason}: {tot:.0f} samples")
+    for i in sorted(range(len(d)), key=lambda i: -float(d[i][ri] or 0))[:top]:
+        print(f"{i:5d} {float(d[i][ri] or 0):7.0f} {d[i][h.index('Source')].strip()}")

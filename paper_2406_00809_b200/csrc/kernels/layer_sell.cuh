@@ -109,6 +109,13 @@ struct SellCfg {
   // + one control warp (MMA, TMA, stores); the strip-window modes add a TMA
   // producer warp, so the MMA issue is not serialised behind the loads
   static constexpr int NPROD = (CSR == 7 || CSR == 8) ? 1 : 0;
+  // strip-window modes: the MMA work that does not need tile t's split —
+  // X_hi·[U_lo; U_hi] and the projection of tile t-1 — is issued as soon as
+  // the epilogues have read TMEM (efull), overlapping the split
+#ifndef GNPC_PW_EARLY
+#define GNPC_PW_EARLY 1
+#endif
+  static constexpr bool EARLY = (CSR == 7 || CSR == 8) && GNPC_PW_EARLY;
   static constexpr int NT = 32 * (NW + 1 + NPROD);
   static constexpr int NQ = NW / 4;              // epilogue column groups (warps per TMEM lane quarter)
   static constexpr int TM = 128;                 // rows per tile (MMA M)
@@ -176,7 +183,7 @@ struct SellCfg {
   static constexpr int NS = DP == 16 ? (CSRL ? GNPC_NS_CSR16 : (WIN ? 4 : GNPC_NS_SELL16))
                                      : (CSR == 2 ? GNPC_NS_TR32
                                                  : ((DEEP || CSR == 5) ? GNPC_NS_DEEP32
-                                                                       : (CSR == 7 ? GNPC_NS_PW : 3)));
+                                                                       : ((CSR == 7 || CSR == 8) ? GNPC_NS_PW : 3)));
   // windows alive: the MMA's window of the current tile plus NS - 1 tiles
   // of lookahead (steady state: one new window per tile), and a strip break
   // needs the MMA's window plus three fresh ones
@@ -242,15 +249,17 @@ struct SellCfg {
   static constexpr uint32_t O_A = O_WIN + NWIN * WINB;    // A2_hi (ÂX), A2_lo
   static constexpr uint32_t O_B = O_A + 2 * OPB;          // Bu_lo, Bu_hi, Bw_lo, Bw_hi
   static constexpr uint32_t O_Y = O_B + 4 * BB;           // Y staging [2]
-  // last layer only: Y_lo staging [2], the dec1 B operand [D1_lo; D1_hi]
-  // (2H rows, swizzled K-major), then dec1 (fp32, CUDA-core fallback), b1, dec2
-  static constexpr uint32_t O_YLO = O_Y + 2 * OPB;
-  static constexpr uint32_t O_D1OP = O_YLO + 2 * OPB;
+  // last layer only: the dec1 B operand [D1_lo; D1_hi] (2H rows, swizzled
+  // K-major, TCP), then dec1 (fp32, CUDA-core projection), b1, dec2
   // training forward at d = 32: the rows' [Y > 0] words staged [2][TM] next
   // to the Y staging, stored with it by one bulk copy
   static constexpr uint32_t O_MST = O_Y + 2 * OPB;
   static constexpr uint32_t o_p(int hidden, bool last) {
-    return last && tc_proj(hidden) ? O_D1OP + 2 * hidden * DP * 4 : O_Y + 2 * OPB + (MBITS ? 2 * TM * 4 : 0);
+    // last layer with the tensor-core projection: no Y staging (the
+    // projection operand lives in TMEM), the dec1 operand [D1_lo; D1_hi] sits
+    // at O_Y, then dec1/b1/dec2.  Otherwise the Y staging stays (the fused
+    // apply's earlier layers use it with the last layer's layout).
+    return last && tc_proj(hidden) ? O_Y + 2 * hidden * DP * 4 : O_Y + 2 * OPB + (MBITS ? 2 * TM * 4 : 0);
   }
   static constexpr uint32_t o_bar(int hidden, bool last) {
     return (o_p(hidden, last) + (last ? (DP + 2) * hidden * 4 : 0) + 15) & ~15u;
@@ -261,12 +270,16 @@ struct SellCfg {
     // barriers + TMEM slot, the schedule, 1024-B alignment slack
     return o_bar(hidden, last) + 128 + 3 * KSCHED * 4 + 1024;
   }
-  static_assert(TR || DEEP || CSR == 5 || CSR == 7 || (DP == 32 ? O_D1OP + 2 * 32 * DP * 4 : O_Y + 2 * OPB) + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
+  static_assert(TR || DEEP || CSR == 5 || CSR == 7 || O_Y + 2 * 32 * DP * 4 + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
                 "last-layer layout must fit shared memory at hidden 32 (larger: host falls back)");
   static_assert(!TR || O_Y + 2 * OPB + 128 + 1024 <= 227 * 1024, "training layout must fit shared memory");
   // TMEM: layer accumulator [0, 2DP); last layer's projection accumulator at
   // [2DP, 2DP + 2H) (tensor-core projection when H % 16 == 0 and H <= 64)
-  static constexpr int TALLOC_LAST = 256;
+  // last layer (tensor-core projection): Y_hi / Y_lo of two tiles in TMEM at
+  // ycol(buf) = 256 + 2 DP buf, so the allocation is the whole 512 columns
+  // (one CTA per SM)
+  static constexpr int TALLOC_LAST = 512;
+  static __host__ __device__ constexpr uint32_t ycol(int buf) { return 256 + 2 * DP * buf; }
   // TMEM column of X_lo, the A operand of X·U's A_lo·B_hi product: written
   // row-per-lane by the math warps (tcgen05.st), read by the TS-form MMA, so
   // it never crosses shared memory.  (ÂX_lo stays in shared memory: moving it
@@ -575,12 +588,12 @@ struct SellPipe {
   uint8_t* A;  // [A2_hi | A2_lo]
   uint8_t* Bs;
   uint8_t* Ystg;
-  uint8_t* Ylo;
   uint8_t* D1op;
   float* D1;
   uint64_t* full;
   uint64_t* mma_bar;
   uint64_t* afull;
+  uint64_t* efull;  // PW: a tile's epilogue (and the previous projection epilogue) read TMEM
   int* prog;
   uint32_t tmem;
   int talloc;
@@ -636,14 +649,14 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
   p.A = base + C::O_A;
   p.Bs = base + C::O_B;
   p.Ystg = base + C::O_Y;
-  p.Ylo = base + C::O_YLO;
-  p.D1op = base + C::O_D1OP;
+  p.D1op = base + C::O_Y;  // last layers only
   p.D1 = reinterpret_cast<float*>(base + C::o_p(hidden, last));
   p.full = reinterpret_cast<uint64_t*>(base + C::o_bar(hidden, last));
   p.talloc = last ? C::TALLOC_LAST : C::TALLOC;
   p.mma_bar = p.full + C::NS;
   p.afull = p.mma_bar + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(p.afull + 1);
+  p.efull = p.afull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(p.efull + 1);
   p.prog = reinterpret_cast<int*>(tslot + 1);  // PW: tiles whose MMA the control warp has issued
   p.sched = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(p.full) + 128);
   const int tid = threadIdx.x;
@@ -653,6 +666,7 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
     for (int s = 0; s < C::NS; ++s) tc::mbar_init(&p.full[s], 1);
     tc::mbar_init(p.mma_bar, 1);
     tc::mbar_init(p.afull, C::NW);
+    tc::mbar_init(p.efull, C::NW);
     *p.prog = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -905,7 +919,40 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       const uint32_t sBstk = tc::smem_u32(p.Bs);
       const uint32_t sA2hi = tc::smem_u32(p.A), sA2lo = sA2hi + C::OPB;
       const uint32_t tAlo = p.tmem + C::alo_col(TCP);
+      const uint32_t sXe0 = tc::smem_u32(p.win) + kPwHalo * DP * 4;
+      auto proj_mma = [&](int t1) {  // projection of tile t1 (its relu'd rows hi / lo in TMEM)
+        // Dp[:, 0:H] = Y_hi·D1_lo, Dp[:, H:2H] = Y_hi·D1_hi + Y_lo·D1_hi
+        const uint32_t tYh = p.tmem + C::ycol((mb + t1) & 1), tYl = tYh + DP;  // A from TMEM
+        const uint32_t sD = tc::smem_u32(p.D1op);
+        const uint32_t sDh = sD + H * DP * 4;
+        const uint32_t iH = tc::idesc_tf32(128, H), i2H = tc::idesc_tf32(128, 2 * H);
+        const uint32_t pacc = p.tmem + 2 * DP;
+#pragma unroll
+        for (int k8 = 0; k8 < DP / 8; ++k8) {
+          tc::mma_tf32_ts(pacc, tYh + 8 * k8, tc::make_desc_swz<DP>(sD + k8 * 32), i2H, k8 > 0);
+          tc::mma_tf32_ts(pacc + H, tYl + 8 * k8, tc::make_desc_swz<DP>(sDh + k8 * 32), iH, 1);
+        }
+      };
       for (int it = 0; it <= (producer ? -1 : my_tiles); ++it) {
+        if constexpr (C::EARLY) {
+          if (it >= 1) {  // epilogue(it-1) and projection epilogue(it-2) have read TMEM
+            tc::mbar_wait_dbg(p.efull, (it - 1) & 1, 5, it);
+            tc::fence_after();
+            if (TCP) proj_mma(it - 1);
+          }
+          if (it < my_tiles) {  // X_hi·[U_lo; U_hi] once the tile's rows landed
+            const int r = rb + it;
+            tc::mbar_wait_dbg(&p.full[r % NS], (r / NS) & 1, 6, it);
+            tc::fence_after();
+            int sa, sc;
+            wsb.next(tile_at(it), a.pw_S, sa, bcur, sc);
+            const uint32_t sX = sXe0 + (bcur % C::NWIN) * C::WINB;
+#pragma unroll
+            for (int k8 = 0; k8 < DP / 8; ++k8)
+              tc::mma_tf32(p.tmem, tc::make_desc_swz<DP>(sX + k8 * 32), tc::make_desc_swz<DP>(sBstk + k8 * 32),
+                           idesc2, k8 > 0);
+          }
+        }
         tc::mbar_wait_dbg(p.afull, (ab + it) & 1, 1, it);
         tc::fence_after();
         // stores issued up to the previous iteration have left the Y staging:
@@ -918,9 +965,11 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         if (it < my_tiles) {
           uint32_t sX = tc::smem_u32(p.ring + ((rb + it) % NS) * C::SLOT);
           if constexpr (C::PW) {  // the tile's own rows: window b(it) past its halo
-            int sa, sc;
-            wsb.next(tile_at(it), a.pw_S, sa, bcur, sc);
-            sX = tc::smem_u32(p.win + (bcur % C::NWIN) * C::WINB + kPwHalo * DP * 4);
+            if constexpr (!C::EARLY) {
+              int sa, sc;
+              wsb.next(tile_at(it), a.pw_S, sa, bcur, sc);
+            }
+            sX = sXe0 + (bcur % C::NWIN) * C::WINB;
           }
           if constexpr (C::WIN)  // the tile's own rows inside the window
             sX += __ldg(a.wdesc + static_cast<size_t>(tile_at(it)) * kWinDesc + 1) * C::BLKB;
@@ -936,11 +985,18 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
             const uint32_t sah = part == 0 ? sX : sA2hi;
             const uint32_t sbs = sBstk + part * 2 * C::BB;  // [B_lo; B_hi] of this part (2DP rows)
             const uint32_t sbh = sbs + C::BB;                // B_hi rows alone
+            // (the A_hi products of a part first, then its A_lo products: the
+            // same accumulation order whether or not EARLY issues part 0's
+            // A_hi products before afull, so every layout gives the same bits)
 #pragma unroll
             for (int k8 = 0; k8 < DP / 8; ++k8) {
-              tc::mma_tf32(p.tmem, tc::make_desc_swz<DP>(sah + k8 * 32),
-                           tc::make_desc_swz<DP>(sbs + k8 * 32), idesc2, accf);
+              if (!(C::EARLY && part == 0))  // (EARLY: issued before afull)
+                tc::mma_tf32(p.tmem, tc::make_desc_swz<DP>(sah + k8 * 32),
+                             tc::make_desc_swz<DP>(sbs + k8 * 32), idesc2, accf);
               accf = 1;
+            }
+#pragma unroll
+            for (int k8 = 0; k8 < DP / 8; ++k8) {
               if (part == 0)
                 tc::mma_tf32_ts(p.tmem + DP, tAlo + 8 * k8, tc::make_desc_swz<DP>(sbh + k8 * 32), idesc, 1);
               else
@@ -949,23 +1005,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
             }
           }
         }
-        if (TCP && it >= 1) {
-          // projection of tile it-1 (its relu'd rows are staged hi/lo):
-          // Dp[:, 0:H] = Y_hi·D1_lo, Dp[:, H:2H] = Y_hi·D1_hi + Y_lo·D1_hi
-          const uint32_t sYh = tc::smem_u32(p.Ystg + ((mb + it - 1) & 1) * C::OPB);
-          const uint32_t sYl = tc::smem_u32(p.Ylo + ((mb + it - 1) & 1) * C::OPB);
-          const uint32_t sD = tc::smem_u32(p.D1op);
-          const uint32_t sDh = sD + H * DP * 4;
-          const uint32_t iH = tc::idesc_tf32(128, H), i2H = tc::idesc_tf32(128, 2 * H);
-          const uint32_t pacc = p.tmem + 2 * DP;
-#pragma unroll
-          for (int k8 = 0; k8 < DP / 8; ++k8) {
-            tc::mma_tf32(pacc, tc::make_desc_swz<DP>(sYh + k8 * 32), tc::make_desc_swz<DP>(sD + k8 * 32), i2H,
-                         k8 > 0);
-            tc::mma_tf32(pacc + H, tc::make_desc_swz<DP>(sYl + k8 * 32), tc::make_desc_swz<DP>(sDh + k8 * 32),
-                         iH, 1);
-          }
-        }
+        if (TCP && it >= 1 && !C::EARLY) proj_mma(it - 1);
         if (KIND == 1 && it < my_tiles) tc::bulk_wait_read0();  // A2_hi is rewritten after the commit
         if (it < my_tiles || (TCP && it >= 1)) tc::mma_commit(p.mma_bar);
         if (!LAST && it >= 1) {  // tile it-1 is fully staged
@@ -1005,7 +1045,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   // registers `y` and projects them after arriving — the groups rotate, so
   // no CTA-wide barrier is needed.
   // With the tensor-core projection (TCP) the last layer stages its relu'd
-  // rows like the others (hi into Ystg, lo into Ylo) for the control warp's
+  // rows hi / lo into TMEM (ycol) for the control warp's
   // projection MMA, and the rotating group reads the projection accumulator
   // one tile later (proj_epilogue).
   auto epilogue = [&](int itp) -> bool {
@@ -1029,6 +1069,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       const int m = 32 * q + lane;
       constexpr int CW = DP / NQ;  // columns per warp: 4 or 8
       uint8_t* ys = p.Ystg + ((mb + itp) & 1) * C::OPB;
+      float yh[LAST ? CW : 1], ylo[LAST ? CW : 1];
       const uint32_t taddr = trow + cq * CW;
       float v[CW];
       if constexpr (CW == 4) {
@@ -1079,10 +1120,26 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           mout |= (v[c] > 0.f ? 1u : 0u) << c | (v[c + 1] > 0.f ? 1u : 0u) << (c + 1) |
                   (v[c + 2] > 0.f ? 1u : 0u) << (c + 2) | (v[c + 3] > 0.f ? 1u : 0u) << (c + 3);
         }
-        *reinterpret_cast<float4*>(ys + tc::swz_off<DP>(m, cq * CW + c)) = yv;
-        if (LAST)
-          *reinterpret_cast<float4*>(p.Ylo + ((mb + itp) & 1) * C::OPB + tc::swz_off<DP>(m, cq * CW + c)) =
-              f4_trunc_lo(yv);
+        if constexpr (LAST) {  // projection operand, kept in TMEM (hi, lo)
+          const float4 yl = f4_trunc_lo(yv);
+          yh[c] = yv.x; yh[c + 1] = yv.y; yh[c + 2] = yv.z; yh[c + 3] = yv.w;
+          ylo[c] = yl.x; ylo[c + 1] = yl.y; ylo[c + 2] = yl.z; ylo[c + 3] = yl.w;
+        } else {
+          *reinterpret_cast<float4*>(ys + tc::swz_off<DP>(m, cq * CW + c)) = yv;
+        }
+      }
+      if constexpr (LAST) {
+        // rows are TMEM lanes as in the accumulator: Y_hi at ycol(buf),
+        // Y_lo DP columns on (the projection MMA reads them as its A operand)
+        const uint32_t ty = p.tmem + C::ycol((mb + itp) & 1) + (static_cast<uint32_t>(32 * q) << 16) + cq * CW;
+        if constexpr (CW == 8) {
+          tc::tmem_st8(ty, yh);
+          tc::tmem_st8(ty + DP, ylo);
+        } else {
+          tc::tmem_st4(ty, yh);
+          tc::tmem_st4(ty + DP, ylo);
+        }
+        tc::tmem_wait_st();
       }
       if constexpr (KIND == 1 && C::MBITS) {  // this warp's CW = 8 columns: one byte of the row's word
         p.Ystg[C::O_MST - C::O_Y + ((mb + itp) & 1) * TM * 4 + 4 * m + cq] = static_cast<uint8_t>(mout);
@@ -1269,6 +1326,12 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       tc::fence_after();
     }
     if (TCP && it >= 2) proj_epilogue(it - 2);
+    if constexpr (C::EARLY) {  // TMEM read for epilogue(it-1): the control warp may issue into it
+      if (it >= 1 && it - 1 < my_tiles) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p.efull);
+      }
+    }
 
     // ---------------------------------------------------------------- split
     if (have) {

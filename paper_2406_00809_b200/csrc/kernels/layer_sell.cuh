@@ -262,7 +262,8 @@ struct SellCfg {
     return last && tc_proj(hidden) ? O_Y + 2 * hidden * DP * 4 : O_Y + 2 * OPB + (MBITS ? 2 * TM * 4 : 0);
   }
   static constexpr uint32_t o_bar(int hidden, bool last) {
-    return (o_p(hidden, last) + (last ? (DP + 2) * hidden * 4 : 0) + 15) & ~15u;
+    // last: dec1 (DP x H), b1, dec2, then the projection partials [2][NQ][TM]
+    return (o_p(hidden, last) + (last ? (DP + 2) * hidden * 4 + 2 * NQ * TM * 4 : 0) + 15) & ~15u;
   }
   // PW: per-CTA schedule table (tile, K, slice offset) after the barriers
   static constexpr int KSCHED = PW ? 256 : 0;
@@ -1151,19 +1152,35 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   // TCP: projection epilogue of local tile itp (its projection MMA completed
   // with the commit this iteration waited for): the rotating group reads its
   // rows' 2H accumulator columns, out = (Σ_h relu(z_h + b1_h) dec2_h + b2)·τ/√n
+  // The projection epilogue runs on all math warps: warp (lane quarter q,
+  // column group cq) reduces relu(z + b1)·dec2 over its H / NQ projection
+  // columns for the quarter's 32 rows into PART; one tile later the rotating
+  // warp of each quarter adds the NQ partials in a fixed order and writes
+  // out[i] (the rotating group alone doing the whole reduction made every
+  // tile wait for it: C5 last layer ~19 % of stalls on the MMA barrier).
+  float* PART = D2 + H;  // [2][NQ][TM]
   auto proj_epilogue = [&](int itp) {
     const int q = warp & 3, cq = warp >> 2;
-    if (cq != itp % NQ) return;
-    const uint32_t prow = p.tmem + 2 * DP + (static_cast<uint32_t>(32 * q) << 16);
+    const int hc = H / NQ;  // H % 16 == 0 (tensor-core projection)
+    const uint32_t prow = p.tmem + 2 * DP + (static_cast<uint32_t>(32 * q) << 16) + cq * hc;
     float o = 0.f;
-    for (int h0 = 0; h0 < H; h0 += 16) {
-      float z1[16], z2[16];
-      tc::tmem_ld16(prow + h0, z1);
-      tc::tmem_ld16(prow + H + h0, z2);
+    for (int h0 = 0; h0 < hc; h0 += 4) {
+      float z1[4], z2[4];
+      tc::tmem_ld4(prow + h0, z1);
+      tc::tmem_ld4(prow + H + h0, z2);
 #pragma unroll
-      for (int c = 0; c < 16; ++c) o = fmaf(relu(z1[c] + z2[c] + B1[h0 + c]), D2[h0 + c], o);
+      for (int c = 0; c < 4; ++c) o = fmaf(relu(z1[c] + z2[c] + B1[cq * hc + h0 + c]), D2[cq * hc + h0 + c], o);
     }
     tc::fence_before();
+    PART[((itp & 1) * NQ + cq) * TM + 32 * q + lane] = o;
+  };
+  auto proj_final = [&](int itp) {
+    const int q = warp & 3, cq = warp >> 2;
+    if (cq != itp % NQ) return;
+    const float* pp = PART + (itp & 1) * NQ * TM + 32 * q + lane;
+    float o = pp[0];
+#pragma unroll
+    for (int c = 1; c < NQ; ++c) o += pp[c * TM];
     const int i = tile_at(itp) * TM + 32 * q + lane;
     if (i < n) out[i] = static_cast<OutT>(static_cast<double>(o + net.dec2_b) * out_scale);
   };
@@ -1204,7 +1221,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   // per tile: K_t | has-long << 16 (SELL, pair-union), has-long (CSR)
   const int* tinfo = C::CSRL ? a.tflag : (C::PAIR ? a.psell_k : (C::PW ? a.pw_k : a.sell_k));
   int kw = TR ? 0 : (use_sched ? sch_k[0] : __ldg(tinfo + tile_at(0)));
-  const int iters = my_tiles + 1 + (TCP ? 1 : 0);
+  const int iters = my_tiles + 1 + (TCP ? 2 : 0);
   WinSeq wsm;                       // strip windows (PW): the control warp's sequence, replayed
   const uint8_t* wtile = nullptr;   // PW: the tile's own rows (window b past its halo)
   for (int it = 0; it < iters; ++it) {
@@ -1325,7 +1342,10 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       tc::mbar_wait_dbg(p.mma_bar, (mb + my_tiles) & 1, 2, it);
       tc::fence_after();
     }
-    if (TCP && it >= 2) proj_epilogue(it - 2);
+    if (TCP && it == my_tiles + 2)  // every warp's last partials are written
+      asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+    if (TCP && it >= 2 && it - 2 < my_tiles) proj_epilogue(it - 2);
+    if (TCP && it >= 3 && it - 3 < my_tiles) proj_final(it - 3);
     if constexpr (C::EARLY) {  // TMEM read for epilogue(it-1): the control warp may issue into it
       if (it >= 1 && it - 1 < my_tiles) {
         __syncwarp();

@@ -595,6 +595,7 @@ struct SellPipe {
   uint64_t* mma_bar;
   uint64_t* afull;
   uint64_t* efull;  // PW: a tile's epilogue (and the previous projection epilogue) read TMEM
+  uint64_t* pbar;   // last layer: the projection MMA of a tile completed
   int* prog;
   uint32_t tmem;
   int talloc;
@@ -657,7 +658,8 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
   p.mma_bar = p.full + C::NS;
   p.afull = p.mma_bar + 1;
   p.efull = p.afull + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(p.efull + 1);
+  p.pbar = p.efull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(p.pbar + 1);
   p.prog = reinterpret_cast<int*>(tslot + 1);  // PW: tiles whose MMA the control warp has issued
   p.sched = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(p.full) + 128);
   const int tid = threadIdx.x;
@@ -668,6 +670,7 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
     tc::mbar_init(p.mma_bar, 1);
     tc::mbar_init(p.afull, C::NW);
     tc::mbar_init(p.efull, C::NW);
+    tc::mbar_init(p.pbar, 1);
     *p.prog = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -774,7 +777,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   const uint64_t pol_keep = hint ? l2_policy_evict_last() : l2_policy_evict_normal();
   const int rb = p.ring_it, mb = p.mma_it, ab = p.af_it;
   // commits: one per tile, plus the last projection MMA's (TCP)
-  const int ncommit = my_tiles + (TCP && my_tiles > 0 ? 1 : 0);
+  const int ncommit = my_tiles;  // (the projection MMAs commit to pbar)
   p.ring_it += my_tiles;
   p.mma_it += ncommit;
   p.af_it += my_tiles > 0 ? my_tiles + 1 : 0;
@@ -939,7 +942,6 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           if (it >= 1) {  // epilogue(it-1) and projection epilogue(it-2) have read TMEM
             tc::mbar_wait_dbg(p.efull, (it - 1) & 1, 5, it);
             tc::fence_after();
-            if (TCP) proj_mma(it - 1);
           }
           if (it < my_tiles) {  // X_hi·[U_lo; U_hi] once the tile's rows landed
             const int r = rb + it;
@@ -1006,9 +1008,14 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
             }
           }
         }
-        if (TCP && it >= 1 && !C::EARLY) proj_mma(it - 1);
         if (KIND == 1 && it < my_tiles) tc::bulk_wait_read0();  // A2_hi is rewritten after the commit
-        if (it < my_tiles || (TCP && it >= 1)) tc::mma_commit(p.mma_bar);
+        if (it < my_tiles) tc::mma_commit(p.mma_bar);
+        // the projection of tile it-1 after MMA(it), on its own barrier: the
+        // epilogues' wait for MMA(it) does not include it
+        if (TCP && it >= 1) {
+          proj_mma(it - 1);
+          tc::mma_commit(p.pbar);
+        }
         if (!LAST && it >= 1) {  // tile it-1 is fully staged
           tc::tma_store_2d(mapy, p.Ystg + ((mb + it - 1) & 1) * C::OPB, 0, tile_at(it - 1) * TM);
           if constexpr (KIND == 1 && C::MBITS) {
@@ -1160,6 +1167,8 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   // tile wait for it: C5 last layer ~19 % of stalls on the MMA barrier).
   float* PART = D2 + H;  // [2][NQ][TM]
   auto proj_epilogue = [&](int itp) {
+    tc::mbar_wait_dbg(p.pbar, itp & 1, 7, itp);  // the projection MMA of tile itp
+    tc::fence_after();
     const int q = warp & 3, cq = warp >> 2;
     const int hc = H / NQ;  // H % 16 == 0 (tensor-core projection)
     const uint32_t prow = p.tmem + 2 * DP + (static_cast<uint32_t>(32 * q) << 16) + cq * hc;
@@ -1336,12 +1345,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
 
     // ------------------------------------------- epilogue of the previous tile
     bool proj = false;
-    if (it >= 1 && it - 1 < my_tiles) {
-      proj = epilogue(it - 1);
-    } else if (TCP && it == my_tiles + 1) {  // drain: wait for the last projection MMA
-      tc::mbar_wait_dbg(p.mma_bar, (mb + my_tiles) & 1, 2, it);
-      tc::fence_after();
-    }
+    if (it >= 1 && it - 1 < my_tiles) proj = epilogue(it - 1);
     if (TCP && it == my_tiles + 2)  // every warp's last partials are written
       asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
     if (TCP && it >= 2 && it - 2 < my_tiles) proj_epilogue(it - 2);

@@ -473,7 +473,14 @@ def apply_leg(capi, torch, cfg_name, args, rank, world, dist, local, full=True):
     # ---- roofline: per-kernel CUDA events on the launching stream
     dp = dp_of(d)
     sell, longr = w["a"].device_layout()[1:3]
-    if dp in (16, 32) and sell:
+    lflags = w["a"].layout_flags()
+    if dp == 32 and lflags & 4:
+        layer_kernel = ("k_layer_sell<DP=32, strip windows> (fused Res-GCONV: X row windows staged in shared "
+                        "memory by TMA along strips of the dominant tile stride, pair-union entries, tcgen05 "
+                        "3xTF32; MMA warp + TMA producer warp)")
+    elif dp == 32 and lflags & 2:
+        layer_kernel = "k_layer_sell<DP=32, pair-union> (fused Res-GCONV, pair-union sliced-ELL TMA pipeline, tcgen05 3xTF32)"
+    elif dp in (16, 32) and sell:
         layer_kernel = f"k_layer_sell<DP={dp}> (fused Res-GCONV, sliced-ELL TMA pipeline, tcgen05 3xTF32)"
     elif dp in (16, 32):
         layer_kernel = (f"k_layer_sell<DP={dp}, CSR> (fused Res-GCONV, short-row CSR TMA pipeline, "

@@ -108,14 +108,20 @@ struct SellCfg {
   static constexpr int CPS = 1;                  // CTAs per SM
   // + one control warp (MMA, TMA, stores); the strip-window modes add a TMA
   // producer warp, so the MMA issue is not serialised behind the loads
-  static constexpr int NPROD = (CSR == 7 || CSR == 8) ? 1 : 0;
+#ifndef GNPC_TR_PROD
+#define GNPC_TR_PROD 0  // measured neutral on C3 (19.34 ms either way)
+#endif
+  static constexpr int NPROD = (CSR == 7 || CSR == 8 || (CSR == 2 && GNPC_TR_PROD)) ? 1 : 0;
   // strip-window modes: the MMA work that does not need tile t's split —
   // X_hi·[U_lo; U_hi] and the projection of tile t-1 — is issued as soon as
   // the epilogues have read TMEM (efull), overlapping the split
 #ifndef GNPC_PW_EARLY
 #define GNPC_PW_EARLY 1
 #endif
-  static constexpr bool EARLY = (CSR == 7 || CSR == 8) && GNPC_PW_EARLY;
+#ifndef GNPC_TR_EARLY
+#define GNPC_TR_EARLY 0
+#endif
+  static constexpr bool EARLY = ((CSR == 7 || CSR == 8) && GNPC_PW_EARLY) || (CSR == 2 && GNPC_TR_EARLY);
   static constexpr int NT = 32 * (NW + 1 + NPROD);
   static constexpr int NQ = NW / 4;              // epilogue column groups (warps per TMEM lane quarter)
   static constexpr int TM = 128;                 // rows per tile (MMA M)
@@ -787,7 +793,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
     // ============================================================ control warp
     // (strip windows: warp NW issues the MMAs and Y stores, warp NW + 1 the
     // ring and window loads, following the MMA warp's progress counter)
-    const bool producer = C::PW && warp == NW + 1;
+    const bool producer = C::NPROD && warp == NW + 1;
     if (lane == 0) {
       tc::tma_prefetch_desc(C::WIN ? mapxw : mapx);
       if (!LAST) tc::tma_prefetch_desc(mapy);
@@ -916,8 +922,20 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           }
         }
       }
-      else
+      else if (C::NPROD == 0 || producer) {
         for (int it = 0; it < NS - 1; ++it) issue(it);
+        if (producer) {
+          for (int it = 0; it < my_tiles; ++it) {  // after MMA(it): its slot's previous tile is done
+            while (true) {
+              int v;
+              asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(tc::smem_u32(p.prog)) : "memory");
+              if (v > it) break;
+              __nanosleep(32);
+            }
+            issue(it + NS - 1);
+          }
+        }
+      }
       constexpr uint32_t idesc = tc::idesc_tf32(128, DP);
       constexpr uint32_t idesc2 = tc::idesc_tf32(128, 2 * DP);
       const uint32_t sBstk = tc::smem_u32(p.Bs);
@@ -947,9 +965,12 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
             const int r = rb + it;
             tc::mbar_wait_dbg(&p.full[r % NS], (r / NS) & 1, 6, it);
             tc::fence_after();
-            int sa, sc;
-            wsb.next(tile_at(it), a.pw_S, sa, bcur, sc);
-            const uint32_t sX = sXe0 + (bcur % C::NWIN) * C::WINB;
+            uint32_t sX = tc::smem_u32(p.ring + (r % NS) * C::SLOT);
+            if constexpr (C::PW) {
+              int sa, sc;
+              wsb.next(tile_at(it), a.pw_S, sa, bcur, sc);
+              sX = sXe0 + (bcur % C::NWIN) * C::WINB;
+            }
 #pragma unroll
             for (int k8 = 0; k8 < DP / 8; ++k8)
               tc::mma_tf32(p.tmem, tc::make_desc_swz<DP>(sX + k8 * 32), tc::make_desc_swz<DP>(sBstk + k8 * 32),
@@ -1028,7 +1049,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           tc::bulk_commit();
         }
         // every warp passed its wait for MMA(it-1): that slot takes tile it+NS-1
-        if constexpr (C::PW) {  // the producer warp refills
+        if constexpr (C::NPROD) {  // the producer warp refills
           if (it < my_tiles)
             asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(tc::smem_u32(p.prog)), "r"(it + 1) : "memory");
         } else {

@@ -180,3 +180,35 @@ def test_trained_gnp_fgmres_iteration_parity_c2(capi, oc, cuda, tmp_path):
     ah = scaled(oc, "c2_convdiff3d", 64, 10.0)
     b = oc.spmv(ah, oc.gaussian_vector(1, ah.n))
     _trained_fgmres_case(capi, oc, ah, b, (16, 32, 8), 600, 1e-6, 30, 300, tmp_path)
+
+
+def test_trained_gnp_fgmres_converges_c5_full_size(capi, oc, cuda):
+    # C5 at its full size (n = 4.19M, d = 32, restart 50, rtol 1e-6, b = A x*):
+    # a device-trained GNP (300 steps, batch 8) converges where the seed-0
+    # weights stall, in fewer iterations than unpreconditioned GMRES, and the
+    # oracle's f64 FGMRES driven by the same device M needs the same count
+    # (+-1): the Krylov machinery matches at full size.  (The oracle's f64 GNP
+    # end to end is ~10 s per apply at this size: profiles/r02_trained_fgmres_c5.json
+    # records the run this test repeats.)
+    ah = scaled(oc, "c5_aniso9pt", 2048, 1e-3, 30.0)
+    A = dev_csr(capi, ah)
+    dims, rtol, restart, maxiters = (32, 32, 8), 1e-6, 50, 500
+    b = oc.spmv(ah, np.random.default_rng(3).standard_normal(ah.n))
+    best, losses, bl = capi.train_preconditioner(A, dims=dims, steps=300, batch=8, spectral=4, arnoldi_m=40,
+                                                 seed=0, monitor_batch=8)
+    assert bl < 0.1 * losses[0]
+    m = capi.Model(A, dims, f32(best))
+    dev = capi.fgmres(A, b, model=m, rtol=rtol, maxiters=maxiters, restart=restart)
+    plain = capi.fgmres(A, b, rtol=rtol, maxiters=maxiters, restart=restart)
+    oc.set_threads(os.cpu_count() or 1)
+    try:
+        cb = oc.fgmres(ah, b, kind=lambda v: m.apply(v), rtol=rtol, maxiters=maxiters, restart=restart)
+    finally:
+        oc.set_threads(1)
+    its = dev["history"][-1][0]
+    print(f"C5 trained GNP: FGMRES {its} iterations (oracle FGMRES + device M {cb['history'][-1][0]}), "
+          f"GMRES {plain['history'][-1][0]}")
+    assert dev["status"] == "converged" and cb["status"] == "converged"
+    assert abs(its - cb["history"][-1][0]) <= 1
+    assert plain["status"] == "converged" and its < plain["history"][-1][0]
+    assert np.linalg.norm(oc.spmv(ah, dev["x"]) - b) / np.linalg.norm(b) <= rtol * 1.01

@@ -55,33 +55,18 @@ k_lift_pw(const T* __restrict__ in, int n, NetView net, const ApplyScalars* __re
   __syncthreads();
   const int gl = threadIdx.x % G;
   const double in_scale = sc->in_scale;
-  // LT rows per pass with their input loads in flight together (one row per
-  // pass left the load latency exposed ~110 times per thread at C5: 113 us)
-  constexpr int LT = 8;
-  const int stride = gridDim.x * NG;
-  for (int r0 = blockIdx.x * NG + threadIdx.x / G; r0 < n; r0 += LT * stride) {
-    T vin[LT];
-#pragma unroll
-    for (int k = 0; k < LT; ++k) {
-      const int row = r0 + k * stride;
-      vin[k] = row < n ? in[row] : T(0);
+  for (int row = blockIdx.x * NG + threadIdx.x / G; row < n; row += gridDim.x * NG) {
+    const float v = static_cast<float>(in_scale * static_cast<double>(in[row]));
+    int lo = 0, hi = nb;  // interval = #kinks <= v
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s_t[mid] <= v) lo = mid + 1;
+      else hi = mid;
     }
-#pragma unroll
-    for (int k = 0; k < LT; ++k) {
-      const int row = r0 + k * stride;
-      if (row >= n) break;
-      const float v = static_cast<float>(in_scale * static_cast<double>(vin[k]));
-      int lo = 0, hi = nb;  // interval = #kinks <= v
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (s_t[mid] <= v) lo = mid + 1;
-        else hi = mid;
-      }
-      const float4 al = *reinterpret_cast<const float4*>(s_a + lo * DP + 4 * gl);
-      const float4 be = *reinterpret_cast<const float4*>(s_b + lo * DP + 4 * gl);
-      st4(X + static_cast<size_t>(row) * DP + 4 * gl,
-          make_float4(fmaf(al.x, v, be.x), fmaf(al.y, v, be.y), fmaf(al.z, v, be.z), fmaf(al.w, v, be.w)));
-    }
+    const float4 al = *reinterpret_cast<const float4*>(s_a + lo * DP + 4 * gl);
+    const float4 be = *reinterpret_cast<const float4*>(s_b + lo * DP + 4 * gl);
+    st4(X + static_cast<size_t>(row) * DP + 4 * gl,
+        make_float4(fmaf(al.x, v, be.x), fmaf(al.y, v, be.y), fmaf(al.z, v, be.z), fmaf(al.w, v, be.w)));
   }
 }
 

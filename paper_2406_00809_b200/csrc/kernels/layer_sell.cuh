@@ -201,9 +201,10 @@ struct SellCfg {
   // of lookahead (steady state: one new window per tile), and a strip break
   // needs the MMA's window plus three fresh ones
   // windows alive: the MMA's window of the current tile plus NS - 1 tiles
-  // of lookahead (steady state: one new window per tile); a strip break
-  // needs the MMA's window plus three fresh ones
-  static constexpr int NWIN = PW ? (NS + 1 > 4 ? NS + 1 : 4) : 0;
+  // of lookahead (steady state: one new window per tile); a break tile
+  // issued right after its predecessor's gathers needs the MMA window b,
+  // the predecessor's c and three fresh seqs: c - b = 4 < NWIN
+  static constexpr int NWIN = PW ? (NS + 1 > 5 ? NS + 1 : 5) : 0;
   static constexpr uint32_t WINB = kPwRows * DP * 4;
 #ifndef GNPC_PW_PF
 #define GNPC_PW_PF 0  // 4 / 8 measured slower with the single control thread (C5 406 / 398 vs 368 us)
@@ -620,12 +621,15 @@ struct SellPipe {
 };
 
 // Window sequence of the strip-window mode, replayed identically by the
-// control warp (which loads the windows) and the math warps (which read them):
-// tile position j gets windows (a, b, c) = those of tiles u - S, u, u + S;
-// window seq q lives in slot q % NWIN.  Along a strip (u = previous + S) only
-// c is new; at a break (chunk start, strip end) three fresh windows follow
-// the previous tile's b: (b+1, b+2, b+3), so only the previous tile's MMA
-// window b stays protected.
+// producer warp (which loads the windows), the MMA warp and the math warps
+// (which read them): tile position j gets windows (a, b, c) = those of tiles
+// u - S, u, u + S; window seq q lives in slot q % NWIN.  Along a strip
+// (u = previous + S) only c is new; at a break (chunk start, strip end) three
+// fresh seqs follow the last one.  Seqs strictly increase, so the issue rule
+// "every seq below the current tile's MMA window b(it) is dead" makes a load
+// into slot q % NWIN safe once q - NWIN < b(it).  (Reusing the previous
+// tile's c seq for a break's a lets a break tile issued two tiles ahead
+// overwrite a window its predecessor still gathers from.)
 struct WinSeq {
   int last = -1, pb = -1, pc = -1, ctr = 0;
   // returns the number of new windows (3 at a break, else 1)
@@ -633,9 +637,9 @@ struct WinSeq {
     const bool brk = last < 0 || tile != last + S;
     int nnew;
     if (brk) {
-      sa = pb + 1;
-      sb = pb + 2;
-      sc = pb + 3;
+      sa = ctr;
+      sb = ctr + 1;
+      sc = ctr + 2;
       nnew = 3;
     } else {
       sa = pb;
@@ -651,7 +655,7 @@ struct WinSeq {
   }
   // c of the next tile without advancing
   __device__ __forceinline__ int peek_c(int tile, int S) const {
-    return (last < 0 || tile != last + S) ? pb + 3 : ctr;
+    return (last < 0 || tile != last + S) ? ctr + 2 : ctr;
   }
 };
 

@@ -91,3 +91,28 @@ def test_c5_full_size_strip_windows_bitwise(capi, cuda):
             for k in env:
                 os.environ.pop(k, None)
     assert np.array_equal(ys[0], ys[1])
+
+
+def test_strip_windows_repeatable_on_break_heavy_grid(capi, oc, gnp, cuda):
+    # 250^2 over 148 CTAs: ~3 tiles per CTA, so most tiles are chunk starts
+    # that load three fresh windows while their predecessor still gathers.  A
+    # window-ring race shows up as run-to-run differences (and only
+    # sometimes as a tolerance failure), so the apply is repeated.
+    a0 = gnp.generate("c5_aniso9pt", 250, 1e-3, 30.0)
+    a = Csr(a0.n, np.array(a0.row_ptr), np.array(a0.col_idx), np.array(a0.values))
+    ah = oc.prescale(a, oc.gershgorin_gamma(a)).rounded_f32()
+    dims = (32, 32, 8)
+    p = f32(oc.init_params(*dims, 0))
+    b = oc.gaussian_vector(3, a.n)
+    os.environ["GNPC_PW_MIN_TILES"] = "0"
+    try:
+        c = capi.Csr.from_arrays(ah.n, ah.row_ptr, ah.col_idx, ah.values)
+        m = capi.Model(c, dims, p)
+        ys = [m.apply(b) for _ in range(12)]
+        assert c.layout_flags() & PW
+    finally:
+        os.environ.pop("GNPC_PW_MIN_TILES", None)
+    for y in ys[1:]:
+        assert np.array_equal(y, ys[0])
+    want = oc.gnn_apply(ah, dims, p, b)
+    assert rel_l2(ys[0], want) <= TOL and max_rel(ys[0], want) <= TOL

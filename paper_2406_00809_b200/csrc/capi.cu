@@ -641,7 +641,7 @@ void gnpc_csr_s::build_order(const std::vector<int>& hrp, const std::vector<int>
   // 28 KB of L1 beside the 198 KB ring cannot hold the three windows)
   if (const char* e = std::getenv("GNPC_TORDER"); !e || std::string(e) != "1") return;
   if (n_long != 0 || T < 4 * 148) return;
-  const int S = dominant_tile_stride(hrp, hci);
+  const int S = dominant_tile_stride(hrp, hci, 128);
   if (S < 2) return;
   std::vector<int> ord;
   ord.reserve(T);
@@ -654,9 +654,8 @@ void gnpc_csr_s::build_order(const std::vector<int>& hrp, const std::vector<int>
 // The tile distance S (>= 2) at which most off-tile columns sit (a row
 // window straddles two tiles, so distances S-1..S+1 count for S); 0 when no
 // distance holds >= 25 % of a row sample's entries.
-int gnpc_csr_s::dominant_tile_stride(const std::vector<int>& hrp, const std::vector<int>& hci) const {
+int gnpc_csr_s::dominant_tile_stride(const std::vector<int>& hrp, const std::vector<int>& hci, int TM) const {
   const std::int64_t n = h.n;
-  constexpr int TM = 128;
   // histogram of |tile distance| for off-tile entries of a row sample
   std::vector<std::int64_t> hist(4097, 0);
   std::int64_t total = 0;
@@ -670,17 +669,99 @@ int gnpc_csr_s::dominant_tile_stride(const std::vector<int>& hrp, const std::vec
     }
   }
   if (total == 0) return 0;
-  std::int64_t best = 0;
+  // the most frequent distance, then the entries within +-1 of it (an exact
+  // multiple of the tile is a spike; a stencil row offset of 128 S +- 1 rows
+  // spills into S - 1 and S + 1)
   int S = 0;
-  for (int d = 2; d <= 4095; ++d) {
-    const std::int64_t c = hist[d - 1] + hist[d] + hist[d + 1];
-    if (c > best) {
-      best = c;
-      S = d;
+  for (int d = 2; d <= 4095; ++d)
+    if (hist[d] > hist[S]) S = d;
+  if (S < 2) return 0;
+  const std::int64_t near = hist[S - 1] + hist[S] + hist[S + 1];
+  if (4 * near < total) return 0;  // no dominant stride: < 25 % of the entries
+  return S;
+}
+
+// Training strip windows (see DevCsr::tw): the batched layers' 128-row tile
+// holds npt = 128 / bs nodes (bs samples each); tile u gathers from the node
+// windows of tiles u - S, u, u + S, each extended by one node on either side
+// (npt + 2 nodes = 128 + 2 bs virtual rows).  Built per batch size, for
+// bs <= 32 (the window slot is sized for 192 rows).  GNPC_NO_TW=1 disables.
+void gnpc_csr_s::bind_tw(int bs, gnpk::DevCsr& d) const {
+  auto it = tws.find(bs);
+  const TwLayout* L = it != tws.end() && it->second->ok ? it->second.get() : nullptr;
+  d.tw = L ? L->sl.p : nullptr;
+  d.tw_off = L ? L->off.p : nullptr;
+  d.tw_k = L ? L->k.p : nullptr;
+  d.tw_order = L ? L->order.p : nullptr;
+  d.tw_S = L ? L->S : 0;
+}
+
+bool gnpc_csr_s::ensure_tw(int bs) {
+  if (auto it = tws.find(bs); it != tws.end()) return it->second->ok;
+  auto& L = tws[bs];
+  L = std::make_unique<TwLayout>();
+  if (const char* e = std::getenv("GNPC_NO_TW"); e && std::string(e) == "1") return false;
+  if (bs < 1 || bs > 32 || 128 % bs != 0) return false;
+  const std::int64_t n = h.n;
+  const int npt = 128 / bs, WN = npt + 2;  // nodes per window
+  const std::int64_t T = (n + npt - 1) / npt;
+  if (T < 4 * 148 || n >= (std::int64_t(1) << 31)) return false;
+  std::vector<int> hrp(n + 1), hci(h.nnz());
+  for (std::int64_t i = 0; i <= n; ++i) hrp[i] = static_cast<int>(h.row_ptr[i]);
+  for (std::int64_t k = 0; k < h.nnz(); ++k) hci[k] = static_cast<int>(h.col_idx[k]);
+  const int S = dominant_tile_stride(hrp, hci, npt);
+  if (S < 2) return false;
+  // node index in the windows (a, b, c) laid end to end at the ring's slot
+  // stride (kTwRowsMax rows = WS nodes per slot)
+  const int WS = gnpk::kTwRowsMax / bs;
+  auto widx = [&](std::int64_t t, std::int64_t c) -> int {
+    for (int w : {1, 0, 2}) {
+      const std::int64_t b0 = (t + (w - 1) * (std::int64_t)S) * npt - 1;
+      if (c >= b0 && c < b0 + WN) return w * WS + static_cast<int>(c - b0);
+    }
+    return -1;
+  };
+  constexpr int KMAX = gnpk::kTwKcap;
+  const int ST = (npt + 1 + 7) & ~7;  // int16 entry starts, padded to 16 bytes
+  std::vector<int> K(T), off(T);
+  std::int64_t total16 = 0;
+  for (std::int64_t t = 0; t < T; ++t) {
+    const std::int64_t n0 = t * npt, n1 = std::min(n, n0 + npt);
+    const int m = hrp[n1] - hrp[n0];
+    const int kr = (m + 7) & ~7;
+    if (kr > KMAX) return false;
+    for (int k = hrp[n0]; k < hrp[n1]; ++k)
+      if (widx(t, hci[k]) < 0) return false;
+    K[t] = kr;
+    off[t] = static_cast<int>(total16);
+    total16 += (2 * ST + 6 * kr) / 16;
+  }
+  std::vector<uint8_t> buf(std::max<std::int64_t>(total16 * 16, 16), 0);
+  for (std::int64_t t = 0; t < T; ++t) {
+    uint8_t* sl = buf.data() + (std::size_t)off[t] * 16;
+    uint16_t* st = reinterpret_cast<uint16_t*>(sl);
+    uint16_t* ri = st + ST;
+    float* vv = reinterpret_cast<float*>(sl + 2 * ST + 2 * K[t]);
+    const std::int64_t n0 = t * npt;
+    const int kb = hrp[n0];
+    for (int i = 0; i <= npt; ++i) st[i] = static_cast<uint16_t>(hrp[std::min(n, n0 + i)] - kb);
+    for (int k = kb; k < hrp[std::min(n, n0 + npt)]; ++k) {
+      ri[k - kb] = static_cast<uint16_t>(widx(t, hci[k]));
+      vv[k - kb] = static_cast<float>(h.values[k]);
     }
   }
-  if (S < 2 || 4 * best < total) return 0;  // no dominant stride: < 25 % of the entries
-  return S;
+  std::vector<int> ord;
+  ord.reserve(T);
+  for (int s0 = 0; s0 < S; ++s0)
+    for (std::int64_t t = s0; t < T; t += S) ord.push_back(static_cast<int>(t));
+  L->sl.upload(buf.data(), buf.size());
+  L->off.upload(off.data(), off.size());
+  L->k.upload(K.data(), K.size());
+  L->order.upload(ord.data(), ord.size());
+  L->S = S;
+  L->ok = true;
+  has_tw = true;
+  return true;
 }
 
 // Strip-window pair-union layout (see DevCsr::pw): tiles ordered in strips
@@ -700,7 +781,7 @@ void gnpc_csr_s::build_pw(const std::vector<int>& hrp, const std::vector<int>& h
   std::int64_t min_tiles = 4 * 148;
   if (const char* e = std::getenv("GNPC_PW_MIN_TILES")) min_tiles = std::atoll(e);
   if (T < min_tiles) return;
-  const int S = dominant_tile_stride(hrp, hci);
+  const int S = dominant_tile_stride(hrp, hci, 128);
   if (S < 2) return;
   // entry index: the row R = 144 w + r of the windows (a, b, c) laid end to
   // end, as the byte offset 128 R with the SWIZZLE_128B chunk bits of lane
@@ -811,6 +892,11 @@ gnpk::DevCsr gnpc_csr_s::dev() {
   d.wsell = has_win ? wsell.p : nullptr;
   d.wdesc = has_win ? wdesc.p : nullptr;
   d.torder = tstride ? torder.p : nullptr;
+  d.tw = nullptr;  // training layouts are per batch size: bind_tw
+  d.tw_off = nullptr;
+  d.tw_k = nullptr;
+  d.tw_order = nullptr;
+  d.tw_S = 0;
   d.pw = has_pw ? pw.p : nullptr;
   d.pw_off = has_pw ? pw_off.p : nullptr;
   d.pw_k = has_pw ? pw_k.p : nullptr;
@@ -1565,7 +1651,8 @@ int gnpc_csr_device_layout(gnpc_csr a, int* uploaded, int* sliced_ell, int* long
     need(a, "null csr");
     if (uploaded) *uploaded = a->dev_ready ? 1 : 0;
     if (sliced_ell)
-      *sliced_ell = (a->has_sell ? 1 : 0) | (a->has_pairs ? 2 : 0) | (a->has_pw ? 4 : 0) | (a->has_win ? 8 : 0);
+      *sliced_ell = (a->has_sell ? 1 : 0) | (a->has_pairs ? 2 : 0) | (a->has_pw ? 4 : 0) | (a->has_win ? 8 : 0) |
+                    (a->has_tw ? 16 : 0);
     if (long_rows) *long_rows = a->n_long;
   });
 }

@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <tuple>
@@ -188,6 +189,19 @@ struct gnpc_csr_s {
   gnpc_impl::DevBuf<int> pw_off, pw_k, pw_order;
   int pw_S = 0;
   bool has_pw = false;
+  // training strip windows (see DevCsr::tw), one layout per batch size (a
+  // training run's trainer and its monitor trainer may differ)
+  struct TwLayout {
+    gnpc_impl::DevBuf<uint8_t> sl;
+    gnpc_impl::DevBuf<int> off, k, order;
+    int S = 0;
+    bool ok = false;
+  };
+  std::map<int, std::unique_ptr<TwLayout>> tws;
+  bool has_tw = false;  // any batch size (introspection)
+  bool ensure_tw(int bs);
+  // the layout for batch size bs into d (null fields when not built)
+  void bind_tw(int bs, gnpk::DevCsr& d) const;
   // tile schedule of the TMA layers (see DevCsr::torder); tstride = the
   // dominant tile stride it was built from (0: round-robin, no order)
   gnpc_impl::DevBuf<int> torder;
@@ -201,7 +215,7 @@ struct gnpc_csr_s {
   void build_order(const std::vector<int>& hrp, const std::vector<int>& hci);
   void build_pairs(const std::vector<int>& hrp, const std::vector<int>& hci, const std::vector<float>& hv);
   void build_pw(const std::vector<int>& hrp, const std::vector<int>& hci, const std::vector<float>& hv);
-  int dominant_tile_stride(const std::vector<int>& hrp, const std::vector<int>& hci) const;
+  int dominant_tile_stride(const std::vector<int>& hrp, const std::vector<int>& hci, int TM) const;
   gnpk::DevCsr dev();
 };
 

@@ -68,6 +68,18 @@ struct DevCsr {
   const int* __restrict__ pw_k;
   const int* __restrict__ pw_order;
   int pw_S;
+  // Training strip windows (batched layers, bs samples per node, npt = 128/bs
+  // nodes per tile): tiles in strips of tw_S (tw_order); tile u gathers from
+  // the node windows of tiles u - S, u, u + S extended by one node (npt + 2
+  // nodes).  Slice at byte 16 tw_off[t]: uint16 starts[ST] (ST = npt+1
+  // rounded to 8: each node's first entry), uint16 node[K] (index in the
+  // three windows laid end to end, npt + 2 nodes each), float val[K];
+  // K = tw_k[t] (entries rounded to 8).
+  const uint8_t* __restrict__ tw;
+  const int* __restrict__ tw_off;
+  const int* __restrict__ tw_k;
+  const int* __restrict__ tw_order;
+  int tw_S;
   // Tile schedule of the TMA layer pipeline (apply path): nullptr = CTA b
   // takes tiles b, b + grid, ...; else CTA b takes positions
   // [b T / grid, (b+1) T / grid) of this permutation of the T tiles, ordered
@@ -83,6 +95,8 @@ constexpr int kWinBlocks = 8, kWinRows = 64, kWinDesc = 2 + kWinBlocks;
 // Row windows of the strip-ordered window mode (d = 32): a window of tile u is
 // rows [128u - kPwHalo, 128u + 128 + kPwHalo), one TMA box of kPwRows rows.
 constexpr int kPwHalo = 8, kPwRows = 128 + 2 * kPwHalo;
+// training strip windows: entries per tile (rounded to 8), window rows max (bs <= 32)
+constexpr int kTwKcap = 48, kTwRowsMax = 128 + 2 * 32;
 
 // Per-apply scalars produced by the norm kernel (scale sandwich,
 // src/gnn.cpp:128-139,191-199).

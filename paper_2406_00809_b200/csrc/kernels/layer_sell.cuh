@@ -106,7 +106,10 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 //          the same with a deeper ring for d = 32 non-last layers);
 // CSR = 1: the short-row CSR ranges of the tile (ragged matrices);
 // CSR = 2: training — B virtual rows per node (v = node*B + k), the full CSR
-//          ranges of the tile's 128/B nodes, plus a mask tile for the backward.
+//          ranges of the tile's 128/B nodes, plus a mask tile for the backward;
+// CSR = 10: training over strip windows (DevCsr::tw, d = 32): CSR 2's virtual
+//          rows with the X rows of the tile's neighbour nodes staged in shared
+//          memory by TMA (node windows along strips, one new per tile).
 template <int DP, int CSR = 0>
 struct SellCfg {
   // one CTA per SM: 16 math warps on one tile at a time (two 8-warp CTAs per
@@ -118,7 +121,7 @@ struct SellCfg {
 #ifndef GNPC_TR_PROD
 #define GNPC_TR_PROD 0  // measured neutral on C3 (19.34 ms either way)
 #endif
-  static constexpr int NPROD = (CSR == 7 || CSR == 8 || (CSR == 2 && GNPC_TR_PROD)) ? 1 : 0;
+  static constexpr int NPROD = (CSR == 7 || CSR == 8 || CSR == 10 || (CSR == 2 && GNPC_TR_PROD)) ? 1 : 0;
   // strip-window modes: the MMA work that does not need tile t's split —
   // X_hi·[U_lo; U_hi] and the projection of tile t-1 — is issued as soon as
   // the epilogues have read TMEM (efull), overlapping the split
@@ -190,26 +193,23 @@ struct SellCfg {
   // strip); 7 = non-last layers (4-deep ring), 8 = last layer (3 deep)
   static constexpr bool PW = CSR == 7 || CSR == 8;
   static_assert(!PW || DP == 32, "strip windows are a d = 32 layout");
+  static constexpr bool TW = CSR == 10;       // training strip windows
+  static_assert(!TW || DP == 32, "training strip windows are a d = 32 layout");
+  static constexpr bool WINS = PW || TW;      // the window ring + producer machinery
 #ifndef GNPC_NS_PW
 #define GNPC_NS_PW 4  // 3 measured slower (C5 409 vs 368 us)
 #endif
   static constexpr int NS = DP == 16 ? (CSRL ? GNPC_NS_CSR16 : (WIN ? 4 : GNPC_NS_SELL16))
                                      : (CSR == 2 ? GNPC_NS_TR32
                                                  : ((DEEP || CSR == 5) ? GNPC_NS_DEEP32
-                                                                       : ((CSR == 7 || CSR == 8) ? GNPC_NS_PW : 3)));
-  // windows alive: the MMA's window of the current tile plus NS - 1 tiles
-  // of lookahead (steady state: one new window per tile), and a strip break
-  // needs the MMA's window plus three fresh ones
+                                                                       : ((CSR == 7 || CSR == 8 || CSR == 10) ? GNPC_NS_PW : 3)));
   // windows alive: the MMA's window of the current tile plus NS - 1 tiles
   // of lookahead (steady state: one new window per tile); a break tile
   // issued right after its predecessor's gathers needs the MMA window b,
   // the predecessor's c and three fresh seqs: c - b = 4 < NWIN
-  static constexpr int NWIN = PW ? (NS + 1 > 5 ? NS + 1 : 5) : 0;
-  static constexpr uint32_t WINB = kPwRows * DP * 4;
-#ifndef GNPC_PW_PF
-#define GNPC_PW_PF 0  // 4 / 8 measured slower with the single control thread (C5 406 / 398 vs 368 us)
-#endif
-  static constexpr int PF = PW ? GNPC_PW_PF : 0;  // L2 prefetch distance (tiles)
+  static constexpr int NWIN = WINS ? (NS + 1 > 5 ? NS + 1 : 5) : 0;
+  // window slot: PW 144 rows (8-row halos), TW up to 128 + 2 bs rows (bs <= 32)
+  static constexpr uint32_t WINB = (TW ? kTwRowsMax : kPwRows) * DP * 4;
   // slices with K <= KCAP are staged; a multiple of US (the last round reads
   // up to round(K, US) words).  Kept small: every KB of shared memory is L1
   // the X-row gathers hit (C5 fused layer 531 -> 499 us going 24 -> 12)
@@ -234,7 +234,7 @@ struct SellCfg {
   static constexpr int TALLOC = 4 * DP;          // power of two >= 3 DP
   static constexpr uint32_t CVB = PW ? KCAP * (TM / 2) * 10 : KCAP * TM * 8;  // staged slice (bytes)
   // CSR: [X tile | row_ptr slice (TM+4 ints, 1 KiB) | col_idx (CAPC) | values (CAPC)]
-  static constexpr bool TR = CSR == 2;
+  static constexpr bool TR = CSR == 2 || CSR == 10;  // training (virtual rows, masks, ÂX out)
 #ifndef GNPC_CAPC16
 #define GNPC_CAPC16 2048
 #endif
@@ -248,7 +248,9 @@ struct SellCfg {
   // (written by the forward layer's epilogue), else the X_l tile itself
   static constexpr bool MBITS = GNPC_MBITS && TR && DP == 32;
   static constexpr uint32_t MASKB = MBITS ? TM * 4 : OPB;
-  static constexpr uint32_t O_MASK = OPB;
+  // TW slot: [mask words | window slice]; the X rows live in the windows
+  static constexpr uint32_t O_MASK = TW ? 0 : OPB;
+  static constexpr uint32_t O_TWS = MASKB;
   static constexpr uint32_t O_RP = TR ? OPB + MASKB : OPB, O_CI = O_RP + 1024, O_V = O_CI + CAPC * 4;
   // windowed: [kWinBlocks 64-row X blocks | slice]; the tile's own rows (the
   // MMA's X tile) are two consecutive blocks of the window
@@ -256,7 +258,8 @@ struct SellCfg {
   static constexpr uint32_t WB = WIN ? kWinBlocks * BLKB : 0;
   static constexpr uint32_t O_SL = WIN ? WB : (PW ? 0 : OPB);  // staged slice (sliced-ELL modes)
   static constexpr uint32_t SLOT =
-      CSRL ? ((O_V + CAPC * 4 + 1023) & ~1023u) : (((O_SL + CVB) + 1023) & ~1023u);
+      TW ? 1024u : (CSRL ? ((O_V + CAPC * 4 + 1023) & ~1023u) : (((O_SL + CVB) + 1023) & ~1023u));
+  static_assert(!TW || O_TWS + 2 * 40 + 6 * kTwKcap <= SLOT, "training window slice exceeds its ring slot");
   // layout (offsets from the 1024-aligned base)
   static constexpr uint32_t O_RING = 0;
   static constexpr uint32_t O_WIN = O_RING + NS * SLOT;   // strip windows [NWIN] (PW)
@@ -280,7 +283,7 @@ struct SellCfg {
     return (o_p(hidden, last) + (last ? (DP + 2) * hidden * 4 + 2 * NQ * TM * 4 : 0) + 15) & ~15u;
   }
   // PW: per-CTA schedule table (tile, K, slice offset) after the barriers
-  static constexpr int KSCHED = PW ? 256 : 0;
+  static constexpr int KSCHED = PW ? 256 : (TW ? 512 : 0);
   static size_t smem_bytes(int hidden, bool last) {
     // barriers + TMEM slot, the schedule, 1024-B alignment slack
     return o_bar(hidden, last) + 128 + 3 * KSCHED * 4 + 1024;
@@ -731,6 +734,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   const int n = nodes * bs;                  // (virtual) rows
   const int ntiles = (n + TM - 1) / TM;
   const int npt = TM / bs;                   // nodes per tile (training: bs divides TM)
+  const int lbs = __ffs(bs) - 1;             // log2(bs)
   const bool use_mask = KIND == 2 && tio->use_mask;
   const int H = net.hidden;
   float* D1 = p.D1;
@@ -766,7 +770,14 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   __syncthreads();
   // tile schedule: round-robin, or a contiguous chunk of the matrix's tile
   // order (a.torder, apply path) so consecutive tiles share X-row windows
-  const int* torder = TR ? nullptr : (C::PW ? a.pw_order : a.torder);
+  // window-mode arrays: the apply layout (pw) or the training layout (tw)
+  const int* w_k = C::TW ? a.tw_k : a.pw_k;
+  const int* w_off = C::TW ? a.tw_off : a.pw_off;
+  const uint8_t* w_sl = C::TW ? a.tw : a.pw;
+  const int w_S = C::TW ? a.tw_S : a.pw_S;
+  // rows of halo on either side of a window's own 128 rows: 8 (PW), one node (TW)
+  const int w_halo = C::TW ? bs : kPwHalo;
+  const int* torder = C::TW ? a.tw_order : (TR ? nullptr : (C::PW ? a.pw_order : a.torder));
   const int chunk0 = torder ? static_cast<int>(static_cast<long long>(blockIdx.x) * ntiles / gridDim.x) : 0;
   const int my_tiles =
       torder ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * ntiles / gridDim.x) - chunk0
@@ -777,13 +788,13 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   int* sch_t = p.sched;
   int* sch_k = p.sched + C::KSCHED;
   int* sch_o = p.sched + 2 * C::KSCHED;
-  const bool use_sched = C::PW && my_tiles <= C::KSCHED;
+  const bool use_sched = C::WINS && my_tiles <= C::KSCHED;
   if (use_sched) {
     for (int j = tid; j < my_tiles; j += C::NT) {
       const int t = __ldg(torder + chunk0 + j);
       sch_t[j] = t;
-      sch_k[j] = __ldg(a.pw_k + t);
-      sch_o[j] = __ldg(a.pw_off + t);
+      sch_k[j] = __ldg(w_k + t);
+      sch_o[j] = __ldg(w_off + t);
     }
     __syncthreads();
   }
@@ -875,53 +886,46 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       // strip windows (PW): tiles are issued in order while the slice ring
       // has room (j <= it + NS - 1) and the new windows' slots are free: every
       // window older than the current tile's MMA window b(it) is dead
-      // L2 prefetch of tile j's new window(s) and slice, C::PF tiles ahead of
-      // its ring load: DRAM latency is covered in L2, the ring only needs to
-      // cover L2 latency (the ring depth is what shared memory allows)
-      auto prefetch_pw = [&](int j) {
-        if (C::PF == 0 || j >= my_tiles) return;
-        const int t = tile_at(j);
-        const bool brk = j == 0 || t != tile_at(j - 1) + a.pw_S;
-        const int K = use_sched ? sch_k[j] : __ldg(a.pw_k + t);
-        const int off = use_sched ? sch_o[j] : __ldg(a.pw_off + t);
-        tc::bulk_prefetch_l2(a.pw + static_cast<size_t>(off) * 16, K * (TM / 2) * 10);
-        if (brk) {
-          tc::tma_prefetch_2d(mapxw, 0, (t - a.pw_S) * TM - kPwHalo);
-          tc::tma_prefetch_2d(mapxw, 0, t * TM - kPwHalo);
-        }
-        tc::tma_prefetch_2d(mapxw, 0, (t + a.pw_S) * TM - kPwHalo);
-      };
       WinSeq ws;   // issue side
       WinSeq wsb;  // MMA side: b(it) of the current tile
       int nxt = 0, bcur = 0;
+      // window box bytes (the TMA map's box: 128 + 2 halo rows)
+      const uint32_t winb = static_cast<uint32_t>(TM + 2 * w_halo) * DP * 4;
       auto issue_pw = [&](int j) {
         const int t = tile_at(j);
         int sa, sb, sc;
-        const int nnew = ws.next(t, a.pw_S, sa, sb, sc);
+        const int nnew = ws.next(t, w_S, sa, sb, sc);
         const int s = (rb + j) % NS;
         uint8_t* slot = p.ring + s * C::SLOT;
-        const int K = use_sched ? sch_k[j] : __ldg(a.pw_k + t);
-        const int off = use_sched ? sch_o[j] : __ldg(a.pw_off + t);
-        tc::mbar_expect_tx(&p.full[s], K * (TM / 2) * 10 + nnew * C::WINB);
-        tc::bulk_load_hint(slot, a.pw + static_cast<size_t>(off) * 16, K * (TM / 2) * 10, &p.full[s], pol_stream);
+        const int K = use_sched ? sch_k[j] : __ldg(w_k + t);
+        const int off = use_sched ? sch_o[j] : __ldg(w_off + t);
+        // slice bytes: pair-union 10 B x 64 pairs per entry; training: the
+        // node starts (ST = npt + 1 rounded to 8) plus 6 B per entry
+        const uint32_t slb = C::TW ? static_cast<uint32_t>(2 * (((TM / bs) + 1 + 7) & ~7) + 6 * K)
+                                   : static_cast<uint32_t>(K * (TM / 2) * 10);
+        const bool mk = C::TW && use_mask;
+        tc::mbar_expect_tx(&p.full[s], slb + nnew * winb + (mk ? C::MASKB : 0));
+        tc::bulk_load_hint(slot + (C::TW ? C::O_TWS : 0), w_sl + static_cast<size_t>(off) * 16, slb, &p.full[s],
+                           pol_stream);
+        if constexpr (C::TW) {
+          if (mk) tc::bulk_load(slot + C::O_MASK, tio->mask_in + static_cast<size_t>(t) * TM, C::MASKB, &p.full[s]);
+        }
         auto load_win = [&](int q, int u) {
-          tc::tma_load_2d_hint(p.win + (q % C::NWIN) * C::WINB, mapxw, 0, u * TM - kPwHalo, &p.full[s], pol_keep);
+          tc::tma_load_2d_hint(p.win + (q % C::NWIN) * C::WINB, mapxw, 0, u * TM - w_halo, &p.full[s], pol_keep);
         };
         if (nnew == 3) {
-          load_win(sa, t - a.pw_S);
+          load_win(sa, t - w_S);
           load_win(sb, t);
         }
-        load_win(sc, t + a.pw_S);
-        prefetch_pw(j + C::PF);
+        load_win(sc, t + w_S);
       };
       auto issue_more = [&](int it) {  // after afull(it) (it = -1: prologue)
         const int prot = it >= 0 ? bcur : 0;
-        while (nxt < my_tiles && nxt <= it + NS - 1 && ws.peek_c(tile_at(nxt), a.pw_S) - prot < C::NWIN)
+        while (nxt < my_tiles && nxt <= it + NS - 1 && ws.peek_c(tile_at(nxt), w_S) - prot < C::NWIN)
           issue_pw(nxt++);
       };
-      if constexpr (C::PW) {
+      if constexpr (C::WINS) {
         if (producer) {
-          for (int j = NS - 1; j < C::PF; ++j) prefetch_pw(j);  // those the first issues do not reach
           issue_more(-1);
           for (int it = 0; it < my_tiles && nxt < my_tiles; ++it) {
             // MMA(it) issued: tile it's gathers are done, its window b(it) in use
@@ -932,7 +936,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
               __nanosleep(32);
             }
             int sa, sc;
-            wsb.next(tile_at(it), a.pw_S, sa, bcur, sc);
+            wsb.next(tile_at(it), w_S, sa, bcur, sc);
             issue_more(it);
           }
         }
@@ -956,7 +960,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       const uint32_t sBstk = tc::smem_u32(p.Bs);
       const uint32_t sA2hi = tc::smem_u32(p.A), sA2lo = sA2hi + C::OPB;
       const uint32_t tAlo = p.tmem + C::alo_col(TCP);
-      const uint32_t sXe0 = tc::smem_u32(p.win) + kPwHalo * DP * 4;
+      const uint32_t sXe0 = tc::smem_u32(p.win) + w_halo * DP * 4;
       auto proj_mma = [&](int t1) {  // projection of tile t1 (its relu'd rows hi / lo in TMEM)
         // Dp[:, 0:H] = Y_hi·D1_lo, Dp[:, H:2H] = Y_hi·D1_hi + Y_lo·D1_hi
         const uint32_t tYh = p.tmem + C::ycol((mb + t1) & 1), tYl = tYh + DP;  // A from TMEM
@@ -981,9 +985,9 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
             tc::mbar_wait_dbg(&p.full[r % NS], (r / NS) & 1, 6, it);
             tc::fence_after();
             uint32_t sX = tc::smem_u32(p.ring + (r % NS) * C::SLOT);
-            if constexpr (C::PW) {
+            if constexpr (C::WINS) {
               int sa, sc;
-              wsb.next(tile_at(it), a.pw_S, sa, bcur, sc);
+              wsb.next(tile_at(it), w_S, sa, bcur, sc);
               sX = sXe0 + (bcur % C::NWIN) * C::WINB;
             }
 #pragma unroll
@@ -1003,10 +1007,10 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         }
         if (it < my_tiles) {
           uint32_t sX = tc::smem_u32(p.ring + ((rb + it) % NS) * C::SLOT);
-          if constexpr (C::PW) {  // the tile's own rows: window b(it) past its halo
+          if constexpr (C::WINS) {  // the tile's own rows: window b(it) past its halo
             if constexpr (!C::EARLY) {
               int sa, sc;
-              wsb.next(tile_at(it), a.pw_S, sa, bcur, sc);
+              wsb.next(tile_at(it), w_S, sa, bcur, sc);
             }
             sX = sXe0 + (bcur % C::NWIN) * C::WINB;
           }
@@ -1280,12 +1284,12 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
     float4 acc[R];
     uint32_t wbase = 0;  // PW: shared address of window a; b, c follow (wrapped in the ring)
     const uint32_t wring0 = tc::smem_u32(p.win);
-    if constexpr (C::PW) {
+    if constexpr (C::WINS) {
       if (have) {
         int sq[3];
-        wsm.next(tile, a.pw_S, sq[0], sq[1], sq[2]);
+        wsm.next(tile, w_S, sq[0], sq[1], sq[2]);
         wbase = wring0 + (sq[0] % C::NWIN) * C::WINB;
-        wtile = p.win + (sq[1] % C::NWIN) * C::WINB + kPwHalo * DP * 4;
+        wtile = p.win + (sq[1] % C::NWIN) * C::WINB + w_halo * DP * 4;
       }
     }
     if (have) {
@@ -1304,7 +1308,33 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           acc[j] = ldg4(axlong + static_cast<size_t>(i) * DP + 4 * gl);
       }
       tc::mbar_wait_dbg(&p.full[r % NS], (r / NS) & 1, 3, it);
-      if constexpr (TR) {
+      if constexpr (C::TW) {
+        // training strip windows: the group's two rows are samples k0, k0 + 1
+        // of one node; each entry names a neighbour node's block (bs rows) in
+        // the three windows laid end to end (slot stride WINB), so its rows
+        // are at wbase + node * bs * 128 + (k0 + j) * 128, swizzled by row
+        const int ST = (npt + 1 + 7) & ~7;
+        const int Kt = use_sched ? sch_k[it] : __ldg(a.tw_k + tile);
+        const uint16_t* st16 = reinterpret_cast<const uint16_t*>(slot + C::O_TWS);
+        const uint16_t* ri = st16 + ST;
+        const float* vv = reinterpret_cast<const float*>(slot + C::O_TWS + 2 * ST + 2 * Kt);
+        const int v0 = row0 + R * gid;
+        const int ln = (v0 >> lbs) - tile * npt, k0 = v0 & (bs - 1);
+        const int e0 = st16[ln], e1 = v0 < n ? st16[ln + 1] : e0;
+        const uint32_t nb = static_cast<uint32_t>(bs) * DP * 4;
+        const uint32_t wlim = wring0 + C::NWIN * C::WINB, wring = C::NWIN * C::WINB;
+        uint32_t off[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          off[j] = (k0 + j) * (DP * 4) + ((gl ^ ((k0 + j) & 7)) << 4);
+        for (int e = e0; e < e1; ++e) {
+          uint32_t b0 = wbase + ri[e] * nb;
+          b0 = b0 >= wlim ? b0 - wring : b0;
+          const float w = vv[e];
+#pragma unroll
+          for (int j = 0; j < R; ++j) fma4(acc[j], w, tc::lds4(b0 + off[j]));
+        }
+      } else if constexpr (TR) {
         // virtual row v = node*bs + k gathers X rows (col*bs + k) of node's
         // neighbours: one staged (col, val) list serves the node's bs rows
         const int n0 = tile * npt;
@@ -1317,7 +1347,8 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
 #pragma unroll
         for (int j = 0; j < R; ++j) {
           const int v = row0 + R * gid + j;
-          const int node = min(v, n - 1) / bs, k = min(v, n - 1) - node * bs;
+          // bs divides 128: a power of two (shift/mask, no integer division)
+          const int vv = min(v, n - 1), node = vv >> lbs, k = vv & (bs - 1);
           const int ln = node - n0;
           const int e0 = rpt[ln], e1 = rpt[ln + 1];
           sj[j] = st ? e0 - a0 : e0;
@@ -1411,7 +1442,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         const int q = warp & 3, cq = warp >> 2, m = 32 * q + lane;
         const uint8_t* xtile = slot;
         if constexpr (C::WIN) xtile += __ldg(a.wdesc + static_cast<size_t>(tile) * kWinDesc + 1) * C::BLKB;
-        if constexpr (C::PW) xtile = wtile;
+        if constexpr (C::WINS) xtile = wtile;
         float lo[CW];
 #pragma unroll
         for (int c = 0; c < CW; c += 4) {
@@ -1459,16 +1490,18 @@ k_layer_sell(DevCsr a, const __grid_constant__ SellMaps maps, const float* __res
 // samples of a node are adjacent virtual rows; bs must divide 128.
 struct TrainMaps {
   CUtensorMap x, y, ax, mask;
+  CUtensorMap xw;  // the gathered input, box {DP, 128 + 2 bs} (training strip windows)
 };
 
-template <int DP, int KIND>
-__global__ void __launch_bounds__(SellCfg<DP, 2>::NT, 1)
+template <int DP, int KIND, int CSR = 2>
+__global__ void __launch_bounds__(SellCfg<DP, CSR>::NT, 1)
 k_train_sell(DevCsr a, const __grid_constant__ TrainMaps maps, const float* __restrict__ X,
              const float* __restrict__ uwp, NetView net, int bs, int use_mask,
              const uint32_t* __restrict__ mask_in, uint8_t* __restrict__ mask_out) {
-  auto p = sell_setup<DP, 2>(net.hidden, false);
+  auto p = sell_setup<DP, CSR>(net.hidden, false);
   const TrainIO tio{&maps.ax, &maps.mask, bs, use_mask, mask_in, mask_out};
-  sell_layer<DP, false, float, 2, KIND>(p, a, &maps.x, &maps.y, X, nullptr, uwp, net, 1.0, nullptr, &tio);
+  sell_layer<DP, false, float, CSR, KIND>(p, a, &maps.x, &maps.y, X, nullptr, uwp, net, 1.0, nullptr, &tio,
+                                          &maps.xw);
   sell_teardown(p);
 }
 

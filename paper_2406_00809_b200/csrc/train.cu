@@ -63,6 +63,11 @@ struct gnpc_trainer_s {
   DevBuf<uint32_t> mbits;
   std::size_t nvpad = 0;
   CUtensorMap mG[2]{};
+  // training strip windows (d = 32, DevCsr::tw on Â and Âᵀ): window maps
+  // (box 128 + 2B rows) over the gathered inputs X_l (forward) and G (backward)
+  bool tw = false;
+  std::vector<CUtensorMap> mXw;
+  CUtensorMap mGw[2]{};
   // batch
   DevBuf<double> xb, bb, out, sgn, gout, colpart, losspart, tmp;
   DevBuf<gnpk::SampleScales> scl;
@@ -277,6 +282,39 @@ struct TrainLaunch {
     gnpc_csr_s& A = fwd ? *T.m->a : *T.At;
     gnpk::DevCsr a = A.dev();
     if constexpr (DP == 16 || DP == 32) {
+      if constexpr (DP == 32) {
+        if (T.tw) {  // strip windows: the gathered rows staged by TMA along strips
+          A.bind_tw(T.B, a);
+          using S = gnpk::SellCfg<32, 10>;
+          const size_t smem = S::smem_bytes(T.H, false);
+          auto kern = fwd ? gnpk::k_train_sell<32, 1, 10> : gnpk::k_train_sell<32, 2, 10>;
+          set_smem_once((const void*)kern, smem);
+          const int tiles = (T.nv + S::TM - 1) / S::TM;
+          const int grid = std::max(1, std::min(tiles, T.sms));
+          gnpk::TrainMaps maps;
+          if (fwd) {
+            maps.x = T.mX[l];
+            maps.y = T.mX[l + 1];
+            maps.ax = T.mAX[l];
+            maps.mask = T.mX[l];
+            maps.xw = T.mXw[l];
+          } else {
+            maps.x = T.mG[gi];
+            maps.y = T.mG[1 - gi];
+            maps.ax = T.mG[gi];
+            maps.mask = T.mX[l];
+            maps.xw = T.mGw[gi];
+          }
+          const float* uwp = (fwd ? T.m->UWP.p : T.UWP_bwd.p) + (size_t)l * 4 * DP * DP;
+          const uint32_t* min_ = nullptr;
+          uint8_t* mout = nullptr;
+          if (fwd && l + 1 <= T.L - 1) mout = reinterpret_cast<uint8_t*>(T.mbits.p + (size_t)(l + 1) * T.nvpad);
+          if (!fwd && mask != nullptr) min_ = T.mbits.p + (size_t)l * T.nvpad;
+          kern<<<grid, S::NT, smem, T.s>>>(a, maps, X, uwp, T.m->view, T.B, mask != nullptr ? 1 : 0, min_, mout);
+          GNPC_LAUNCHED();
+          return;
+        }
+      }
       if (T.sell) {
         using S = gnpk::SellCfg<DP, 2>;
         const size_t smem = S::smem_bytes(T.H, false);
@@ -595,6 +633,12 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
     for (int l = 0; l <= T->L; ++l) T->mX.push_back(make_rows_map(T->Xs.p + l * act, T->nv, T->dp, 128, sw));
     for (int l = 0; l < T->L; ++l) T->mAX.push_back(make_rows_map(T->AXs.p + l * act, T->nv, T->dp, 128, sw));
     for (int g = 0; g < 2; ++g) T->mG[g] = make_rows_map(T->G[g].p, T->nv, T->dp, 128, sw);
+    if (T->dp == 32 && gnpk::SellCfg<32, 10>::MBITS && T->m->a->ensure_tw(T->B) && T->At->ensure_tw(T->B)) {
+      T->tw = true;
+      const int wr = 128 + 2 * T->B;
+      for (int l = 0; l <= T->L; ++l) T->mXw.push_back(make_rows_map(T->Xs.p + l * act, T->nv, T->dp, wr, sw));
+      for (int g = 0; g < 2; ++g) T->mGw[g] = make_rows_map(T->G[g].p, T->nv, T->dp, wr, sw);
+    }
     if (gnpk::SellCfg<32, 2>::MBITS && T->dp == 32) {
       T->nvpad = ((std::size_t)T->nv + 127) / 128 * 128;
       T->mbits.alloc(T->nvpad * T->L);

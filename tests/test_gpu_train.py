@@ -2,6 +2,8 @@
 the oracle.  The device computes in fp32 (tf32x3 on the tensor cores for
 d = 16/32) with f64 reductions; tolerance per parameter tensor, norm-wise:
 1e-4 for gradients (north_star's GNP bar), tighter for the loss."""
+import os
+
 import numpy as np
 import pytest
 from conftest import csr_of, f32, golden, rel_l2
@@ -290,3 +292,31 @@ def test_trained_model_refuses_apply_until_synced(capi, oc, cuda):
     y = m.apply(b)
     want = oc.gnn_apply(a, dims, t.params(), b)
     assert rel_l2(y, want) <= 1e-4
+
+
+def test_training_strip_windows_match_csr_layers(capi, oc, cuda):
+    # d = 32, B = 32 on a 160^2 var-coeff grid (25,600 nodes = 6,400 tiles of
+    # 4 nodes; the grid-line offset is 40 tiles): the training layers over
+    # strip windows (node windows staged by TMA) against the CSR layers
+    # (GNPC_NO_TW=1).  Each virtual row sums its node's entries in stored order
+    # either way and the MMAs are the same, so loss and gradients are equal.
+    a = oc.prescale(oc.gen_named("c3_varcoeff2d", 160, 2.0, 0.0, 2), 8.0).rounded_f32()
+    dims = (32, 32, 8)
+    p = f32(oc.init_params(*dims, 1))
+    x, b = oc.gaussian_batch(a, 32, 0, 32)
+    outs = []
+    for off in ("0", "1"):
+        os.environ["GNPC_NO_TW"] = off
+        try:
+            A = dev_csr(capi, a)
+            t = capi.Trainer(capi.Model(A, dims, p), 32)
+            loss, g, _ = t.forward_backward(x, b)
+            flags = A.layout_flags()
+            steps = [t.step(x, b) for _ in range(3)]
+        finally:
+            os.environ.pop("GNPC_NO_TW", None)
+        assert bool(flags & 16) == (off == "0"), flags
+        outs.append((loss, np.array(g), steps))
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]

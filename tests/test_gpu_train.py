@@ -294,13 +294,16 @@ def test_trained_model_refuses_apply_until_synced(capi, oc, cuda):
     assert rel_l2(y, want) <= 1e-4
 
 
-def test_training_strip_windows_match_csr_layers(capi, oc, cuda):
-    # d = 32, B = 32 on a 160^2 var-coeff grid (25,600 nodes = 6,400 tiles of
-    # 4 nodes; the grid-line offset is 40 tiles): the training layers over
-    # strip windows (node windows staged by TMA) against the CSR layers
-    # (GNPC_NO_TW=1).  Each virtual row sums its node's entries in stored order
+@pytest.mark.parametrize("grid,tw", [(160, True), (157, True), (158, False)])
+def test_training_strip_windows_match_csr_layers(capi, oc, cuda, grid, tw):
+    # d = 32, B = 32 on var-coeff grids: 160^2 (25,600 nodes = 6,400 tiles of
+    # 4 nodes, grid-line offset 40 tiles), 157^2 (offset 39 tiles + 1 node,
+    # inside the one-node halo; a partial last tile) and 158^2 (39 tiles + 2
+    # nodes: outside the halo, so the CSR layers run).  The training layers
+    # over strip windows (node windows staged by TMA) against the CSR layers
+    # (GNPC_NO_TW=1): each virtual row sums its node's entries in stored order
     # either way and the MMAs are the same, so loss and gradients are equal.
-    a = oc.prescale(oc.gen_named("c3_varcoeff2d", 160, 2.0, 0.0, 2), 8.0).rounded_f32()
+    a = oc.prescale(oc.gen_named("c3_varcoeff2d", grid, 2.0, 0.0, 2), 8.0).rounded_f32()
     dims = (32, 32, 8)
     p = f32(oc.init_params(*dims, 1))
     x, b = oc.gaussian_batch(a, 32, 0, 32)
@@ -315,7 +318,7 @@ def test_training_strip_windows_match_csr_layers(capi, oc, cuda):
             steps = [t.step(x, b) for _ in range(3)]
         finally:
             os.environ.pop("GNPC_NO_TW", None)
-        assert bool(flags & 16) == (off == "0"), flags
+        assert bool(flags & 16) == (off == "0" and tw), flags
         outs.append((loss, np.array(g), steps))
     assert outs[0][0] == outs[1][0]
     assert np.array_equal(outs[0][1], outs[1][1])

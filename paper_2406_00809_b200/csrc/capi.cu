@@ -106,11 +106,9 @@ struct ApplyLaunch {
       // DP=16 only: at DP=32 the in-kernel layers measured slower than
       // separate launches (C5: 499 vs 450 us per layer) while DP=16 gains
       // (C2: 17 vs 24 us per layer: no launch gap or prologue per layer)
-      // pipeline mode: 3 windowed sliced-ELL (d = 16), 0 sliced-ELL, 1 CSR ranges
-      const int mode = (DP == 16 && a.wdesc) ? 3 : (a.sell ? 0 : 1);
+      // pipeline mode: 0 sliced-ELL, 1 CSR ranges
+      const int mode = a.sell ? 0 : 1;
       auto smem_of = [&](int md, bool last) -> size_t {
-        if constexpr (DP == 16)
-          if (md == 3) return SellCfg<16, 3>::smem_bytes(net.hidden, last);
         return md == 0 ? SellCfg<DP, 0>::smem_bytes(net.hidden, last) : SellCfg<DP, 1>::smem_bytes(net.hidden, last);
       };
       const bool fits = smem_of(mode, true) <= 226 * 1024;
@@ -118,9 +116,7 @@ struct ApplyLaunch {
           n > 0) {
         using S = SellCfg<DP, false>;
         const size_t smem = smem_of(mode, true);
-        auto kern = mode == 1 ? k_apply_sell<DP, InT, OutT, 1>
-                              : (mode == 3 ? k_apply_sell<DP, InT, OutT, (DP == 16 ? 3 : 0)>
-                                           : k_apply_sell<DP, InT, OutT, 0>);
+        auto kern = mode == 1 ? k_apply_sell<DP, InT, OutT, 1> : k_apply_sell<DP, InT, OutT, 0>;
         {
           cudaFuncAttributes fa{};
           GNPC_CUDA(cudaFuncGetAttributes(&fa, (const void*)kern));  // static smem counts against 227 KB
@@ -227,25 +223,20 @@ struct ApplyLaunch {
         }
       }
       if constexpr (DP == 16 || DP == 32) {
-        const int lmode = (DP == 16 && a.wdesc && A.n_long == 0) ? 3 : (a.sell ? 0 : 1);
-        const size_t smem = lmode == 3 ? SellCfg<DP, (DP == 16 ? 3 : 0)>::smem_bytes(net.hidden, last)
-                                       : (lmode == 0 ? SellCfg<DP, 0>::smem_bytes(net.hidden, last)
-                                                     : SellCfg<DP, 1>::smem_bytes(net.hidden, last));
+        const int lmode = a.sell ? 0 : 1;
+        const size_t smem = lmode == 0 ? SellCfg<DP, 0>::smem_bytes(net.hidden, last)
+                                       : SellCfg<DP, 1>::smem_bytes(net.hidden, last);
         const bool sell_fits = smem <= 227 * 1024;
         if (m.use_tc && !sell_off && sell_fits) {
-          // TMA pipeline, one 544-thread CTA per SM: windowed or plain
-          // sliced-ELL slices on regular matrices, the short-row CSR ranges
-          // on ragged ones
+          // TMA pipeline, one 544-thread CTA per SM: sliced-ELL slices on
+          // regular matrices, the short-row CSR ranges on ragged ones
           using S = SellCfg<DP, false>;
-          constexpr int W = DP == 16 ? 3 : 0;
           // d = 32 non-last sliced-ELL layers: the 4-deep ring (mode 4)
           constexpr int D4 = DP == 32 ? 4 : 0;
           const bool deep = DP == 32 && lmode == 0 && !last;
           auto kern = lmode == 1 ? (last ? k_layer_sell<DP, true, OutT, 1> : k_layer_sell<DP, false, OutT, 1>)
-                                 : (lmode == 3 ? (last ? k_layer_sell<DP, true, OutT, W> : k_layer_sell<DP, false, OutT, W>)
-                                               : (last ? k_layer_sell<DP, true, OutT>
-                                                       : (deep ? k_layer_sell<DP, false, OutT, D4>
-                                                               : k_layer_sell<DP, false, OutT>)));
+                                 : (last ? k_layer_sell<DP, true, OutT>
+                                         : (deep ? k_layer_sell<DP, false, OutT, D4> : k_layer_sell<DP, false, OutT>));
           const size_t smem_l = deep ? SellCfg<DP, D4>::smem_bytes(net.hidden, false) : smem;
           set_smem_attr((const void*)kern, 227 * 1024);
           const int tiles_s = (n + S::TM - 1) / S::TM;
@@ -492,47 +483,6 @@ void gnpc_csr_s::build_sell(const std::vector<int>& hrp, const std::vector<int>&
   sell_off.upload(off.data(), off.size());
   sell_k.upload(K.data(), K.size());
   has_sell = true;
-  // windows: every tile's columns (and its own rows, the MMA's X tile) within
-  // at most kWinBlocks 64-row blocks, no long rows
-  // opt-in (GNPC_WIN=1): measured slower on C2 (34 vs 24 us per d = 16 layer:
-  // the 32 KB of window blocks per tile arrive slower than the L1-cached gathers)
-  if (const char* e = std::getenv("GNPC_WIN"); !e || std::string(e) != "1") return;
-  if (n_long != 0) return;
-  constexpr int BR = gnpk::kWinRows, NB = gnpk::kWinBlocks, WD = gnpk::kWinDesc;
-  std::vector<int> desc((std::size_t)ntiles * WD, 0);
-  std::vector<int2> went(ent.size());
-  std::vector<int> blocks;
-  for (std::int64_t t = 0; t < ntiles; ++t) {
-    const int kt = K[t] & 0xffff;
-    blocks.clear();
-    const int own = (int)(t * TM / BR);
-    blocks.push_back(own);
-    blocks.push_back(own + 1);
-    const int rows = (int)std::min<std::int64_t>(TM, n - t * TM);  // rows past n: padding only
-    for (int k = 0; k < kt; ++k)
-      for (int r = 0; r < rows; ++r) blocks.push_back(ent[off[t] + (std::size_t)k * TM + r].x / BR);
-    std::sort(blocks.begin(), blocks.end());
-    blocks.erase(std::unique(blocks.begin(), blocks.end()), blocks.end());
-    if ((int)blocks.size() > NB) return;  // not windowed
-    int* d = desc.data() + t * WD;
-    d[0] = (int)blocks.size();
-    d[1] = (int)(std::lower_bound(blocks.begin(), blocks.end(), own) - blocks.begin());
-    for (std::size_t i = 0; i < blocks.size(); ++i) d[2 + i] = blocks[i];
-    for (int k = 0; k < kt; ++k)
-      for (int r = 0; r < TM; ++r) {
-        const std::size_t q = off[t] + (std::size_t)k * TM + r;
-        if (r >= rows) {
-          went[q] = make_int2(d[1] * BR, 0);
-          continue;
-        }
-        const int c = ent[q].x;
-        const int slot = (int)(std::lower_bound(blocks.begin(), blocks.end(), c / BR) - blocks.begin());
-        went[q] = make_int2(slot * BR + c % BR, ent[q].y);
-      }
-  }
-  wsell.upload(went.data(), went.size());
-  wdesc.upload(desc.data(), desc.size());
-  has_win = true;
 }
 
 // Pair-union sliced-ELL (see DevCsr::psell).  Built for matrices without long
@@ -889,8 +839,6 @@ gnpk::DevCsr gnpc_csr_s::dev() {
   d.sell = has_sell ? sell.p : nullptr;
   d.sell_off = has_sell ? sell_off.p : nullptr;
   d.sell_k = has_sell ? sell_k.p : nullptr;
-  d.wsell = has_win ? wsell.p : nullptr;
-  d.wdesc = has_win ? wdesc.p : nullptr;
   d.torder = tstride ? torder.p : nullptr;
   d.tw = nullptr;  // training layouts are per batch size: bind_tw
   d.tw_off = nullptr;
@@ -1138,9 +1086,8 @@ void gnpc_model_s::ensure_workspace() {
       if (tm_base[c] != X[c].p) {
         tmX[c] = make_rows_map(X[c].p, (std::int64_t)n, dp, 128,
                                dp == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
-        // windows: 64-row blocks (d = 16 windowed sliced-ELL) or the strip
-        // windows' halo-extended tiles (d = 32)
-        tmXw[c] = make_rows_map(X[c].p, (std::int64_t)n, dp, dp == 32 ? gnpk::kPwRows : gnpk::kWinRows,
+        // the strip windows' halo-extended tiles (d = 32; unused at d = 16)
+        tmXw[c] = make_rows_map(X[c].p, (std::int64_t)n, dp, dp == 32 ? gnpk::kPwRows : 128,
                                 dp == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
         tm_base[c] = X[c].p;
       }
@@ -1151,9 +1098,8 @@ bool gnpc_model_s::fused_eligible() {
   a->upload();
   if (dp != 16 || !use_tc || a->n_long != 0 || a->h.n == 0) return false;
   if (gnpc_impl::sell_kernel_off() || gnpc_impl::fused_apply_off()) return false;
-  const size_t smem = a->has_win    ? gnpk::SellCfg<16, 3>::smem_bytes(dims.hidden, true)
-                      : a->has_sell ? gnpk::SellCfg<16, 0>::smem_bytes(dims.hidden, true)
-                                    : gnpk::SellCfg<16, 1>::smem_bytes(dims.hidden, true);
+  const size_t smem = a->has_sell ? gnpk::SellCfg<16, 0>::smem_bytes(dims.hidden, true)
+                                  : gnpk::SellCfg<16, 1>::smem_bytes(dims.hidden, true);
   return smem <= 226 * 1024;
 }
 
@@ -1575,6 +1521,11 @@ int gnpc_synchronize(void) {
     GNPC_CUDA(cudaDeviceSynchronize());
   });
 }
+#ifdef GNPC_TILE_TRACE
+extern "C" int gnpc_debug_tile_trace(unsigned long long* out) {  // 64 x 16 stamps (debug builds only)
+  return cudaMemcpyFromSymbol(out, gnpk::g_trace, sizeof(unsigned long long) * 64 * 16) == cudaSuccess ? 0 : 1;
+}
+#endif
 int gnpc_launch_count(int64_t* count) {
   return guarded([&] {
     need(count, "null count");
@@ -1651,7 +1602,7 @@ int gnpc_csr_device_layout(gnpc_csr a, int* uploaded, int* sliced_ell, int* long
     need(a, "null csr");
     if (uploaded) *uploaded = a->dev_ready ? 1 : 0;
     if (sliced_ell)
-      *sliced_ell = (a->has_sell ? 1 : 0) | (a->has_pairs ? 2 : 0) | (a->has_pw ? 4 : 0) | (a->has_win ? 8 : 0) |
+      *sliced_ell = (a->has_sell ? 1 : 0) | (a->has_pairs ? 2 : 0) | (a->has_pw ? 4 : 0) |
                     (a->has_tw ? 16 : 0);
     if (long_rows) *long_rows = a->n_long;
   });

@@ -173,10 +173,6 @@ struct gnpc_csr_s {
   gnpc_impl::DevBuf<int2> sell;
   gnpc_impl::DevBuf<int> sell_off, sell_k;
   bool has_sell = false;
-  // windowed sliced-ELL (see DevCsr::wsell)
-  gnpc_impl::DevBuf<int2> wsell;
-  gnpc_impl::DevBuf<int> wdesc;
-  bool has_win = false;
   // padded short-row CSR + per-tile long flags for the TMA CSR layer (see DevCsr)
   gnpc_impl::DevBuf<int> rps, cis, tflag;
   gnpc_impl::DevBuf<float> vs;

@@ -36,14 +36,6 @@ struct DevCsr {
   const int* __restrict__ cis;
   const float* __restrict__ vs;
   const int* __restrict__ tflag;
-  // Windowed sliced-ELL (d = 16 apply, matrices without long rows whose
-  // tiles each reference at most kWinBlocks 64-row blocks of X, e.g.
-  // stencils): wdesc[t*kWinDesc] = {nblk, xslot, blk_0 .. blk_7} (sorted
-  // block ids; xslot = position of the tile's own first block), wsell = the
-  // sell entries with the column replaced by its row in the tile's staged
-  // window (slot i*64 + col%64).  nullptr when not built.
-  const int2* __restrict__ wsell;
-  const int* __restrict__ wdesc;
   // Pair-union sliced-ELL (d = 32 apply, stencil-like matrices without long
   // rows): the two adjacent rows (2g, 2g+1) of a 128-row tile share one entry
   // list, the sorted union of their columns, with one weight per row (0 where
@@ -91,7 +83,6 @@ struct DevCsr {
   // L2-resident while Â streams past it; 0 = evict_normal everywhere.
   int l2hint;
 };
-constexpr int kWinBlocks = 8, kWinRows = 64, kWinDesc = 2 + kWinBlocks;
 // Row windows of the strip-ordered window mode (d = 32): a window of tile u is
 // rows [128u - kPwHalo, 128u + 128 + kPwHalo), one TMA box of kPwRows rows.
 constexpr int kPwHalo = 8, kPwRows = 128 + 2 * kPwHalo;

@@ -100,8 +100,6 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 
 }  // namespace tc
 
-// CSR = 3: windowed sliced-ELL (d = 16): the tile's X rows arrive as up to
-//          kWinBlocks 64-row blocks (TMA) and the gathers read shared memory;
 // CSR = 0: sliced-ELL slices (k_layer_sell on regular matrices; CSR = 4:
 //          the same with a deeper ring for d = 32 non-last layers);
 // CSR = 1: the short-row CSR ranges of the tile (ragged matrices);
@@ -134,6 +132,8 @@ struct SellCfg {
 #ifndef GNPC_TW_EARLY
 #define GNPC_TW_EARLY 1  // C3 18.18 -> 18.02 ms
 #endif
+  // (measured neutral to slower on the d = 16 sliced-ELL / CSR layers: C2
+  // 4820 vs 4980 applies/s, C4 unchanged, so those keep the plain order)
   static constexpr bool EARLY = ((CSR == 7 || CSR == 8) && GNPC_PW_EARLY) || (CSR == 2 && GNPC_TR_EARLY) ||
                                 (CSR == 10 && GNPC_TW_EARLY);
   static constexpr int NT = 32 * (NW + 1 + NPROD);
@@ -166,9 +166,7 @@ struct SellCfg {
   // TMA ring depth (tiles), measured per format: SELL DP16 (C2) best at 4
   // (an epilogue lag of 2 tiles with double-buffered A/TMEM and NS 5 measured
   // 25.7 vs 24.4 us); CSR DP16 (C4) at 5 (166 vs 197 us at 4); DP32 fills smem
-  static constexpr bool WIN = CSR == 3;                // windowed sliced-ELL
   static constexpr bool CSRL = CSR == 1 || CSR == 2;    // CSR ranges staged per tile
-  static_assert(!WIN || DP == 16, "windowed slices are built for d = 16");
 #ifndef GNPC_MBITS
 #define GNPC_MBITS 1  // per-row mask words instead of the X_l tile: frees 15.5 KB per ring slot
 #endif
@@ -203,7 +201,7 @@ struct SellCfg {
 #ifndef GNPC_NS_PW
 #define GNPC_NS_PW 4  // 3 measured slower (C5 409 vs 368 us)
 #endif
-  static constexpr int NS = DP == 16 ? (CSRL ? GNPC_NS_CSR16 : (WIN ? 4 : GNPC_NS_SELL16))
+  static constexpr int NS = DP == 16 ? (CSRL ? GNPC_NS_CSR16 : GNPC_NS_SELL16)
                                      : (CSR == 2 ? GNPC_NS_TR32
                                                  : ((DEEP || CSR == 5) ? GNPC_NS_DEEP32
                                                                        : ((CSR == 7 || CSR == 8 || CSR == 10) ? GNPC_NS_PW : 3)));
@@ -222,14 +220,12 @@ struct SellCfg {
 #endif
   // (pair-union: entries per pair; a union entry is 16 B for 2 rows, so the
   // staged bytes K * TM * 8 match the sliced-ELL formula)
-  static constexpr int KCAP = WIN ? 8
-                                 : (DP == 16 ? GNPC_KCAP16
-                                             : ((CSR == 5 || CSR == 6) ? GNPC_KCAPP
-                                                                       : ((CSR == 7 || CSR == 8) ? GNPC_KCAPPW
-                                                                                                 : GNPC_KCAP32)));
+  static constexpr int KCAP = DP == 16 ? GNPC_KCAP16
+                                       : ((CSR == 5 || CSR == 6) ? GNPC_KCAPP
+                                                                 : ((CSR == 7 || CSR == 8) ? GNPC_KCAPPW : GNPC_KCAP32));
   // the staged gather reads round(K, US) words of a slice: KCAP must be a
   // multiple of US or the last round would read past the staged slice
-  static_assert(WIN || PW || KCAP % US == 0, "GNPC_KCAP16/GNPC_KCAP32 must be a multiple of the gather round");
+  static_assert(PW || KCAP % US == 0, "GNPC_KCAP16/GNPC_KCAP32 must be a multiple of the gather round");
   static_assert(!PW || KCAP % 4 == 0, "strip-window slices hold a multiple of 4 entries per pair");
   static constexpr uint32_t OPB = TM * DP * 4;   // one A-type operand / X tile / Y tile (bytes)
   static constexpr uint32_t BB = DP * DP * 4;    // one B operand (bytes)
@@ -256,11 +252,7 @@ struct SellCfg {
   static constexpr uint32_t O_MASK = TW ? 0 : OPB;
   static constexpr uint32_t O_TWS = MASKB;
   static constexpr uint32_t O_RP = TR ? OPB + MASKB : OPB, O_CI = O_RP + 1024, O_V = O_CI + CAPC * 4;
-  // windowed: [kWinBlocks 64-row X blocks | slice]; the tile's own rows (the
-  // MMA's X tile) are two consecutive blocks of the window
-  static constexpr uint32_t BLKB = kWinRows * DP * 4;
-  static constexpr uint32_t WB = WIN ? kWinBlocks * BLKB : 0;
-  static constexpr uint32_t O_SL = WIN ? WB : (PW ? 0 : OPB);  // staged slice (sliced-ELL modes)
+  static constexpr uint32_t O_SL = PW ? 0 : OPB;  // staged slice (sliced-ELL modes)
   static constexpr uint32_t SLOT =
       TW ? 1024u : (CSRL ? ((O_V + CAPC * 4 + 1023) & ~1023u) : (((O_SL + CVB) + 1023) & ~1023u));
   static_assert(!TW || O_TWS + 2 * 40 + 6 * kTwKcap <= SLOT, "training window slice exceeds its ring slot");
@@ -325,7 +317,7 @@ static_assert(SellCfg<32, 8>::o_bar(32, true) + 128 + 3 * SellCfg<32, 8>::KSCHED
 struct SellMaps {
   CUtensorMap x;   // layer input  [n][DP], box {DP, 128}, swizzled
   CUtensorMap y;   // layer output [n][DP] (unused by the last layer)
-  CUtensorMap xw;  // layer input, box {DP, kWinRows} (windowed mode)
+  CUtensorMap xw;  // layer input, box {DP, kPwRows} (strip windows, d = 32)
 };
 
 // Sliced-ELL gather, R rows per group, rounds of US entries.  Slots past K
@@ -461,39 +453,6 @@ __device__ __forceinline__ void gather_pw_rows(const uint8_t* sl, int K, int gid
   }
 }
 
-// Windowed gather: entries hold the row's position in the tile's staged
-// window; the X rows are read from shared memory (swizzled as the TMA wrote
-// them, 64-row blocks at BLKB-aligned offsets), otherwise as gather_sell_rows.
-template <int DP, int R, int US, int TM, bool SMEM>
-__device__ __forceinline__ void gather_win_rows(const uint8_t* win, int gl, const int2* cv, int K, int gid,
-                                                float4 (&acc)[R]) {
-  for (int k = 0; k < K; k += US) {
-    int c[R][US];
-    float w[R][US];
-#pragma unroll
-    for (int u = 0; u < US; ++u) {
-      const bool on = k + u < K;
-      const int2* src = cv + (k + u) * TM + R * gid;
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        int2 e;
-        if constexpr (SMEM) {
-          e = src[j];
-        } else {
-          e = on ? __ldg(src + j) : make_int2(0, 0);
-        }
-        c[j][u] = on ? e.x : 0;
-        w[j][u] = on ? __int_as_float(e.y) : 0.f;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < US; ++u)
-#pragma unroll
-      for (int j = 0; j < R; ++j)
-        fma4(acc[j], w[j][u], *reinterpret_cast<const float4*>(win + tc::swz_off<DP>(c[j][u], 4 * gl)));
-  }
-}
-
 // CSR gather: row r = R*gid + j of the tile spans [s_j, s_j + len_j) of the
 // staged (or global) col/val arrays; rounds of US entries up to the longer
 // of the group's rows.  Slots past a row's end get weight 0 and the row's own
@@ -591,6 +550,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
 }
 
+#ifdef GNPC_TILE_TRACE
+// debug (tools/tile_trace.py): per-tile clock stamps of block 0 (math warp 0
+// and the MMA warp) for the GNPC_TILE_TRACE-th sell_layer call of the process
+__device__ unsigned long long g_trace[64 * 16];
+__device__ int g_trace_layer, g_trace_on;
+// (math warps: the LAST warp to reach the stamp, by atomicMax)
+#define GNPC_TR_STAMP(k)                                                                    \
+  do {                                                                                      \
+    if (tr_on && lane == 0 && it < 64) atomicMax(&g_trace[it * 16 + (k)], (unsigned long long)clock64()); \
+  } while (0)
+#else
+#define GNPC_TR_STAMP(k) \
+  do {                   \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // The layer pipeline as device functions shared by the per-layer kernel
 // (k_layer_sell) and the whole-apply persistent kernel (k_apply_sell).
@@ -625,6 +600,7 @@ struct SellPipe {
   uint32_t tmem;
   int talloc;
   int ring_it = 0, mma_it = 0, af_it = 0;  // phase counters (identical in every thread)
+  int ef_it = 0;                           // efull phases (EARLY), across the layers of one launch
 };
 
 // Window sequence of the strip-window mode, replayed identically by the
@@ -811,13 +787,20 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   const bool hint = a.l2hint && !TR;
   const uint64_t pol_stream = hint ? l2_policy_evict_first() : l2_policy_evict_normal();
   const uint64_t pol_keep = hint ? l2_policy_evict_last() : l2_policy_evict_normal();
-  const int rb = p.ring_it, mb = p.mma_it, ab = p.af_it;
+  const int rb = p.ring_it, mb = p.mma_it, ab = p.af_it, eb = p.ef_it;
   // commits: one per tile, plus the last projection MMA's (TCP)
   const int ncommit = my_tiles;  // (the projection MMAs commit to pbar)
   p.ring_it += my_tiles;
   p.mma_it += ncommit;
   p.af_it += my_tiles > 0 ? my_tiles + 1 : 0;
+  p.ef_it += my_tiles;  // one efull completion per tile
   if (my_tiles == 0) return;
+#ifdef GNPC_TILE_TRACE
+  // (no static shared memory: the layer kernels take all 227 KB dynamically)
+  if (tid == 0 && blockIdx.x == 0) g_trace_on = atomicAdd(&g_trace_layer, 1) == GNPC_TILE_TRACE;
+  __syncthreads();
+  const bool tr_on = blockIdx.x == 0 && *reinterpret_cast<volatile int*>(&g_trace_on) != 0 && warp <= NW;
+#endif
 
   if (warp >= NW) {
     // ============================================================ control warp
@@ -825,7 +808,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
     // ring and window loads, following the MMA warp's progress counter)
     const bool producer = C::NPROD && warp == NW + 1;
     if (lane == 0) {
-      tc::tma_prefetch_desc(C::WIN ? mapxw : mapx);
+      tc::tma_prefetch_desc(C::WINS ? mapxw : mapx);
       if (!LAST) tc::tma_prefetch_desc(mapy);
       auto issue = [&](int it) {  // tile `it` of this CTA into ring slot (rb + it) % NS
         if (it >= my_tiles) return;
@@ -866,15 +849,6 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
             tc::bulk_load_hint(slot + C::O_CI, a.cis + a0, 4 * cnt, &p.full[s], pol_stream);
             tc::bulk_load_hint(slot + C::O_V, a.vs + a0, 4 * cnt, &p.full[s], pol_stream);
           }
-        } else if constexpr (C::WIN) {
-          const int* wd = a.wdesc + static_cast<size_t>(t) * kWinDesc;
-          const int nbk = __ldg(wd);
-          const int K = __ldg(a.sell_k + t) & 0xffff;
-          const bool staged = K > 0 && K <= C::KCAP;
-          tc::mbar_expect_tx(&p.full[s], nbk * C::BLKB + (staged ? K * TM * 8 : 0));
-          for (int i = 0; i < nbk; ++i)
-            tc::tma_load_2d(slot + i * C::BLKB, mapxw, 0, __ldg(wd + 2 + i) * kWinRows, &p.full[s]);
-          if (staged) tc::bulk_load(slot + C::O_SL, a.wsell + __ldg(a.sell_off + t), K * TM * 8, &p.full[s]);
         } else {
           const int K = __ldg((C::PAIR ? a.psell_k : a.sell_k) + t) & 0xffff;
           const bool staged = K > 0 && K <= C::KCAP;
@@ -981,9 +955,10 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       for (int it = 0; it <= (producer ? -1 : my_tiles); ++it) {
         if constexpr (C::EARLY) {
           if (it >= 1) {  // epilogue(it-1) and projection epilogue(it-2) have read TMEM
-            tc::mbar_wait_dbg(p.efull, (it - 1) & 1, 5, it);
+            tc::mbar_wait_dbg(p.efull, (eb + it - 1) & 1, 5, it);
             tc::fence_after();
           }
+          GNPC_TR_STAMP(8);
           if (it < my_tiles) {  // X_hi·[U_lo; U_hi] once the tile's rows landed
             const int r = rb + it;
             tc::mbar_wait_dbg(&p.full[r % NS], (r / NS) & 1, 6, it);
@@ -1000,10 +975,13 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
                            idesc2, k8 > 0);
           }
         }
+        GNPC_TR_STAMP(9);
         tc::mbar_wait_dbg(p.afull, (ab + it) & 1, 1, it);
         tc::fence_after();
+        GNPC_TR_STAMP(10);
         // stores issued up to the previous iteration have left the Y staging:
-        // the buffer the epilogue after this MMA writes is free
+        // the buffer the epilogue after this MMA writes is free (waiting
+        // after the MMA issue instead measured the same: C2, C4)
         tc::bulk_wait_read0();
         if (KIND == 1 && it < my_tiles) {  // training forward: the tile's ÂX (A2_hi) to HBM
           tc::tma_store_2d(tio->mapax, p.A, 0, tile_at(it) * TM);
@@ -1018,8 +996,6 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
             }
             sX = sXe0 + (bcur % C::NWIN) * C::WINB;
           }
-          if constexpr (C::WIN)  // the tile's own rows inside the window
-            sX += __ldg(a.wdesc + static_cast<size_t>(tile_at(it)) * kWinDesc + 1) * C::BLKB;
           // 3xTF32 with the two A_hi products stacked along N (A_hi is read
           // once for both): D[:, 0:DP] = A_hi·B_lo, D[:, DP:2DP] = A_hi·B_hi +
           // A_lo·B_hi; the epilogue adds the halves.  Each part's B operands
@@ -1054,6 +1030,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         }
         if (KIND == 1 && it < my_tiles) tc::bulk_wait_read0();  // A2_hi is rewritten after the commit
         if (it < my_tiles) tc::mma_commit(p.mma_bar);
+        GNPC_TR_STAMP(11);
         // the projection of tile it-1 after MMA(it), on its own barrier: the
         // epilogues' wait for MMA(it) does not include it
         if (TCP && it >= 1) {
@@ -1105,6 +1082,11 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   auto epilogue = [&](int itp) -> bool {
     tc::mbar_wait_dbg(p.mma_bar, (mb + itp) & 1, 2, itp);
     tc::fence_after();
+    {
+      const int it = itp + 1;
+      (void)it;
+      GNPC_TR_STAMP(3);
+    }
     const int q = warp & 3, cq = warp >> 2;  // lane quarter, column group
     const uint32_t trow = p.tmem + (static_cast<uint32_t>(32 * q) << 16);
     if (LAST && !TCP) {
@@ -1311,7 +1293,9 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         if (haslong && i < n && __ldg(a.rp + i + 1) - __ldg(a.rp + i) > kLongRow)
           acc[j] = ldg4(axlong + static_cast<size_t>(i) * DP + 4 * gl);
       }
+      GNPC_TR_STAMP(0);
       tc::mbar_wait_dbg(&p.full[r % NS], (r / NS) & 1, 3, it);
+      GNPC_TR_STAMP(1);
       if constexpr (C::TW) {
         // training strip windows: the group's two rows are samples k0, k0 + 1
         // of one node; each entry names a neighbour node's block (bs rows) in
@@ -1390,14 +1374,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         else
           gather_csr_rows<DP, R, C::USC>(xbj, DP * 4ull, a.cis, a.vs, sj, lj, self, acc, pol_keep);
       } else {
-        if constexpr (C::WIN) {
-          // window rows in shared memory (swizzled like the TMA wrote them)
-          if (staged)
-            gather_win_rows<DP, R, C::US, TM, true>(slot, gl, reinterpret_cast<const int2*>(slot + C::O_SL), K,
-                                                    gid, acc);
-          else
-            gather_win_rows<DP, R, C::US, TM, false>(slot, gl, a.wsell + __ldg(a.sell_off + tile), K, gid, acc);
-        } else if constexpr (C::PW) {
+        if constexpr (C::PW) {
           if constexpr (R == 2)
             gather_pw_rows<C::NG>(slot, K, gid, gl, wbase, wring0 + C::NWIN * C::WINB, C::NWIN * C::WINB, acc);
         } else if constexpr (C::PAIR) {
@@ -1416,6 +1393,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       }
     }
 
+    GNPC_TR_STAMP(2);
     // ------------------------------------------- epilogue of the previous tile
     bool proj = false;
     if (it >= 1 && it - 1 < my_tiles) proj = epilogue(it - 1);
@@ -1430,6 +1408,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       }
     }
 
+    GNPC_TR_STAMP(4);
     // ---------------------------------------------------------------- split
     if (have) {
 #pragma unroll
@@ -1445,7 +1424,6 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         constexpr int CW = DP / NQ;
         const int q = warp & 3, cq = warp >> 2, m = 32 * q + lane;
         const uint8_t* xtile = slot;
-        if constexpr (C::WIN) xtile += __ldg(a.wdesc + static_cast<size_t>(tile) * kWinDesc + 1) * C::BLKB;
         if constexpr (C::WINS) xtile = wtile;
         float lo[CW];
 #pragma unroll
@@ -1463,7 +1441,9 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         tc::fence_before();
       }
     }
+    GNPC_TR_STAMP(5);
     if (it <= my_tiles) arrive();
+    GNPC_TR_STAMP(6);
     if (proj) project(tile_at(it - 1) * TM);
   }
 }
@@ -1517,7 +1497,7 @@ k_train_sell(DevCsr a, const __grid_constant__ TrainMaps maps, const float* __re
 // ApplyLaunch for matrices without long rows (src/gnn.cpp:120-201).
 struct ApplyFused {
   CUtensorMap x0, x1;           // TMA maps over X[0], X[1]
-  CUtensorMap x0w, x1w;         // the same, box {DP, kWinRows} (windowed mode)
+  CUtensorMap x0w, x1w;         // the same with the strip windows' box (unused at d = 16)
   float* X0;
   float* X1;
   const float* uwp;             // [L][4 DP DP] B operands

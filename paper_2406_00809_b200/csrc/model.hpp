@@ -58,7 +58,7 @@ struct gnpc_model_s {
   std::vector<unsigned char> part_pair;
   // TMA maps over the two activation buffers (k_layer_sell)
   CUtensorMap tmX[2]{};
-  CUtensorMap tmXw[2]{};  // box {DP, kWinRows}: windowed sliced-ELL (d = 16)
+  CUtensorMap tmXw[2]{};  // box {DP, kPwRows}: the strip windows' halo-extended tiles (d = 32)
   const float* tm_base[2] = {nullptr, nullptr};
   std::size_t o_enc1 = 0, o_enc1b = 0, o_enc2 = 0, o_enc2b = 0, o_uw = 0, o_dec1 = 0,
               o_dec1b = 0, o_dec2 = 0, o_dec2b = 0;

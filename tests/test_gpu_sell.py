@@ -189,21 +189,3 @@ def test_fused_apply_zero_copy_pinned_host(capi, oc, cuda):
         check(y, oc.gnn_apply(a, dims, p, b))
         assert np.array_equal(y, m.apply(b))  # same kernels as the staged path
 
-
-@pytest.mark.parametrize("grid", [45, 64])
-def test_windowed_sell_opt_in(capi, oc, cuda, grid):
-    # GNPC_WIN=1: d = 16 layers gather from TMA-staged 64-row X blocks
-    # (windowed sliced-ELL, opt-in); per-layer and whole-apply launches
-    a = stencil_plus(oc, grid)
-    dims = (16, 32, 8)
-    p = f32(oc.init_params(*dims, 3))
-    b = oc.gaussian_vector(4, a.n)
-    want = oc.gnn_apply(a, dims, p, b)
-    os.environ["GNPC_WIN"] = "1"
-    try:
-        c = capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
-        y = capi.Model(c, dims, p).apply(b)
-    finally:
-        os.environ.pop("GNPC_WIN", None)
-    check(y, want)
-    assert rel_l2(y, apply_path(capi, a, dims, p, b, True)) <= 2e-6

@@ -124,8 +124,9 @@ int gnpc_apply_device_f32(gnpc_model m, const float* b, float* out, void* stream
 int gnpc_apply_device_f64(gnpc_model m, const double* b, double* out, void* stream);
 /* Same as gnpc_apply_device_f32 with CUDA events between the pipeline's
  * kernels on `stream`; adds per-kind durations (ms) and launch counts into
- * ms_by_kind[5] / count_by_kind[5]: 0 norm, 1 lift, 2 long-row ÂX,
- * 3 fused layer, 4 last layer + projection.  Used by bench.py's roofline. */
+ * ms_by_kind[5] / count_by_kind[5]: 0 norm, 1 lift (d = 32 strip windows:
+ * the lift fused into the first layer, one kernel), 2 long-row ÂX, 3 fused
+ * layer, 4 last layer + projection.  Used by bench.py's roofline. */
 int gnpc_apply_profile(gnpc_model m, const float* b, float* out, void* stream, double* ms_by_kind,
                        int64_t* count_by_kind);
 

@@ -151,8 +151,18 @@ struct ApplyLaunch {
     mark(0);
     k_apply_norm<InT><<<m.norm_grid, kThreads, 0, s>>>(in, n, m.partials.p, m.ticket.p, m.sc.p, skip);
     GNPC_LAUNCHED();
+    // d = 32 strip windows: the lift is fused into the first layer (its lift
+    // warps compute the row windows; x1 never crosses HBM).  GNPC_NO_LIFT_FUSE=1
+    // keeps the separate lift kernel.
+    bool fuse_lift = false;
+    if constexpr (DP == 32) {
+      const char* off = std::getenv("GNPC_NO_LIFT_FUSE");  // (read per apply: tests toggle it)
+      fuse_lift = !(off && off[0] == '1') && a.pw && m.use_tc && !sell_off && A.n_long == 0 && net.layers >= 2 && net.nbreak <= 32 &&
+                  SellCfg<32, 8>::smem_bytes(net.hidden, true) <= 227 * 1024 &&
+                  SellCfg<32, 9>::smem_bytes(net.hidden, false) <= 227 * 1024;
+    }
     // lift
-    {
+    if (!fuse_lift) {
       const size_t smem = (size_t)(net.nbreak + 1) * DP * 8 + (size_t)net.nbreak * 4 + 16;
       auto kern = k_lift_pw<DP, InT>;
       set_smem_attr((const void*)kern, 160 * 1024);
@@ -184,10 +194,25 @@ struct ApplyLaunch {
         axl = m.AXL.p;
       }
       const bool last = l + 1 == net.layers;
-      mark(last ? 4 : 3);
+      // (profile: the fused lift + first layer is timed in the lift's slot, so
+      // slot 3 stays the per-launch time of the plain layer kernel)
+      mark(last ? 4 : (l == 0 && fuse_lift ? 1 : 3));
       if constexpr (DP == 32) {
         // strip windows (stencil-like d = 32 matrices with a dominant tile
         // stride): X rows staged in shared memory, one new window per tile
+        if (l == 0 && fuse_lift) {
+          using S = SellCfg<DP, 9>;
+          auto kern = k_layer_sell_lift<DP, OutT>;
+          set_smem_attr((const void*)kern, 227 * 1024);
+          const int tiles_s = (n + S::TM - 1) / S::TM;
+          const int grid = std::max(1, std::min(tiles_s, sms));
+          SellMaps maps{m.tmX[cur], m.tmX[1 - cur], m.tmXw[cur]};
+          kern<<<grid, S::NT, S::smem_bytes(net.hidden, false), s>>>(a, maps, (const void*)in, sizeof(InT) == 8 ? 1 : 0,
+                                                                      m.UWP.p, net, m.sc.p, skip);
+          GNPC_LAUNCHED();
+          cur = 1 - cur;
+          continue;
+        }
         if (a.pw && m.use_tc && !sell_off && SellCfg<32, 8>::smem_bytes(net.hidden, true) <= 227 * 1024) {
           using S = SellCfg<DP, 7>;
           auto kern = last ? k_layer_sell<DP, true, OutT, 8> : k_layer_sell<DP, false, OutT, 7>;

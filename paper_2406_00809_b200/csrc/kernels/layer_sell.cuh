@@ -105,6 +105,11 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 // CSR = 1: the short-row CSR ranges of the tile (ragged matrices);
 // CSR = 2: training — B virtual rows per node (v = node*B + k), the full CSR
 //          ranges of the tile's 128/B nodes, plus a mask tile for the backward;
+// CSR = 7 / 8 / 9: strip windows (DevCsr::pw, d = 32): 7 the non-last layers,
+//          8 the last layer, 9 the FIRST layer with the lift fused in — its
+//          windows are not loaded but computed from the scaled input by two
+//          lift warps (x1 = lift_a[p] v + lift_b[p], src/gnn.cpp:138-157), so
+//          the first activation never crosses HBM;
 // CSR = 10: training over strip windows (DevCsr::tw, d = 32): CSR 2's virtual
 //          rows with the X rows of the tile's neighbour nodes staged in shared
 //          memory by TMA (node windows along strips, one new per tile).
@@ -119,7 +124,10 @@ struct SellCfg {
 #ifndef GNPC_TR_PROD
 #define GNPC_TR_PROD 0  // measured neutral on C3 (19.34 ms either way)
 #endif
-  static constexpr int NPROD = (CSR == 7 || CSR == 8 || CSR == 10 || (CSR == 2 && GNPC_TR_PROD)) ? 1 : 0;
+  static constexpr int NPROD = (CSR == 7 || CSR == 8 || CSR == 9 || CSR == 10 || (CSR == 2 && GNPC_TR_PROD)) ? 1 : 0;
+  // CSR = 9: + lift warps filling the strip windows from the layer-0 input
+  static constexpr bool LIFT = CSR == 9;
+  static constexpr int NLIFT = LIFT ? 5 : 0;
   // strip-window modes: the MMA work that does not need tile t's split —
   // X_hi·[U_lo; U_hi] and the projection of tile t-1 — is issued as soon as
   // the epilogues have read TMEM (efull), overlapping the split
@@ -134,9 +142,9 @@ struct SellCfg {
 #endif
   // (measured neutral to slower on the d = 16 sliced-ELL / CSR layers: C2
   // 4820 vs 4980 applies/s, C4 unchanged, so those keep the plain order)
-  static constexpr bool EARLY = ((CSR == 7 || CSR == 8) && GNPC_PW_EARLY) || (CSR == 2 && GNPC_TR_EARLY) ||
+  static constexpr bool EARLY = ((CSR == 7 || CSR == 8 || CSR == 9) && GNPC_PW_EARLY) || (CSR == 2 && GNPC_TR_EARLY) ||
                                 (CSR == 10 && GNPC_TW_EARLY);
-  static constexpr int NT = 32 * (NW + 1 + NPROD);
+  static constexpr int NT = 32 * (NW + 1 + NPROD + NLIFT);
   static constexpr int NQ = NW / 4;              // epilogue column groups (warps per TMEM lane quarter)
   static constexpr int TM = 128;                 // rows per tile (MMA M)
   static constexpr int G = DP / 4;               // lanes per row
@@ -193,7 +201,7 @@ struct SellCfg {
   // CSR = 7 / 8: strip-window pair-union (d = 32, DevCsr::pw): the ring holds
   // only the slices; X rows come from NWIN row windows (one new per tile in a
   // strip); 7 = non-last layers (4-deep ring), 8 = last layer (3 deep)
-  static constexpr bool PW = CSR == 7 || CSR == 8;
+  static constexpr bool PW = CSR == 7 || CSR == 8 || CSR == 9;
   static_assert(!PW || DP == 32, "strip windows are a d = 32 layout");
   static constexpr bool TW = CSR == 10;       // training strip windows
   static_assert(!TW || DP == 32, "training strip windows are a d = 32 layout");
@@ -204,7 +212,7 @@ struct SellCfg {
   static constexpr int NS = DP == 16 ? (CSRL ? GNPC_NS_CSR16 : GNPC_NS_SELL16)
                                      : (CSR == 2 ? GNPC_NS_TR32
                                                  : ((DEEP || CSR == 5) ? GNPC_NS_DEEP32
-                                                                       : ((CSR == 7 || CSR == 8 || CSR == 10) ? GNPC_NS_PW : 3)));
+                                                                       : ((PW || CSR == 10) ? GNPC_NS_PW : 3)));
   // windows alive: the MMA's window of the current tile plus NS - 1 tiles
   // of lookahead (steady state: one new window per tile); a break tile
   // issued right after its predecessor's gathers needs the MMA window b,
@@ -222,7 +230,7 @@ struct SellCfg {
   // staged bytes K * TM * 8 match the sliced-ELL formula)
   static constexpr int KCAP = DP == 16 ? GNPC_KCAP16
                                        : ((CSR == 5 || CSR == 6) ? GNPC_KCAPP
-                                                                 : ((CSR == 7 || CSR == 8) ? GNPC_KCAPPW : GNPC_KCAP32));
+                                                                 : (PW ? GNPC_KCAPPW : GNPC_KCAP32));
   // the staged gather reads round(K, US) words of a slice: KCAP must be a
   // multiple of US or the last round would read past the staged slice
   static_assert(PW || KCAP % US == 0, "GNPC_KCAP16/GNPC_KCAP32 must be a multiple of the gather round");
@@ -280,11 +288,14 @@ struct SellCfg {
   }
   // PW: per-CTA schedule table (tile, K, slice offset) after the barriers
   static constexpr int KSCHED = PW ? 256 : (TW ? 512 : 0);
+  // CSR = 9: the lift tables [kLiftIv][DP] a, b and the kinks (hidden <= 32)
+  static constexpr int kLiftIv = 33;
+  static constexpr uint32_t LIFTB = LIFT ? 2 * kLiftIv * DP * 4 + 32 * 4 : 0;
   static size_t smem_bytes(int hidden, bool last) {
-    // barriers + TMEM slot, the schedule, 1024-B alignment slack
-    return o_bar(hidden, last) + 128 + 3 * KSCHED * 4 + 1024;
+    // barriers + TMEM slot, the schedule, the lift tables, 1024-B alignment slack
+    return o_bar(hidden, last) + 128 + 3 * KSCHED * 4 + LIFTB + 1024;
   }
-  static_assert(TR || DEEP || CSR == 5 || CSR == 7 || O_Y + 2 * 32 * DP * 4 + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
+  static_assert(TR || DEEP || CSR == 5 || CSR == 7 || CSR == 9 || O_Y + 2 * 32 * DP * 4 + (DP + 2) * 32 * 4 + 128 + 1024 <= 227 * 1024,
                 "last-layer layout must fit shared memory at hidden 32 (larger: host falls back)");
   static_assert(!TR || O_Y + 2 * OPB + 128 + 1024 <= 227 * 1024, "training layout must fit shared memory");
   // TMEM: layer accumulator [0, 2DP); last layer's projection accumulator at
@@ -311,6 +322,9 @@ struct SellCfg {
 // the strip-window layouts fit one SM's shared memory (hidden 32)
 static_assert(SellCfg<32, 7>::o_bar(32, false) + 128 + 3 * SellCfg<32, 7>::KSCHED * 4 + 1024 <= 227 * 1024,
               "strip-window layer layout exceeds shared memory");
+static_assert(SellCfg<32, 9>::o_bar(32, false) + 128 + 3 * SellCfg<32, 9>::KSCHED * 4 + SellCfg<32, 9>::LIFTB + 1024 <=
+                  227 * 1024,
+              "fused-lift first-layer layout exceeds shared memory");
 static_assert(SellCfg<32, 8>::o_bar(32, true) + 128 + 3 * SellCfg<32, 8>::KSCHED * 4 + 1024 <= 227 * 1024,
               "strip-window last-layer layout exceeds shared memory");
 
@@ -530,6 +544,14 @@ __device__ __forceinline__ void gather_csr_node(const char* xb0, unsigned long l
 // mapax, and at d = 32 the rows' [Y > 0] bits (mask_out, one 32-bit word per
 // row); KIND 2 (backward) multiplies by [X_l > 0] when use_mask, from those
 // bits (mask_in, d = 32) or from the X_l tile (mapmask).
+// Fused-lift extras (CSR = 9): the apply's input vector (f32 or f64) and the
+// scale sandwich's scalars.
+struct LiftIO {
+  const void* in;
+  int f64;
+  const ApplyScalars* sc;
+};
+
 struct TrainIO {
   const CUtensorMap* mapax;
   const CUtensorMap* mapmask;
@@ -586,6 +608,7 @@ struct SellPipe {
   uint8_t* ring;
   uint8_t* win;  // strip windows (PW)
   int* sched;    // PW: the CTA's tile schedule [3][KSCHED]
+  float* lift;   // CSR = 9: lift tables a[33][DP], b[33][DP], t[32]
   uint8_t* A;  // [A2_hi | A2_lo]
   uint8_t* Bs;
   uint8_t* Ystg;
@@ -666,11 +689,13 @@ __device__ __forceinline__ SellPipe<DP, CSR> sell_setup(int hidden, bool last) {
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p.pbar + 1);
   p.prog = reinterpret_cast<int*>(tslot + 1);  // PW: tiles whose MMA the control warp has issued
   p.sched = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(p.full) + 128);
+  p.lift = reinterpret_cast<float*>(p.sched + 3 * C::KSCHED);
   const int tid = threadIdx.x;
   for (int t = tid; t < int(C::NS * C::SLOT / 16); t += C::NT)  // stale slice words must be valid columns
     reinterpret_cast<float4*>(p.ring)[t] = f4zero();
   if (tid == 0) {
-    for (int s = 0; s < C::NS; ++s) tc::mbar_init(&p.full[s], 1);
+    // (CSR = 9: + one arrival per lift warp, after it wrote the slot's new windows)
+    for (int s = 0; s < C::NS; ++s) tc::mbar_init(&p.full[s], 1 + C::NLIFT);
     tc::mbar_init(p.mma_bar, 1);
     tc::mbar_init(p.afull, C::NW);
     tc::mbar_init(p.efull, C::NW);
@@ -704,7 +729,8 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
                                            const CUtensorMap* mapy, const float* __restrict__ X,
                                            const float* __restrict__ axlong, const float* __restrict__ uwp,
                                            const NetView& net, double out_scale, OutT* __restrict__ out,
-                                           const TrainIO* tio = nullptr, const CUtensorMap* mapxw = nullptr) {
+                                           const TrainIO* tio = nullptr, const CUtensorMap* mapxw = nullptr,
+                                           const LiftIO* lio = nullptr) {
   using C = SellCfg<DP, CSR>;
   constexpr int TM = C::TM, G = C::G, R = C::R, NS = C::NS, NW = C::NW, NQ = C::NQ;
   constexpr bool TR = C::TR;
@@ -745,6 +771,14 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       B1[t] = net.dec1_b[t];
       D2[t] = net.dec2[t];
     }
+  }
+  if constexpr (C::LIFT) {  // the piecewise-linear lift's tables (k_lift_pw's)
+    const int nb = net.nbreak;
+    for (int t = tid; t < (nb + 1) * DP; t += C::NT) {
+      p.lift[t] = net.lift_a[t];
+      p.lift[C::kLiftIv * DP + t] = net.lift_b[t];
+    }
+    for (int t = tid; t < nb; t += C::NT) p.lift[2 * C::kLiftIv * DP + t] = net.lift_t[t];
   }
   tc::fence_proxy_async();
   __syncthreads();
@@ -802,13 +836,117 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   const bool tr_on = blockIdx.x == 0 && *reinterpret_cast<volatile int*>(&g_trace_on) != 0 && warp <= NW;
 #endif
 
+  if constexpr (C::LIFT) {
+    if (warp >= NW + 2) {
+      // ============================================================ lift warps
+      // They replay the producer's issue sequence (same gating on the MMA
+      // warp's progress counter) and, where the producer of the other modes
+      // loads a window by TMA, compute it: window row r of tile u is global
+      // row c = 128 u - halo + r, x1[c] = a[p] v + b[p] with v the scaled
+      // input and p its kink interval (k_lift_pw's arithmetic, bit for bit);
+      // rows outside [0, n) are zero, as the TMA's out-of-bounds fill.
+      const int lw = warp - (NW + 2);
+      const float* s_a = p.lift;
+      const float* s_b = s_a + C::kLiftIv * DP;
+      const float* s_t = s_b + C::kLiftIv * DP;
+      const int nb = net.nbreak;
+      const double in_scale = lio->sc->in_scale;
+      constexpr int WR = TM + 2 * kPwHalo;             // 144 rows
+      constexpr int NP = (WR + 32 * C::NLIFT - 1) / (32 * C::NLIFT);  // passes per window
+      WinSeq ws, wsb;
+      int nxt = 0, bcur = 0;
+      // lane -> row of a 32-row block and chunk rotation chosen so that both
+      // the table reads (lanes of a quarter-warp in different intervals: chunk
+      // ch ^ i differs per lane) and the swizzled window stores (physical chunk
+      // ch ^ i ^ (r & 7) differs per lane) are free of bank conflicts
+      const int li = lane & 7, lg = lane >> 3;
+      const int lrow = 8 * (li & 3) + 2 * lg + (li >> 2);
+      const size_t esz = lio->f64 ? 8 : 4;
+      auto fill = [&](int q, int u) {
+        uint8_t* wb = p.win + (q % C::NWIN) * C::WINB;
+        float v[NP];
+        {  // the next window along the strip into L1 (its loads then skip the L2 round trip)
+          const long long c0 = static_cast<long long>(u + w_S) * TM - kPwHalo;
+          const long long cp = c0 + 32 * lane;
+          if (lane < (WR + 31) / 32 + 1 && cp >= 0 && cp < n)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(static_cast<const char*>(lio->in) + cp * esz));
+        }
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const int r = (k * C::NLIFT + lw) * 32 + lrow;
+          const long long c = static_cast<long long>(u) * TM - kPwHalo + r;
+          v[k] = 0.f;
+          if (r < WR && c >= 0 && c < n) {
+            const double x = lio->f64 ? static_cast<const double*>(lio->in)[c]
+                                      : static_cast<double>(static_cast<const float*>(lio->in)[c]);
+            v[k] = static_cast<float>(in_scale * x);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const int r = (k * C::NLIFT + lw) * 32 + lrow;
+          if (r >= WR) continue;
+          const long long c = static_cast<long long>(u) * TM - kPwHalo + r;
+          const bool in_rows = c >= 0 && c < n;
+          int lo = 0, hi = nb;  // interval = #kinks <= v
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s_t[mid] <= v[k]) lo = mid + 1;
+            else hi = mid;
+          }
+          uint8_t* row = wb + r * (DP * 4);
+#pragma unroll
+          for (int c8 = 0; c8 < DP / 4; ++c8) {
+            const int ch = c8 ^ li;
+            const float4 al = *reinterpret_cast<const float4*>(s_a + lo * DP + 4 * ch);
+            const float4 be = *reinterpret_cast<const float4*>(s_b + lo * DP + 4 * ch);
+            const float4 o = in_rows ? make_float4(fmaf(al.x, v[k], be.x), fmaf(al.y, v[k], be.y),
+                                                   fmaf(al.z, v[k], be.z), fmaf(al.w, v[k], be.w))
+                                     : f4zero();
+            *reinterpret_cast<float4*>(row + ((ch ^ (r & 7)) << 4)) = o;
+          }
+        }
+      };
+      auto issue_lift = [&](int j) {
+        const int t = tile_at(j);
+        int sa, sb, sc;
+        const int nnew = ws.next(t, w_S, sa, sb, sc);
+        if (nnew == 3) {
+          fill(sa, t - w_S);
+          fill(sb, t);
+        }
+        fill(sc, t + w_S);
+        tc::fence_proxy_async();  // window b is also the MMA's A operand (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p.full[(rb + j) % NS]);
+      };
+      auto issue_more = [&](int it) {
+        const int prot = it >= 0 ? bcur : 0;
+        while (nxt < my_tiles && nxt <= it + NS - 1 && ws.peek_c(tile_at(nxt), w_S) - prot < C::NWIN)
+          issue_lift(nxt++);
+      };
+      issue_more(-1);
+      for (int it = 0; it < my_tiles && nxt < my_tiles; ++it) {
+        while (true) {
+          int v;
+          asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(tc::smem_u32(p.prog)) : "memory");
+          if (v > it) break;
+          __nanosleep(32);
+        }
+        int sa, sc;
+        wsb.next(tile_at(it), w_S, sa, bcur, sc);
+        issue_more(it);
+      }
+      return;
+    }
+  }
   if (warp >= NW) {
     // ============================================================ control warp
     // (strip windows: warp NW issues the MMAs and Y stores, warp NW + 1 the
     // ring and window loads, following the MMA warp's progress counter)
     const bool producer = C::NPROD && warp == NW + 1;
     if (lane == 0) {
-      tc::tma_prefetch_desc(C::WINS ? mapxw : mapx);
+      if constexpr (!C::LIFT) tc::tma_prefetch_desc(C::WINS ? mapxw : mapx);
       if (!LAST) tc::tma_prefetch_desc(mapy);
       auto issue = [&](int it) {  // tile `it` of this CTA into ring slot (rb + it) % NS
         if (it >= my_tiles) return;
@@ -882,7 +1020,8 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         const uint32_t slb = C::TW ? static_cast<uint32_t>(2 * (((TM / bs) + 1 + 7) & ~7) + 6 * K)
                                    : static_cast<uint32_t>(K * (TM / 2) * 10);
         const bool mk = C::TW && use_mask;
-        tc::mbar_expect_tx(&p.full[s], slb + nnew * winb + (mk ? C::MASKB : 0));
+        // (CSR = 9: the lift warps write the windows and arrive for them)
+        tc::mbar_expect_tx(&p.full[s], slb + (C::LIFT ? 0 : nnew * winb) + (mk ? C::MASKB : 0));
         tc::bulk_load_hint(slot + (C::TW ? C::O_TWS : 0), w_sl + static_cast<size_t>(off) * 16, slb, &p.full[s],
                            pol_stream);
         if constexpr (C::TW) {
@@ -891,11 +1030,13 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         auto load_win = [&](int q, int u) {
           tc::tma_load_2d_hint(p.win + (q % C::NWIN) * C::WINB, mapxw, 0, u * TM - w_halo, &p.full[s], pol_keep);
         };
-        if (nnew == 3) {
-          load_win(sa, t - w_S);
-          load_win(sb, t);
+        if constexpr (!C::LIFT) {
+          if (nnew == 3) {
+            load_win(sa, t - w_S);
+            load_win(sb, t);
+          }
+          load_win(sc, t + w_S);
         }
-        load_win(sc, t + w_S);
       };
       auto issue_more = [&](int it) {  // after afull(it) (it = -1: prologue)
         const int prot = it >= 0 ? bcur : 0;
@@ -1465,6 +1606,21 @@ k_layer_sell(DevCsr a, const __grid_constant__ SellMaps maps, const float* __res
   auto p = sell_setup<DP, CSR>(net.hidden, LAST);
   sell_layer<DP, LAST, OutT, CSR>(p, a, &maps.x, &maps.y, X, axlong, uwp, net, sc->out_scale, out, nullptr,
                                   &maps.xw);
+  sell_teardown(p);
+}
+
+// The first layer with the lift fused in (CSR = 9): no layer input in HBM.
+template <int DP, typename OutT>
+__global__ void __launch_bounds__(SellCfg<DP, 9>::NT, 1)
+k_layer_sell_lift(DevCsr a, const __grid_constant__ SellMaps maps, const void* __restrict__ in, int in_f64,
+                  const float* __restrict__ uwp, NetView net, const ApplyScalars* __restrict__ sc,
+                  const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  if (sc->zero) return;  // the last layer writes M(0) = 0
+  auto p = sell_setup<DP, 9>(net.hidden, false);
+  const LiftIO lio{in, in_f64, sc};
+  sell_layer<DP, false, OutT, 9>(p, a, &maps.x, &maps.y, nullptr, nullptr, uwp, net, sc->out_scale, nullptr, nullptr,
+                                 &maps.xw, &lio);
   sell_teardown(p);
 }
 

@@ -57,6 +57,11 @@ def test_strip_windows_vs_oracle_and_sell(capi, oc, gnp, cuda, grid):
         assert rel_l2(y, want) <= TOL and max_rel(y, want) <= TOL, (rel_l2(y, want), max_rel(y, want))
     assert np.array_equal(y_pw, y_sell)
     assert np.array_equal(y_pair, y_sell)
+    # the default strip-window apply fuses the lift into the first layer (its
+    # lift warps compute the row windows); the separate lift kernel must give
+    # the same bits
+    y_nofuse, _ = layout_apply(capi, ah, dims, p, b, {"GNPC_PW_MIN_TILES": "0", "GNPC_NO_LIFT_FUSE": "1"})
+    assert np.array_equal(y_pw, y_nofuse)
 
 
 def test_strip_windows_not_built_off_stride(capi, oc, gnp, cuda):
@@ -116,3 +121,47 @@ def test_strip_windows_repeatable_on_break_heavy_grid(capi, oc, gnp, cuda):
         assert np.array_equal(y, ys[0])
     want = oc.gnn_apply(ah, dims, p, b)
     assert rel_l2(ys[0], want) <= TOL and max_rel(ys[0], want) <= TOL
+
+
+def test_fused_lift_f32_device_input_and_repeats(capi, oc, gnp, cuda):
+    # the fused-lift first layer reading an fp32 device vector (the FGMRES /
+    # bench path), against the separate lift kernel, repeated (a lift-warp /
+    # window-ring race would show as run-to-run noise); 262^2: partial last
+    # tile, windows that run past both ends of the matrix
+    import torch
+
+    a0 = gnp.generate("c5_aniso9pt", 262, 1e-3, 30.0)
+    a = Csr(a0.n, np.array(a0.row_ptr), np.array(a0.col_idx), np.array(a0.values))
+    ah = oc.prescale(a, oc.gershgorin_gamma(a)).rounded_f32()
+    dims = (32, 32, 8)
+    p = f32(oc.init_params(*dims, 2))
+    b = torch.tensor(oc.gaussian_vector(9, ah.n), dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+
+    def run(env, reps):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            c = capi.Csr.from_arrays(ah.n, ah.row_ptr, ah.col_idx, ah.values)
+            m = capi.Model(c, dims, p)
+            outs = []
+            for _ in range(reps):
+                o = torch.full_like(b, float("nan"))
+                m.apply_device_f32(b.data_ptr(), o.data_ptr(), st)
+                torch.cuda.synchronize()
+                outs.append(o.cpu().numpy())
+            assert c.layout_flags() & PW
+            return outs
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+
+    fused = run({"GNPC_PW_MIN_TILES": "0"}, 10)
+    plain = run({"GNPC_PW_MIN_TILES": "0", "GNPC_NO_LIFT_FUSE": "1"}, 1)[0]
+    for y in fused:
+        assert np.array_equal(y, plain)
+    want = oc.gnn_apply(ah, dims, p, b.cpu().numpy().astype(np.float64))
+    assert rel_l2(plain, want) <= TOL and max_rel(plain, want) <= TOL

@@ -80,7 +80,8 @@ int gnpc_csr_info(gnpc_csr a, int64_t* n, int64_t* nnz);
  * *uploaded = 1 once it exists; *sliced_ell = 0 when no TMA-pipeline layout
  * was built, else a bit mask: 1 the 128-row sliced-ELL copy, 2 its pair-union
  * form (d = 32), 4 the strip-window pair-union form (d = 32), 16 the
- * training strip windows (built when a trainer uses the matrix); *long_rows = rows routed to the chunked long-row path (> 32
+ * training strip windows (built when a trainer uses the matrix), 32 the
+ * apply path's length-sorted node order (ragged matrices); *long_rows = rows routed to the chunked long-row path (> 32
  * nonzeros).  No reference counterpart. */
 int gnpc_csr_device_layout(gnpc_csr a, int* uploaded, int* sliced_ell, int* long_rows);
 int gnpc_csr_export(gnpc_csr a, int64_t* row_ptr, int64_t* col_idx, double* values);

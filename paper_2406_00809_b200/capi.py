@@ -132,7 +132,8 @@ class Csr:
 
     def layout_flags(self):
         """Bit mask of the device layouts built: 1 sliced-ELL, 2 pair-union,
-        4 strip-window pair-union (d = 32), 16 training strip windows."""
+        4 strip-window pair-union (d = 32), 16 training strip windows,
+        32 length-sorted node order for the apply (ragged matrices)."""
         u, s, l = C.c_int(), C.c_int(), C.c_int()
         check(lib().gnpc_csr_device_layout(self.h, C.byref(u), C.byref(s), C.byref(l)))
         return s.value

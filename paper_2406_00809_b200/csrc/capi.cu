@@ -86,11 +86,31 @@ int tc_ctas_per_sm(const void* kern, size_t smem, int tcols) {
 template <int DP>
 struct ApplyLaunch {
   template <typename InT, typename OutT>
+  // Ragged matrices: the pipeline runs on length-sorted nodes (DevCsr::perm);
+  // the input is gathered into that order first (τ is taken from it: the same
+  // values in another order) and the result scattered back at the end.
   static void run(gnpc_model_s& m, const InT* in, OutT* out, cudaStream_t s, const int* skip,
                   ApplyProf* prof) {
+    gnpc_csr_s& A = *m.a;
+    if (!A.has_perm) return run_ordered<InT, OutT>(m, in, out, s, skip, prof);
+    const int n = (int)A.h.n;
+    m.PIN.ensure((std::size_t)n);
+    m.POUT.ensure((std::size_t)n);
+    InT* pin = reinterpret_cast<InT*>(m.PIN.p);
+    OutT* pout = reinterpret_cast<OutT*>(m.POUT.p);
+    const int grid = std::max(1, std::min((n + gnpk::kThreads - 1) / gnpk::kThreads, m.sms * 8));
+    gnpk::k_perm_gather<InT><<<grid, gnpk::kThreads, 0, s>>>(in, A.perm.p, n, pin, skip);
+    GNPC_LAUNCHED();
+    run_ordered<InT, OutT>(m, pin, pout, s, skip, prof);
+    gnpk::k_perm_scatter<OutT><<<grid, gnpk::kThreads, 0, s>>>(pout, A.perm.p, n, out, skip);
+    GNPC_LAUNCHED();
+  }
+  template <typename InT, typename OutT>
+  static void run_ordered(gnpc_model_s& m, const InT* in, OutT* out, cudaStream_t s, const int* skip,
+                          ApplyProf* prof) {
     using namespace gnpk;
     gnpc_csr_s& A = *m.a;
-    DevCsr a = A.dev();
+    DevCsr a = A.dev_apply();
     const int n = a.n;
     const NetView& net = m.view;
     const int sms = m.sms;
@@ -376,11 +396,7 @@ void gnpc_csr_s::upload() {
     hci[k] = static_cast<int>(h.col_idx[k]);
     hv[k] = static_cast<float>(h.values[k]);
   }
-  for (std::int64_t i = 0; i < h.n; ++i) {
-    const int len = hrp[i + 1] - hrp[i];
-    max_row = std::max(max_row, len);
-    if (len > gnpk::kLongRow) longs.push_back(static_cast<int>(i));
-  }
+  for (std::int64_t i = 0; i < h.n; ++i) max_row = std::max(max_row, hrp[i + 1] - hrp[i]);
   // padded copies (row_ptr + 132 entries of nnz, col/val + 4 zeros): the
   // training TMA layers bulk-copy 16-byte-aligned supersets of a tile's range
   {
@@ -394,6 +410,57 @@ void gnpc_csr_s::upload() {
     ci.upload(pci.data(), pci.size());
     v.upload(pv.data(), pv.size());
   }
+  // Ragged matrices (the natural order pads a sliced-ELL copy by > 25 %): the
+  // apply path renumbers the nodes by row length (stable sort, ascending; a
+  // symmetric permutation of Â), so every 128-row tile holds rows of one
+  // length — no lane idles behind a longer neighbour, the sliced-ELL layout
+  // applies, and the long rows fill the last tiles.  Each row keeps its
+  // entries in stored order, so every sum and the output are bit-identical to
+  // the natural order's; M(b) gathers b and scatters its result through
+  // `perm`.  The FGMRES SpMV and the training kernels keep the natural order
+  // (rp / ci / v above).  GNPC_NO_ROWSORT=1 disables it.
+  has_perm = false;
+  build_sell(hrp, hci, hv);
+  {
+    const char* e = std::getenv("GNPC_NO_ROWSORT");
+    const char* ns = std::getenv("GNPC_NO_SELL");
+    if (!has_sell && !(e && e[0] == '1') && !(ns && ns[0] == '1') && h.n >= 128) {
+      const std::int64_t n = h.n;
+      std::vector<int> pm(n), inv(n);
+      for (std::int64_t i = 0; i < n; ++i) pm[i] = static_cast<int>(i);
+      std::stable_sort(pm.begin(), pm.end(), [&](int x, int y) { return hrp[x + 1] - hrp[x] < hrp[y + 1] - hrp[y]; });
+      for (std::int64_t i = 0; i < n; ++i) inv[pm[i]] = static_cast<int>(i);
+      std::vector<int> qrp(n + 1), qci(hci.size());
+      std::vector<float> qv(hv.size());
+      qrp[0] = 0;
+      for (std::int64_t i = 0; i < n; ++i) {
+        const int s0 = hrp[pm[i]], len = hrp[pm[i] + 1] - s0, d0 = qrp[i];
+        for (int k = 0; k < len; ++k) {
+          qci[d0 + k] = inv[hci[s0 + k]];
+          qv[d0 + k] = hv[s0 + k];
+        }
+        qrp[i + 1] = d0 + len;
+      }
+      hrp.swap(qrp);
+      hci.swap(qci);
+      hv.swap(qv);
+      std::vector<int> prp(hrp);
+      prp.resize(hrp.size() + 132, hrp.back());
+      std::vector<int> pci(hci);
+      pci.resize(hci.size() + 4, 0);
+      std::vector<float> pv(hv);
+      pv.resize(hv.size() + 4, 0.f);
+      prm_rp.upload(prp.data(), prp.size());
+      prm_ci.upload(pci.data(), pci.size());
+      prm_v.upload(pv.data(), pv.size());
+      perm.upload(pm.data(), pm.size());
+      has_perm = true;
+      build_sell(hrp, hci, hv);  // uniform tiles: the padding test passes now
+    }
+  }
+  // (from here on hrp / hci / hv are the apply path's view: permuted when has_perm)
+  for (std::int64_t i = 0; i < h.n; ++i)
+    if (hrp[i + 1] - hrp[i] > gnpk::kLongRow) longs.push_back(static_cast<int>(i));
   n_long = static_cast<int>(longs.size());
   if (n_long) {
     long_rows.upload(longs.data(), longs.size());
@@ -412,7 +479,6 @@ void gnpc_csr_s::upload() {
     ch_k1.upload(ck1.data(), ck1.size());
     long_c0.upload(c0.data(), c0.size());
   }
-  build_sell(hrp, hci, hv);
   build_pairs(hrp, hci, hv);
   build_pw(hrp, hci, hv);
   build_order(hrp, hci);
@@ -847,6 +913,19 @@ void gnpc_csr_s::build_pw(const std::vector<int>& hrp, const std::vector<int>& h
   has_pw = true;
 }
 
+// The apply path's view: the length-sorted renumbering when it was built
+// (has_perm), else dev() itself.
+gnpk::DevCsr gnpc_csr_s::dev_apply() {
+  gnpk::DevCsr d = dev();
+  if (has_perm) {
+    d.rp = prm_rp.p;
+    d.ci = prm_ci.p;
+    d.v = prm_v.p;
+    d.perm = perm.p;
+  }
+  return d;
+}
+
 gnpk::DevCsr gnpc_csr_s::dev() {
   upload();
   gnpk::DevCsr d;
@@ -855,6 +934,7 @@ gnpk::DevCsr gnpc_csr_s::dev() {
   d.rp = rp.p;
   d.ci = ci.p;
   d.v = v.p;
+  d.perm = nullptr;
   d.long_rows = n_long ? long_rows.p : nullptr;
   d.n_long = n_long;
   d.rps = rps.p;
@@ -1121,7 +1201,9 @@ void gnpc_model_s::ensure_workspace() {
 
 bool gnpc_model_s::fused_eligible() {
   a->upload();
-  if (dp != 16 || !use_tc || a->n_long != 0 || a->h.n == 0) return false;
+  // (length-sorted nodes: the input gather / output scatter would touch host
+  // memory at random; those applies stage through device buffers)
+  if (dp != 16 || !use_tc || a->n_long != 0 || a->h.n == 0 || a->has_perm) return false;
   if (gnpc_impl::sell_kernel_off() || gnpc_impl::fused_apply_off()) return false;
   const size_t smem = a->has_sell ? gnpk::SellCfg<16, 0>::smem_bytes(dims.hidden, true)
                                   : gnpk::SellCfg<16, 1>::smem_bytes(dims.hidden, true);
@@ -1627,7 +1709,7 @@ int gnpc_csr_device_layout(gnpc_csr a, int* uploaded, int* sliced_ell, int* long
     need(a, "null csr");
     if (uploaded) *uploaded = a->dev_ready ? 1 : 0;
     if (sliced_ell)
-      *sliced_ell = (a->has_sell ? 1 : 0) | (a->has_pairs ? 2 : 0) | (a->has_pw ? 4 : 0) |
+      *sliced_ell = (a->has_sell ? 1 : 0) | (a->has_pairs ? 2 : 0) | (a->has_pw ? 4 : 0) | (a->has_perm ? 32 : 0) |
                     (a->has_tw ? 16 : 0);
     if (long_rows) *long_rows = a->n_long;
   });
@@ -1803,7 +1885,7 @@ int gnpc_apply(gnpc_model m, const double* b, double* out) {
     // per-layer apply with a pinned output buffer: the last layer writes M(b)
     // through its device alias, so the device->host transfer overlaps that
     // layer instead of following it (C5: 33.5 MB of f64 over PCIe)
-    if (cudaPointerGetAttributes(&po, out) == cudaSuccess && po.type == cudaMemoryTypeHost &&
+    if (!m->a->has_perm && cudaPointerGetAttributes(&po, out) == cudaSuccess && po.type == cudaMemoryTypeHost &&
         po.devicePointer != nullptr) {
       m->launch_apply<double, double>(m->io_in.p, static_cast<double*>(po.devicePointer), m->stream, nullptr);
       GNPC_CUDA(cudaStreamSynchronize(m->stream));

@@ -173,6 +173,10 @@ struct gnpc_csr_s {
   gnpc_impl::DevBuf<int2> sell;
   gnpc_impl::DevBuf<int> sell_off, sell_k;
   bool has_sell = false;
+  // length-sorted renumbering of the apply path (ragged matrices; see upload())
+  gnpc_impl::DevBuf<int> perm, prm_rp, prm_ci;
+  gnpc_impl::DevBuf<float> prm_v;
+  bool has_perm = false;
   // padded short-row CSR + per-tile long flags for the TMA CSR layer (see DevCsr)
   gnpc_impl::DevBuf<int> rps, cis, tflag;
   gnpc_impl::DevBuf<float> vs;
@@ -213,6 +217,7 @@ struct gnpc_csr_s {
   void build_pw(const std::vector<int>& hrp, const std::vector<int>& hci, const std::vector<float>& hv);
   int dominant_tile_stride(const std::vector<int>& hrp, const std::vector<int>& hci, int TM) const;
   gnpk::DevCsr dev();
+  gnpk::DevCsr dev_apply();
 };
 
 // build_spectral_sampler (src/sampler.cpp:10-39): Arnoldi on the device,

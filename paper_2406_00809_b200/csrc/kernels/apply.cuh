@@ -32,6 +32,24 @@ struct NetView {
   int nbreak;
 };
 
+// ------------------------------------------------------------------ node renumbering
+// Ragged matrices run the apply on length-sorted nodes (DevCsr::perm):
+// dst[i] = src[perm[i]] before the lift, dst[perm[i]] = src[i] after the last layer.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+k_perm_gather(const T* __restrict__ src, const int* __restrict__ perm, int n, T* __restrict__ dst,
+              const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[perm[i]];
+}
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+k_perm_scatter(const T* __restrict__ src, const int* __restrict__ perm, int n, T* __restrict__ dst,
+               const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[perm[i]] = src[i];
+}
+
 // ------------------------------------------------------------------ lift (piecewise)
 // Same map as k_lift: per row one binary search over <= hidden kinks, then
 // DP FMAs (the H x DP MLP collapses because its input is a scalar).

@@ -22,6 +22,10 @@ struct DevCsr {
   const float* __restrict__ v;
   const int* __restrict__ long_rows;
   int n_long;
+  // Apply path on ragged matrices: nodes renumbered by row length; perm[i] =
+  // the original index of node i (nullptr: natural order).  With it rp / ci /
+  // v and every apply layout below are in the renumbered order.
+  const int* __restrict__ perm;
   // Sliced-ELL copy (128-row slices, entry (r, k) of slice t at
   // sell_off[t] + k*128 + r, padding (row, 0.0)); nullptr when the matrix's
   // row lengths are too ragged for it.  sell_k[t] = K_t | (has long row) << 16.

@@ -144,9 +144,13 @@ def test_fused_apply_zero_and_device_entry(capi, oc, cuda):
     check(out.double().cpu().numpy(), oc.gnn_apply(a, dims, p, b.astype(np.float32).astype(np.float64)))
 
 
-def test_fused_apply_csr_ragged_rows(capi, oc, cuda):
-    # ragged rows (1..32 entries, no long rows): no sliced-ELL copy, the fused
-    # launch runs the CSR-staged variant
+@pytest.mark.parametrize("rowsort", [False, True])
+def test_fused_apply_csr_ragged_rows(capi, oc, cuda, rowsort):
+    # ragged rows (1..32 entries, no long rows).  Natural order
+    # (GNPC_NO_ROWSORT=1): no sliced-ELL copy, the one-launch apply runs the
+    # CSR-staged variant.  Default: the apply renumbers the nodes by row length
+    # (flag 32), which makes the sliced-ELL copy applicable; each row keeps
+    # its stored order, so both give the same bits.
     n = 3000
     rng = np.random.default_rng(21)
     rows, cols, vals = [], [], []
@@ -161,11 +165,58 @@ def test_fused_apply_csr_ragged_rows(capi, oc, cuda):
     dims = (16, 32, 8)
     p = f32(oc.init_params(*dims, 4))
     b = oc.gaussian_vector(8, n)
-    A = capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
-    y = capi.Model(A, dims, p).apply(b)
-    uploaded, sell_built, nlong = A.device_layout()
-    assert uploaded and not sell_built and nlong == 0
+
+    def run(nosort):
+        if nosort:
+            os.environ["GNPC_NO_ROWSORT"] = "1"
+        try:
+            A = capi.Csr.from_arrays(a.n, a.row_ptr, a.col_idx, a.values)
+            y = capi.Model(A, dims, p).apply(b)
+            return y, A.layout_flags(), A.device_layout()[2]
+        finally:
+            os.environ.pop("GNPC_NO_ROWSORT", None)
+
+    y, flags, nlong = run(not rowsort)
+    assert nlong == 0
+    assert (flags & 32 and flags & 1) if rowsort else flags == 0, flags
     check(y, oc.gnn_apply(a, dims, p, b))
+    if rowsort:
+        assert np.array_equal(y, run(True)[0])
+
+
+def test_length_sorted_apply_bitwise_with_long_rows(capi, oc, gnp, cuda):
+    # power-law rows (long rows up to 2049 entries, the C4 generator at 2^15):
+    # the length-sorted apply (default) against the natural order, bit for
+    # bit, through the host f64 entry and the device f32 entry
+    import torch
+
+    a0 = gnp.generate("c4_powerlaw", 1 << 15, 2.2, 0.0, 4)
+    a = Csr(a0.n, np.array(a0.row_ptr), np.array(a0.col_idx), np.array(a0.values))
+    ah = oc.prescale(a, oc.gershgorin_gamma(a)).rounded_f32()
+    dims = (16, 32, 8)
+    p = f32(oc.init_params(*dims, 0))
+    b = oc.gaussian_vector(4, a.n)
+    bt = torch.tensor(b, dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    res = []
+    for nosort in (False, True):
+        if nosort:
+            os.environ["GNPC_NO_ROWSORT"] = "1"
+        try:
+            A = capi.Csr.from_arrays(ah.n, ah.row_ptr, ah.col_idx, ah.values)
+            m = capi.Model(A, dims, p)
+            y = m.apply(b)
+            o = torch.full_like(bt, float("nan"))
+            m.apply_device_f32(bt.data_ptr(), o.data_ptr(), st)
+            torch.cuda.synchronize()
+            flags, nlong = A.layout_flags(), A.device_layout()[2]
+            assert nlong > 0 and bool(flags & 32) == (not nosort), (flags, nlong)
+            res.append((y, o.cpu().numpy()))
+        finally:
+            os.environ.pop("GNPC_NO_ROWSORT", None)
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
+    check(res[0][0], oc.gnn_apply(ah, dims, p, b))
 
 
 def test_fused_apply_zero_copy_pinned_host(capi, oc, cuda):

@@ -559,6 +559,7 @@ struct TrainIO {
   int use_mask;
   const uint32_t* mask_in;
   uint8_t* mask_out;
+  int no_ax;  // KIND 1: skip the ÂX store (forward-only passes: the monitoring batch)
 };
 
 __device__ __forceinline__ float4 f4_trunc_lo(float4 v) {
@@ -1124,7 +1125,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
         // the buffer the epilogue after this MMA writes is free (waiting
         // after the MMA issue instead measured the same: C2, C4)
         tc::bulk_wait_read0();
-        if (KIND == 1 && it < my_tiles) {  // training forward: the tile's ÂX (A2_hi) to HBM
+        if (KIND == 1 && it < my_tiles && !tio->no_ax) {  // training forward: the tile's ÂX (A2_hi) to HBM
           tc::tma_store_2d(tio->mapax, p.A, 0, tile_at(it) * TM);
           tc::bulk_commit();
         }
@@ -1169,7 +1170,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
             }
           }
         }
-        if (KIND == 1 && it < my_tiles) tc::bulk_wait_read0();  // A2_hi is rewritten after the commit
+        if (KIND == 1 && it < my_tiles && !tio->no_ax) tc::bulk_wait_read0();  // A2_hi is rewritten after the commit
         if (it < my_tiles) tc::mma_commit(p.mma_bar);
         GNPC_TR_STAMP(11);
         // the projection of tile it-1 after MMA(it), on its own barrier: the
@@ -1639,7 +1640,8 @@ k_train_sell(DevCsr a, const __grid_constant__ TrainMaps maps, const float* __re
              const float* __restrict__ uwp, NetView net, int bs, int use_mask,
              const uint32_t* __restrict__ mask_in, uint8_t* __restrict__ mask_out) {
   auto p = sell_setup<DP, CSR>(net.hidden, false);
-  const TrainIO tio{&maps.ax, &maps.mask, bs, use_mask, mask_in, mask_out};
+  const TrainIO tio{&maps.ax, &maps.mask, bs, KIND == 2 ? use_mask : 0, mask_in, mask_out,
+                    KIND == 1 && (use_mask & 2) ? 1 : 0};
   sell_layer<DP, false, float, CSR, KIND>(p, a, &maps.x, &maps.y, X, nullptr, uwp, net, 1.0, nullptr, &tio,
                                           &maps.xw);
   sell_teardown(p);

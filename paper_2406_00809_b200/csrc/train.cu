@@ -44,6 +44,9 @@ struct gnpc_trainer_s {
   std::int64_t t = 0;
   std::int64_t P = 0;
   bool tc = false;
+  // forward-only trainer (the monitoring batch of train_preconditioner): the
+  // TMA layers skip the ÂX and mask-word stores only a backward would read
+  bool fwd_only = false;
   int sms = 0;
   cudaStream_t s = nullptr;
   // flat f64 master parameters, gradient, Adam moments
@@ -308,9 +311,12 @@ struct TrainLaunch {
           const float* uwp = (fwd ? T.m->UWP.p : T.UWP_bwd.p) + (size_t)l * 4 * DP * DP;
           const uint32_t* min_ = nullptr;
           uint8_t* mout = nullptr;
-          if (fwd && l + 1 <= T.L - 1) mout = reinterpret_cast<uint8_t*>(T.mbits.p + (size_t)(l + 1) * T.nvpad);
+          if (fwd && l + 1 <= T.L - 1 && !T.fwd_only)
+            mout = reinterpret_cast<uint8_t*>(T.mbits.p + (size_t)(l + 1) * T.nvpad);
           if (!fwd && mask != nullptr) min_ = T.mbits.p + (size_t)l * T.nvpad;
-          kern<<<grid, S::NT, smem, T.s>>>(a, maps, X, uwp, T.m->view, T.B, mask != nullptr ? 1 : 0, min_, mout);
+          // (forward: bit 1 of the mask argument = no ÂX store)
+          kern<<<grid, S::NT, smem, T.s>>>(a, maps, X, uwp, T.m->view, T.B,
+                                           fwd ? (T.fwd_only ? 2 : 0) : (mask != nullptr ? 1 : 0), min_, mout);
           GNPC_LAUNCHED();
           return;
         }
@@ -338,11 +344,12 @@ struct TrainLaunch {
         const uint32_t* min_ = nullptr;
         uint8_t* mout = nullptr;
         if (T.mbits.p) {
-          if (fwd && l + 1 <= T.L - 1) mout = reinterpret_cast<uint8_t*>(T.mbits.p + (size_t)(l + 1) * T.nvpad);
+          if (fwd && l + 1 <= T.L - 1 && !T.fwd_only)
+            mout = reinterpret_cast<uint8_t*>(T.mbits.p + (size_t)(l + 1) * T.nvpad);
           if (!fwd && mask != nullptr) min_ = T.mbits.p + (size_t)l * T.nvpad;
         }
-        kern<<<grid, S::NT, smem, T.s>>>(a, maps, X, uwp, T.m->view, T.B, mask != nullptr ? 1 : 0, min_,
-                                         mout);
+        kern<<<grid, S::NT, smem, T.s>>>(a, maps, X, uwp, T.m->view, T.B,
+                                         fwd ? (T.fwd_only ? 2 : 0) : (mask != nullptr ? 1 : 0), min_, mout);
         GNPC_LAUNCHED();
         return;
       }
@@ -1083,6 +1090,7 @@ void train_run(gnpc_csr_s* a, const gnpc_train_config* cfg, double* best, double
   std::unique_ptr<gnpc_trainer_s> tr(create(model.get(), B, cfg->lr));
   std::unique_ptr<gnpc_trainer_s> mon(MB == B ? nullptr : create(model.get(), MB, cfg->lr));
   gnpc_trainer_s& M = mon ? *mon : *tr;
+  if (mon) mon->fwd_only = true;  // the monitoring trainer never runs a backward
   cudaStream_t s = tr->s;  // every trainer of a model runs on the model's stream
   // the monitoring batch: drawn once on the host (Rng(seed+2)), resident
   DevBuf<double> mxd, mbd;

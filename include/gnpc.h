@@ -233,6 +233,12 @@ int gnpc_sampler_export(gnpc_sampler s, double* v, double* zsv, double* sv);
  * s may be NULL when spectral_count == 0. */
 int gnpc_assemble_batch(gnpc_sampler s, gnpc_csr a, uint64_t seed, int64_t skip_batches,
                         int64_t batch, int64_t spectral_count, double* x, double* b);
+/* The same batch from the device generator gnpc_train_preconditioner uses
+ * (reference Rng stream: host MT19937-64 words, device tempering and
+ * Box-Muller; spectral x = V (Zsv S^-1 eps) and b = A x on the device,
+ * src/sampler.cpp:41-83).  For parity tests against gnpc_assemble_batch. */
+int gnpc_device_pairs(gnpc_sampler s, gnpc_csr a, uint64_t seed, int64_t skip_batches, int64_t batch,
+                      int64_t spectral_count, double* x, double* b);
 
 /* train_preconditioner (src/gnn.cpp:401-451): Gaussian and spectral pairs
  * (spectral_count of each batch), monitor batch, best snapshot.

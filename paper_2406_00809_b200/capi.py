@@ -440,6 +440,18 @@ def assemble_batch(csr: Csr, sampler: Sampler | None, seed, skip_batches, batch,
     return x, b
 
 
+def device_pairs(csr: Csr, sampler: Sampler | None, seed, skip_batches, batch, spectral_count):
+    """The same batch from the device pair generator of train_preconditioner."""
+    n = csr.info()[0]
+    x = np.empty(n * batch)
+    b = np.empty(n * batch)
+    check(lib().gnpc_device_pairs(sampler.h if sampler else None, csr.h, C.c_uint64(seed),
+                                  C.c_int64(skip_batches), C.c_int64(batch),
+                                  C.c_int64(spectral_count), x.ctypes.data_as(vp),
+                                  b.ctypes.data_as(vp)))
+    return x, b
+
+
 def train_preconditioner(csr: Csr, dims=(16, 32, 8), lr=1e-3, steps=2000, batch=16, spectral=8,
                          arnoldi_m=40, seed=0, monitor_batch=16):
     cfg = TrainConfig(lr, steps, batch, spectral, arnoldi_m, seed, monitor_batch, *dims)

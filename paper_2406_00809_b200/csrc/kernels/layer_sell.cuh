@@ -67,6 +67,22 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
   for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld4x2(uint32_t ta, uint32_t tb, float (&u)[4], float (&v)[4]) {
+  uint32_t r[4], q[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(ta));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3])
+               : "r"(tb));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    u[i] = __uint_as_float(r[i]);
+    v[i] = __uint_as_float(q[i]);
+  }
+}
+
 // 2-D tile store smem -> global (bulk-group completion), under an L2 policy
 __device__ __forceinline__ void tma_store_2d_hint(const void* tmap, const void* src, int x, int y, uint64_t pol) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
@@ -1252,16 +1268,14 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
       float v[CW];
       if constexpr (CW == 4) {
         float v2[4];
-        tc::tmem_ld4(taddr, v);
-        tc::tmem_ld4(taddr + DP, v2);
+        tc::tmem_ld4x2(taddr, taddr + DP, v, v2);  // both halves in flight, one wait
 #pragma unroll
         for (int c = 0; c < 4; ++c) v[c] += v2[c];
       } else {
 #pragma unroll
         for (int c0 = 0; c0 < CW; c0 += 8) {
           float u1[8], u2[8];
-          tc::tmem_ld8(taddr + c0, u1);
-          tc::tmem_ld8(taddr + DP + c0, u2);
+          tc::tmem_ld8x2(taddr + c0, taddr + DP + c0, u1, u2);  // both halves in flight, one wait
 #pragma unroll
           for (int c = 0; c < 8; ++c) v[c0 + c] = u1[c] + u2[c];
         }
@@ -1336,6 +1350,18 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   // out[i] (the rotating group alone doing the whole reduction made every
   // tile wait for it: C5 last layer ~19 % of stalls on the MMA barrier).
   float* PART = D2 + H;  // [2][NQ][TM]
+  // hidden 32: the warp's 8 projection columns' b1 / dec2 live in registers
+  // (they were two shared-memory reads per element: the hottest line of the
+  // last layer's profile), and both accumulator halves load under one wait
+  float b1r[8], d2r[8];
+  const bool proj8 = TCP && H / NQ == 8;
+  if (proj8) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      b1r[c] = B1[(warp >> 2) * 8 + c];
+      d2r[c] = D2[(warp >> 2) * 8 + c];
+    }
+  }
   auto proj_epilogue = [&](int itp) {
     tc::mbar_wait_dbg(p.pbar, itp & 1, 7, itp);  // the projection MMA of tile itp
     tc::fence_after();
@@ -1343,6 +1369,12 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
     const int hc = H / NQ;  // H % 16 == 0 (tensor-core projection)
     const uint32_t prow = p.tmem + 2 * DP + (static_cast<uint32_t>(32 * q) << 16) + cq * hc;
     float o = 0.f;
+    if (proj8) {
+      float z1[8], z2[8];
+      tc::tmem_ld8x2(prow, prow + H, z1, z2);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) o = fmaf(relu(z1[c] + z2[c] + b1r[c]), d2r[c], o);
+    } else
     for (int h0 = 0; h0 < hc; h0 += 4) {
       float z1[4], z2[4];
       tc::tmem_ld4(prow + h0, z1);

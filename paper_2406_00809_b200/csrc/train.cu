@@ -1288,7 +1288,58 @@ void train_run(gnpc_csr_s* a, const gnpc_train_config* cfg, double* best, double
   }
 }
 
+// One batch of training pairs from the DEVICE generator train_run uses
+// (host MT19937-64 words -> device tempering / Box-Muller; spectral columns
+// x = V coef as a device tall-skinny product; b = A x in f64 on the device),
+// after dropping skip_batches batches; returned as n x batch col-major like
+// assemble_batch (src/sampler.cpp:68-83), for parity tests against it.
+void device_pairs(gnpc_csr_s* a, const gnpc_sampler_s* smp, std::uint64_t seed, std::int64_t skip_batches,
+                  std::int64_t B, std::int64_t S, double* x, double* b) {
+  need(a && x && b, "device_pairs: null argument");
+  if (B < 1) throw std::invalid_argument("assemble_batch: empty batch");
+  if (S < 0 || S > B) throw std::invalid_argument("device_pairs: spectral_count must be in [0, batch]");
+  if (S > 0 && !smp) throw std::invalid_argument("device_pairs: spectral columns need a sampler");
+  if (skip_batches < 0) throw std::invalid_argument("device_pairs: skip_batches must be >= 0");
+  require_device();
+  const gnp_b200::SpectralSampler* sp = smp ? &smp->s : nullptr;
+  const std::int64_t n = a->h.n;
+  gnp_b200::PairStream ps(seed, n, B, S, sp);
+  const gnp_b200::PairBatchLayout& lay = ps.layout();
+  PinnedBuf hs(lay.bytes);
+  for (std::int64_t q = 0; q <= skip_batches; ++q) ps.fill(hs.p);
+  cudaStream_t s = nullptr;
+  DevBuf<unsigned char> ds(lay.bytes);
+  DevBuf<double> a64, vdev, xd((std::size_t)n * B), bd((std::size_t)n * B);
+  a64.upload(a->h.values.data(), a->h.values.size(), s);
+  if (S > 0) vdev.upload(sp->v.data(), sp->v.size(), s);
+  GNPC_CUDA(cudaMemcpyAsync(ds.p, hs.p, lay.bytes, cudaMemcpyHostToDevice, s));
+  const gnpk::DevCsr adev = a->dev();
+  const int pgrid = (int)((n * B + kTh - 1) / kTh);
+  gnpk::k_pairs_x<<<pgrid, kTh, 0, s>>>(reinterpret_cast<const gnpk::PairColDev*>(ds.p + lay.cols_off),
+                                        reinterpret_cast<const double*>(ds.p + lay.coef_off),
+                                        reinterpret_cast<const unsigned long long*>(ds.p + lay.words_off), vdev.p,
+                                        (int)lay.m, (int)n, (int)B, xd.p);
+  GNPC_LAUNCHED();
+  const int grid = grid_for(n * 32, kTh, num_sms() * 8);
+  gnpk::k_spmm_nb_f64<<<grid, kTh, 0, s>>>(adev, a64.p, (int)B, xd.p, bd.p);
+  GNPC_LAUNCHED();
+  std::vector<double> hx((std::size_t)n * B), hb((std::size_t)n * B);
+  GNPC_CUDA(cudaMemcpyAsync(hx.data(), xd.p, hx.size() * 8, cudaMemcpyDeviceToHost, s));
+  GNPC_CUDA(cudaMemcpyAsync(hb.data(), bd.p, hb.size() * 8, cudaMemcpyDeviceToHost, s));
+  GNPC_CUDA(cudaStreamSynchronize(s));
+  for (std::int64_t i = 0; i < n; ++i)  // [n][B] -> col-major n x B
+    for (std::int64_t c = 0; c < B; ++c) {
+      x[c * n + i] = hx[i * B + c];
+      b[c * n + i] = hb[i * B + c];
+    }
+}
+
 }  // namespace
+
+int gnpc_device_pairs(gnpc_sampler s, gnpc_csr a, uint64_t seed, int64_t skip_batches, int64_t batch,
+                      int64_t spectral_count, double* x, double* b) {
+  return guarded([&] { device_pairs(a, s, seed, skip_batches, batch, spectral_count, x, b); });
+}
 
 int gnpc_train_preconditioner(gnpc_csr a, const gnpc_train_config* cfg, double* best,
                               double* losses, double* best_loss) {

@@ -65,6 +65,31 @@ def test_sampler_errors(capi, cuda):
         capi.Sampler(B, 0, 0)  # m < 1
 
 
+@pytest.mark.parametrize("grid,m,batch,spectral,skip", [(16, 20, 8, 4, 1), (24, 40, 16, 8, 0), (24, 40, 6, 0, 2)])
+def test_device_pairs_match_oracle_sampling(capi, oc, cuda, grid, m, batch, spectral, skip):
+    # the training loop's DEVICE pair generator (host MT19937-64 words, device
+    # tempering + Box-Muller; spectral x = V (Zsv S^-1 eps) as a device
+    # tall-skinny product; b = A x in f64 on the device) against the oracle's
+    # assemble_batch (src/sampler.cpp:41-83) on the same factors and stream:
+    # 1e-12 (the Gaussian columns differ by libm-vs-device log/cos rounding,
+    # the spectral columns by the product's summation order)
+    a = oc.prescale(oc.gen_convection_diffusion(grid, 0.5), 8.0).rounded_f32()
+    s = capi.Sampler(dev_csr(capi, a), m, 3)
+    v, z, sv = s.factors()
+    fac = {"v": v, "zsv": z, "s": sv, "k": s.k, "m_eff": s.m_eff}
+    xd, bd = capi.device_pairs(s.csr, s if spectral else None, 11, skip, batch, spectral)
+    xo, bo = oc.assemble_batch(a, fac, 11, skip, batch, spectral)
+    n = a.n
+    for c in range(batch):
+        xs, xr = xd[c * n:(c + 1) * n], xo[c * n:(c + 1) * n]
+        bs, br = bd[c * n:(c + 1) * n], bo[c * n:(c + 1) * n]
+        assert np.max(np.abs(xs - xr)) <= 1e-12 * max(1.0, np.max(np.abs(xr))), (c, np.max(np.abs(xs - xr)))
+        assert np.max(np.abs(bs - br)) <= 1e-12 * max(1.0, np.max(np.abs(br))), (c, np.max(np.abs(bs - br)))
+    # and it is the host assemble_batch of the product up to the same level
+    xh, bh = capi.assemble_batch(s.csr, s if spectral else None, 11, skip, batch, spectral)
+    assert np.max(np.abs(xd - xh)) <= 1e-12 * np.max(np.abs(xh))
+
+
 def test_train_preconditioner_spectral_tracks_reference(capi, oc, cuda):
     # reference train_preconditioner with 4 spectral + 4 Gaussian pairs per batch
     g = golden("train_run_spectral.npz")

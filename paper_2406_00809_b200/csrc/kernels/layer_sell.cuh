@@ -453,7 +453,9 @@ __device__ __forceinline__ void gather_pair_rows(const float* __restrict__ X, in
 // — R = 144 w + row, idx = 128 R + 16 (R & 7), i.e. with the SWIZZLE_128B
 // chunk bits of lane group 0 — so lane gl reads (wbase + idx) ^ (gl << 4),
 // wrapped once around the NWIN-window ring.  Padding entries carry weight 0.
-template <int NG>
+// WRAP = false: the tile's three windows sit in consecutive ring slots
+// without wrapping (3 tiles of NWIN = 5), so the per-entry wrap test is dropped.
+template <int NG, bool WRAP>
 __device__ __forceinline__ void gather_pw_rows(const uint8_t* sl, int K, int gid, int gl, uint32_t wbase,
                                                uint32_t wlim, uint32_t wring, float4 (&acc)[2]) {
   const uint16_t* idx = reinterpret_cast<const uint16_t*>(sl) + gid * K;
@@ -469,7 +471,7 @@ __device__ __forceinline__ void gather_pw_rows(const uint8_t* sl, int K, int gid
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       uint32_t v = wbase + e[u];
-      v = v >= wlim ? v - wring : v;
+      if constexpr (WRAP) v = v >= wlim ? v - wring : v;
       x[u] = tc::lds4(v ^ gx);
     }
     fma4(acc[0], a0.x, x[0]);
@@ -1238,6 +1240,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   // projection MMA, and the rotating group reads the projection accumulator
   // one tile later (proj_epilogue).
   auto epilogue = [&](int itp) -> bool {
+    // (a suspend-time hint on this try_wait measured the same: C5, C2)
     tc::mbar_wait_dbg(p.mma_bar, (mb + itp) & 1, 2, itp);
     tc::fence_after();
     {
@@ -1454,7 +1457,8 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
     }
     if (have) {
       const int K = C::CSRL ? 0 : (kw & 0xffff);
-      const bool haslong = !TR && (C::CSRL ? kw != 0 : (kw >> 16) != 0);
+      // (strip-window layouts are built only for matrices without long rows)
+      const bool haslong = !TR && !C::WINS && (C::CSRL ? kw != 0 : (kw >> 16) != 0);
       const bool staged = K > 0 && K <= C::KCAP;
       if (!TR)  // prefetch
         kw = it + 1 < my_tiles ? (use_sched ? sch_k[it + 1] : __ldg(tinfo + tile_at(it + 1))) : 0;
@@ -1549,8 +1553,11 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
           gather_csr_rows<DP, R, C::USC>(xbj, DP * 4ull, a.cis, a.vs, sj, lj, self, acc, pol_keep);
       } else {
         if constexpr (C::PW) {
+          // (a second, wrap-free instance of the gather for the 3 tiles in 5
+          // whose windows do not wrap measured slower: C5 layer 331 vs 326 us)
           if constexpr (R == 2)
-            gather_pw_rows<C::NG>(slot, K, gid, gl, wbase, wring0 + C::NWIN * C::WINB, C::NWIN * C::WINB, acc);
+            gather_pw_rows<C::NG, true>(slot, K, gid, gl, wbase, wring0 + C::NWIN * C::WINB, C::NWIN * C::WINB,
+                                        acc);
         } else if constexpr (C::PAIR) {
           if (staged)
             gather_pair_rows<DP, C::US, C::NG, true>(X, gl, reinterpret_cast<const int4*>(slot + C::OPB), K, gid,

@@ -87,21 +87,17 @@ template <int DP>
 struct ApplyLaunch {
   template <typename InT, typename OutT>
   // Ragged matrices: the pipeline runs on length-sorted nodes (DevCsr::perm);
-  // the input is gathered into that order first (τ is taken from it: the same
-  // values in another order) and the result scattered back at the end.
+  // the lift reads b through the permutation (the norm reads b as it is, so τ
+  // has the natural order's bits) and the result is scattered back at the end.
   static void run(gnpc_model_s& m, const InT* in, OutT* out, cudaStream_t s, const int* skip,
                   ApplyProf* prof) {
     gnpc_csr_s& A = *m.a;
     if (!A.has_perm) return run_ordered<InT, OutT>(m, in, out, s, skip, prof);
     const int n = (int)A.h.n;
-    m.PIN.ensure((std::size_t)n);
     m.POUT.ensure((std::size_t)n);
-    InT* pin = reinterpret_cast<InT*>(m.PIN.p);
     OutT* pout = reinterpret_cast<OutT*>(m.POUT.p);
     const int grid = std::max(1, std::min((n + gnpk::kThreads - 1) / gnpk::kThreads, m.sms * 8));
-    gnpk::k_perm_gather<InT><<<grid, gnpk::kThreads, 0, s>>>(in, A.perm.p, n, pin, skip);
-    GNPC_LAUNCHED();
-    run_ordered<InT, OutT>(m, pin, pout, s, skip, prof);
+    run_ordered<InT, OutT>(m, in, pout, s, skip, prof);
     gnpk::k_perm_scatter<OutT><<<grid, gnpk::kThreads, 0, s>>>(pout, A.perm.p, n, out, skip);
     GNPC_LAUNCHED();
   }
@@ -190,7 +186,7 @@ struct ApplyLaunch {
       const int ng = kThreads / (DP / 4);
       int grid = std::min((n + ng - 1) / ng, sms * 8);
       grid = std::max(grid, 1);
-      kern<<<grid, kThreads, smem, s>>>(in, n, net, m.sc.p, m.X[0].p, skip);
+      kern<<<grid, kThreads, smem, s>>>(in, n, net, m.sc.p, m.X[0].p, skip, a.perm);
       GNPC_LAUNCHED();
     }
     using Cfg = LayerCfg<DP>;

@@ -33,15 +33,9 @@ struct NetView {
 };
 
 // ------------------------------------------------------------------ node renumbering
-// Ragged matrices run the apply on length-sorted nodes (DevCsr::perm):
-// dst[i] = src[perm[i]] before the lift, dst[perm[i]] = src[i] after the last layer.
-template <typename T>
-__global__ void __launch_bounds__(kThreads)
-k_perm_gather(const T* __restrict__ src, const int* __restrict__ perm, int n, T* __restrict__ dst,
-              const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[perm[i]];
-}
+// Ragged matrices run the apply on length-sorted nodes (DevCsr::perm): the
+// lift reads b[perm[i]] (the norm reads b in its own order, so τ does not
+// depend on the layout), and dst[perm[i]] = src[i] after the last layer.
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
 k_perm_scatter(const T* __restrict__ src, const int* __restrict__ perm, int n, T* __restrict__ dst,
@@ -56,7 +50,7 @@ k_perm_scatter(const T* __restrict__ src, const int* __restrict__ perm, int n, T
 template <int DP, typename T>
 __global__ void __launch_bounds__(kThreads)
 k_lift_pw(const T* __restrict__ in, int n, NetView net, const ApplyScalars* __restrict__ sc,
-          float* __restrict__ X, const int* __restrict__ skip) {
+          float* __restrict__ X, const int* __restrict__ skip, const int* __restrict__ perm = nullptr) {
   if (skip && *skip) return;
   if (sc->zero) return;
   constexpr int G = DP / 4, NG = kThreads / G;
@@ -74,7 +68,7 @@ k_lift_pw(const T* __restrict__ in, int n, NetView net, const ApplyScalars* __re
   const int gl = threadIdx.x % G;
   const double in_scale = sc->in_scale;
   for (int row = blockIdx.x * NG + threadIdx.x / G; row < n; row += gridDim.x * NG) {
-    const float v = static_cast<float>(in_scale * static_cast<double>(in[row]));
+    const float v = static_cast<float>(in_scale * static_cast<double>(in[perm ? perm[row] : row]));
     int lo = 0, hi = nb;  // interval = #kinks <= v
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;

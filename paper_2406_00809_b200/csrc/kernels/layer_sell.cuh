@@ -1818,7 +1818,8 @@ k_apply_sell(DevCsr a, const __grid_constant__ ApplyFused f, const InT* __restri
 #pragma unroll
       for (int k = 0; k < LT; ++k) {
         const int row = (t0 + k * gridDim.x) * C::TM + r;
-        v[k] = row < n ? static_cast<float>(in_scale * static_cast<double>(src[row])) : 0.f;
+        // (length-sorted nodes: row i of the pipeline is node perm[i] of b)
+        v[k] = row < n ? static_cast<float>(in_scale * static_cast<double>(src[a.perm ? a.perm[row] : row])) : 0.f;
       }
 #pragma unroll
       for (int k = 0; k < LT; ++k) {

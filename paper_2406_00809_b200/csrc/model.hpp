@@ -47,8 +47,8 @@ struct gnpc_model_s {
   void* fused_stash = nullptr;  // gnpc_apply zero-copy: device copy of the host input
   bool fused_eligible();        // the apply runs as the single persistent launch
   gnpc_impl::DevBuf<gnpk::ApplyScalars> sc;
-  // input / output in the apply path's length-sorted node order (ragged matrices)
-  gnpc_impl::DevBuf<double> PIN, POUT;
+  // M(b) in the apply path's length-sorted node order (ragged matrices), before the scatter
+  gnpc_impl::DevBuf<double> POUT;
   int sms = 0, norm_grid = 0;
   cudaStream_t stream = nullptr;
 

@@ -251,3 +251,43 @@ print(json.dumps({"h": [e[1] for e in s["history"]], "st": s["status"], "hg": [e
     want = oc.fgmres(a, b, rtol=1e-8, maxiters=120, restart=30)
     assert want["status"] == o["st"] and len(want["history"]) == len(o["h"])
     assert abs(want["history"][-1][1] - o["h"][-1]) <= 1e-6 * want["history"][-1][1]
+
+
+def test_fgmres_on_length_sorted_ragged_matrix(capi, oc, gnp, cuda):
+    # power-law rows (the C4 generator at 2^12): the apply inside FGMRES runs
+    # on length-sorted nodes (gather b / scatter M(b)), the SpMV and the MGS
+    # on the natural order; against the oracle's f64 FGMRES on the same
+    # fp32-rounded inputs, and against the natural-order apply bit for bit
+    import os
+
+    from oracle import Csr
+
+    a0 = gnp.generate("c4_powerlaw", 1 << 12, 2.2, 0.0, 4)
+    a = Csr(a0.n, np.array(a0.row_ptr), np.array(a0.col_idx), np.array(a0.values))
+    ah = oc.prescale(a, oc.gershgorin_gamma(a)).rounded_f32()
+    dims = (16, 32, 8)
+    p = f32(oc.init_params(*dims, 0))
+    b = oc.spmv(ah, oc.gaussian_vector(2, ah.n))
+    res = []
+    for nosort in (False, True):
+        if nosort:
+            os.environ["GNPC_NO_ROWSORT"] = "1"
+        try:
+            A = dev_csr(capi, ah)
+            m = capi.Model(A, dims, p)
+            s = capi.fgmres(A, b, model=m, rtol=1e-6, maxiters=40, restart=20)
+            assert bool(A.layout_flags() & 32) == (not nosort)
+            res.append(s)
+        finally:
+            os.environ.pop("GNPC_NO_ROWSORT", None)
+    want = oc.fgmres(ah, b, kind=1, dims=dims, params=p, rtol=1e-6, maxiters=40, restart=20)
+    s = res[0]
+    assert s["status"] == want["status"]
+    assert abs(s["history"][-1][0] - want["history"][-1][0]) <= 1
+    hw = np.array([h[1] for h in want["history"]])
+    hs = np.array([h[1] for h in s["history"]])
+    k = min(len(hw), len(hs))
+    assert np.max(np.abs(hs[:k] - hw[:k]) / hw[:k]) <= 5e-2
+    # same bits as the natural order: the permuted apply changes no sum
+    assert np.array_equal(res[0]["x"], res[1]["x"])
+    assert [h[1] for h in res[0]["history"]] == [h[1] for h in res[1]["history"]]

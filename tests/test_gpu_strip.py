@@ -165,3 +165,29 @@ def test_fused_lift_f32_device_input_and_repeats(capi, oc, gnp, cuda):
         assert np.array_equal(y, plain)
     want = oc.gnn_apply(ah, dims, p, b.cpu().numpy().astype(np.float64))
     assert rel_l2(plain, want) <= TOL and max_rel(plain, want) <= TOL
+
+
+def test_zero_input_through_fused_lift_and_sorted_apply(capi, oc, gnp, cuda):
+    # M(0) = 0 (tau = 0: src/gnn.cpp:128-136) through the fused-lift first
+    # layer (d = 32 strip windows) and through the length-sorted apply
+    a0 = gnp.generate("c5_aniso9pt", 256, 1e-3, 30.0)
+    os.environ["GNPC_PW_MIN_TILES"] = "0"
+    try:
+        c = capi.Csr.from_arrays(a0.n, np.array(a0.row_ptr), np.array(a0.col_idx), np.array(a0.values))
+        ch = c.prescale(c.gamma())
+        m = capi.Model(ch, (32, 32, 8), capi.init_params(32, 32, 8, 0))
+        y = m.apply(np.zeros(a0.n))
+        assert ch.layout_flags() & PW
+    finally:
+        os.environ.pop("GNPC_PW_MIN_TILES", None)
+    assert np.all(y == 0.0)
+    # a nonzero apply afterwards is unaffected
+    b = np.random.default_rng(0).standard_normal(a0.n)
+    y1 = m.apply(b)
+    assert np.all(np.isfinite(y1)) and np.any(y1 != 0.0) and np.array_equal(y1, m.apply(b))
+    r0 = gnp.generate("c4_powerlaw", 1 << 12, 2.2, 0.0, 4)
+    r = capi.Csr.from_arrays(r0.n, np.array(r0.row_ptr), np.array(r0.col_idx), np.array(r0.values))
+    rh = r.prescale(r.gamma())
+    mr = capi.Model(rh, (16, 32, 8), capi.init_params(16, 32, 8, 0))
+    assert np.all(mr.apply(np.zeros(r0.n)) == 0.0)
+    assert rh.layout_flags() & 32

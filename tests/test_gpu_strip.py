@@ -191,3 +191,22 @@ def test_zero_input_through_fused_lift_and_sorted_apply(capi, oc, gnp, cuda):
     mr = capi.Model(rh, (16, 32, 8), capi.init_params(16, 32, 8, 0))
     assert np.all(mr.apply(np.zeros(r0.n)) == 0.0)
     assert rh.layout_flags() & 32
+
+
+@pytest.mark.parametrize("dims", [(32, 16, 2), (32, 32, 3), (32, 8, 4), (32, 64, 2), (24, 32, 3)])
+def test_strip_windows_other_network_shapes(capi, oc, gnp, cuda, dims):
+    # strip windows + fused lift with other hidden widths and depths: two
+    # layers (the fused first layer feeds the last layer directly), hidden 16 /
+    # 64 (tensor-core projection), hidden 8 (CUDA-core projection), d = 24
+    # (padded to 32), against the oracle and the sliced-ELL path
+    a0 = gnp.generate("c5_aniso9pt", 250, 1e-3, 30.0)
+    a = Csr(a0.n, np.array(a0.row_ptr), np.array(a0.col_idx), np.array(a0.values))
+    ah = oc.prescale(a, oc.gershgorin_gamma(a)).rounded_f32()
+    p = f32(oc.init_params(*dims, 5))
+    b = oc.gaussian_vector(7, a.n)
+    y_pw, f_pw = layout_apply(capi, ah, dims, p, b, {"GNPC_PW_MIN_TILES": "0"})
+    assert f_pw & PW, f_pw
+    y_sell, _ = layout_apply(capi, ah, dims, p, b, {"GNPC_NO_PW": "1", "GNPC_NO_PAIR": "1"})
+    want = oc.gnn_apply(ah, dims, p, b)
+    assert rel_l2(y_pw, want) <= TOL and max_rel(y_pw, want) <= TOL, (rel_l2(y_pw, want), max_rel(y_pw, want))
+    assert np.array_equal(y_pw, y_sell)

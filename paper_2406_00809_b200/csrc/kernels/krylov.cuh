@@ -40,6 +40,41 @@ __device__ __forceinline__ double row_dot_q(const DevCsr& a, int i, bool valid,
   return s;
 }
 
+// Eight rows per warp: rows of up to kSpmvLong entries by their quad
+// (row_dot_q); longer rows (power-law matrices: up to thousands of entries,
+// which left seven quads idle behind one) one after another by the whole
+// warp, 32 lanes striding the row with two accumulators, then a shuffle tree.
+// Every lane returns the sum of its quad's row.
+constexpr int kSpmvLong = 64;
+__device__ __forceinline__ double row_dot_warp8(const DevCsr& a, int base, const double* __restrict__ x,
+                                                int lane) {
+  const int q = lane & 3, g = lane >> 2;
+  const int i = base + g;
+  const bool valid = i < a.n;
+  const int len = valid ? __ldg(a.rp + i + 1) - __ldg(a.rp + i) : 0;
+  const bool is_long = len > kSpmvLong;
+  double s = row_dot_q(a, i, valid && !is_long, x, q);
+  unsigned m = __ballot_sync(0xffffffffu, is_long && q == 0);
+  while (m) {
+    const int gl = (__ffs(m) - 1) >> 2;
+    m &= m - 1;
+    const int ii = base + gl;
+    const int e0 = __ldg(a.rp + ii), e1 = __ldg(a.rp + ii + 1);
+    double t0 = 0.0, t1 = 0.0;
+    int k = e0 + lane;
+    for (; k + 32 < e1; k += 64) {
+      t0 = fma(static_cast<double>(__ldg(a.v + k)), x[__ldg(a.ci + k)], t0);
+      t1 = fma(static_cast<double>(__ldg(a.v + k + 32)), x[__ldg(a.ci + k + 32)], t1);
+    }
+    if (k < e1) t0 = fma(static_cast<double>(__ldg(a.v + k)), x[__ldg(a.ci + k)], t0);
+    double t = t0 + t1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (g == gl) s = t;
+  }
+  return s;
+}
+
 // y = A x (fp64 vectors).
 __global__ void __launch_bounds__(kThreads)
 k_spmv_f64(DevCsr a, const double* __restrict__ x, double* __restrict__ y) {
@@ -48,7 +83,7 @@ k_spmv_f64(DevCsr a, const double* __restrict__ x, double* __restrict__ y) {
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int base = wg * 8; base < a.n; base += nw * 8) {
     const int i = base + (lane >> 2);
-    const double s = row_dot_q(a, i, i < a.n, x, q);
+    const double s = row_dot_warp8(a, base, x, lane);
     if (q == 0 && i < a.n) y[i] = s;
   }
 }
@@ -63,7 +98,7 @@ __global__ void __launch_bounds__(kThreads) k_krylov_spmv(DevCsr a, KrylovDev k)
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int base = wg * 8; base < a.n; base += nw * 8) {
     const int i = base + (lane >> 2);
-    const double s = row_dot_q(a, i, i < a.n, z, q);
+    const double s = row_dot_warp8(a, base, z, lane);
     if (q == 0 && i < a.n) {
       k.w[i] = s;
       if (k.Z) k.Z[static_cast<size_t>(j) * k.n + i] = z[i];
@@ -358,7 +393,7 @@ __global__ void __launch_bounds__(kThreads) k_residual(DevCsr a, KrylovDev k) {
   double p = 0.0;
   for (int base = wg * 8; base < a.n; base += nw * 8) {
     const int i = base + (lane >> 2);
-    const double s = row_dot_q(a, i, i < a.n, k.x, q);
+    const double s = row_dot_warp8(a, base, k.x, lane);
     if (q == 0 && i < a.n) {
       const double ri = k.b[i] + -1.0 * s;
       k.r[i] = ri;

@@ -330,6 +330,8 @@ struct SellCfg {
   // DP=16: the CUDA-core projection is cheap (DP*H FMAs per row) and the
   // staging it saves is L1 for the gathers (fused C2: 27.3 vs 26.5 us LAST,
   // 18 vs 17 us per layer with the larger layout)
+  // (re-measured in round 2 with the TMEM-resident projection operand, which
+  // needs no staging: C2 4,809 vs 4,953 applies/s, C4 last layer 145 vs 140 us)
   static __host__ __device__ constexpr bool tc_proj(int hidden) {
     return DP == 32 && hidden % 16 == 0 && hidden <= 64;
   }

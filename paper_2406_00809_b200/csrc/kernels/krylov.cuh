@@ -212,9 +212,18 @@ __global__ void __launch_bounds__(kThreads) k_krylov_ortho(KrylovDev k) {
   // One MGS pass over v_0..v_j; returns ||w|| afterwards.  With w in
   // registers, v_s also stays in registers from its dot (step s) to its axpy
   // (step s + 1): every basis vector is read once per pass.
-  double vc[E];
+  // v_{s+1} is requested before step s's grid barrier (vnx), so its load
+  // latency hides behind the barrier instead of following it.
+  double vc[E], vnx[E];
   auto mgs_pass = [&](bool add) -> double {
     double hprev = 0.0;
+    if constexpr (EPT > 0) {
+#pragma unroll
+      for (int t = 0; t < EPT; ++t) {
+        const int e = gt + t * T;
+        vnx[t] = e < n ? k.V[e] : 0.0;  // v_0
+      }
+    }
     for (int s = 0; s <= j + 1; ++s) {
       const double* vprev = k.V + static_cast<size_t>(s > 0 ? s - 1 : 0) * n;
       const double* vs = k.V + static_cast<size_t>(s) * n;
@@ -226,11 +235,19 @@ __global__ void __launch_bounds__(kThreads) k_krylov_ortho(KrylovDev k) {
           if (e < n) {
             if (s > 0) w[t] = fma(-hprev, vc[t], w[t]);
             if (s <= j) {
-              vc[t] = vs[e];
+              vc[t] = vnx[t];
               part = fma(w[t], vc[t], part);
             } else {
               part = fma(w[t], w[t], part);
             }
+          }
+        }
+        if (s + 1 <= j) {
+          const double* vn1 = vs + n;
+#pragma unroll
+          for (int t = 0; t < EPT; ++t) {
+            const int e = gt + t * T;
+            if (e < n) vnx[t] = vn1[e];
           }
         }
       } else {

@@ -355,7 +355,27 @@ __global__ void __launch_bounds__(kOnchipThreads, 1) k_krylov_ortho_onchip(Krylo
           }
         }
       }
-      for (int c = RB + tid; c < len; c += kOnchipThreads) {
+      // (four elements per trip with their loads issued together: the loop
+      // was latency-bound at one v_s / v_{s-1} pair in flight per thread)
+      int c = RB + tid;
+      for (; c + 3 * kOnchipThreads < len; c += 4 * kOnchipThreads) {
+        double vp[4], vv[4], we[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          vp[u] = s > 0 ? vprev[c + u * kOnchipThreads] : 0.0;
+          vv[u] = s <= j ? vs[c + u * kOnchipThreads] : 0.0;
+          we[u] = wsm[c + u * kOnchipThreads - RB];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (s > 0) {
+            we[u] = fma(-hprev, vp[u], we[u]);
+            wsm[c + u * kOnchipThreads - RB] = we[u];
+          }
+          part = s <= j ? fma(we[u], vv[u], part) : fma(we[u], we[u], part);
+        }
+      }
+      for (; c < len; c += kOnchipThreads) {
         double we = wsm[c - RB];
         if (s > 0) {
           we = fma(-hprev, vprev[c], we);

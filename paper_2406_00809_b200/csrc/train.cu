@@ -73,6 +73,16 @@ struct gnpc_trainer_s {
   CUtensorMap mGw[2]{};
   // batch
   DevBuf<double> xb, bb, out, sgn, gout, colpart, losspart, tmp;
+  // host-batch steps: x is uploaded on a copy stream while the forward runs
+  // on b (x is first read by the loss)
+  DevBuf<double> tmp2;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_b = nullptr, ev_x = nullptr;
+  ~gnpc_trainer_s() {
+    if (ev_b) cudaEventDestroy(ev_b);
+    if (ev_x) cudaEventDestroy(ev_x);
+    if (cs) cudaStreamDestroy(cs);
+  }
   DevBuf<gnpk::SampleScales> scl;
   // activations
   DevBuf<float> Xs, AXs, G[2], vv, hb1, hb2, gyv;
@@ -857,9 +867,24 @@ gnpc_trainer_s* create(gnpc_model_s* m, std::int64_t batch, double lr) {
 
 // x, b host n x B column-major: forward + loss (+ grad + backward)
 double step_fb(gnpc_trainer_s& T, const double* x, const double* b, bool bwd) {
-  upload_batch(T, x, T.xb);
+  // b first (the forward starts on it); x follows on the copy stream, behind
+  // b on the link, and lands while the forward runs: the loss is its first reader
   upload_batch(T, b, T.bb);
+  if (!T.cs) {
+    GNPC_CUDA(cudaStreamCreateWithFlags(&T.cs, cudaStreamNonBlocking));
+    GNPC_CUDA(cudaEventCreateWithFlags(&T.ev_b, cudaEventDisableTiming));
+    GNPC_CUDA(cudaEventCreateWithFlags(&T.ev_x, cudaEventDisableTiming));
+  }
+  const std::size_t cnt = (std::size_t)T.n * T.B;
+  T.tmp2.ensure(cnt);
+  GNPC_CUDA(cudaEventRecord(T.ev_b, T.s));  // after b's copy and every earlier reader of xb
+  GNPC_CUDA(cudaStreamWaitEvent(T.cs, T.ev_b, 0));
+  GNPC_CUDA(cudaMemcpyAsync(T.tmp2.p, x, cnt * 8, cudaMemcpyHostToDevice, T.cs));
+  gnpk::k_colmajor_to_nb<<<(int)((cnt + kTh - 1) / kTh), kTh, 0, T.cs>>>(T.tmp2.p, T.n, T.B, T.xb.p);
+  GNPC_LAUNCHED();
+  GNPC_CUDA(cudaEventRecord(T.ev_x, T.cs));
   forward(T);
+  GNPC_CUDA(cudaStreamWaitEvent(T.s, T.ev_x, 0));
   const double loss = loss_and_grad(T, bwd);
   if (bwd) backward(T);
   return loss;

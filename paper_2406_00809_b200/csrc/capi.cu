@@ -477,7 +477,6 @@ void gnpc_csr_s::upload() {
   }
   build_pairs(hrp, hci, hv);
   build_pw(hrp, hci, hv);
-  build_order(hrp, hci);
   // short-row CSR (long rows emptied), padded for the TMA pipeline's bulk copies
   {
     const std::int64_t n = h.n;
@@ -659,33 +658,6 @@ void gnpc_csr_s::build_pairs(const std::vector<int>& hrp, const std::vector<int>
   psell_off.upload(off.data(), off.size());
   psell_k.upload(K.data(), K.size());
   has_pairs = true;
-}
-
-// Tile schedule for the TMA layer pipeline.  A CTA walks a contiguous chunk
-// of this order, so its consecutive tiles should gather from overlapping row
-// windows and hit L1.  For matrices whose off-tile columns concentrate at one
-// tile distance S (stencils: the grid-line offset, e.g. 2048 rows = 16 tiles on
-// C5's 2048^2 grid, 4096 rows = 32 tiles on C2's 64^3), tiles are ordered
-// t = s + S k (s < S, k ascending): tile s + S(k+1) then reuses two of the
-// three row windows of tile s + S k.  Ragged/random matrices have no dominant
-// stride and keep round-robin.
-void gnpc_csr_s::build_order(const std::vector<int>& hrp, const std::vector<int>& hci) {
-  tstride = 0;
-  const std::int64_t n = h.n;
-  constexpr int TM = 128;
-  const std::int64_t T = (n + TM - 1) / TM;
-  // opt-in (GNPC_TORDER=1): C5 measured 427 vs 418 us per layer with it (its
-  // 28 KB of L1 beside the 198 KB ring cannot hold the three windows)
-  if (const char* e = std::getenv("GNPC_TORDER"); !e || std::string(e) != "1") return;
-  if (n_long != 0 || T < 4 * 148) return;
-  const int S = dominant_tile_stride(hrp, hci, 128);
-  if (S < 2) return;
-  std::vector<int> ord;
-  ord.reserve(T);
-  for (int s0 = 0; s0 < S; ++s0)
-    for (std::int64_t t = s0; t < T; t += S) ord.push_back(static_cast<int>(t));
-  torder.upload(ord.data(), ord.size());
-  tstride = S;
 }
 
 // The tile distance S (>= 2) at which most off-tile columns sit (a row
@@ -940,7 +912,6 @@ gnpk::DevCsr gnpc_csr_s::dev() {
   d.sell = has_sell ? sell.p : nullptr;
   d.sell_off = has_sell ? sell_off.p : nullptr;
   d.sell_k = has_sell ? sell_k.p : nullptr;
-  d.torder = tstride ? torder.p : nullptr;
   d.tw = nullptr;  // training layouts are per batch size: bind_tw
   d.tw_off = nullptr;
   d.tw_k = nullptr;

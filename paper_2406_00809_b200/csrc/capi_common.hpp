@@ -202,17 +202,12 @@ struct gnpc_csr_s {
   bool ensure_tw(int bs);
   // the layout for batch size bs into d (null fields when not built)
   void bind_tw(int bs, gnpk::DevCsr& d) const;
-  // tile schedule of the TMA layers (see DevCsr::torder); tstride = the
-  // dominant tile stride it was built from (0: round-robin, no order)
-  gnpc_impl::DevBuf<int> torder;
-  int tstride = 0;
   bool l2hint = true;
   std::unique_ptr<gnpc_csr_s> tr;  // Âᵀ (lazy, for training backward)
   std::unique_ptr<gnpc_impl::KrylovWs> kws;
   void upload();
   void build_sell(const std::vector<int>& hrp, const std::vector<int>& hci,
                   const std::vector<float>& hv);
-  void build_order(const std::vector<int>& hrp, const std::vector<int>& hci);
   void build_pairs(const std::vector<int>& hrp, const std::vector<int>& hci, const std::vector<float>& hv);
   void build_pw(const std::vector<int>& hrp, const std::vector<int>& hci, const std::vector<float>& hv);
   int dominant_tile_stride(const std::vector<int>& hrp, const std::vector<int>& hci, int TM) const;

@@ -76,12 +76,6 @@ struct DevCsr {
   const int* __restrict__ tw_k;
   const int* __restrict__ tw_order;
   int tw_S;
-  // Tile schedule of the TMA layer pipeline (apply path): nullptr = CTA b
-  // takes tiles b, b + grid, ...; else CTA b takes positions
-  // [b T / grid, (b+1) T / grid) of this permutation of the T tiles, ordered
-  // so consecutive tiles of a CTA reuse each other's X-row windows in L1
-  // (built from the matrix's dominant tile stride, gnpc_csr_s::build_order).
-  const int* __restrict__ torder;
   // L2 policy: 1 = the streamed matrix (slices, CSR ranges) is loaded
   // evict_first and the X-row gathers evict_last, so the layer input stays
   // L2-resident while Â streams past it; 0 = evict_normal everywhere.

@@ -803,8 +803,8 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   }
   tc::fence_proxy_async();
   __syncthreads();
-  // tile schedule: round-robin, or a contiguous chunk of the matrix's tile
-  // order (a.torder, apply path) so consecutive tiles share X-row windows
+  // tile schedule: round-robin, or (strip windows) a contiguous chunk of the
+  // layout's strip order, so consecutive tiles share X-row windows
   // window-mode arrays: the apply layout (pw) or the training layout (tw)
   const int* w_k = C::TW ? a.tw_k : a.pw_k;
   const int* w_off = C::TW ? a.tw_off : a.pw_off;
@@ -812,7 +812,7 @@ __device__ __forceinline__ void sell_layer(SellPipe<DP, CSR>& p, const DevCsr& a
   const int w_S = C::TW ? a.tw_S : a.pw_S;
   // rows of halo on either side of a window's own 128 rows: 8 (PW), one node (TW)
   const int w_halo = C::TW ? bs : kPwHalo;
-  const int* torder = C::TW ? a.tw_order : (TR ? nullptr : (C::PW ? a.pw_order : a.torder));
+  const int* torder = C::TW ? a.tw_order : (C::PW ? a.pw_order : nullptr);
   const int chunk0 = torder ? static_cast<int>(static_cast<long long>(blockIdx.x) * ntiles / gridDim.x) : 0;
   const int my_tiles =
       torder ? static_cast<int>(static_cast<long long>(blockIdx.x + 1) * ntiles / gridDim.x) - chunk0
